@@ -1,0 +1,190 @@
+/*
+ * sfairsc.h — C ABI of the B200 (sm_100a) s-FairSC eigensolver library.
+ *
+ * Method: Scalable FairSC, Wang, Lu, Davidson, Bai (arXiv 2210.16435),
+ * Algorithm 3.  The library computes the k smallest
+ * eigenpairs of the Hotelling-deflated, nullspace-projected fair-SC operator
+ *
+ *     L^sigma = P L P + sigma (I - P)                       Eq. asigma
+ *     L^sigma w = P(L(P w)) - sigma P w + sigma w
+ *
+ * with P = I - Q Q^T the orthogonal projector onto null(C^T) (Eq. pmat2,
+ * P:566-569; P = I - C (C^T C)^{-1} C^T) and
+ *   normalized: L = L_n = D^{-1/2}(D - W)D^{-1/2}, C = D^{-1/2} F;
+ *   unnormalized (reading R1): L = D - W, C = F;
+ * F = F_0(:, 1:h-1), F_0 = G - 1_n z^T, z = G^T 1_n / n (Lemma 2.1);
+ * sigma = ||L||_1.  By Prop. 3.4 the k smallest
+ * eigenvectors X of L^sigma solve the fair-SC problem, with
+ * H = D^{-1/2} X (H = X for R1).
+ *
+ * Conventions for every entry point
+ *  - Return value: SFAIRSC_OK or an error status; on error, outputs are left
+ *    untouched (exception: SFAIRSC_E_NO_CONVERGENCE still fills the best
+ *    Ritz values/vectors and stats).  sfairsc_last_error() gives
+ *    a thread-local message for the last non-OK status.
+ *  - Ownership: input arrays are borrowed for the duration of the call only;
+ *    the context copies what it needs into library-owned device memory and
+ *    owns it until sfairsc_destroy().  Output arrays are caller-allocated.
+ *  - memspace: SFAIRSC_MEM_HOST = ordinary host pointer (pinned or pageable),
+ *    SFAIRSC_MEM_DEVICE = CUDA device pointer on the context's device.
+ *  - Matrices of n-vectors are column-major with leading dimension n.
+ *  - All work is enqueued on the context's stream (opts.cuda_stream, or a
+ *    stream the library creates); every call returns with that stream
+ *    synchronised.  Calls on one context must not run concurrently.
+ *  - Determinism: for fixed inputs, options and GPU, results are bitwise
+ *    reproducible (fixed-order reductions, no floating-point atomics).
+ *  - Precision: fp64 arithmetic throughout (indices int32).
+ */
+#ifndef SFAIRSC_H
+#define SFAIRSC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sfairsc_ctx sfairsc_ctx; /* opaque; owns all device memory */
+
+typedef enum {
+  SFAIRSC_OK = 0,
+  SFAIRSC_E_INVALID_ARG = 1,      /* bad scalar argument / null pointer / group id out of [0,h) */
+  SFAIRSC_E_DIM_MISMATCH = 2,     /* n_rows != n_cols, ... */
+  SFAIRSC_E_CSR_INVALID = 3,      /* row_ptr not monotone / col out of range / unsorted or duplicate columns / nonzero diagonal (w_ii = 0) */
+  SFAIRSC_E_ASYMMETRIC = 4,       /* W != W^T (undirected graph) */
+  SFAIRSC_E_NEGATIVE_WEIGHT = 5,  /* w_ij < 0 */
+  SFAIRSC_E_ISOLATED_VERTEX = 6,  /* d_i = 0; the paper assumes D > 0 */
+  SFAIRSC_E_EMPTY_GROUP = 7,      /* some V_s empty */
+  SFAIRSC_E_RANK_DEFICIENT = 8,   /* rank F < h-1 (cannot happen for non-empty groups, Lemma 2.1(i)) */
+  SFAIRSC_E_K_TOO_LARGE = 9,      /* k > n - h + 1 (dimension of null(C^T)) or k > build k */
+  SFAIRSC_E_SHIFT_TOO_SMALL = 10, /* some wanted lambda_i >= sigma (1 - 1e-8): Prop. 3.4 precondition violated */
+  SFAIRSC_E_NO_CONVERGENCE = 11,  /* max_restarts reached; best Ritz pairs returned */
+  SFAIRSC_E_STATE = 12,           /* call order (build -> eigs -> embed_kmeans) violated */
+  SFAIRSC_E_OOM = 13,             /* device allocation failed */
+  SFAIRSC_E_CUDA = 14,            /* CUDA runtime error (message in sfairsc_last_error) */
+  SFAIRSC_E_NCCL = 15             /* reserved: multi-GPU communicator error */
+} sfairsc_status;
+
+enum { SFAIRSC_MEM_HOST = 0, SFAIRSC_MEM_DEVICE = 1 };
+
+/* Weighted adjacency W as CSR: row_ptr[n_rows+1], col_idx[nnz],
+ * values[nnz]; both triangles stored; columns strictly increasing within a
+ * row; w_ij >= 0; no stored nonzero diagonal.  Single-GPU: n_rows == n_cols,
+ * row_offset == 0.  int32 indices: nnz < 2^31. */
+typedef struct {
+  int64_t n_rows, n_cols, nnz, row_offset;
+  const int32_t *row_ptr;
+  const int32_t *col_idx;
+  const double *values;
+  int32_t memspace;
+} sfairsc_csr;
+
+/* Options of the extended build.  sfairsc_default_opts() fills defaults. */
+typedef struct {
+  double sigma_override;  /* <= 0: sigma = ||L||_1; > 0: use this shift (must exceed lambda_k, Prop. 3.4) */
+  int32_t max_basis;      /* Lanczos basis size m; 0: max(2k+10, 20), capped at n */
+  int32_t keep;           /* Ritz vectors kept at a thick restart; 0: k + (m-k)/2 */
+  int32_t max_restarts;   /* 0: 100000 */
+  uint64_t start_seed;    /* Philox key for the Lanczos start / breakdown vectors */
+  double tol_eff_cap;     /* residual target = min(tol, tol_eff_cap) * sigma; <= 0: 1e-10 (reading R7) */
+  void *cuda_stream;      /* cudaStream_t to run on (e.g. torch.cuda.current_stream()); NULL: library-created */
+  int32_t check_symmetry; /* 1 (default): verify W == W^T at build (one O(nnz log deg) pass) */
+  int32_t spmv_vector;    /* 0: auto; else lanes per row in the SpMV (2,4,8,16,32) */
+} sfairsc_opts;
+
+typedef struct {
+  int64_t applies;       /* operator applications L^sigma w performed by eigs (incl. final residual check) */
+  int64_t steps;         /* Lanczos expansion steps */
+  int64_t restarts;      /* thick restarts */
+  int64_t breakdowns;    /* invariant-subspace breakdowns (fresh random vector injected) */
+  double sigma;          /* the shift used */
+  double max_resid_rel;  /* max_i ||L^sigma x_i - lambda_i x_i||_2 / sigma, recomputed with k fresh applies */
+  double gap_est;        /* theta_{k+1} - theta_k from the final Rayleigh-Ritz (NaN if unavailable) */
+  double t_build_s;      /* wall time of the build call */
+  double t_eigs_s;       /* wall time of the last eigs call */
+  int32_t converged;     /* 1 if the residual target was met */
+  int32_t basis_size;    /* m used */
+  int32_t kept;          /* Ritz vectors kept per restart */
+  int32_t reserved;
+} sfairsc_stats;
+
+typedef struct {
+  int64_t n, nnz;
+  int32_t h, k_build, normalized, spmv_vector;
+  double sigma;
+  int32_t device, num_sms;
+} sfairsc_info;
+
+void sfairsc_default_opts(sfairsc_opts *opts);
+
+/* Alg. 3 steps 1-2 + shift: validate W and
+ * groups (A0), copy them into library-owned device memory, compute degrees
+ * d = W 1, the scaling s = d^{-1/2} (normalized: stored values
+ * become s_i w_ij s_j), sigma = ||L||_1, and the factored basis Q of
+ * range(C) (DESIGN.md §Factored projector; no dense Q is formed).
+ * groups[n] in the same memspace as W, values in [0, h); h = 0 infers
+ * h = max(groups)+1; 1 <= h <= 255.  k = number of eigenpairs the context
+ * must be able to return (sizes the Krylov basis).  *out receives a new
+ * context on success. */
+sfairsc_status sfairsc_build_operator(const sfairsc_csr *W, const int32_t *groups, int32_t h,
+                                      int32_t k, int32_t normalized, sfairsc_ctx **out);
+sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr *W, const int32_t *groups, int32_t h,
+                                         int32_t k, int32_t normalized, const sfairsc_opts *opts,
+                                         sfairsc_ctx **out);
+
+/* Alg. 3 step 3: the k smallest eigenpairs of L^sigma by
+ * thick-restart Lanczos with full CGS2 reorthogonalisation (replaces
+ * MATLAB eigs / ARPACK).  Stops when every wanted Ritz pair has
+ * ||L^sigma x - theta x|| <= min(tol, tol_eff_cap) * sigma.
+ * evals_out[k] (host, ascending); evecs_out = X (n x k, column-major,
+ * orthonormal, C^T X = 0) in evecs_memspace, or NULL.  stats may be NULL. */
+sfairsc_status sfairsc_eigs(sfairsc_ctx *ctx, int32_t k, double tol, double *evals_out,
+                            double *evecs_out, int32_t evecs_memspace, sfairsc_stats *stats);
+
+/* Alg. 3 step 4: k-means on the rows of H = D^{-1/2} X (normalized)
+ * or H = X (unnormalized) from the last eigs call, with the k-means variant
+ * of reading R16 (k-means++ seeding, Lloyd, best of 10 restarts by WCSS,
+ * Philox4x32-10 draws keyed by `seed`).  labels_out[n] in memspace;
+ * objective_out (host, may be NULL) = best WCSS. */
+sfairsc_status sfairsc_embed_kmeans(sfairsc_ctx *ctx, uint64_t seed, int32_t *labels_out,
+                                    int32_t memspace, double *objective_out);
+
+/* y = L^sigma x for nvec column vectors: four fused kernels —
+ * group sums B^T x, p = P x, SpMV t = L p with B^T t in its epilogue,
+ * y = t - s o (gamma_t - sigma gamma_x)_g.  x, y: n x nvec, same memspace. */
+sfairsc_status sfairsc_apply(sfairsc_ctx *ctx, const double *x, double *y, int32_t nvec,
+                             int32_t memspace);
+
+/* y = P x (P:807-818 in factored form) for nvec column vectors. */
+sfairsc_status sfairsc_project(sfairsc_ctx *ctx, const double *x, double *y, int32_t nvec,
+                               int32_t memspace);
+
+/* y = L x (normalized: L_n; unnormalized: D - W) — the bare SpMV, for tests. */
+sfairsc_status sfairsc_laplacian(sfairsc_ctx *ctx, const double *x, double *y, int32_t memspace);
+
+sfairsc_status sfairsc_get_info(const sfairsc_ctx *ctx, sfairsc_info *info);
+
+/* Per-kernel device timing with CUDA events on the context stream (for the
+ * bench roofline).  kind: 0 spmv, 1 reorth sweep (dots), 2 reorth sweep
+ * (update+dots), 3 reorth sweep (update+norm), 4 normalize, 5 ritz gemm,
+ * 6 project/group-sum, 7 apply-finish, 8 kmeans, 9 other.  Enabling adds
+ * one event pair per launch. */
+sfairsc_status sfairsc_profile_enable(sfairsc_ctx *ctx, int32_t enable);
+sfairsc_status sfairsc_profile_read(sfairsc_ctx *ctx, int32_t kind, double *total_ms,
+                                    int64_t *launches);
+sfairsc_status sfairsc_profile_reset(sfairsc_ctx *ctx);
+
+/* Host-only utility: the dense symmetric eigensolver of the Rayleigh-Ritz step
+ * (Householder tridiagonalisation + implicit QL).  A: m x m row-major
+ * symmetric; evals[m] ascending; evecs (m x m row-major, column c = vector c,
+ * may be NULL).  Returns 0 on success.  Exported so tests can pin it on CPU. */
+int sfairsc_host_symeig(int32_t m, const double *A, double *evals, double *evecs);
+
+void sfairsc_destroy(sfairsc_ctx *ctx);
+const char *sfairsc_last_error(void);
+const char *sfairsc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFAIRSC_H */

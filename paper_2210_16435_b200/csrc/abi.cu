@@ -1,0 +1,930 @@
+// libsfairsc — C ABI (include/sfairsc.h): context, operator build (A0-A3),
+// operator apply (A4-A6), thick-restart Lanczos driver (A7-A11).
+#include "sfairsc.h"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+namespace sfz {
+void symeig(int m, std::vector<double>& A, std::vector<double>& evals);
+sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, int32_t memspace, double* objective);
+}  // namespace sfz
+
+using namespace sfz;
+
+static thread_local std::string g_err;
+
+static sfairsc_status fail(sfairsc_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CU(expr)                                                                                        \
+  do {                                                                                                  \
+    cudaError_t e_ = (expr);                                                                            \
+    if (e_ != cudaSuccess)                                                                              \
+      return fail(e_ == cudaErrorMemoryAllocation ? SFAIRSC_E_OOM : SFAIRSC_E_CUDA, "%s: %s (%s:%d)", \
+                  #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                                    \
+  } while (0)
+
+#define CHECK_LAUNCH() CU(cudaGetLastError())
+#define TRY(expr)                              \
+  do {                                         \
+    sfairsc_status s_ = (expr);                \
+    if (s_ != SFAIRSC_OK) return s_;           \
+  } while (0)
+
+// --------------------------------------------------------------------------
+// per-kernel event timing (sfairsc_profile_*)
+// --------------------------------------------------------------------------
+struct Prof {
+  bool on = false;
+  struct Pending {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  double total_ms[10] = {};
+  int64_t launches[10] = {};
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void resolve() {
+    for (auto& p : pending) {
+      cudaEventSynchronize(p.b);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, p.a, p.b);
+      total_ms[p.kind] += ms;
+      launches[p.kind] += 1;
+      pool.push_back(p.a);
+      pool.push_back(p.b);
+    }
+    pending.clear();
+  }
+  ~Prof() {
+    for (auto& p : pending) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+enum { K_SPMV = 0, K_DOTS = 1, K_UPDDOT = 2, K_UPDNORM = 3, K_NORMALIZE = 4, K_RITZ = 5, K_PROJ = 6, K_FINISH = 7,
+       K_KMEANS = 8, K_OTHER = 9 };
+
+struct sfairsc_ctx {
+  int device = 0, num_sms = 148;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  int n = 0, nnz = 0, h = 1, k_build = 1;
+  bool normalized = false;
+  long long ldv = 0;
+  int vs = 8, spmv_grid = 1, sgrid = 1;
+  double sigma = 0.0, tol_cap = 1e-10;
+  uint64_t seed = 0x5F41C5EEDull;
+  int m = 20, keep = 0, max_restarts = 100000;
+  int check_symmetry = 1;
+  // device buffers
+  int *rp = nullptr, *ci = nullptr, *row_split = nullptr;
+  double *vv = nullptr, *dg = nullptr, *s = nullptr;
+  uint8_t* grp = nullptr;
+  double *isb = nullptr, *uh = nullptr;
+  double* partials = nullptr;
+  size_t partials_cnt = 0;
+  unsigned* counters = nullptr;
+  double *bs_w = nullptr, *bs_t = nullptr, *bs_v = nullptr, *nb = nullptr, *scal = nullptr;
+  double *c1 = nullptr, *c2 = nullptr;
+  double *vp = nullptr, *vt = nullptr, *vr = nullptr, *vy = nullptr;
+  double *V = nullptr, *Vb = nullptr, *Ydev = nullptr, *X = nullptr;
+  int* flags = nullptr;
+  double* hp = nullptr;  // pinned host staging (4 KB)
+  // results
+  bool have_eigs = false;
+  int k_eigs = 0;
+  std::vector<double> evals;
+  std::vector<int32_t> groups_host;
+  std::vector<int64_t> group_count;
+  sfairsc_stats last{};
+  double t_build = 0.0;
+  Prof prof;
+  // kmeans scratch (allocated lazily by kmeans.cu)
+  void* km = nullptr;
+  void (*km_free)(void*) = nullptr;
+
+  GraphDev g() const {
+    GraphDev G;
+    G.n = n;
+    G.nnz = nnz;
+    G.rp = rp;
+    G.ci = ci;
+    G.vv = vv;
+    G.dg = dg;
+    G.s = s;
+    G.grp = grp;
+    G.normalized = normalized;
+    return G;
+  }
+  ProjDesc pd() const { return ProjDesc{h, isb, uh}; }
+};
+
+// accessors used by kmeans.cu
+namespace sfz {
+cudaStream_t ctx_stream(sfairsc_ctx* c) { return c->st; }
+int ctx_n(sfairsc_ctx* c) { return c->n; }
+int ctx_k(sfairsc_ctx* c) { return c->k_eigs; }
+bool ctx_have_eigs(sfairsc_ctx* c) { return c->have_eigs; }
+const double* ctx_X(sfairsc_ctx* c, long long* ld) {
+  *ld = c->ldv;
+  return c->X;
+}
+const double* ctx_s(sfairsc_ctx* c) { return c->normalized ? c->s : nullptr; }
+int ctx_num_sms(sfairsc_ctx* c) { return c->num_sms; }
+void** ctx_km(sfairsc_ctx* c, void (**freer)(void*)) {
+  *freer = c->km_free;
+  return &c->km;
+}
+void ctx_set_km_free(sfairsc_ctx* c, void (*f)(void*)) { c->km_free = f; }
+void ctx_prof_begin(sfairsc_ctx* c, cudaEvent_t* a);
+void ctx_prof_end(sfairsc_ctx* c, int kind, cudaEvent_t a);
+sfairsc_status ctx_fail(sfairsc_status st, const char* msg) { return fail(st, "%s", msg); }
+}  // namespace sfz
+
+// profiling wrappers
+struct ProfScope {
+  sfairsc_ctx* c;
+  int kind;
+  cudaEvent_t a = nullptr;
+  ProfScope(sfairsc_ctx* c_, int kind_) : c(c_), kind(kind_) {
+    if (c->prof.on) {
+      a = c->prof.get();
+      cudaEventRecord(a, c->st);
+    }
+  }
+  ~ProfScope() {
+    if (c->prof.on) {
+      cudaEvent_t b = c->prof.get();
+      cudaEventRecord(b, c->st);
+      c->prof.pending.push_back({kind, a, b});
+    }
+  }
+};
+namespace sfz {
+void ctx_prof_begin(sfairsc_ctx* c, cudaEvent_t* a) {
+  *a = nullptr;
+  if (c->prof.on) {
+    *a = c->prof.get();
+    cudaEventRecord(*a, c->st);
+  }
+}
+void ctx_prof_end(sfairsc_ctx* c, int kind, cudaEvent_t a) {
+  if (c->prof.on && a) {
+    cudaEvent_t b = c->prof.get();
+    cudaEventRecord(b, c->st);
+    c->prof.pending.push_back({kind, a, b});
+  }
+}
+}  // namespace sfz
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+}
+
+static void free_ctx(sfairsc_ctx* c) {
+  if (!c) return;
+  if (c->km && c->km_free) c->km_free(c->km);
+  void* ptrs[] = {c->rp, c->ci, c->row_split, c->vv, c->dg, c->s, c->grp, c->isb, c->uh, c->partials, c->counters,
+                  c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
+                  c->Vb, c->Ydev, c->X, c->flags};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->hp) cudaFreeHost(c->hp);
+  if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// --------------------------------------------------------------------------
+// options / info
+// --------------------------------------------------------------------------
+extern "C" void sfairsc_default_opts(sfairsc_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->sigma_override = 0.0;
+  o->max_basis = 0;
+  o->keep = 0;
+  o->max_restarts = 0;
+  o->start_seed = 0x5F41C5EEDull;
+  o->tol_eff_cap = 1e-10;
+  o->cuda_stream = nullptr;
+  o->check_symmetry = 1;
+  o->spmv_vector = 0;
+}
+
+extern "C" const char* sfairsc_last_error(void) { return g_err.c_str(); }
+extern "C" const char* sfairsc_version(void) { return "sfairsc-b200 0.1 (sm_100a, fp64)"; }
+
+extern "C" sfairsc_status sfairsc_get_info(const sfairsc_ctx* c, sfairsc_info* info) {
+  if (!c || !info) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
+  info->n = c->n;
+  info->nnz = c->nnz;
+  info->h = c->h;
+  info->k_build = c->k_build;
+  info->normalized = c->normalized;
+  info->spmv_vector = c->vs;
+  info->sigma = c->sigma;
+  info->device = c->device;
+  info->num_sms = c->num_sms;
+  return SFAIRSC_OK;
+}
+
+// --------------------------------------------------------------------------
+// group sums for h > 16 (the fused epilogues cover groups [0,16))
+// --------------------------------------------------------------------------
+static void extra_gsums(sfairsc_ctx* c, const double* x, double* bsum) {
+  for (int gb = kHB; gb < c->h; gb += kHB)
+    launch_gsum(c->g(), x, gb, c->partials, c->counters + 3, bsum, c->st);
+}
+
+static void gsum_all(sfairsc_ctx* c, const double* x, double* bsum) {
+  for (int gb = 0; gb < c->h; gb += kHB) launch_gsum(c->g(), x, gb, c->partials, c->counters + 3, bsum, c->st);
+}
+
+// y = L^sigma x on device vectors (4 kernels; A4-A6)
+static sfairsc_status apply_dev(sfairsc_ctx* c, const double* x, double* y) {
+  {
+    ProfScope ps(c, K_PROJ);
+    gsum_all(c, x, c->bs_w);
+    launch_project(c->g(), c->pd(), x, c->bs_w, 1.0, c->vp, c->st);
+  }
+  {
+    ProfScope ps(c, K_SPMV);
+    launch_spmv(c->g(), c->vs, c->row_split, c->spmv_grid, c->vp, c->vt, c->partials, c->counters + 1, c->bs_t,
+                c->st);
+  }
+  if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
+  {
+    ProfScope ps(c, K_FINISH);
+    launch_finish(c->g(), c->pd(), c->vt, c->bs_t, c->bs_w, c->sigma, y, c->st);
+  }
+  CHECK_LAUNCH();
+  return SFAIRSC_OK;
+}
+
+// --------------------------------------------------------------------------
+// build (A0-A3)
+// --------------------------------------------------------------------------
+extern "C" sfairsc_status sfairsc_build_operator(const sfairsc_csr* W, const int32_t* groups, int32_t h, int32_t k,
+                                                 int32_t normalized, sfairsc_ctx** out) {
+  return sfairsc_build_operator_ex(W, groups, h, k, normalized, nullptr, out);
+}
+
+extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const int32_t* groups, int32_t h,
+                                                    int32_t k, int32_t normalized, const sfairsc_opts* opts_in,
+                                                    sfairsc_ctx** out) {
+  const double t0 = now_s();
+  if (!W || !groups || !out) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  sfairsc_opts opts;
+  sfairsc_default_opts(&opts);
+  if (opts_in) opts = *opts_in;
+  if (W->memspace != SFAIRSC_MEM_HOST && W->memspace != SFAIRSC_MEM_DEVICE)
+    return fail(SFAIRSC_E_INVALID_ARG, "bad memspace");
+  if (W->n_rows != W->n_cols) return fail(SFAIRSC_E_DIM_MISMATCH, "n_rows != n_cols (multi-GPU row blocks not built)");
+  if (W->row_offset != 0) return fail(SFAIRSC_E_INVALID_ARG, "row_offset must be 0 on a single GPU");
+  if (W->n_rows < 1 || W->n_rows >= (1LL << 31) - 1024) return fail(SFAIRSC_E_INVALID_ARG, "n out of range");
+  if (W->nnz < 0 || W->nnz >= (1LL << 31) - 1) return fail(SFAIRSC_E_INVALID_ARG, "nnz out of int32 range");
+  if (W->nnz > 0 && (!W->col_idx || !W->values)) return fail(SFAIRSC_E_INVALID_ARG, "null CSR arrays");
+  if (!W->row_ptr) return fail(SFAIRSC_E_INVALID_ARG, "null row_ptr");
+  if (k < 1) return fail(SFAIRSC_E_INVALID_ARG, "k must be >= 1");
+  if (h < 0 || h > 255) return fail(SFAIRSC_E_INVALID_ARG, "h must be in [0, 255]");
+  const int n = (int)W->n_rows, nnz = (int)W->nnz;
+  const bool dev_in = W->memspace == SFAIRSC_MEM_DEVICE;
+
+  // groups on host: counts, inferred h, range check
+  std::vector<int32_t> hg(n);
+  if (dev_in) {
+    cudaError_t e = cudaMemcpy(hg.data(), groups, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(SFAIRSC_E_CUDA, "groups copy: %s", cudaGetErrorString(e));
+  } else {
+    std::memcpy(hg.data(), groups, sizeof(int32_t) * n);
+  }
+  int hh = h;
+  if (hh == 0) {
+    int mx = -1;
+    for (int i = 0; i < n; ++i) mx = std::max(mx, hg[i]);
+    hh = mx + 1;
+    if (hh < 1 || hh > 255) return fail(SFAIRSC_E_INVALID_ARG, "inferred h out of range");
+  }
+  std::vector<int64_t> cnt(hh, 0);
+  for (int i = 0; i < n; ++i) {
+    if (hg[i] < 0 || hg[i] >= hh) return fail(SFAIRSC_E_INVALID_ARG, "group id %d out of [0,%d) at vertex %d", hg[i], hh, i);
+    cnt[hg[i]]++;
+  }
+  for (int s = 0; s < hh; ++s)
+    if (cnt[s] == 0) return fail(SFAIRSC_E_EMPTY_GROUP, "group %d is empty (P:152)", s);
+  if ((int64_t)k > (int64_t)n - hh + 1) return fail(SFAIRSC_E_K_TOO_LARGE, "k=%d > n-h+1=%lld", k, (long long)n - hh + 1);
+
+  sfairsc_ctx* c = new sfairsc_ctx();
+  c->n = n;
+  c->nnz = nnz;
+  c->h = hh;
+  c->k_build = k;
+  c->normalized = normalized != 0;
+  c->groups_host = hg;
+  c->group_count = cnt;
+  c->tol_cap = opts.tol_eff_cap > 0 ? opts.tol_eff_cap : 1e-10;
+  c->seed = opts.start_seed;
+  c->max_restarts = opts.max_restarts > 0 ? opts.max_restarts : 100000;
+  c->check_symmetry = opts.check_symmetry;
+  auto bail = [&](sfairsc_status st) {
+    free_ctx(c);
+    return st;
+  };
+#define CUB(expr)                                                                                          \
+  do {                                                                                                     \
+    cudaError_t e_ = (expr);                                                                               \
+    if (e_ != cudaSuccess)                                                                                 \
+      return bail(fail(e_ == cudaErrorMemoryAllocation ? SFAIRSC_E_OOM : SFAIRSC_E_CUDA, "%s: %s (%s:%d)", \
+                       #expr, cudaGetErrorString(e_), __FILE__, __LINE__));                                 \
+  } while (0)
+
+  CUB(cudaGetDevice(&c->device));
+  CUB(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  if (opts.cuda_stream) {
+    c->st = (cudaStream_t)opts.cuda_stream;
+  } else {
+    CUB(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  c->ldv = ((long long)n + 255) / 256 * 256;
+  // Krylov basis size (SPEC S:342 default), capped so that v_{m+1} exists
+  int m = opts.max_basis > 0 ? opts.max_basis : std::max(2 * k + 10, 20);
+  m = std::min(m, kMaxJ - 1);
+  m = std::min(m, std::max(n - 1, 1));
+  m = std::max(m, std::min(k + 1, n));
+  if (m > n) m = n;
+  c->m = m;
+  c->keep = opts.keep > 0 ? opts.keep : k + (m - k) / 2;
+  c->keep = std::max(std::min(c->keep, m - 1), std::min(k, m - 1));
+
+  // device allocations
+  CUB(dalloc(&c->rp, n + 1));
+  CUB(dalloc(&c->ci, nnz));
+  CUB(dalloc(&c->vv, nnz));
+  CUB(dalloc(&c->dg, n));
+  if (c->normalized) CUB(dalloc(&c->s, n));
+  CUB(dalloc(&c->grp, n));
+  CUB(dalloc(&c->isb, 256));
+  CUB(dalloc(&c->uh, 256));
+  CUB(dalloc(&c->counters, 16));
+  CUB(cudaMemset(c->counters, 0, 16 * sizeof(unsigned)));
+  CUB(dalloc(&c->flags, 4));
+  CUB(cudaMemset(c->flags, 0, 4 * sizeof(int)));
+  for (double** p : {&c->bs_w, &c->bs_t, &c->bs_v, &c->nb, &c->scal}) {
+    CUB(dalloc(p, 512));
+    CUB(cudaMemset(*p, 0, 512 * sizeof(double)));
+  }
+  CUB(dalloc(&c->c1, kMaxJ));
+  CUB(dalloc(&c->c2, kMaxJ));
+  for (double** p : {&c->vp, &c->vt, &c->vr, &c->vy}) {
+    CUB(dalloc(p, c->ldv));
+    CUB(cudaMemsetAsync(*p, 0, c->ldv * sizeof(double), c->st));
+  }
+  CUB(cudaMallocHost((void**)&c->hp, 4096 * sizeof(double)));
+
+  // A0: library-owned copies of W and groups
+  const cudaMemcpyKind kind = dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CUB(cudaMemcpyAsync(c->rp, W->row_ptr, sizeof(int) * (n + 1), kind, c->st));
+  if (nnz > 0) {
+    CUB(cudaMemcpyAsync(c->ci, W->col_idx, sizeof(int) * nnz, kind, c->st));
+    CUB(cudaMemcpyAsync(c->vv, W->values, sizeof(double) * nnz, kind, c->st));
+  }
+  {
+    int32_t* dgroups = nullptr;
+    CUB(dalloc(&dgroups, n));
+    CUB(cudaMemcpyAsync(dgroups, hg.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->st));
+    launch_group_check(dgroups, n, hh, c->grp, c->flags, c->st);
+    CUB(cudaStreamSynchronize(c->st));
+    cudaFree(dgroups);
+  }
+  // row_ptr on host (nnz-balanced SpMV partition)
+  std::vector<int32_t> hrp(n + 1);
+  if (dev_in) {
+    CUB(cudaMemcpy(hrp.data(), W->row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(hrp.data(), W->row_ptr, sizeof(int32_t) * (n + 1));
+  }
+  launch_validate_csr(c->g(), c->check_symmetry, c->flags, c->st);
+  CUB(cudaGetLastError());
+  int hflags = 0;
+  CUB(cudaMemcpyAsync(&hflags, c->flags, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CUB(cudaStreamSynchronize(c->st));
+  if (hflags & 1) return bail(fail(SFAIRSC_E_CSR_INVALID, "CSR invalid (row_ptr/col range, unsorted or duplicate columns, or nonzero diagonal)"));
+  if (hflags & 2) return bail(fail(SFAIRSC_E_NEGATIVE_WEIGHT, "negative or NaN weight (P:121)"));
+  if (hflags & 4) return bail(fail(SFAIRSC_E_ASYMMETRIC, "W is not symmetric"));
+  // A1: degrees d = W 1
+  launch_degrees(c->g(), c->dg, c->flags, c->st);
+  CUB(cudaMemcpyAsync(&hflags, c->flags, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CUB(cudaStreamSynchronize(c->st));
+  if (hflags & 8) return bail(fail(SFAIRSC_E_ISOLATED_VERTEX, "isolated vertex: d_i = 0 (P:127-128)"));
+  if (c->normalized) {
+    launch_inv_sqrt(c->dg, c->s, n, c->st);                   // s = d^{-1/2}
+    launch_scale_values(c->rp, c->ci, c->vv, c->s, n, c->st);  // stored values s_i w_ij s_j
+  }
+  // A2: sigma = ||L||_1
+  launch_sigma(c->g(), c->vt, c->counters + 0, c->scal, c->st);
+  CUB(cudaGetLastError());
+  double hsig = 0.0;
+  CUB(cudaMemcpyAsync(&hsig, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUB(cudaStreamSynchronize(c->st));
+  c->sigma = opts.sigma_override > 0 ? opts.sigma_override : hsig;
+
+  // A3: factored basis of range(C): beta_s = sum_{V_s} s_i^2, u_s = |V_s| beta_s^{-1/2}
+  c->sgrid = sweep_grid(n, c->num_sms);
+  // SpMV partition: CTA b owns rows with cumulative (nnz + 4 rows) weight in [b, b+1)/G
+  {
+    const long long total = (long long)nnz + 4LL * n;
+    int G = std::max(1, std::min(c->num_sms * 8, (n + 31) / 32));
+    std::vector<int32_t> split(G + 1);
+    split[0] = 0;
+    split[G] = n;
+    for (int b = 1; b < G; ++b) {
+      const long long target = total * b / G;
+      int lo = 0, hi = n;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((long long)hrp[mid] + 4LL * mid < target) lo = mid + 1; else hi = mid;
+      }
+      split[b] = std::max(split[b - 1], lo);
+    }
+    c->spmv_grid = G;
+    CUB(dalloc(&c->row_split, G + 1));
+    CUB(cudaMemcpyAsync(c->row_split, split.data(), sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, c->st));
+    const double mean_deg = n > 0 ? (double)nnz / n : 0.0;
+    int vs = 2;
+    while (vs < 32 && vs * 4 <= mean_deg) vs *= 2;
+    c->vs = opts.spmv_vector > 0 ? opts.spmv_vector : vs;
+    if (c->vs != 2 && c->vs != 4 && c->vs != 8 && c->vs != 16 && c->vs != 32)
+      return bail(fail(SFAIRSC_E_INVALID_ARG, "spmv_vector must be 2,4,8,16 or 32"));
+  }
+  // partial buffers: max over users
+  {
+    size_t need = std::max<size_t>((size_t)c->sgrid * (kMaxJ + 1), (size_t)c->spmv_grid * kHB);
+    need = std::max<size_t>(need, (size_t)c->num_sms * 16 * (kHB + 1));
+    need = std::max<size_t>(need, (size_t)c->sgrid * (kHB + 1));
+    c->partials_cnt = need;
+    CUB(dalloc(&c->partials, need));
+  }
+  {
+    std::vector<double> beta(hh), isb(hh), uh(hh);
+    if (c->normalized) {
+      gsum_all(c, c->s, c->bs_w);  // B^T s = sum_{V_s} s_i^2
+      CUB(cudaGetLastError());
+      CUB(cudaMemcpyAsync(c->hp, c->bs_w, sizeof(double) * hh, cudaMemcpyDeviceToHost, c->st));
+      CUB(cudaStreamSynchronize(c->st));
+      for (int s = 0; s < hh; ++s) beta[s] = c->hp[s];
+    } else {
+      for (int s = 0; s < hh; ++s) beta[s] = (double)cnt[s];
+    }
+    double un = 0.0;
+    for (int s = 0; s < hh; ++s) {
+      if (!(beta[s] > 0)) return bail(fail(SFAIRSC_E_RANK_DEFICIENT, "group %d has zero weight", s));
+      isb[s] = 1.0 / std::sqrt(beta[s]);
+      uh[s] = (double)cnt[s] * isb[s];
+      un += uh[s] * uh[s];
+    }
+    un = std::sqrt(un);
+    for (int s = 0; s < hh; ++s) uh[s] /= un;
+    CUB(cudaMemcpyAsync(c->isb, isb.data(), sizeof(double) * hh, cudaMemcpyHostToDevice, c->st));
+    CUB(cudaMemcpyAsync(c->uh, uh.data(), sizeof(double) * hh, cudaMemcpyHostToDevice, c->st));
+  }
+  // Krylov basis (double-buffered for thick restarts) and eigenvector block
+  CUB(dalloc(&c->V, (size_t)(m + 1) * c->ldv));
+  CUB(dalloc(&c->Vb, (size_t)(m + 1) * c->ldv));
+  CUB(cudaMemsetAsync(c->V, 0, sizeof(double) * (m + 1) * c->ldv, c->st));
+  CUB(cudaMemsetAsync(c->Vb, 0, sizeof(double) * (m + 1) * c->ldv, c->st));
+  CUB(dalloc(&c->Ydev, (size_t)(m + 1) * (m + 1)));
+  CUB(dalloc(&c->X, (size_t)k * c->ldv));
+  CUB(cudaMemsetAsync(c->X, 0, sizeof(double) * k * c->ldv, c->st));
+  CUB(cudaStreamSynchronize(c->st));
+  c->t_build = now_s() - t0;
+  *out = c;
+#undef CUB
+  return SFAIRSC_OK;
+}
+
+extern "C" void sfairsc_destroy(sfairsc_ctx* c) {
+  if (!c) return;
+  if (c->st) cudaStreamSynchronize(c->st);
+  free_ctx(c);
+}
+
+// --------------------------------------------------------------------------
+// apply / project / laplacian entry points
+// --------------------------------------------------------------------------
+static sfairsc_status vec_io(sfairsc_ctx* c, const double* x, double* y, int32_t nvec, int32_t memspace,
+                             sfairsc_status (*op)(sfairsc_ctx*, const double*, double*)) {
+  if (!c || !x || !y || nvec < 0) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
+  if (memspace != SFAIRSC_MEM_HOST && memspace != SFAIRSC_MEM_DEVICE) return fail(SFAIRSC_E_INVALID_ARG, "memspace");
+  const size_t nb = sizeof(double) * c->n;
+  for (int v = 0; v < nvec; ++v) {
+    const double* xv = x + (size_t)v * c->n;
+    double* yv = y + (size_t)v * c->n;
+    if (memspace == SFAIRSC_MEM_HOST) {
+      CU(cudaMemcpyAsync(c->vr, xv, nb, cudaMemcpyHostToDevice, c->st));
+      TRY(op(c, c->vr, c->vy));
+      CU(cudaMemcpyAsync(yv, c->vy, nb, cudaMemcpyDeviceToHost, c->st));
+    } else {
+      TRY(op(c, xv, yv));
+    }
+  }
+  CU(cudaStreamSynchronize(c->st));
+  if (c->prof.on) c->prof.resolve();
+  return SFAIRSC_OK;
+}
+
+static sfairsc_status project_dev(sfairsc_ctx* c, const double* x, double* y) {
+  ProfScope ps(c, K_PROJ);
+  gsum_all(c, x, c->bs_w);
+  launch_project(c->g(), c->pd(), x, c->bs_w, 1.0, y, c->st);
+  CHECK_LAUNCH();
+  return SFAIRSC_OK;
+}
+
+static sfairsc_status lap_dev(sfairsc_ctx* c, const double* x, double* y) {
+  ProfScope ps(c, K_SPMV);
+  launch_spmv(c->g(), c->vs, c->row_split, c->spmv_grid, x, y, c->partials, c->counters + 1, c->bs_t, c->st);
+  CHECK_LAUNCH();
+  return SFAIRSC_OK;
+}
+
+extern "C" sfairsc_status sfairsc_apply(sfairsc_ctx* c, const double* x, double* y, int32_t nvec, int32_t memspace) {
+  return vec_io(c, x, y, nvec, memspace, apply_dev);
+}
+extern "C" sfairsc_status sfairsc_project(sfairsc_ctx* c, const double* x, double* y, int32_t nvec,
+                                          int32_t memspace) {
+  return vec_io(c, x, y, nvec, memspace, project_dev);
+}
+extern "C" sfairsc_status sfairsc_laplacian(sfairsc_ctx* c, const double* x, double* y, int32_t memspace) {
+  if (c && x == y) return fail(SFAIRSC_E_INVALID_ARG, "x and y must not alias");
+  return vec_io(c, x, y, 1, memspace, lap_dev);
+}
+
+// --------------------------------------------------------------------------
+// profiling
+// --------------------------------------------------------------------------
+extern "C" sfairsc_status sfairsc_profile_enable(sfairsc_ctx* c, int32_t enable) {
+  if (!c) return fail(SFAIRSC_E_INVALID_ARG, "null ctx");
+  CU(cudaStreamSynchronize(c->st));
+  c->prof.resolve();
+  c->prof.on = enable != 0;
+  return SFAIRSC_OK;
+}
+extern "C" sfairsc_status sfairsc_profile_read(sfairsc_ctx* c, int32_t kind, double* total_ms, int64_t* launches) {
+  if (!c || kind < 0 || kind >= 10) return fail(SFAIRSC_E_INVALID_ARG, "bad argument");
+  CU(cudaStreamSynchronize(c->st));
+  c->prof.resolve();
+  if (total_ms) *total_ms = c->prof.total_ms[kind];
+  if (launches) *launches = c->prof.launches[kind];
+  return SFAIRSC_OK;
+}
+extern "C" sfairsc_status sfairsc_profile_reset(sfairsc_ctx* c) {
+  if (!c) return fail(SFAIRSC_E_INVALID_ARG, "null ctx");
+  CU(cudaStreamSynchronize(c->st));
+  c->prof.resolve();
+  for (int i = 0; i < 10; ++i) {
+    c->prof.total_ms[i] = 0;
+    c->prof.launches[i] = 0;
+  }
+  return SFAIRSC_OK;
+}
+
+// --------------------------------------------------------------------------
+// thick-restart Lanczos (A7-A11)
+// --------------------------------------------------------------------------
+struct Lanczos {
+  sfairsc_ctx* c;
+  int m, keep, k;
+  int pk = 0;  // number of locked Ritz vectors heading the basis (arrow part of T)
+  std::vector<double> alpha, beta, arrow;
+  int64_t applies = 0, steps = 0, restarts = 0, breakdowns = 0;
+  unsigned inject = 0;
+
+  double* col(int j) const { return c->V + (long long)j * c->ldv; }
+
+  SweepArgs sargs(int J, const double* xin, double* xout, const double* coef) const {
+    SweepArgs a{};
+    a.V = c->V;
+    a.ld = c->ldv;
+    a.J = J;
+    a.xin = xin;
+    a.xout = xout;
+    a.coef = coef;
+    a.bsum_t = c->bs_t;
+    a.bsum_w = c->bs_v;
+    a.sigma = c->sigma;
+    a.partials = c->partials;
+    a.counter = c->counters + 2;
+    a.norm_bsum = c->nb;
+    return a;
+  }
+
+  // CGS2 of vr against V[:, 0:J] (dots already in c1 when pre_dots) then
+  // |r''|^2 and B^T r'' into nb.  mode0=true: r = finish(t) fused with dots.
+  sfairsc_status cgs2(int J, bool from_t) {
+    GraphDev g = c->g();
+    ProjDesc pd = c->pd();
+    if (J > 0) {
+      {
+        ProfScope ps(c, K_DOTS);
+        launch_sweep(from_t ? 0 : 3, g, pd, sargs(J, from_t ? c->vt : c->vr, c->vr, nullptr), c->sgrid, c->st);
+        launch_reduce_cols(c->partials, c->sgrid, J, c->c1, c->st);
+      }
+      {
+        ProfScope ps(c, K_UPDDOT);
+        launch_sweep(1, g, pd, sargs(J, c->vr, c->vr, c->c1), c->sgrid, c->st);
+        launch_reduce_cols(c->partials, c->sgrid, J, c->c2, c->st);
+      }
+    } else if (from_t) {
+      ProfScope ps(c, K_DOTS);
+      launch_finish(g, pd, c->vt, c->bs_t, c->bs_v, c->sigma, c->vr, c->st);
+    }
+    {
+      ProfScope ps(c, K_UPDNORM);
+      launch_sweep(2, g, pd, sargs(J, c->vr, c->vr, c->c2), c->sgrid, c->st);
+    }
+    if (c->h > kHB) extra_gsums(c, c->vr, c->nb + 1);
+    CHECK_LAUNCH();
+    return SFAIRSC_OK;
+  }
+
+  sfairsc_status normalize_into(int j, double b) {
+    ProfScope ps(c, K_NORMALIZE);
+    launch_normalize(c->g(), c->pd(), c->vr, b, c->nb + 1, col(j), c->bs_v, c->vp, c->st);
+    CHECK_LAUNCH();
+    return SFAIRSC_OK;
+  }
+
+  // fetch nb[0] (and optionally c1[j], c2[j]) to the host
+  sfairsc_status fetch(int j, double* nrm2, double* a) {
+    CU(cudaMemcpyAsync(c->hp, c->nb, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    if (a) {
+      CU(cudaMemcpyAsync(c->hp + 1, c->c1 + j, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CU(cudaMemcpyAsync(c->hp + 2, c->c2 + j, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    }
+    CU(cudaStreamSynchronize(c->st));
+    if (c->prof.on) c->prof.resolve();
+    *nrm2 = c->hp[0];
+    if (a) *a = c->hp[1] + c->hp[2];
+    return SFAIRSC_OK;
+  }
+
+  // random vector orthogonalised against V[:, 0:J], normalised into column J
+  sfairsc_status random_vector(int J, bool project_first, double* beta_out) {
+    for (int attempt = 0; attempt < 5; ++attempt) {
+      if (project_first) {  // r = P u
+        launch_random(c->vt, c->n, c->seed, inject++, 7u, c->st);
+        gsum_all(c, c->vt, c->bs_w);
+        launch_project(c->g(), c->pd(), c->vt, c->bs_w, 1.0, c->vr, c->st);
+      } else {
+        launch_random(c->vr, c->n, c->seed, inject++, 7u, c->st);
+      }
+      TRY(cgs2(J, false));
+      if (J > 0) {  // second full CGS2 pass for a fresh vector (twice is enough)
+        TRY(cgs2(J, false));
+      }
+      double nrm2;
+      TRY(fetch(0, &nrm2, nullptr));
+      const double b = std::sqrt(nrm2);
+      if (b > 1e-8) {
+        TRY(normalize_into(J, b));
+        *beta_out = b;
+        return SFAIRSC_OK;
+      }
+    }
+    return fail(SFAIRSC_E_NO_CONVERGENCE, "could not generate a random vector outside the Krylov basis");
+  }
+};
+
+extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, double* evals_out, double* evecs_out,
+                                       int32_t evecs_memspace, sfairsc_stats* stats) {
+  const double t0 = now_s();
+  if (!c || !evals_out) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
+  if (k < 1 || k > c->k_build) return fail(SFAIRSC_E_K_TOO_LARGE, "k=%d must be in [1, build k=%d]", k, c->k_build);
+  if ((int64_t)k > (int64_t)c->n - c->h + 1) return fail(SFAIRSC_E_K_TOO_LARGE, "k > n-h+1");
+  if (!(tol > 0)) return fail(SFAIRSC_E_INVALID_ARG, "tol must be > 0");
+  if (evecs_out && evecs_memspace != SFAIRSC_MEM_HOST && evecs_memspace != SFAIRSC_MEM_DEVICE)
+    return fail(SFAIRSC_E_INVALID_ARG, "memspace");
+  c->have_eigs = false;
+  Lanczos L;
+  L.c = c;
+  L.m = c->m;
+  L.k = k;
+  L.keep = std::max(std::min(c->keep, L.m - 1), std::min(k, L.m - 1));
+  L.alpha.assign(L.m + 1, 0.0);
+  L.beta.assign(L.m + 1, 0.0);
+  L.arrow.assign(L.m + 1, 0.0);
+  const double tol_eff = std::min(tol, c->tol_cap);
+  const double target = tol_eff * c->sigma;
+  const double bd_tol = std::min(1e-12, 0.01 * tol_eff) * c->sigma;
+  const int n = c->n;
+
+  // start vector v_0 = P r / |P r|, r from Philox stream 7
+  double b0;
+  L.inject = 0;
+  TRY(L.random_vector(0, true, &b0));
+  int j = 0;
+  bool converged = false, complete = false;
+  std::vector<double> theta, Y;
+  int m_eff = 0;
+  double gap = std::numeric_limits<double>::quiet_NaN();
+  double last_maxres = 0.0;
+  for (;;) {
+    // ---- expand column j: r = L^sigma v_j, CGS2 against V[:, 0:j+1] ----
+    {
+      ProfScope ps(c, K_SPMV);
+      launch_spmv(c->g(), c->vs, c->row_split, c->spmv_grid, c->vp, c->vt, c->partials, c->counters + 1, c->bs_t,
+                  c->st);
+    }
+    if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
+    TRY(L.cgs2(j + 1, true));
+    double nrm2, a;
+    TRY(L.fetch(j, &nrm2, &a));
+    L.applies++;
+    L.steps++;
+    L.alpha[j] = a;
+    double b = std::sqrt(nrm2);
+    if (b <= bd_tol) {
+      L.breakdowns++;
+      L.beta[j] = 0.0;
+      if (j + 1 >= n) {
+        complete = true;
+        m_eff = j + 1;
+      } else {
+        double bb;
+        TRY(L.random_vector(j + 1, false, &bb));
+      }
+    } else {
+      L.beta[j] = b;
+      TRY(L.normalize_into(j + 1, b));
+    }
+    ++j;
+    if (!complete && j < L.m) continue;
+    if (!complete) m_eff = L.m;
+
+    // ---- Rayleigh-Ritz on T (m_eff x m_eff): arrowhead + tridiagonal ----
+    const int me = m_eff;
+    std::vector<double> T((size_t)me * me, 0.0);
+    for (int i = 0; i < me; ++i) T[(size_t)i * me + i] = L.alpha[i];
+    for (int i = 0; i < L.pk && i < me; ++i) {
+      if (L.pk < me) {
+        T[(size_t)i * me + L.pk] = L.arrow[i];
+        T[(size_t)L.pk * me + i] = L.arrow[i];
+      }
+    }
+    for (int i = L.pk; i + 1 < me; ++i) {
+      T[(size_t)i * me + i + 1] = L.beta[i];
+      T[(size_t)(i + 1) * me + i] = L.beta[i];
+    }
+    Y = T;
+    symeig(me, Y, theta);
+    const double bm = complete ? 0.0 : L.beta[me - 1];
+    double maxres = 0.0;
+    for (int i = 0; i < k; ++i) maxres = std::max(maxres, std::fabs(bm * Y[(size_t)(me - 1) * me + i]));
+    last_maxres = maxres;
+    if (k < me) gap = theta[k] - theta[k - 1];
+    converged = complete || maxres <= target;
+    if (converged || L.restarts >= c->max_restarts) {
+      // X = V[:, 0:me] Y[:, 0:k]
+      std::vector<double> Yc((size_t)me * k);
+      for (int cc = 0; cc < k; ++cc)
+        for (int l = 0; l < me; ++l) Yc[(size_t)cc * me + l] = Y[(size_t)l * me + cc];
+      CU(cudaMemcpyAsync(c->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, c->st));
+      {
+        ProfScope ps(c, K_RITZ);
+        launch_ritz(c->V, c->ldv, n, me, c->Ydev, k, c->X, c->st);
+      }
+      CHECK_LAUNCH();
+      break;
+    }
+    // ---- thick restart: keep the `keep` smallest Ritz pairs ----
+    const int pk = std::min(L.keep, me - 1);
+    std::vector<double> Yc((size_t)me * pk);
+    for (int cc = 0; cc < pk; ++cc)
+      for (int l = 0; l < me; ++l) Yc[(size_t)cc * me + l] = Y[(size_t)l * me + cc];
+    CU(cudaMemcpyAsync(c->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, c->st));
+    {
+      ProfScope ps(c, K_RITZ);
+      launch_ritz(c->V, c->ldv, n, me, c->Ydev, pk, c->Vb, c->st);
+    }
+    CU(cudaMemcpyAsync(c->Vb + (long long)pk * c->ldv, c->V + (long long)me * c->ldv, sizeof(double) * c->ldv,
+                       cudaMemcpyDeviceToDevice, c->st));
+    CHECK_LAUNCH();
+    std::swap(c->V, c->Vb);
+    for (int i = 0; i < pk; ++i) {
+      L.alpha[i] = theta[i];
+      L.arrow[i] = bm * Y[(size_t)(me - 1) * me + i];
+    }
+    L.pk = pk;
+    j = pk;
+    L.restarts++;
+  }
+
+  // ---- A11: true residuals with k fresh applies ----
+  double max_resid = 0.0;
+  {
+    std::vector<double> res(k);
+    for (int i = 0; i < k; ++i) {
+      const double* xi = c->X + (long long)i * c->ldv;
+      TRY(apply_dev(c, xi, c->vy));
+      launch_resid(c->vy, xi, theta[i], n, c->partials, c->counters + 4, c->scal + 8 + i % 64, c->st);
+      CHECK_LAUNCH();
+      if (i % 64 == 63 || i == k - 1) {
+        const int base = i - i % 64;
+        CU(cudaMemcpyAsync(c->hp, c->scal + 8, sizeof(double) * (i - base + 1), cudaMemcpyDeviceToHost, c->st));
+        CU(cudaStreamSynchronize(c->st));
+        for (int q = base; q <= i; ++q) res[q] = std::sqrt(c->hp[q - base]) / c->sigma;
+      }
+    }
+    L.applies += k;
+    for (int i = 0; i < k; ++i) max_resid = std::max(max_resid, res[i]);
+  }
+  if (c->prof.on) c->prof.resolve();
+  c->evals.assign(theta.begin(), theta.begin() + k);
+  c->k_eigs = k;
+  c->have_eigs = true;
+  for (int i = 0; i < k; ++i) evals_out[i] = theta[i];
+  if (evecs_out) {
+    const cudaMemcpyKind kind = evecs_memspace == SFAIRSC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CU(cudaMemcpy2DAsync(evecs_out, sizeof(double) * n, c->X, sizeof(double) * c->ldv, sizeof(double) * n, k, kind,
+                         c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
+  sfairsc_stats S{};
+  S.applies = L.applies;
+  S.steps = L.steps;
+  S.restarts = L.restarts;
+  S.breakdowns = L.breakdowns;
+  S.sigma = c->sigma;
+  S.max_resid_rel = max_resid;
+  S.gap_est = gap;
+  S.t_build_s = c->t_build;
+  S.t_eigs_s = now_s() - t0;
+  S.converged = converged ? 1 : 0;
+  S.basis_size = L.m;
+  S.kept = L.keep;
+  c->last = S;
+  if (stats) *stats = S;
+  (void)last_maxres;
+  if (!converged) return fail(SFAIRSC_E_NO_CONVERGENCE, "no convergence after %lld restarts", (long long)L.restarts);
+  if (theta[k - 1] >= c->sigma * (1.0 - 1e-8))
+    return fail(SFAIRSC_E_SHIFT_TOO_SMALL, "lambda_k=%g >= sigma(1-1e-8)=%g (Prop. 3.4)", theta[k - 1], c->sigma);
+  return SFAIRSC_OK;
+}
+
+extern "C" sfairsc_status sfairsc_embed_kmeans(sfairsc_ctx* c, uint64_t seed, int32_t* labels_out, int32_t memspace,
+                                               double* objective_out) {
+  if (!c || !labels_out) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
+  if (!c->have_eigs) return fail(SFAIRSC_E_STATE, "sfairsc_eigs must succeed before sfairsc_embed_kmeans");
+  if (memspace != SFAIRSC_MEM_HOST && memspace != SFAIRSC_MEM_DEVICE) return fail(SFAIRSC_E_INVALID_ARG, "memspace");
+  return kmeans_run(c, seed, labels_out, memspace, objective_out);
+}
+
+// host utility exported for tests of the Rayleigh-Ritz step
+extern "C" int sfairsc_host_symeig(int32_t m, const double* A, double* evals, double* evecs) {
+  if (m < 0 || (m > 0 && (!A || !evals))) return 1;
+  std::vector<double> M(A, A + (size_t)m * m), ev;
+  symeig(m, M, ev);
+  for (int i = 0; i < m; ++i) evals[i] = ev[i];
+  if (evecs)
+    for (size_t i = 0; i < (size_t)m * m; ++i) evecs[i] = M[i];
+  return 0;
+}

@@ -1,0 +1,668 @@
+// libsfairsc — sm_100a fp64 kernels for the s-FairSC hot path.
+//
+// The path:
+//   apply  y = L^sigma w = P(L(P w)) - sigma P w + sigma w
+//     gsum      b_w = B^T w                                       (A4, factored Q)
+//     project   p   = w - s o gam(b_w)_g          = P w            (A4)
+//     spmv      t   = L p,  epilogue b_t = B^T t                   (A5)
+//     finish    y   = t - s o (gam(b_t) - sigma gam(b_w))_g        (A6, Eq. asigma)
+//   Lanczos step (A7-A9): sweep0 (finish + V^T y), sweep1 (update + V^T r'),
+//   sweep2 (update + |r''|^2 + B^T r''), normalize (v, p of the next apply);
+//   restart (A10): ritz  V Y.
+//
+// All reductions are two-stage with a fixed partition and fixed order (no
+// floating-point atomics), so results are bitwise reproducible per GPU.
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace sfz {
+
+// ----------------------------------------------------------------------------
+// helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// streaming (read-once) loads: bypass L1 allocation, read-only path
+__device__ __forceinline__ int ld_stream(const int* p) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// Block-wide fixed-order reduction of NV per-thread values; thread q < NV
+// writes the CTA partial to out[q].
+template <int NV>
+__device__ __forceinline__ void block_reduce_store(const double (&v)[NV], double* out) {
+  __shared__ double red[kThreads / 32][NV];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const double x = warp_sum(v[q]);
+    if (lane == 0) red[w][q] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double acc = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kThreads / 32; ++ww) acc += red[ww][threadIdx.x];
+    out[threadIdx.x] = acc;
+  }
+}
+
+// Last-CTA-done finalisation: the CTA that takes the last ticket sums the
+// grid's partial rows [gridDim.x][NV] in a fixed order and writes out[q]
+// for q < nout.  Resets the ticket for the next launch.
+template <int NV>
+__device__ __forceinline__ void ticket_finalize(const double* partials, unsigned* counter, double* out, int nout) {
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int q = w; q < nout; q += kThreads / 32) {
+    double acc = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(partials + (size_t)b * NV + q);
+    acc = warp_sum(acc);
+    if (lane == 0) out[q] = acc;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// gam[s] for the factored projector; executed by thread 0, result in smem.
+__device__ __forceinline__ void gamma_serial(const double* bsum, double scale, const ProjDesc& pd, double* gam) {
+  double pi = 0.0;
+  for (int s = 0; s < pd.h; ++s) {
+    const double c = scale * bsum[s] * pd.isb[s];
+    gam[s] = c;
+    pi = fma(pd.uh[s], c, pi);
+  }
+  for (int s = 0; s < pd.h; ++s) gam[s] = (gam[s] - pd.uh[s] * pi) * pd.isb[s];
+}
+
+__device__ __forceinline__ void add_group(double (&acc)[kHB], int g, double v) {
+#pragma unroll
+  for (int q = 0; q < kHB; ++q)
+    if (q == g) acc[q] += v;
+}
+
+// Philox4x32-10 (Salmon et al. SC'11), device implementation.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+  const unsigned M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k.x += W0;
+      k.y += W1;
+    }
+    const unsigned hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    const unsigned hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+__device__ __forceinline__ double philox_uniform(uint64_t seed, unsigned c0, unsigned c1, unsigned c2, unsigned c3) {
+  const uint4 x = philox4x32_10(make_uint4(c0, c1, c2, c3), make_uint2((unsigned)seed, (unsigned)(seed >> 32)));
+  return ((double)(x.x >> 5) * 67108864.0 + (double)(x.y >> 6)) / 9007199254740992.0;
+}
+
+static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ----------------------------------------------------------------------------
+// build-time kernels (A0-A3)
+// ----------------------------------------------------------------------------
+enum { F_CSR = 1, F_NEG = 2, F_ASYM = 4, F_ISO = 8, F_GRP = 16 };
+
+__global__ void k_validate(GraphDev g, int check_sym, int* flags) {
+  const int n = g.n;
+  int f = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (g.rp[0] != 0 || g.rp[n] != g.nnz) f |= F_CSR;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int a = g.rp[i], b = g.rp[i + 1];
+    if (b < a || a < 0 || b > g.nnz) {
+      f |= F_CSR;
+      continue;
+    }
+    int prev = -1;
+    for (int e = a; e < b; ++e) {
+      const int j = g.ci[e];
+      const double w = g.vv[e];
+      if (j < 0 || j >= n || j <= prev) f |= F_CSR;
+      prev = j;
+      if (!(w >= 0.0)) f |= F_NEG;  // also NaN
+      if (j == i && w != 0.0) f |= F_CSR;
+      if (check_sym && j >= 0 && j < n && j != i) {
+        int lo = g.rp[j], hi = g.rp[j + 1] - 1, found = -1;
+        while (lo <= hi) {
+          const int mid = (lo + hi) >> 1;
+          const int cm = g.ci[mid];
+          if (cm == i) {
+            found = mid;
+            break;
+          }
+          if (cm < i) lo = mid + 1; else hi = mid - 1;
+        }
+        if (found < 0 || g.vv[found] != w) f |= F_ASYM;
+      }
+    }
+  }
+  if (f) atomicOr(flags, f);
+}
+
+__global__ void k_degrees(GraphDev g, double* d, int* flags) {
+  int f = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int e = g.rp[i]; e < g.rp[i + 1]; ++e) acc += g.vv[e];
+    d[i] = acc;
+    if (!(acc > 0.0)) f |= F_ISO;
+  }
+  if (f) atomicOr(flags, f);
+}
+
+__global__ void k_inv_sqrt(const double* d, double* s, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) s[i] = 1.0 / sqrt(d[i]);
+}
+
+__global__ void k_scale_values(const int* rp, const int* ci, double* vv, const double* s, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double si = s[i];
+    for (int e = rp[i]; e < rp[i + 1]; ++e) vv[e] = si * vv[e] * s[ci[e]];
+  }
+}
+
+// sigma = ||L||_1 = max_j sum_i |L_ij|.  By symmetry column j = row j:
+// normalized  1 + sum_i s_j w_ji s_i ; unnormalized  2 d_j.
+__global__ void k_sigma(GraphDev g, double* partials, unsigned* counter, double* out) {
+  double mx = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    double v;
+    if (g.normalized) {
+      double acc = 0.0;
+      for (int e = g.rp[i]; e < g.rp[i + 1]; ++e) acc += g.vv[e];
+      v = 1.0 + acc;
+    } else {
+      v = 2.0 * g.dg[i];
+    }
+    mx = fmax(mx, v);
+  }
+  __shared__ double red[kThreads];
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    double m = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) m = fmax(m, __ldcg(partials + b));
+    *out = m;
+    *counter = 0u;
+  }
+}
+
+__global__ void k_group_check(const int32_t* groups, int n, int h, uint8_t* grp, int* flags) {
+  int f = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v = groups[i];
+    if (v < 0 || v >= h) f |= F_GRP;
+    grp[i] = (uint8_t)v;
+  }
+  if (f) atomicOr(flags, f);
+}
+
+// ----------------------------------------------------------------------------
+// factored-projector kernels (A4, A6)
+// ----------------------------------------------------------------------------
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) k_gsum(GraphDev g, const double* __restrict__ x, int g_base,
+                                                   double* partials, unsigned* counter, double* bsum, int nout) {
+  double acc[kHB];
+#pragma unroll
+  for (int q = 0; q < kHB; ++q) acc[q] = 0.0;
+  const int n = g.n;
+  const int i0 = (int)((long long)n * blockIdx.x / gridDim.x), i1 = (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
+  for (int i = i0 + threadIdx.x; i < i1; i += kThreads) {
+    const double v = NORM ? g.s[i] * x[i] : x[i];
+    add_group(acc, (int)g.grp[i] - g_base, v);
+  }
+  block_reduce_store<kHB>(acc, partials + (size_t)blockIdx.x * kHB);
+  ticket_finalize<kHB>(partials, counter, bsum + g_base, nout);
+}
+
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) k_project(GraphDev g, ProjDesc pd, const double* __restrict__ x,
+                                                      const double* bsum, double scale, double* __restrict__ p) {
+  __shared__ double gam[256];
+  if (threadIdx.x == 0) gamma_serial(bsum, scale, pd, gam);
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const double gi = gam[g.grp[i]];
+    p[i] = NORM ? fma(-g.s[i], gi, x[i]) : x[i] - gi;
+  }
+}
+
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) k_finish(GraphDev g, ProjDesc pd, const double* __restrict__ t,
+                                                     const double* bsum_t, const double* bsum_w, double sigma,
+                                                     double* __restrict__ y) {
+  __shared__ double gt[256], gw[256];
+  if (threadIdx.x == 0) {
+    gamma_serial(bsum_t, 1.0, pd, gt);
+    gamma_serial(bsum_w, 1.0, pd, gw);
+    for (int s = 0; s < pd.h; ++s) gt[s] = gt[s] - sigma * gw[s];
+  }
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const double gi = gt[g.grp[i]];
+    y[i] = NORM ? fma(-g.s[i], gi, t[i]) : t[i] - gi;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// SpMV t = L p with fused B^T t epilogue (A5).
+// CTA b owns rows [row_split[b], row_split[b+1]) (balanced by nnz + rows);
+// VS lanes per row, consecutive row groups -> contiguous col/val streams.
+// normalized: t_i = p_i - sum_j (s_i w_ij s_j) p_j ; unnormalized: d_i p_i - sum_j w_ij p_j
+// ----------------------------------------------------------------------------
+template <int VS, bool NORM>
+__global__ void __launch_bounds__(kThreads) k_spmv(GraphDev g, const int* __restrict__ row_split,
+                                                   const double* __restrict__ p, double* __restrict__ t,
+                                                   double* partials, unsigned* counter, double* bsum_t, int nout) {
+  constexpr int NG = kThreads / VS;
+  const int r0 = row_split[blockIdx.x], r1 = row_split[blockIdx.x + 1];
+  const int lane = threadIdx.x % VS, gid = threadIdx.x / VS;
+  const int* __restrict__ rp = g.rp;
+  const int* __restrict__ ci = g.ci;
+  const double* __restrict__ vv = g.vv;
+  double acc[kHB];
+#pragma unroll
+  for (int q = 0; q < kHB; ++q) acc[q] = 0.0;
+  for (int base = r0; base < r1; base += NG) {
+    const int row = base + gid;
+    const bool valid = row < r1;
+    double sum = 0.0;
+    if (valid) {
+      const int a = __ldg(rp + row), b = __ldg(rp + row + 1);
+      int e = a + lane;
+      for (; e + 3 * VS < b; e += 4 * VS) {
+        const int c0 = ld_stream(ci + e), c1 = ld_stream(ci + e + VS);
+        const int c2 = ld_stream(ci + e + 2 * VS), c3 = ld_stream(ci + e + 3 * VS);
+        const double w0 = ld_stream(vv + e), w1 = ld_stream(vv + e + VS);
+        const double w2 = ld_stream(vv + e + 2 * VS), w3 = ld_stream(vv + e + 3 * VS);
+        const double x0 = __ldg(p + c0), x1 = __ldg(p + c1), x2 = __ldg(p + c2), x3 = __ldg(p + c3);
+        sum = fma(w0, x0, sum);
+        sum = fma(w1, x1, sum);
+        sum = fma(w2, x2, sum);
+        sum = fma(w3, x3, sum);
+      }
+      for (; e < b; e += VS) sum = fma(ld_stream(vv + e), __ldg(p + ld_stream(ci + e)), sum);
+    }
+#pragma unroll
+    for (int o = VS / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (valid && lane == 0) {
+      const double pi = __ldg(p + row);
+      const double ti = (NORM ? pi : __ldg(g.dg + row) * pi) - sum;
+      t[row] = ti;
+      add_group(acc, g.grp[row], NORM ? g.s[row] * ti : ti);
+    }
+  }
+  block_reduce_store<kHB>(acc, partials + (size_t)blockIdx.x * kHB);
+  ticket_finalize<kHB>(partials, counter, bsum_t, nout);
+}
+
+// ----------------------------------------------------------------------------
+// Krylov sweeps (A7-A9)
+// ----------------------------------------------------------------------------
+template <int MODE, int MAXCW, bool NORM>
+__global__ void __launch_bounds__(kThreads) k_sweep(GraphDev g, ProjDesc pd, SweepArgs a) {
+  __shared__ double xs[kThreads];
+  __shared__ double coef[kMaxJ];
+  __shared__ double gam[256];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int n = g.n, J = a.J;
+  if (MODE == 1 || MODE == 2)
+    for (int l = tid; l < J; l += kThreads) coef[l] = a.coef[l];
+  if (MODE == 0 && tid == 0) {
+    __shared__ double gw[256];
+    gamma_serial(a.bsum_t, 1.0, pd, gam);
+    gamma_serial(a.bsum_w, 1.0, pd, gw);
+    for (int s = 0; s < pd.h; ++s) gam[s] = gam[s] - a.sigma * gw[s];
+  }
+  __syncthreads();
+  const int nchunks = (n + kThreads - 1) / kThreads;
+  const int c0 = (int)((long long)nchunks * blockIdx.x / gridDim.x);
+  const int c1 = (int)((long long)nchunks * (blockIdx.x + 1) / gridDim.x);
+  double colacc[MAXCW];
+#pragma unroll
+  for (int cc = 0; cc < MAXCW; ++cc) colacc[cc] = 0.0;
+  double gacc[kHB];
+#pragma unroll
+  for (int q = 0; q < kHB; ++q) gacc[q] = 0.0;
+  double nrm = 0.0;
+  const long long ld = a.ld;
+  for (int c = c0; c < c1; ++c) {
+    const int i = c * kThreads + tid;
+    double x = 0.0;
+    if (i < n) {
+      if (MODE == 0) {
+        x = NORM ? fma(-g.s[i], gam[g.grp[i]], a.xin[i]) : a.xin[i] - gam[g.grp[i]];
+        a.xout[i] = x;
+      } else if (MODE == 3) {
+        x = a.xin[i];
+      } else {
+        double acc = a.xin[i];
+        const double* __restrict__ vp = a.V + i;
+        int l = 0;
+        for (; l + 8 <= J; l += 8) {
+          double v0 = vp[(l + 0) * ld], v1 = vp[(l + 1) * ld], v2 = vp[(l + 2) * ld], v3 = vp[(l + 3) * ld];
+          double v4 = vp[(l + 4) * ld], v5 = vp[(l + 5) * ld], v6 = vp[(l + 6) * ld], v7 = vp[(l + 7) * ld];
+          acc = fma(-v0, coef[l + 0], acc);
+          acc = fma(-v1, coef[l + 1], acc);
+          acc = fma(-v2, coef[l + 2], acc);
+          acc = fma(-v3, coef[l + 3], acc);
+          acc = fma(-v4, coef[l + 4], acc);
+          acc = fma(-v5, coef[l + 5], acc);
+          acc = fma(-v6, coef[l + 6], acc);
+          acc = fma(-v7, coef[l + 7], acc);
+        }
+        for (; l < J; ++l) acc = fma(-vp[l * ld], coef[l], acc);
+        x = acc;
+        a.xout[i] = x;
+        if (MODE == 2) {
+          nrm = fma(x, x, nrm);
+          add_group(gacc, g.grp[i], NORM ? g.s[i] * x : x);
+        }
+      }
+    }
+    if (MODE != 2) {
+      xs[tid] = x;
+      __syncthreads();
+      const long long base = (long long)c * kThreads + lane;
+#pragma unroll
+      for (int cc = 0; cc < MAXCW; ++cc) {
+        const int l = w + cc * (kThreads / 32);
+        if (l < J) {
+          const double* __restrict__ vp = a.V + (long long)l * ld + base;
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < kThreads / 32; ++q) s = fma(vp[q * 32], xs[lane + 32 * q], s);
+          colacc[cc] += s;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (MODE != 2) {
+#pragma unroll
+    for (int cc = 0; cc < MAXCW; ++cc) {
+      const int l = w + cc * (kThreads / 32);
+      if (l < J) {
+        const double s = warp_sum(colacc[cc]);
+        if (lane == 0) a.partials[(size_t)blockIdx.x * J + l] = s;
+      }
+    }
+  } else {
+    double v[1 + kHB];
+    v[0] = nrm;
+#pragma unroll
+    for (int q = 0; q < kHB; ++q) v[1 + q] = gacc[q];
+    block_reduce_store<1 + kHB>(v, a.partials + (size_t)blockIdx.x * (1 + kHB));
+    ticket_finalize<1 + kHB>(a.partials, a.counter, a.norm_bsum, 1 + min(pd.h, kHB));
+  }
+}
+
+__global__ void k_reduce_cols(const double* __restrict__ partials, int G, int J, double* out) {
+  const int l = blockIdx.x;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < G; b += blockDim.x) acc += partials[(size_t)b * J + l];
+  __shared__ double red[32];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    out[l] = s;
+  }
+}
+
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) k_normalize(GraphDev g, ProjDesc pd, const double* __restrict__ r,
+                                                        double beta, const double* bsum_r, double* __restrict__ v,
+                                                        double* bsum_v, double* __restrict__ p) {
+  __shared__ double gam[256];
+  const double inv = 1.0 / beta;
+  if (threadIdx.x == 0) gamma_serial(bsum_r, inv, pd, gam);
+  if (blockIdx.x == 0)
+    for (int s = threadIdx.x; s < pd.h; s += blockDim.x) bsum_v[s] = bsum_r[s] * inv;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const double vi = r[i] / beta;
+    v[i] = vi;
+    const double gi = gam[g.grp[i]];
+    p[i] = NORM ? fma(-g.s[i], gi, vi) : vi - gi;
+  }
+}
+
+__global__ void k_random(double* x, int n, uint64_t seed, unsigned c1, unsigned stream) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = philox_uniform(seed, (unsigned)i, c1, stream, 0u) - 0.5;
+}
+
+// Ritz vectors Vout[:, c] = sum_{l<m} V[:, l] Y[l, c]  (A10).  64 rows x 4 column
+// groups per CTA; Y (m x p) staged in shared memory, row-major.
+template <int PC>
+__global__ void __launch_bounds__(kThreads) k_ritz(const double* __restrict__ V, long long ld, int n, int m,
+                                                   const double* __restrict__ Y, int p, double* __restrict__ Vout) {
+  extern __shared__ double Ys[];  // [m][p]
+  for (int e = threadIdx.x; e < m * p; e += kThreads) {
+    const int l = e / p, c = e % p;
+    Ys[e] = Y[(size_t)c * m + l];
+  }
+  __syncthreads();
+  const int r = threadIdx.x & 63, cg = threadIdx.x >> 6;
+  for (int chunk = blockIdx.x; chunk * 64 < n; chunk += gridDim.x) {
+    const int i = chunk * 64 + r;
+    if (i >= n) continue;
+    double acc[PC];
+#pragma unroll
+    for (int cc = 0; cc < PC; ++cc) acc[cc] = 0.0;
+    for (int l = 0; l < m; ++l) {
+      const double v = V[(long long)l * ld + i];
+      const double* yr = Ys + l * p + cg;
+#pragma unroll
+      for (int cc = 0; cc < PC; ++cc)
+        if (cg + 4 * cc < p) acc[cc] = fma(v, yr[4 * cc], acc[cc]);
+    }
+#pragma unroll
+    for (int cc = 0; cc < PC; ++cc)
+      if (cg + 4 * cc < p) Vout[(long long)(cg + 4 * cc) * ld + i] = acc[cc];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_resid(const double* __restrict__ y, const double* __restrict__ x,
+                                                    double theta, int n, double* partials, unsigned* counter,
+                                                    double* out) {
+  double v[1] = {0.0};
+  const int i0 = (int)((long long)n * blockIdx.x / gridDim.x), i1 = (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
+  for (int i = i0 + threadIdx.x; i < i1; i += kThreads) {
+    const double r = fma(-theta, x[i], y[i]);
+    v[0] = fma(r, r, v[0]);
+  }
+  block_reduce_store<1>(v, partials + blockIdx.x);
+  ticket_finalize<1>(partials, counter, out, 1);
+}
+
+// ----------------------------------------------------------------------------
+// launch wrappers
+// ----------------------------------------------------------------------------
+static int num_sms_cached() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+static int stream_grid(int n) { return std::max(1, std::min(cdiv(n, kThreads), num_sms_cached() * 8)); }
+static int reduce_grid(int n) { return std::max(1, std::min(cdiv(n, 4 * kThreads), num_sms_cached() * 2)); }
+
+void launch_validate_csr(const GraphDev& g, int check_sym, int* flags, cudaStream_t st) {
+  k_validate<<<stream_grid(g.n), kThreads, 0, st>>>(g, check_sym, flags);
+}
+void launch_degrees(const GraphDev& g, double* d, int* flags, cudaStream_t st) {
+  k_degrees<<<stream_grid(g.n), kThreads, 0, st>>>(g, d, flags);
+}
+void launch_inv_sqrt(const double* d, double* s, int n, cudaStream_t st) {
+  k_inv_sqrt<<<stream_grid(n), kThreads, 0, st>>>(d, s, n);
+}
+void launch_scale_values(const int* rp, const int* ci, double* vv, const double* s, int n, cudaStream_t st) {
+  k_scale_values<<<stream_grid(n), kThreads, 0, st>>>(rp, ci, vv, s, n);
+}
+void launch_sigma(const GraphDev& g, double* partials, unsigned* counter, double* out, cudaStream_t st) {
+  k_sigma<<<reduce_grid(g.n), kThreads, 0, st>>>(g, partials, counter, out);
+}
+void launch_group_check(const int32_t* groups, int n, int h, uint8_t* grp, int* flags, cudaStream_t st) {
+  k_group_check<<<stream_grid(n), kThreads, 0, st>>>(groups, n, h, grp, flags);
+}
+
+void launch_gsum(const GraphDev& g, const double* x, int g_base, double* partials, unsigned* counter, double* bsum,
+                 cudaStream_t st) {
+  // bsum points at the h-array base; groups [g_base, g_base+16) are written
+  const int G = reduce_grid(g.n);
+  const int nout = kHB;  // caller guarantees room for kHB entries past g_base
+  if (g.normalized)
+    k_gsum<true><<<G, kThreads, 0, st>>>(g, x, g_base, partials, counter, bsum, nout);
+  else
+    k_gsum<false><<<G, kThreads, 0, st>>>(g, x, g_base, partials, counter, bsum, nout);
+}
+void launch_project(const GraphDev& g, const ProjDesc& pd, const double* x, const double* bsum, double scale,
+                    double* p, cudaStream_t st) {
+  if (g.normalized)
+    k_project<true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, x, bsum, scale, p);
+  else
+    k_project<false><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, x, bsum, scale, p);
+}
+
+void launch_finish(const GraphDev& g, const ProjDesc& pd, const double* t, const double* bsum_t,
+                   const double* bsum_w, double sigma, double* y, cudaStream_t st) {
+  if (g.normalized)
+    k_finish<true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_w, sigma, y);
+  else
+    k_finish<false><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_w, sigma, y);
+}
+
+template <int VS>
+static void spmv_vs(const GraphDev& g, const int* row_split, int grid, const double* p, double* t, double* partials,
+                    unsigned* counter, double* bsum_t, cudaStream_t st) {
+  if (g.normalized)
+    k_spmv<VS, true><<<grid, kThreads, 0, st>>>(g, row_split, p, t, partials, counter, bsum_t, kHB);
+  else
+    k_spmv<VS, false><<<grid, kThreads, 0, st>>>(g, row_split, p, t, partials, counter, bsum_t, kHB);
+}
+void launch_spmv(const GraphDev& g, int vs, const int* row_split, int grid, const double* p, double* t,
+                 double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
+  switch (vs) {
+    case 2: spmv_vs<2>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
+    case 4: spmv_vs<4>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
+    case 8: spmv_vs<8>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
+    case 16: spmv_vs<16>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
+    default: spmv_vs<32>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
+  }
+}
+
+int sweep_grid(int n, int num_sms) { return std::max(1, std::min(cdiv(n, kThreads), num_sms * 4)); }
+
+template <int MODE, bool NORM>
+static void sweep_m(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  if (a.J <= 64)
+    k_sweep<MODE, 8, NORM><<<grid, kThreads, 0, st>>>(g, pd, a);
+  else if (a.J <= 128)
+    k_sweep<MODE, 16, NORM><<<grid, kThreads, 0, st>>>(g, pd, a);
+  else if (a.J <= 256)
+    k_sweep<MODE, 32, NORM><<<grid, kThreads, 0, st>>>(g, pd, a);
+  else
+    k_sweep<MODE, 64, NORM><<<grid, kThreads, 0, st>>>(g, pd, a);
+}
+template <int MODE>
+static void sweep_n(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  if (g.normalized) sweep_m<MODE, true>(g, pd, a, grid, st);
+  else sweep_m<MODE, false>(g, pd, a, grid, st);
+}
+void launch_sweep(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  switch (mode) {
+    case 0: sweep_n<0>(g, pd, a, grid, st); break;
+    case 1: sweep_n<1>(g, pd, a, grid, st); break;
+    case 2: sweep_n<2>(g, pd, a, grid, st); break;
+    default: sweep_n<3>(g, pd, a, grid, st); break;
+  }
+}
+void launch_reduce_cols(const double* partials, int G, int J, double* out, cudaStream_t st) {
+  if (J <= 0) return;
+  k_reduce_cols<<<J, 128, 0, st>>>(partials, G, J, out);
+}
+void launch_normalize(const GraphDev& g, const ProjDesc& pd, const double* r, double beta, const double* bsum_r,
+                      double* vout, double* bsum_v, double* p, cudaStream_t st) {
+  if (g.normalized)
+    k_normalize<true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, r, beta, bsum_r, vout, bsum_v, p);
+  else
+    k_normalize<false><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, r, beta, bsum_r, vout, bsum_v, p);
+}
+void launch_random(double* x, int n, uint64_t seed, unsigned c1, unsigned stream, cudaStream_t st) {
+  k_random<<<stream_grid(n), kThreads, 0, st>>>(x, n, seed, c1, stream);
+}
+
+template <int PC>
+static void ritz_pc(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout, cudaStream_t st) {
+  const size_t smem = (size_t)m * p * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_ritz<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  const int grid = std::max(1, std::min(cdiv(n, 64), num_sms_cached() * 2));
+  k_ritz<PC><<<grid, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
+}
+void launch_ritz(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout, cudaStream_t st) {
+  // column tiles so that the Y tile fits the shared-memory budget
+  const int max_cols = std::max(1, std::min(4 * 32, (int)((96 * 1024) / (sizeof(double) * std::max(m, 1)))));
+  for (int c0 = 0; c0 < p; c0 += max_cols) {
+    const int pc = std::min(max_cols, p - c0);
+    const double* Yt = Y + (size_t)c0 * m;
+    double* Vo = Vout + (long long)c0 * ld;
+    if (pc <= 32) ritz_pc<8>(V, ld, n, m, Yt, pc, Vo, st);
+    else if (pc <= 64) ritz_pc<16>(V, ld, n, m, Yt, pc, Vo, st);
+    else ritz_pc<32>(V, ld, n, m, Yt, pc, Vo, st);
+  }
+}
+void launch_resid(const double* y, const double* x, double theta, int n, double* partials, unsigned* counter,
+                  double* out, cudaStream_t st) {
+  k_resid<<<reduce_grid(n), kThreads, 0, st>>>(y, x, theta, n, partials, counter, out);
+}
+
+}  // namespace sfz

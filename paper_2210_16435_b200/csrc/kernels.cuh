@@ -1,0 +1,112 @@
+// Internal kernel launch interface of libsfairsc (not part of the C ABI).
+// All launches are asynchronous on `st`; callers check errors.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sfz {
+
+constexpr int kThreads = 256;  // CTA size of every streaming kernel
+constexpr int kHB = 16;        // group sums fused per kernel (h > 16: extra gsum passes)
+constexpr int kMaxJ = 512;     // max Krylov basis columns handled by the sweep kernels
+
+// Factored projector coefficients (DESIGN.md §Factored projector).
+//   b_s   = sum_{i in V_s} s_i x_i          (B^T x, B = [s o g_1 ... s o g_h])
+//   c_s   = scale * b_s * isb_s              (isb_s = beta_s^{-1/2}, beta_s = sum_{i in V_s} s_i^2)
+//   pi    = sum_s uh_s c_s                   (uh = u/|u|, u_s = |V_s| isb_s)
+//   gam_s = (c_s - uh_s pi) * isb_s          so that  Q Q^T x = s o gam_{g(i)}
+struct ProjDesc {
+  int h;
+  const double* isb;  // device, h
+  const double* uh;   // device, h
+};
+
+struct GraphDev {
+  int n;
+  int nnz;
+  const int* rp;
+  const int* ci;
+  const double* vv;   // normalized: s_i w_ij s_j ; unnormalized: w_ij
+  const double* dg;   // degrees d (unnormalized diagonal of L)
+  const double* s;    // d^{-1/2} (normalized only; nullptr otherwise)
+  const uint8_t* grp;
+  bool normalized;
+};
+
+// ---- build-time kernels -----------------------------------------------------
+void launch_validate_csr(const GraphDev& g, int check_sym, int* flags, cudaStream_t st);
+void launch_degrees(const GraphDev& g, double* d, int* flags, cudaStream_t st);
+void launch_scale_values(const int* rp, const int* ci, double* vv, const double* s, int n, cudaStream_t st);
+void launch_inv_sqrt(const double* d, double* s, int n, cudaStream_t st);
+// row sums of |L| columns -> max into *out (sigma = ||L||_1)
+void launch_sigma(const GraphDev& g, double* partials, unsigned* counter, double* out, cudaStream_t st);
+void launch_group_check(const int32_t* groups, int n, int h, uint8_t* grp, int* flags, cudaStream_t st);
+
+// ---- per-apply kernels --------------------------------------------------------
+// bsum[g_base .. g_base+16) = sum over V_s of (s_i) x_i
+void launch_gsum(const GraphDev& g, const double* x, int g_base, double* partials, unsigned* counter,
+                 double* bsum, cudaStream_t st);
+// p = x - s o gam(bsum, scale)_g
+void launch_project(const GraphDev& g, const ProjDesc& pd, const double* x, const double* bsum, double scale,
+                    double* p, cudaStream_t st);
+// t = L p ; bsum_t[0..16) = B^T t (fused epilogue)
+void launch_spmv(const GraphDev& g, int vs, const int* row_split, int grid, const double* p, double* t,
+                 double* partials, unsigned* counter, double* bsum_t, cudaStream_t st);
+// y = t - s o (gam_t - sigma gam_w)_g ;  optional dot w^T y -> *dot
+void launch_finish(const GraphDev& g, const ProjDesc& pd, const double* t, const double* bsum_t,
+                   const double* bsum_w, double sigma, double* y, cudaStream_t st);
+
+// ---- Krylov kernels -------------------------------------------------------------
+// mode 0: r = finish(t); partial dots V[:,0:J]^T r
+// mode 1: r' = r - V c ; partial dots V^T r'
+// mode 2: r'' = r - V c ; partial |r''|^2 and B^T r''  (ticket-reduced into norm_bsum[0..17))
+// mode 3: partial dots V^T x (x unchanged)
+struct SweepArgs {
+  const double* V;
+  long long ld;
+  int J;
+  const double* xin;   // mode 0: t ; else r
+  double* xout;        // r out (modes 0,1,2)
+  const double* coef;  // device coef (modes 1,2)
+  const double* bsum_t;
+  const double* bsum_w;
+  double sigma;
+  double* partials;    // [grid][J] (modes 0,1,3) or [grid][17] (mode 2)
+  unsigned* counter;
+  double* norm_bsum;   // mode 2 output: [0] = |r''|^2, [1..17) = B^T r''
+};
+int sweep_grid(int n, int num_sms);
+void launch_sweep(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st);
+// out[l] = sum_b partials[b*J + l], fixed order
+void launch_reduce_cols(const double* partials, int G, int J, double* out, cudaStream_t st);
+// v = r / beta -> vout ; bsum_v = bsum_r / beta ; p = v - s o gam(bsum_v)
+void launch_normalize(const GraphDev& g, const ProjDesc& pd, const double* r, double beta, const double* bsum_r,
+                      double* vout, double* bsum_v, double* p, cudaStream_t st);
+// x_i = u_i - 1/2, u = Philox4x32-10(key=seed, ctr=(i, c1, stream, 0))
+void launch_random(double* x, int n, uint64_t seed, unsigned c1, unsigned stream, cudaStream_t st);
+// Vout[:, c] = sum_l V[:, l] Y[l, c]   (c < p, l < m), Y column-major m x p on device
+void launch_ritz(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout,
+                 cudaStream_t st);
+// out = |y - theta x|^2 (ticket reduced)
+void launch_resid(const double* y, const double* x, double theta, int n, double* partials, unsigned* counter,
+                  double* out, cudaStream_t st);
+
+// ---- k-means ----------------------------------------------------------------------
+void launch_build_rows(const double* X, long long ldx, int n, int k, const double* s, double* H, cudaStream_t st);
+void launch_d2_update(const double* H, int n, int k, const double* center, int first, double* D2, double* blocksum,
+                      int nblk, cudaStream_t st);
+void launch_pp_select(const double* D2, const double* blocksum, int nblk, int n, double u, int* chosen,
+                      cudaStream_t st);
+void launch_gather_center(const double* H, int k, const int* idx, double* center, cudaStream_t st);
+void launch_assign(const double* H, int n, int k, int K, const double* mu, int* labels, double* dist,
+                   int* changes, cudaStream_t st);
+void launch_centroid_partials(const double* H, int n, int k, int K, const int* labels, double* partials, int grid,
+                              cudaStream_t st);
+int centroid_grid(int n, int num_sms);
+void launch_centroid_finish(const double* partials, int grid, int k, int K, double* mu, double* counts,
+                            cudaStream_t st);
+void launch_argmax_excluding(const double* dist, const int* used_mask, int n, int* out, double* scratch,
+                             cudaStream_t st);
+void launch_sum(const double* x, int n, double* partials, unsigned* counter, double* out, cudaStream_t st);
+
+}  // namespace sfz

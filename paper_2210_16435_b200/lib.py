@@ -1,0 +1,294 @@
+"""Thin Python binding of libsfairsc (include/sfairsc.h) — argument marshalling only.
+
+Every step of the s-FairSC path runs in the CUDA library; this module only
+converts numpy arrays / torch tensors to pointers, calls the C ABI and raises
+`SfairscError` on a non-OK status.  There is no CPU fallback: if the shared
+library is missing or fails to load, importing this module raises.
+
+Names mirror the C ABI: sfairsc_build_operator, sfairsc_eigs,
+sfairsc_embed_kmeans, sfairsc_apply, sfairsc_project, sfairsc_laplacian, ...
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsfairsc.so")
+
+MEM_HOST = 0
+MEM_DEVICE = 1
+
+STATUS = {
+    0: "OK", 1: "E_INVALID_ARG", 2: "E_DIM_MISMATCH", 3: "E_CSR_INVALID", 4: "E_ASYMMETRIC",
+    5: "E_NEGATIVE_WEIGHT", 6: "E_ISOLATED_VERTEX", 7: "E_EMPTY_GROUP", 8: "E_RANK_DEFICIENT",
+    9: "E_K_TOO_LARGE", 10: "E_SHIFT_TOO_SMALL", 11: "E_NO_CONVERGENCE", 12: "E_STATE", 13: "E_OOM",
+    14: "E_CUDA", 15: "E_NCCL",
+}
+
+PROFILE_KINDS = {"spmv": 0, "dots": 1, "upd_dots": 2, "upd_norm": 3, "normalize": 4, "ritz": 5,
+                 "project": 6, "finish": 7, "kmeans": 8, "other": 9}
+
+
+class SfairscError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{self.name}: {msg}")
+
+
+class CSR(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64), ("row_offset", C.c_int64),
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p), ("memspace", C.c_int32)]
+
+
+class Opts(C.Structure):
+    _fields_ = [("sigma_override", C.c_double), ("max_basis", C.c_int32), ("keep", C.c_int32),
+                ("max_restarts", C.c_int32), ("start_seed", C.c_uint64), ("tol_eff_cap", C.c_double),
+                ("cuda_stream", C.c_void_p), ("check_symmetry", C.c_int32), ("spmv_vector", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("applies", C.c_int64), ("steps", C.c_int64), ("restarts", C.c_int64), ("breakdowns", C.c_int64),
+                ("sigma", C.c_double), ("max_resid_rel", C.c_double), ("gap_est", C.c_double),
+                ("t_build_s", C.c_double), ("t_eigs_s", C.c_double), ("converged", C.c_int32),
+                ("basis_size", C.c_int32), ("kept", C.c_int32), ("reserved", C.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
+
+
+class Info(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("h", C.c_int32), ("k_build", C.c_int32),
+                ("normalized", C.c_int32), ("spmv_vector", C.c_int32), ("sigma", C.c_double),
+                ("device", C.c_int32), ("num_sms", C.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libsfairsc.so not built at {LIB_PATH}; run `python -m paper_2210_16435_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    sig = {
+        "sfairsc_default_opts": (None, [C.POINTER(Opts)]),
+        "sfairsc_build_operator": (C.c_int, [C.POINTER(CSR), P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
+        "sfairsc_build_operator_ex": (C.c_int, [C.POINTER(CSR), P, C.c_int32, C.c_int32, C.c_int32,
+                                                C.POINTER(Opts), C.POINTER(P)]),
+        "sfairsc_eigs": (C.c_int, [P, C.c_int32, C.c_double, P, P, C.c_int32, C.POINTER(Stats)]),
+        "sfairsc_embed_kmeans": (C.c_int, [P, C.c_uint64, P, C.c_int32, P]),
+        "sfairsc_apply": (C.c_int, [P, P, P, C.c_int32, C.c_int32]),
+        "sfairsc_project": (C.c_int, [P, P, P, C.c_int32, C.c_int32]),
+        "sfairsc_laplacian": (C.c_int, [P, P, P, C.c_int32]),
+        "sfairsc_get_info": (C.c_int, [P, C.POINTER(Info)]),
+        "sfairsc_profile_enable": (C.c_int, [P, C.c_int32]),
+        "sfairsc_profile_read": (C.c_int, [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+        "sfairsc_profile_reset": (C.c_int, [P]),
+        "sfairsc_destroy": (None, [P]),
+        "sfairsc_last_error": (C.c_char_p, []),
+        "sfairsc_version": (C.c_char_p, []),
+        "sfairsc_host_symeig": (C.c_int, [C.c_int32, P, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def version() -> str:
+    return _lib.sfairsc_version().decode()
+
+
+def _check(status: int):
+    if status != 0:
+        raise SfairscError(status, _lib.sfairsc_last_error().decode())
+
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+def _ptr(x, dtype):
+    """(pointer, memspace) of a contiguous numpy array or torch tensor of `dtype`."""
+    if _is_torch(x):
+        import torch
+        tdt = {np.float64: torch.float64, np.int32: torch.int32}[dtype]
+        if x.dtype != tdt or not x.is_contiguous():
+            raise TypeError(f"expected contiguous {tdt} tensor")
+        return x.data_ptr(), (MEM_DEVICE if x.is_cuda else MEM_HOST)
+    if not isinstance(x, np.ndarray) or x.dtype != dtype or not x.flags.c_contiguous:
+        raise TypeError(f"expected C-contiguous numpy {np.dtype(dtype)} array")
+    return x.ctypes.data, MEM_HOST
+
+
+def default_opts(**kw) -> Opts:
+    o = Opts()
+    _lib.sfairsc_default_opts(C.byref(o))
+    for k, v in kw.items():
+        if k == "cuda_stream" and v is not None and not isinstance(v, int):
+            v = v.cuda_stream  # torch.cuda.Stream
+        setattr(o, k, v)
+    return o
+
+
+class Context:
+    """Owns one sfairsc_ctx (library-owned device memory)."""
+
+    def __init__(self, handle, n: int, k: int):
+        self._h = C.c_void_p(handle)
+        self.n = n
+        self.k = k
+        self.last_stats: dict | None = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> dict:
+        i = Info()
+        _check(_lib.sfairsc_get_info(self._h, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in i._fields_}
+
+    def close(self):
+        if self._h:
+            _lib.sfairsc_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def sfairsc_build_operator(row_ptr, col_idx, values, groups, k: int, normalized: bool, h: int = 0,
+                           opts: Opts | None = None, **opt_kw) -> Context:
+    """Build the operator from CSR arrays (numpy host arrays or CUDA tensors;
+    all four in the same memspace).  See include/sfairsc.h."""
+    rp, ms = _ptr(row_ptr, np.int32)
+    ci, ms2 = _ptr(col_idx, np.int32)
+    vv, ms3 = _ptr(values, np.float64)
+    gp, ms4 = _ptr(groups, np.int32)
+    if len({ms, ms2, ms3, ms4}) != 1:
+        raise ValueError("row_ptr, col_idx, values and groups must share one memspace")
+    n = len(row_ptr) - 1
+    nnz = len(col_idx)
+    csr = CSR(n, n, nnz, 0, rp, ci, vv, ms)
+    if opts is None and opt_kw:
+        opts = default_opts(**opt_kw)
+    out = C.c_void_p()
+    if opts is None:
+        _check(_lib.sfairsc_build_operator(C.byref(csr), gp, h, k, int(bool(normalized)), C.byref(out)))
+    else:
+        _check(_lib.sfairsc_build_operator_ex(C.byref(csr), gp, h, k, int(bool(normalized)), C.byref(opts),
+                                              C.byref(out)))
+    return Context(out.value, n, k)
+
+
+def sfairsc_eigs(ctx: Context, k: int, tol: float, evecs=None, want_evecs: bool = True):
+    """k smallest eigenpairs of L^sigma.  `evecs` may be a preallocated
+    (k, n) C-contiguous float64 numpy array or CUDA tensor (= X^T, i.e. X
+    column-major); if None and want_evecs, a numpy array is returned.
+    Returns (evals ndarray, evecs (k x n) or None, stats dict)."""
+    ev = np.zeros(k)
+    st = Stats()
+    if evecs is None and want_evecs:
+        evecs = np.zeros((k, ctx.n))
+    if evecs is not None:
+        ep, ms = _ptr(evecs, np.float64)
+    else:
+        ep, ms = None, MEM_HOST
+    status = _lib.sfairsc_eigs(ctx.handle, k, float(tol), ev.ctypes.data, ep, ms, C.byref(st))
+    ctx.last_stats = st.as_dict()
+    _check(status)
+    return ev, evecs, ctx.last_stats
+
+
+def sfairsc_embed_kmeans(ctx: Context, seed: int, labels=None):
+    """Alg. 3 step 4: labels (n,) int32 (numpy or CUDA tensor) and the WCSS."""
+    if labels is None:
+        labels = np.zeros(ctx.n, dtype=np.int32)
+    lp, ms = _ptr(labels, np.int32)
+    obj = C.c_double()
+    _check(_lib.sfairsc_embed_kmeans(ctx.handle, C.c_uint64(seed), lp, ms, C.byref(obj)))
+    return labels, obj.value
+
+
+def _vec_call(fn, ctx, x, y):
+    xp, ms = _ptr(x, np.float64)
+    nvec = 1 if x.ndim == 1 else x.shape[0]
+    if y is None:
+        if ms == MEM_DEVICE:
+            import torch
+            y = torch.empty_like(x)
+        else:
+            y = np.empty_like(x)
+    yp, ms2 = _ptr(y, np.float64)
+    if ms != ms2:
+        raise ValueError("x and y must share a memspace")
+    _check(fn(ctx.handle, xp, yp, nvec, ms))
+    return y
+
+
+def sfairsc_apply(ctx: Context, x, y=None):
+    """y = L^sigma x; x is (n,) or (nvec, n) (rows = vectors)."""
+    return _vec_call(_lib.sfairsc_apply, ctx, x, y)
+
+
+def sfairsc_project(ctx: Context, x, y=None):
+    """y = P x; x is (n,) or (nvec, n)."""
+    return _vec_call(_lib.sfairsc_project, ctx, x, y)
+
+
+def sfairsc_laplacian(ctx: Context, x, y=None):
+    """y = L x (L_n or D - W) for one vector."""
+    xp, ms = _ptr(x, np.float64)
+    if y is None:
+        if ms == MEM_DEVICE:
+            import torch
+            y = torch.empty_like(x)
+        else:
+            y = np.empty_like(x)
+    yp, _ = _ptr(y, np.float64)
+    _check(_lib.sfairsc_laplacian(ctx.handle, xp, yp, ms))
+    return y
+
+
+def profile_enable(ctx: Context, on: bool = True):
+    _check(_lib.sfairsc_profile_enable(ctx.handle, int(on)))
+
+
+def profile_reset(ctx: Context):
+    _check(_lib.sfairsc_profile_reset(ctx.handle))
+
+
+def profile_read(ctx: Context) -> dict:
+    out = {}
+    for name, kind in PROFILE_KINDS.items():
+        ms = C.c_double()
+        cnt = C.c_int64()
+        _check(_lib.sfairsc_profile_read(ctx.handle, kind, C.byref(ms), C.byref(cnt)))
+        out[name] = {"ms": ms.value, "launches": cnt.value}
+    return out
+
+
+def host_symeig(A: np.ndarray):
+    """Rayleigh-Ritz eigensolver of the library (host code) — for tests."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    m = A.shape[0]
+    ev = np.zeros(m)
+    V = np.zeros((m, m))
+    _check(_lib.sfairsc_host_symeig(m, A.ctypes.data, ev.ctypes.data, V.ctypes.data))
+    return ev, V

@@ -1,0 +1,201 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the
+same seeded inputs.
+
+Tolerances:
+  * operator pieces (SpMV, P, L^sigma): fp64 with a different summation
+    order -> |y - y_ref|_inf <= 1e-13 * sigma * |x|_inf (n <= 1e5 terms of a
+    row are <= deg ~ 1e2; 1e-13 is ~500 ulps of slack);
+  * eigenvalues: |d lambda_i| <= 1e-8 |lambda_i| + 1e-12 sigma (north star
+    relative 1e-8, floor for lambda_1 = 0, reading R6);
+  * subspace: sin(angle) <= 1e-6 when the Davis-Kahan bound
+    (|R_gpu| + |R_oracle|) / gap permits (reading R8);
+  * residual |L^sigma x - lambda x| / sigma <= 1e-9 (north star).
+"""
+import numpy as np
+import pytest
+
+from oracle import fairsc, sfairsc_cpu
+from oracle.metrics import subspace_sin
+from synth import baseline_config, planted_cliques, random_graph
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(lib, g, k, normalized, **kw):
+    return lib.sfairsc_build_operator(g.row_ptr, g.col, g.val, g.groups.astype(np.int32), k, normalized,
+                                      h=g.h, **kw)
+
+
+def _graphs():
+    # (graph, normalized) — ragged sizes (not multiples of 256), h = 1, 2, 5, 20 (> 16 fused groups)
+    return [
+        (random_graph(37, 2, p=0.3, seed=1), False),
+        (random_graph(300, 3, p=0.05, seed=2), True),
+        (random_graph(1031, 5, p=0.01, seed=3), False),
+        (random_graph(777, 1, p=0.02, seed=4), True),
+        (random_graph(2000, 20, p=0.01, seed=5), True),
+        (random_graph(2000, 20, p=0.01, seed=6), False),
+    ]
+
+
+@pytest.mark.parametrize("idx", range(6))
+def test_operator_pieces_match_oracle(gpu_lib, idx):
+    g, normalized = _graphs()[idx]
+    lib = gpu_lib
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, normalized)
+    ctx = _ctx(lib, g, 1, normalized)
+    info = ctx.info()
+    assert info["sigma"] == pytest.approx(op.sigma, rel=1e-14)
+    rng = np.random.default_rng(idx)
+    X = rng.standard_normal((3, g.n))
+    tol = 1e-13 * op.sigma * np.abs(X).max()
+    # bare Laplacian (A5)
+    y = lib.sfairsc_laplacian(ctx, np.ascontiguousarray(X[0]))
+    assert np.abs(y - op.Ln @ X[0]).max() <= tol
+    # projector (A4): P x by the factored form vs the normal-equations form
+    Y = lib.sfairsc_project(ctx, X)
+    ref = np.stack([op.P(x) for x in X])
+    assert np.abs(Y - ref).max() <= 1e-13 * np.abs(X).max() * 10
+    # full operator L^sigma
+    Y = lib.sfairsc_apply(ctx, X)
+    ref = np.stack([op.apply(x) for x in X])
+    assert np.abs(Y - ref).max() <= tol
+    ctx.close()
+
+
+def test_operator_device_tensors(gpu_lib):
+    import torch
+    g, _ = baseline_config(1)
+    lib = gpu_lib
+    d = torch.device("cuda:0")
+    ctx = lib.sfairsc_build_operator(torch.from_numpy(g.row_ptr).to(d), torch.from_numpy(g.col).to(d),
+                                     torch.from_numpy(g.val).to(d), torch.from_numpy(g.groups.astype(np.int32)).to(d),
+                                     5, False)
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, False)
+    x = torch.randn(2, g.n, dtype=torch.float64, device=d)
+    y = lib.sfairsc_apply(ctx, x)
+    ref = np.stack([op.apply(v) for v in x.cpu().numpy()])
+    assert np.abs(y.cpu().numpy() - ref).max() <= 1e-13 * op.sigma * x.abs().max().item()
+    ctx.close()
+
+
+def _check_eigs(lib, g, k, normalized, tol, dense=None, ref_evals=None, ref_X=None, gap=None):
+    ctx = _ctx(lib, g, k, normalized)
+    ev, Xt, st = lib.sfairsc_eigs(ctx, k, tol)
+    X = Xt.T
+    sigma = st["sigma"]
+    assert st["converged"] == 1
+    assert st["max_resid_rel"] <= 1e-9
+    if dense is not None:
+        ref_evals, ref_X, gap = dense.evals[:k], dense.X, dense.gap
+    assert np.all(np.abs(ev - ref_evals) <= 1e-8 * np.abs(ref_evals) + 1e-12 * sigma), (ev, ref_evals)
+    # orthonormal, fair (C^T X = 0)
+    assert np.abs(X.T @ X - np.eye(k)).max() <= 1e-12
+    W = g.to_scipy()
+    C = fairsc.constraint_matrix(W.toarray(), g.groups, g.h, normalized) if g.n <= 3000 else None
+    if C is not None:
+        assert np.linalg.norm(C.T @ X) <= 1e-10 * np.linalg.norm(X)
+    if ref_X is not None and gap is not None and gap > 0:
+        bound = 2 * (st["max_resid_rel"] * sigma * np.sqrt(k) + 1e-12 * sigma) / gap
+        sin = subspace_sin(X, ref_X)
+        assert sin <= max(1e-6, bound), (sin, bound)
+        if bound <= 1e-7:
+            assert sin <= 1e-6
+    ctx.close()
+    return ev, X, st
+
+
+def test_eigs_config1_vs_dense_fairsc(gpu_lib):
+    g, cfg = baseline_config(1)
+    dense = fairsc.fairsc_dense(g.dense(), g.groups, g.h, cfg["k_eig"], cfg["normalized"])
+    _check_eigs(gpu_lib, g, cfg["k_eig"], cfg["normalized"], cfg["tol"], dense=dense)
+
+
+@pytest.mark.parametrize("n,h,normalized,k,seed", [(200, 2, True, 4, 1), (513, 5, False, 6, 2),
+                                                   (400, 3, True, 8, 3), (300, 1, False, 5, 4),
+                                                   (1500, 20, True, 5, 5)])
+def test_eigs_random_vs_dense(gpu_lib, n, h, normalized, k, seed):
+    g = random_graph(n, h, p=min(0.5, 8.0 / n), seed=seed, weights="uniform")
+    dense = fairsc.fairsc_dense(g.dense(), g.groups, h, k, normalized)
+    _check_eigs(gpu_lib, g, k, normalized, 1e-10, dense=dense)
+
+
+@pytest.mark.parametrize("normalized", [False, True])
+def test_eigs_planted_cliques_closed_form(gpu_lib, normalized):
+    """Disconnected planted graph (P-closed-1): spec = {0^k, m or m/(m-1)},
+    eigenspace span{1_{C_l}} (D^{1/2} 1_{C_l}).  Exercises Lanczos breakdown."""
+    k, m, h = 4, 6, 3
+    g = planted_cliques(k, m, h, seed=7)
+    ev, X, st = _check_eigs(gpu_lib, g, k, normalized, 1e-10, ref_evals=np.zeros(k))
+    d = np.diff(g.row_ptr).astype(float)
+    E = np.zeros((g.n, k))
+    E[np.arange(g.n), g.clusters] = 1.0
+    if normalized:
+        E *= np.sqrt(d)[:, None]
+    assert subspace_sin(X, E) <= 1e-8
+    assert st["breakdowns"] >= 1
+
+
+def test_eigs_h1_is_spectral_clustering(gpu_lib):
+    g = random_graph(400, 1, p=0.03, seed=8)
+    dense = fairsc.fairsc_dense(g.dense(), g.groups, 1, 6, True)
+    _check_eigs(gpu_lib, g, 6, True, 1e-10, dense=dense)
+
+
+def test_eigs_deterministic(gpu_lib):
+    g, cfg = baseline_config(1)
+    a = _check_eigs(gpu_lib, g, 5, False, 1e-10, dense=fairsc.fairsc_dense(g.dense(), g.groups, g.h, 5, False))
+    b = _check_eigs(gpu_lib, g, 5, False, 1e-10, dense=fairsc.fairsc_dense(g.dense(), g.groups, g.h, 5, False))
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_eigs_config2_vs_tier_s(gpu_lib):
+    g, cfg = baseline_config(2)
+    k = cfg["k_eig"]
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, True)
+    ref = sfairsc_cpu.sfairsc_arpack(op, k, tol=1e-13, seed=2)
+    gap = ref.evals[k] - ref.evals[k - 1]
+    _check_eigs(gpu_lib, g, k, True, cfg["tol"], ref_evals=ref.evals[:k], ref_X=ref.X, gap=gap)
+
+
+# --- error vocabulary ----------------------------------------------------------
+
+def test_errors(gpu_lib):
+    lib = gpu_lib
+    g = random_graph(50, 2, p=0.2, seed=1)
+    grp = g.groups.astype(np.int32)
+    # asymmetric
+    v = g.val.copy()
+    v[0] += 1.0
+    with pytest.raises(lib.SfairscError) as e:
+        lib.sfairsc_build_operator(g.row_ptr, g.col, v, grp, 2, False)
+    assert e.value.name == "E_ASYMMETRIC"
+    # negative weight (symmetric)
+    v = -g.val
+    with pytest.raises(lib.SfairscError) as e:
+        lib.sfairsc_build_operator(g.row_ptr, g.col, v, grp, 2, False)
+    assert e.value.name == "E_NEGATIVE_WEIGHT"
+    # empty group
+    with pytest.raises(lib.SfairscError) as e:
+        lib.sfairsc_build_operator(g.row_ptr, g.col, g.val, np.zeros(50, np.int32), 2, False, h=2)
+    assert e.value.name == "E_EMPTY_GROUP"
+    # k too large
+    with pytest.raises(lib.SfairscError) as e:
+        lib.sfairsc_build_operator(g.row_ptr, g.col, g.val, grp, 50, False)
+    assert e.value.name == "E_K_TOO_LARGE"
+    # isolated vertex: drop all edges of vertex 0 (both directions)
+    import scipy.sparse as sp
+    W = g.to_scipy().tolil()
+    W[0, :] = 0
+    W[:, 0] = 0
+    W = sp.csr_matrix(W)
+    W.eliminate_zeros()
+    with pytest.raises(lib.SfairscError) as e:
+        lib.sfairsc_build_operator(W.indptr.astype(np.int32), W.indices.astype(np.int32), W.data, grp, 2, False)
+    assert e.value.name == "E_ISOLATED_VERTEX"
+    # call order
+    ctx = lib.sfairsc_build_operator(g.row_ptr, g.col, g.val, grp, 2, False)
+    with pytest.raises(lib.SfairscError) as e:
+        lib.sfairsc_embed_kmeans(ctx, 1)
+    assert e.value.name == "E_STATE"
+    ctx.close()
