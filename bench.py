@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""s-FairSC on B200 — benchmark (contract in the task statement).
+
+Workload (N=1): BASELINE config 4 — normalized s-FairSC on an m-SBM with
+n = 4,000,000, h = 10 (Zipf 1.1 groups), k = 50, mean degree 32 (~1.28e8
+nnz), tol 1e-8; the configuration the north star's "applies/s & HBM % at
+n = 4M" target names (configs 1-3 are parity-test cases).
+
+One STEP = one pass of the whole hot path: build
+the operator from the device-resident CSR (validation, degrees, sigma,
+factored projector) and run the thick-restart Lanczos eigensolve to the
+k = 50 smallest eigenpairs at the residual target, incl. the final true
+residual check.  `value` = operator applies L^sigma w executed per second
+over the timed steps (whole job); `ms_per_step` = time-to-k-eigenvectors.
+
+Also reported: an apply-only measurement (back-to-back L^sigma applies),
+`roofline` of the dominant kernel from CUDA events recorded around every
+launch inside the timed region, `e2e` through the C ABI from host buffers,
+and `cpu_baseline` = the oracle (Tier S, the paper's matrix-free operator in
+scipy) timed on a bounded sample.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C] [--n N] [--tol T]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [x.strip() for x in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_graph(cfg_id, n_override, rank):
+    from synth import baseline_config, msbm
+    from synth.msbm import CONFIGS
+    if rank == 0:
+        g, cfg = baseline_config(cfg_id, n=n_override)
+    else:  # weak scaling: independent problem per rank (same law, rank-shifted seed)
+        cfg = dict(CONFIGS[cfg_id])
+        params = {k: cfg[k] for k in ("probs", "rel", "mean_degree", "group_probs", "group_counts", "weights")
+                  if k in cfg}
+        nn = cfg["n"] if n_override is None else n_override
+        if n_override is not None and "group_counts" in params:
+            params.pop("group_counts")
+            params["group_probs"] = tuple(np.asarray(cfg["group_counts"]) / cfg["n"])
+        g = msbm(nn, cfg["h"], cfg["k"], seed=16435 + cfg_id + 1000 * rank, name=f"cfg{cfg_id}-r{rank}", **params)
+    return g, cfg
+
+
+def cpu_baseline(g, cfg, budget_s=15.0):
+    """The oracle as it stands (Tier S matrix-free L^sigma apply, scipy) on a
+    bounded sample: as many applies as fit in ~budget_s.  cores = CPU-time /
+    wall-time actually used."""
+    from oracle import sfairsc_cpu
+    t0 = time.perf_counter()
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, cfg["normalized"])
+    t_build = time.perf_counter() - t0
+    w = np.random.default_rng(0).standard_normal(g.n)
+    c0 = time.process_time()
+    t0 = time.perf_counter()
+    cnt = 0
+    while True:
+        w = op.apply(w)
+        w /= np.linalg.norm(w)
+        cnt += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    wall = time.perf_counter() - t0
+    cpu = time.process_time() - c0
+    return {"value": cnt / wall, "unit": "applies/s", "cores": max(1, round(cpu / wall)), "kind": "oracle",
+            "sample": f"{cnt} Tier-S L^sigma applies (scipy CSR SpMV + normal-equations projector, P:799-818) on "
+                      f"the same n={g.n} graph in {wall:.1f} s (operator build {t_build:.1f} s excluded); "
+                      f"host has {os.cpu_count()} logical cores",
+            "s_per_apply": wall / cnt}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    g, cfg = make_graph(args.config, args.n, 0)
+    from oracle import sfairsc_cpu
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, cfg["normalized"])
+    w = np.random.default_rng(0).standard_normal(g.n)
+    per_step = args.ref_applies
+    for _ in range(args.warmup):
+        for _ in range(per_step):
+            w = op.apply(w)
+            w /= np.linalg.norm(w)
+    c0 = time.process_time()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for _ in range(per_step):
+            w = op.apply(w)
+            w /= np.linalg.norm(w)
+    wall = time.perf_counter() - t0
+    cpu = time.process_time() - c0
+    value = args.steps * per_step / wall
+    cores = max(1, round(cpu / wall))
+    line = {"metric": "projected-operator applies/s (L^sigma, s-FairSC)", "value": value, "unit": "applies/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"BASELINE config {args.config}: m-SBM n={g.n}, h={g.h}, k={cfg['k_eig']}, "
+                                   f"normalized={cfg['normalized']}, nnz={g.nnz}",
+                       "step": f"{per_step} oracle applies (the full ARPACK solve does not finish in minutes at this size)"},
+            "cpu_baseline": {"value": value, "unit": "applies/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps}x{per_step} Tier-S applies, scipy, n={g.n}"},
+            "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--n", type=int, default=None, help="override n (reduced-size runs; not a bench value)")
+    ap.add_argument("--tol", type=float, default=None)
+    ap.add_argument("--apply-reps", type=int, default=200)
+    ap.add_argument("--ref-applies", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--apply-only", action="store_true", help="exploration: skip the solves")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = _dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2210_16435_b200 import lib
+
+    t_gen = time.perf_counter()
+    g, cfg = make_graph(args.config, args.n, rank)
+    t_gen = time.perf_counter() - t_gen
+    k = cfg["k_eig"]
+    tol = args.tol if args.tol is not None else cfg["tol"]
+    normalized = cfg["normalized"]
+    rp = torch.from_numpy(g.row_ptr).to(dev)
+    ci = torch.from_numpy(g.col).to(dev)
+    vv = torch.from_numpy(g.val).to(dev)
+    gr = torch.from_numpy(g.groups.astype(np.int32)).to(dev)
+    X = torch.empty((k, g.n), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(profile=False):
+        ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, normalized, h=g.h, cuda_stream=stream.cuda_stream)
+        if profile:
+            lib.profile_enable(ctx, True)
+        ev, _, st = lib.sfairsc_eigs(ctx, k, tol, evecs=X)
+        prof = lib.profile_read(ctx) if profile else None
+        info = ctx.info()
+        ctx.close()
+        return ev, st, prof, info
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    if args.apply_only:
+        args.warmup = 0
+        args.steps = 0
+    # ---- warm-up ----
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    torch.cuda.synchronize()
+    # ---- timed region (device clock, CUDA events on the launching stream) ----
+    launches0 = lib.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    stats, profs = [], []
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            ev, st, prof, info = step(profile=True)
+            stats.append(st)
+            profs.append(prof)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    launches = lib.launch_count() - launches0
+    ms_t = torch.tensor([ms], device=dev)
+    if ws > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    applies = sum(s["applies"] for s in stats)
+    app_t = torch.tensor([float(applies)], device=dev)
+    if ws > 1:
+        dist.all_reduce(app_t)
+    value = float(app_t.item()) / (ms / 1e3) if ms > 0 else 0.0
+
+    # ---- per-kernel roofline (events around every launch inside the timed region) ----
+    peak, peak_kind = _peaks()
+    kinds = {}
+    for p in profs:
+        for name, d in p.items():
+            a = kinds.setdefault(name, {"ms": 0.0, "launches": 0, "alg_bytes": 0.0})
+            for f in a:
+                a[f] += d[f]
+    if not kinds:
+        kinds = {"spmv": {"ms": 0.0, "launches": 0, "alg_bytes": 0.0}}
+    tot_kernel_ms = sum(v["ms"] for v in kinds.values())
+    dom = max(kinds, key=lambda x: kinds[x]["ms"])
+    d = kinds[dom]
+    achieved = d["alg_bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs copy bandwidth)",
+                "traffic": traffic, "share_of_step": d["ms"] / ms if ms > 0 else None,
+                "alg_bytes_per_launch": d["alg_bytes"] / max(1, d["launches"]),
+                "us_per_launch": 1e3 * d["ms"] / max(1, d["launches"]),
+                "per_kernel": {kk: {"ms": v["ms"], "launches": v["launches"],
+                                    "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
+                                    "share": v["ms"] / tot_kernel_ms if tot_kernel_ms else None}
+                               for kk, v in sorted(kinds.items(), key=lambda x: -x[1]["ms"]) if v["launches"]}}
+
+    # ---- apply-only: back-to-back L^sigma applies (north-star apply metric) ----
+    ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, normalized, h=g.h, cuda_stream=stream.cuda_stream)
+    info = ctx.info()
+    nv = 8
+    xs = torch.randn((nv, g.n), dtype=torch.float64, device=dev)
+    ys = torch.empty_like(xs)
+    for _ in range(2):
+        lib.sfairsc_apply(ctx, xs, ys)
+    lib.profile_enable(ctx, True)
+    reps = max(1, args.apply_reps // nv)
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(reps):
+        lib.sfairsc_apply(ctx, xs, ys)
+    a1.record(stream)
+    torch.cuda.synchronize()
+    apply_ms = a0.elapsed_time(a1) / (reps * nv)
+    ap_prof = lib.profile_read(ctx)
+    ctx.close()
+    n, nnz = g.n, g.nnz
+    alg_apply = 12.0 * nnz + 4.0 * (n + 1) + 8.0 * n * 2 + (8.0 * n if True else 0) + 1.0 * n  # CSR + w + y + d|s + g
+    spmv_alg = ap_prof["spmv"]["alg_bytes"] / max(1, ap_prof["spmv"]["launches"])
+    spmv_us = 1e3 * ap_prof["spmv"]["ms"] / max(1, ap_prof["spmv"]["launches"])
+    apply_only = {"applies_per_s": 1e3 / apply_ms, "us_per_apply": 1e3 * apply_ms,
+                  "alg_bytes_per_apply": alg_apply, "alg_GBps": alg_apply / (apply_ms / 1e3) / 1e9,
+                  "frac_of_peak": alg_apply / (apply_ms / 1e3) / 1e9 / peak,
+                  "frac_of_8TBps_nominal": alg_apply / (apply_ms / 1e3) / 1e9 / 8000.0,
+                  "spmv_us": spmv_us, "spmv_alg_GBps": spmv_alg / (spmv_us / 1e6) / 1e9,
+                  "note": "events around each of the 4 kernels add ~1-2 us per kernel; the us_per_apply bracket is one event pair per batch"}
+
+    # ---- e2e through the C ABI from pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        hrp = torch.from_numpy(g.row_ptr).pin_memory()
+        hci = torch.from_numpy(g.col).pin_memory()
+        hvv = torch.from_numpy(g.val).pin_memory()
+        hgr = torch.from_numpy(g.groups.astype(np.int32)).pin_memory()
+        hX = torch.empty((k, g.n), dtype=torch.float64).pin_memory()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_app = 0
+        for _ in range(args.steps):
+            ctx = lib.sfairsc_build_operator(hrp, hci, hvv, hgr, k, normalized, h=g.h, cuda_stream=stream.cuda_stream)
+            ev, _, st = lib.sfairsc_eigs(ctx, k, tol, evecs=hX)
+            e2e_app += st["applies"]
+            ctx.close()
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        el_t = torch.tensor([el], device=dev)
+        if ws > 1:
+            dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
+        h2d = g.row_ptr.nbytes + g.col.nbytes + g.val.nbytes + 4 * g.n
+        d2h = 8 * g.n * k + 8 * k
+        e2e = {"value": e2e_app * ws / float(el_t.item()), "unit": "applies/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(el_t.item()) / args.steps,
+               "note": "host-timed (perf_counter) with device synchronised; CSR+groups H2D inside build, X D2H inside eigs"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(g, cfg)
+
+    if rank == 0 and args.apply_only:
+        print(json.dumps({"apply_only": apply_only, "n": g.n, "nnz": g.nnz, "spmv_vector": info["spmv_vector"],
+                          "generator_s": t_gen, "apply_profile": ap_prof}), flush=True)
+    elif rank == 0:
+        last = stats[-1]
+        line = {
+            "metric": "projected-operator applies/s (L^sigma inside the full s-FairSC eigensolve); time-to-k-eigvecs = ms_per_step",
+            "value": value, "unit": "applies/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / max(1, args.steps), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE config {args.config}" + (" (reduced n)" if args.n else "")
+                                   + f": normalized={normalized} m-SBM n={g.n}, nnz={g.nnz}, h={g.h}, k={k}, tol={tol}",
+                       "step": "build operator from device CSR (A0-A3) + thick-restart Lanczos to k eigenpairs (A4-A11)",
+                       "l2": f"inputs larger than L2 (CSR {(12 * g.nnz + 4 * g.n) / 1e9:.2f} GB, Krylov basis "
+                             f"{8 * g.n * (last['basis_size'] + 1) / 1e9:.2f} GB >> 126 MB)",
+                       "parallelism": "1 GPU" if ws == 1 else f"{ws} independent problems (one per rank)",
+                       "generator_s": t_gen},
+            "solve": {"applies_per_step": applies / args.steps, "steps": last["steps"], "restarts": last["restarts"],
+                      "breakdowns": last["breakdowns"], "max_resid_rel": last["max_resid_rel"],
+                      "gap_est": last["gap_est"], "sigma": last["sigma"], "converged": last["converged"],
+                      "basis": last["basis_size"], "kept": last["kept"], "lambda_k": float(ev[-1]),
+                      "lambda_2": float(ev[1]) if len(ev) > 1 else None},
+            "apply_only": apply_only,
+            "roofline": roofline,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "spmv_vector": info["spmv_vector"],
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -165,13 +165,20 @@ sfairsc_status sfairsc_laplacian(sfairsc_ctx *ctx, const double *x, double *y, i
 sfairsc_status sfairsc_get_info(const sfairsc_ctx *ctx, sfairsc_info *info);
 
 /* Per-kernel device timing with CUDA events on the context stream (for the
- * bench roofline).  kind: 0 spmv, 1 reorth sweep (dots), 2 reorth sweep
+ * bench roofline); one event pair brackets each profiled launch group.  kind: 0 spmv, 1 reorth sweep (dots), 2 reorth sweep
  * (update+dots), 3 reorth sweep (update+norm), 4 normalize, 5 ritz gemm,
  * 6 project/group-sum, 7 apply-finish, 8 kmeans, 9 other.  Enabling adds
  * one event pair per launch. */
 sfairsc_status sfairsc_profile_enable(sfairsc_ctx *ctx, int32_t enable);
 sfairsc_status sfairsc_profile_read(sfairsc_ctx *ctx, int32_t kind, double *total_ms,
-                                    int64_t *launches);
+                                    int64_t *launches, double *alg_bytes);
+/* alg_bytes = sum over the kind's launches of its algorithmic bytes (each
+ * operand read or written once; SpMV: CSR 12 nnz + 4(n+1) + p, t, d or s,
+ * group ids; sweeps: J basis columns + the vectors). */
+
+/* Total kernel launches issued by this library in this process (all
+ * contexts) — the bench's gpu_launches evidence. */
+int64_t sfairsc_launch_count(void);
 sfairsc_status sfairsc_profile_reset(sfairsc_ctx *ctx);
 
 /* Host-only utility: the dense symmetric eigensolver of the Rayleigh-Ritz step

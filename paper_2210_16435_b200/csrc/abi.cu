@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -57,11 +58,13 @@ struct Prof {
   struct Pending {
     int kind;
     cudaEvent_t a, b;
+    double bytes;
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> pool;
   double total_ms[10] = {};
   int64_t launches[10] = {};
+  double bytes[10] = {};
   cudaEvent_t get() {
     if (pool.empty()) {
       cudaEvent_t e;
@@ -79,6 +82,7 @@ struct Prof {
       cudaEventElapsedTime(&ms, p.a, p.b);
       total_ms[p.kind] += ms;
       launches[p.kind] += 1;
+      bytes[p.kind] += p.bytes;
       pool.push_back(p.a);
       pool.push_back(p.b);
     }
@@ -108,6 +112,9 @@ struct sfairsc_ctx {
   uint64_t seed = 0x5F41C5EEDull;
   int m = 20, keep = 0, max_restarts = 100000;
   int check_symmetry = 1;
+  int debug = 0;
+  int sweep_kind = 2;  // 0 register sweeps, 1 smem-staged, 2 TMA 2-D tensor (default), 3 TMA 1-D (env SFAIRSC_SWEEP)
+  int tma_mode2 = 0;   // update+norm sweep: register kernel (measured faster); env SFAIRSC_TMA_MODE2=1: TMA
   // device buffers
   int *rp = nullptr, *ci = nullptr, *row_split = nullptr;
   double *vv = nullptr, *dg = nullptr, *s = nullptr;
@@ -120,6 +127,7 @@ struct sfairsc_ctx {
   double *c1 = nullptr, *c2 = nullptr;
   double *vp = nullptr, *vt = nullptr, *vr = nullptr, *vy = nullptr;
   double *V = nullptr, *Vb = nullptr, *Ydev = nullptr, *X = nullptr;
+  double *talpha = nullptr, *tbeta = nullptr;  // Lanczos T entries recorded on device
   int* flags = nullptr;
   double* hp = nullptr;  // pinned host staging (4 KB)
   // results
@@ -149,6 +157,11 @@ struct sfairsc_ctx {
     return G;
   }
   ProjDesc pd() const { return ProjDesc{h, isb, uh}; }
+  // algorithmic bytes: one read/write of each operand
+  double vb() const { return 8.0 * n; }                      // one fp64 n-vector
+  double sgb() const { return (normalized ? 8.0 * n : 0.0) + 1.0 * n; }  // s (normalized) + group ids
+  double csr_bytes() const { return 12.0 * nnz + 4.0 * (n + 1); }
+  int gpasses() const { return (h + kHB - 1) / kHB; }
 };
 
 // accessors used by kmeans.cu
@@ -177,8 +190,9 @@ sfairsc_status ctx_fail(sfairsc_status st, const char* msg) { return fail(st, "%
 struct ProfScope {
   sfairsc_ctx* c;
   int kind;
+  double bytes;
   cudaEvent_t a = nullptr;
-  ProfScope(sfairsc_ctx* c_, int kind_) : c(c_), kind(kind_) {
+  ProfScope(sfairsc_ctx* c_, int kind_, double bytes_ = 0.0) : c(c_), kind(kind_), bytes(bytes_) {
     if (c->prof.on) {
       a = c->prof.get();
       cudaEventRecord(a, c->st);
@@ -188,7 +202,7 @@ struct ProfScope {
     if (c->prof.on) {
       cudaEvent_t b = c->prof.get();
       cudaEventRecord(b, c->st);
-      c->prof.pending.push_back({kind, a, b});
+      c->prof.pending.push_back({kind, a, b, bytes});
     }
   }
 };
@@ -204,7 +218,7 @@ void ctx_prof_end(sfairsc_ctx* c, int kind, cudaEvent_t a) {
   if (c->prof.on && a) {
     cudaEvent_t b = c->prof.get();
     cudaEventRecord(b, c->st);
-    c->prof.pending.push_back({kind, a, b});
+    c->prof.pending.push_back({kind, a, b, 0.0});
   }
 }
 }  // namespace sfz
@@ -219,7 +233,7 @@ static void free_ctx(sfairsc_ctx* c) {
   if (c->km && c->km_free) c->km_free(c->km);
   void* ptrs[] = {c->rp, c->ci, c->row_split, c->vv, c->dg, c->s, c->grp, c->isb, c->uh, c->partials, c->counters,
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
-                  c->Vb, c->Ydev, c->X, c->flags};
+                  c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hp) cudaFreeHost(c->hp);
@@ -280,18 +294,18 @@ static void gsum_all(sfairsc_ctx* c, const double* x, double* bsum) {
 // y = L^sigma x on device vectors (4 kernels; A4-A6)
 static sfairsc_status apply_dev(sfairsc_ctx* c, const double* x, double* y) {
   {
-    ProfScope ps(c, K_PROJ);
+    ProfScope ps(c, K_PROJ, c->gpasses() * (c->vb() + c->sgb()) + 2 * c->vb() + c->sgb());
     gsum_all(c, x, c->bs_w);
     launch_project(c->g(), c->pd(), x, c->bs_w, 1.0, c->vp, c->st);
   }
   {
-    ProfScope ps(c, K_SPMV);
+    ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
     launch_spmv(c->g(), c->vs, c->row_split, c->spmv_grid, c->vp, c->vt, c->partials, c->counters + 1, c->bs_t,
                 c->st);
   }
   if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
   {
-    ProfScope ps(c, K_FINISH);
+    ProfScope ps(c, K_FINISH, 2 * c->vb() + c->sgb());
     launch_finish(c->g(), c->pd(), c->vt, c->bs_t, c->bs_w, c->sigma, y, c->st);
   }
   CHECK_LAUNCH();
@@ -364,6 +378,13 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   c->seed = opts.start_seed;
   c->max_restarts = opts.max_restarts > 0 ? opts.max_restarts : 100000;
   c->check_symmetry = opts.check_symmetry;
+  c->debug = getenv("SFAIRSC_DEBUG") ? atoi(getenv("SFAIRSC_DEBUG")) : 0;
+  if (getenv("SFAIRSC_SWEEP")) c->sweep_kind = atoi(getenv("SFAIRSC_SWEEP"));
+  if (getenv("SFAIRSC_TMA_MODE2")) c->tma_mode2 = atoi(getenv("SFAIRSC_TMA_MODE2"));
+  if (c->sweep_kind == 3) {  // TMA with one 1-D copy per column (A/B only)
+    sfz::g_tma_use2d = 0;
+    c->sweep_kind = 2;
+  }
   auto bail = [&](sfairsc_status st) {
     free_ctx(c);
     return st;
@@ -399,9 +420,15 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   CUB(dalloc(&c->rp, n + 1));
   CUB(dalloc(&c->ci, nnz));
   CUB(dalloc(&c->vv, nnz));
-  CUB(dalloc(&c->dg, n));
-  if (c->normalized) CUB(dalloc(&c->s, n));
-  CUB(dalloc(&c->grp, n));
+  // per-vertex arrays padded to ldv rows (the TMA sweeps stage whole 64-row chunks)
+  CUB(dalloc(&c->dg, c->ldv));
+  CUB(cudaMemset(c->dg, 0, sizeof(double) * c->ldv));
+  if (c->normalized) {
+    CUB(dalloc(&c->s, c->ldv));
+    CUB(cudaMemset(c->s, 0, sizeof(double) * c->ldv));
+  }
+  CUB(dalloc(&c->grp, c->ldv));
+  CUB(cudaMemset(c->grp, 0, c->ldv));
   CUB(dalloc(&c->isb, 256));
   CUB(dalloc(&c->uh, 256));
   CUB(dalloc(&c->counters, 16));
@@ -532,6 +559,8 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   CUB(cudaMemsetAsync(c->V, 0, sizeof(double) * (m + 1) * c->ldv, c->st));
   CUB(cudaMemsetAsync(c->Vb, 0, sizeof(double) * (m + 1) * c->ldv, c->st));
   CUB(dalloc(&c->Ydev, (size_t)(m + 1) * (m + 1)));
+  CUB(dalloc(&c->talpha, m + 1));
+  CUB(dalloc(&c->tbeta, m + 1));
   CUB(dalloc(&c->X, (size_t)k * c->ldv));
   CUB(cudaMemsetAsync(c->X, 0, sizeof(double) * k * c->ldv, c->st));
   CUB(cudaStreamSynchronize(c->st));
@@ -572,7 +601,7 @@ static sfairsc_status vec_io(sfairsc_ctx* c, const double* x, double* y, int32_t
 }
 
 static sfairsc_status project_dev(sfairsc_ctx* c, const double* x, double* y) {
-  ProfScope ps(c, K_PROJ);
+  ProfScope ps(c, K_PROJ, c->gpasses() * (c->vb() + c->sgb()) + 2 * c->vb() + c->sgb());
   gsum_all(c, x, c->bs_w);
   launch_project(c->g(), c->pd(), x, c->bs_w, 1.0, y, c->st);
   CHECK_LAUNCH();
@@ -580,7 +609,7 @@ static sfairsc_status project_dev(sfairsc_ctx* c, const double* x, double* y) {
 }
 
 static sfairsc_status lap_dev(sfairsc_ctx* c, const double* x, double* y) {
-  ProfScope ps(c, K_SPMV);
+  ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
   launch_spmv(c->g(), c->vs, c->row_split, c->spmv_grid, x, y, c->partials, c->counters + 1, c->bs_t, c->st);
   CHECK_LAUNCH();
   return SFAIRSC_OK;
@@ -608,12 +637,14 @@ extern "C" sfairsc_status sfairsc_profile_enable(sfairsc_ctx* c, int32_t enable)
   c->prof.on = enable != 0;
   return SFAIRSC_OK;
 }
-extern "C" sfairsc_status sfairsc_profile_read(sfairsc_ctx* c, int32_t kind, double* total_ms, int64_t* launches) {
+extern "C" sfairsc_status sfairsc_profile_read(sfairsc_ctx* c, int32_t kind, double* total_ms, int64_t* launches,
+                                               double* alg_bytes) {
   if (!c || kind < 0 || kind >= 10) return fail(SFAIRSC_E_INVALID_ARG, "bad argument");
   CU(cudaStreamSynchronize(c->st));
   c->prof.resolve();
   if (total_ms) *total_ms = c->prof.total_ms[kind];
   if (launches) *launches = c->prof.launches[kind];
+  if (alg_bytes) *alg_bytes = c->prof.bytes[kind];
   return SFAIRSC_OK;
 }
 extern "C" sfairsc_status sfairsc_profile_reset(sfairsc_ctx* c) {
@@ -623,6 +654,7 @@ extern "C" sfairsc_status sfairsc_profile_reset(sfairsc_ctx* c) {
   for (int i = 0; i < 10; ++i) {
     c->prof.total_ms[i] = 0;
     c->prof.launches[i] = 0;
+    c->prof.bytes[i] = 0;
   }
   return SFAIRSC_OK;
 }
@@ -633,10 +665,11 @@ extern "C" sfairsc_status sfairsc_profile_reset(sfairsc_ctx* c) {
 struct Lanczos {
   sfairsc_ctx* c;
   int m, keep, k;
-  int pk = 0;  // number of locked Ritz vectors heading the basis (arrow part of T)
+  int pk = 0;  // number of kept Ritz vectors heading the basis (arrow part of T)
   std::vector<double> alpha, beta, arrow;
   int64_t applies = 0, steps = 0, restarts = 0, breakdowns = 0;
   unsigned inject = 0;
+  double bd_tol = 0.0;
 
   double* col(int j) const { return c->V + (long long)j * c->ldv; }
 
@@ -657,58 +690,71 @@ struct Lanczos {
     return a;
   }
 
-  // CGS2 of vr against V[:, 0:J] (dots already in c1 when pre_dots) then
-  // |r''|^2 and B^T r'' into nb.  mode0=true: r = finish(t) fused with dots.
+  // one sweep; returns the grid used (= number of partial rows)
+  int sweep(int mode, const SweepArgs& a) {
+    if (c->sweep_kind == 1 && mode != 2 && sweep_tma_ok(a.J)) {  // smem-staged dots sweeps
+      const int G = sweep_smem_grid(c->n, a.J, c->num_sms);
+      launch_sweep_smem(mode, c->g(), c->pd(), a, G, c->st);
+      return G;
+    }
+    if (c->sweep_kind == 2 && sweep_tma_ok(a.J) && (mode != 2 || c->tma_mode2)) {
+      const int G = sweep_tma_grid(c->n, c->num_sms);
+      launch_sweep_tma(mode, c->g(), c->pd(), a, G, c->st);
+      return G;
+    }
+    launch_sweep(mode, c->g(), c->pd(), a, c->sgrid, c->st);
+    return c->sgrid;
+  }
+
+  // CGS2 of r against V[:, 0:J]: |r''|^2 and B^T r'' land in nb.
+  // from_t: r = finish(t) (= L^sigma v_j) fused into the first sweep.
   sfairsc_status cgs2(int J, bool from_t) {
     GraphDev g = c->g();
     ProjDesc pd = c->pd();
     if (J > 0) {
       {
-        ProfScope ps(c, K_DOTS);
-        launch_sweep(from_t ? 0 : 3, g, pd, sargs(J, from_t ? c->vt : c->vr, c->vr, nullptr), c->sgrid, c->st);
-        launch_reduce_cols(c->partials, c->sgrid, J, c->c1, c->st);
+        ProfScope ps(c, K_DOTS, J * c->vb() + (from_t ? 2 * c->vb() + c->sgb() : c->vb()));
+        const int G = sweep(from_t ? 0 : 3, sargs(J, from_t ? c->vt : c->vr, c->vr, nullptr));
+        launch_reduce_cols(c->partials, G, J, c->c1, c->st);
       }
       {
-        ProfScope ps(c, K_UPDDOT);
-        launch_sweep(1, g, pd, sargs(J, c->vr, c->vr, c->c1), c->sgrid, c->st);
-        launch_reduce_cols(c->partials, c->sgrid, J, c->c2, c->st);
+        ProfScope ps(c, K_UPDDOT, J * c->vb() + 2 * c->vb());
+        const int G = sweep(1, sargs(J, c->vr, c->vr, c->c1));
+        launch_reduce_cols(c->partials, G, J, c->c2, c->st);
       }
     } else if (from_t) {
-      ProfScope ps(c, K_DOTS);
+      ProfScope ps(c, K_DOTS, 2 * c->vb() + c->sgb());
       launch_finish(g, pd, c->vt, c->bs_t, c->bs_v, c->sigma, c->vr, c->st);
     }
     {
-      ProfScope ps(c, K_UPDNORM);
-      launch_sweep(2, g, pd, sargs(J, c->vr, c->vr, c->c2), c->sgrid, c->st);
+      ProfScope ps(c, K_UPDNORM, J * c->vb() + 2 * c->vb() + c->sgb());
+      sweep(2, sargs(J, c->vr, c->vr, c->c2));
     }
     if (c->h > kHB) extra_gsums(c, c->vr, c->nb + 1);
     CHECK_LAUNCH();
     return SFAIRSC_OK;
   }
 
-  sfairsc_status normalize_into(int j, double b) {
-    ProfScope ps(c, K_NORMALIZE);
-    launch_normalize(c->g(), c->pd(), c->vr, b, c->nb + 1, col(j), c->bs_v, c->vp, c->st);
+  // v_{j+1} = r''/beta into column j+1 (beta from device), recording T entries
+  sfairsc_status normalize_step(int j) {
+    ProfScope ps(c, K_NORMALIZE, 3 * c->vb() + c->sgb());
+    NormArgs na{};
+    na.nb = c->nb;
+    na.beta_host = 0.0;
+    na.bd_tol = bd_tol;
+    na.j = j;
+    na.c1 = c->c1;
+    na.c2 = c->c2;
+    na.alpha_dev = c->talpha;
+    na.beta_dev = c->tbeta;
+    na.flag = c->flags + 1;
+    launch_normalize(c->g(), c->pd(), c->vr, na, col(j + 1), c->bs_v, c->vp, c->st);
     CHECK_LAUNCH();
     return SFAIRSC_OK;
   }
 
-  // fetch nb[0] (and optionally c1[j], c2[j]) to the host
-  sfairsc_status fetch(int j, double* nrm2, double* a) {
-    CU(cudaMemcpyAsync(c->hp, c->nb, sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    if (a) {
-      CU(cudaMemcpyAsync(c->hp + 1, c->c1 + j, sizeof(double), cudaMemcpyDeviceToHost, c->st));
-      CU(cudaMemcpyAsync(c->hp + 2, c->c2 + j, sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    }
-    CU(cudaStreamSynchronize(c->st));
-    if (c->prof.on) c->prof.resolve();
-    *nrm2 = c->hp[0];
-    if (a) *a = c->hp[1] + c->hp[2];
-    return SFAIRSC_OK;
-  }
-
-  // random vector orthogonalised against V[:, 0:J], normalised into column J
-  sfairsc_status random_vector(int J, bool project_first, double* beta_out) {
+  // random vector orthogonalised (CGS2 twice) against V[:, 0:J], normalised into column J
+  sfairsc_status random_vector(int J, bool project_first) {
     for (int attempt = 0; attempt < 5; ++attempt) {
       if (project_first) {  // r = P u
         launch_random(c->vt, c->n, c->seed, inject++, 7u, c->st);
@@ -718,25 +764,47 @@ struct Lanczos {
         launch_random(c->vr, c->n, c->seed, inject++, 7u, c->st);
       }
       TRY(cgs2(J, false));
-      if (J > 0) {  // second full CGS2 pass for a fresh vector (twice is enough)
-        TRY(cgs2(J, false));
-      }
-      double nrm2;
-      TRY(fetch(0, &nrm2, nullptr));
-      const double b = std::sqrt(nrm2);
+      if (J > 0) TRY(cgs2(J, false));
+      CU(cudaMemcpyAsync(c->hp, c->nb, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CU(cudaStreamSynchronize(c->st));
+      const double b = std::sqrt(c->hp[0]);
       if (b > 1e-8) {
-        TRY(normalize_into(J, b));
-        *beta_out = b;
+        ProfScope ps(c, K_NORMALIZE, 3 * c->vb() + c->sgb());
+        NormArgs na{};
+        na.nb = c->nb;
+        na.beta_host = b;
+        na.bd_tol = 0.0;
+        launch_normalize(c->g(), c->pd(), c->vr, na, col(J), c->bs_v, c->vp, c->st);
+        CHECK_LAUNCH();
         return SFAIRSC_OK;
       }
     }
     return fail(SFAIRSC_E_NO_CONVERGENCE, "could not generate a random vector outside the Krylov basis");
+  }
+
+  // sync point: T entries [from, to) and the breakdown flag to the host
+  sfairsc_status fetch_T(int from, int to, int* flag) {
+    const int cnt = to - from;
+    if (cnt > 0) {
+      CU(cudaMemcpyAsync(c->hp, c->talpha + from, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->st));
+      CU(cudaMemcpyAsync(c->hp + 1024, c->tbeta + from, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->st));
+    }
+    CU(cudaMemcpyAsync(c->hp + 2048, c->flags + 1, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    if (c->prof.on) c->prof.resolve();
+    for (int i = 0; i < cnt; ++i) {
+      alpha[from + i] = c->hp[i];
+      beta[from + i] = c->hp[1024 + i];
+    }
+    std::memcpy(flag, c->hp + 2048, sizeof(int));
+    return SFAIRSC_OK;
   }
 };
 
 extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, double* evals_out, double* evecs_out,
                                        int32_t evecs_memspace, sfairsc_stats* stats) {
   const double t0 = now_s();
+  if (c && c->debug) fprintf(stderr, "[sfairsc] eigs enter k=%d tol=%g\n", k, tol);
   if (!c || !evals_out) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
   if (k < 1 || k > c->k_build) return fail(SFAIRSC_E_K_TOO_LARGE, "k=%d must be in [1, build k=%d]", k, c->k_build);
   if ((int64_t)k > (int64_t)c->n - c->h + 1) return fail(SFAIRSC_E_K_TOO_LARGE, "k > n-h+1");
@@ -754,61 +822,81 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
   L.arrow.assign(L.m + 1, 0.0);
   const double tol_eff = std::min(tol, c->tol_cap);
   const double target = tol_eff * c->sigma;
-  const double bd_tol = std::min(1e-12, 0.01 * tol_eff) * c->sigma;
+  L.bd_tol = std::min(1e-12, 0.01 * tol_eff) * c->sigma;
   const int n = c->n;
+  CU(cudaMemsetAsync(c->flags + 1, 0, sizeof(int), c->st));
 
-  // start vector v_0 = P r / |P r|, r from Philox stream 7
-  double b0;
+  // start vector v_0 = P u / |P u|, u from Philox stream 7
   L.inject = 0;
-  TRY(L.random_vector(0, true, &b0));
-  int j = 0;
+  if (c->debug) fprintf(stderr, "[sfairsc] eigs start m=%d keep=%d\n", L.m, L.keep);
+  TRY(L.random_vector(0, true));
+  if (c->debug) fprintf(stderr, "[sfairsc] start vector ok\n");
+  int j = 0;       // column being expanded
+  int jsync = 0;   // first T index not yet fetched
   bool converged = false, complete = false;
   std::vector<double> theta, Y;
   int m_eff = 0;
   double gap = std::numeric_limits<double>::quiet_NaN();
-  double last_maxres = 0.0;
   for (;;) {
-    // ---- expand column j: r = L^sigma v_j, CGS2 against V[:, 0:j+1] ----
+    // ---- expand column j: r = L^sigma v_j, CGS2 against V[:, 0:j+1], v_{j+1} = r/|r| ----
+    // (no host synchronisation inside the expansion; breakdowns are detected at the next sync)
     {
-      ProfScope ps(c, K_SPMV);
+      ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
       launch_spmv(c->g(), c->vs, c->row_split, c->spmv_grid, c->vp, c->vt, c->partials, c->counters + 1, c->bs_t,
                   c->st);
     }
     if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
     TRY(L.cgs2(j + 1, true));
-    double nrm2, a;
-    TRY(L.fetch(j, &nrm2, &a));
+    TRY(L.normalize_step(j));
     L.applies++;
     L.steps++;
-    L.alpha[j] = a;
-    double b = std::sqrt(nrm2);
-    if (b <= bd_tol) {
-      L.breakdowns++;
-      L.beta[j] = 0.0;
-      if (j + 1 >= n) {
-        complete = true;
-        m_eff = j + 1;
-      } else {
-        double bb;
-        TRY(L.random_vector(j + 1, false, &bb));
-      }
-    } else {
-      L.beta[j] = b;
-      TRY(L.normalize_into(j + 1, b));
+    if (c->debug > 1) {
+      cudaError_t e = cudaStreamSynchronize(c->st);
+      fprintf(stderr, "[sfairsc] step j=%d done (%s)\n", j, cudaGetErrorString(e));
     }
     ++j;
-    if (!complete && j < L.m) continue;
-    if (!complete) m_eff = L.m;
+    if (j < L.m) continue;
+
+    // ---- sync: fetch T, handle a breakdown by rolling back to it ----
+    int flag = 0;
+    const int jfrom = jsync;  // T entries [jfrom, m) are new since the last sync
+    TRY(L.fetch_T(jsync, L.m, &flag));
+    if (c->debug)
+      fprintf(stderr, "[sfairsc] sync restarts=%lld jsync=%d m=%d pk=%d flag=%d steps=%lld\n", (long long)L.restarts,
+              jsync, L.m, L.pk, flag, (long long)L.steps);
+    jsync = L.m;
+    m_eff = L.m;
+    if (flag) {
+      int jb = -1;
+      for (int i = jfrom; i < L.m; ++i)
+        if (!(L.beta[i] > L.bd_tol)) {
+          jb = i;
+          break;
+        }
+      if (jb < 0) return fail(SFAIRSC_E_CUDA, "breakdown flag without a small beta");
+      if (c->debug) fprintf(stderr, "[sfairsc] breakdown at j=%d beta=%g\n", jb, L.beta[jb]);
+      L.breakdowns++;
+      L.beta[jb] = 0.0;
+      CU(cudaMemsetAsync(c->flags + 1, 0, sizeof(int), c->st));
+      if (jb + 1 >= n) {
+        complete = true;
+        m_eff = jb + 1;
+      } else {
+        TRY(L.random_vector(jb + 1, false));
+        j = jb + 1;
+        jsync = j;
+        if (j < L.m) continue;
+        m_eff = L.m;
+      }
+    }
 
     // ---- Rayleigh-Ritz on T (m_eff x m_eff): arrowhead + tridiagonal ----
     const int me = m_eff;
     std::vector<double> T((size_t)me * me, 0.0);
     for (int i = 0; i < me; ++i) T[(size_t)i * me + i] = L.alpha[i];
-    for (int i = 0; i < L.pk && i < me; ++i) {
-      if (L.pk < me) {
-        T[(size_t)i * me + L.pk] = L.arrow[i];
-        T[(size_t)L.pk * me + i] = L.arrow[i];
-      }
+    for (int i = 0; i < L.pk && L.pk < me; ++i) {
+      T[(size_t)i * me + L.pk] = L.arrow[i];
+      T[(size_t)L.pk * me + i] = L.arrow[i];
     }
     for (int i = L.pk; i + 1 < me; ++i) {
       T[(size_t)i * me + i + 1] = L.beta[i];
@@ -819,9 +907,11 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
     const double bm = complete ? 0.0 : L.beta[me - 1];
     double maxres = 0.0;
     for (int i = 0; i < k; ++i) maxres = std::max(maxres, std::fabs(bm * Y[(size_t)(me - 1) * me + i]));
-    last_maxres = maxres;
     if (k < me) gap = theta[k] - theta[k - 1];
     converged = complete || maxres <= target;
+    if (c->debug)
+      fprintf(stderr, "[sfairsc] RR me=%d maxres=%g target=%g theta0=%.17g theta_k-1=%.17g\n", me, maxres, target,
+              theta[0], theta[k - 1]);
     if (converged || L.restarts >= c->max_restarts) {
       // X = V[:, 0:me] Y[:, 0:k]
       std::vector<double> Yc((size_t)me * k);
@@ -829,7 +919,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
         for (int l = 0; l < me; ++l) Yc[(size_t)cc * me + l] = Y[(size_t)l * me + cc];
       CU(cudaMemcpyAsync(c->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, c->st));
       {
-        ProfScope ps(c, K_RITZ);
+        ProfScope ps(c, K_RITZ, (double)(me + k) * c->vb());
         launch_ritz(c->V, c->ldv, n, me, c->Ydev, k, c->X, c->st);
       }
       CHECK_LAUNCH();
@@ -842,7 +932,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
       for (int l = 0; l < me; ++l) Yc[(size_t)cc * me + l] = Y[(size_t)l * me + cc];
     CU(cudaMemcpyAsync(c->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, c->st));
     {
-      ProfScope ps(c, K_RITZ);
+      ProfScope ps(c, K_RITZ, (double)(me + pk) * c->vb());
       launch_ritz(c->V, c->ldv, n, me, c->Ydev, pk, c->Vb, c->st);
     }
     CU(cudaMemcpyAsync(c->Vb + (long long)pk * c->ldv, c->V + (long long)me * c->ldv, sizeof(double) * c->ldv,
@@ -855,6 +945,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
     }
     L.pk = pk;
     j = pk;
+    jsync = pk;
     L.restarts++;
   }
 
@@ -903,7 +994,6 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
   S.kept = L.keep;
   c->last = S;
   if (stats) *stats = S;
-  (void)last_maxres;
   if (!converged) return fail(SFAIRSC_E_NO_CONVERGENCE, "no convergence after %lld restarts", (long long)L.restarts);
   if (theta[k - 1] >= c->sigma * (1.0 - 1e-8))
     return fail(SFAIRSC_E_SHIFT_TOO_SMALL, "lambda_k=%g >= sigma(1-1e-8)=%g (Prop. 3.4)", theta[k - 1], c->sigma);
@@ -917,6 +1007,8 @@ extern "C" sfairsc_status sfairsc_embed_kmeans(sfairsc_ctx* c, uint64_t seed, in
   if (memspace != SFAIRSC_MEM_HOST && memspace != SFAIRSC_MEM_DEVICE) return fail(SFAIRSC_E_INVALID_ARG, "memspace");
   return kmeans_run(c, seed, labels_out, memspace, objective_out);
 }
+
+extern "C" int64_t sfairsc_launch_count(void) { return (int64_t)launch_count(); }
 
 // host utility exported for tests of the Rayleigh-Ritz step
 extern "C" int sfairsc_host_symeig(int32_t m, const double* A, double* evals, double* evecs) {

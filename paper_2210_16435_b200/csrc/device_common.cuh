@@ -1,0 +1,109 @@
+// Device helpers shared by the libsfairsc kernel files (warp/block reductions,
+// last-CTA ticket finalisation, factored-projector coefficients, Philox).
+#pragma once
+#include "kernels.cuh"
+
+namespace sfz {
+
+// ----------------------------------------------------------------------------
+// helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// streaming (read-once) loads: bypass L1 allocation, read-only path
+__device__ __forceinline__ int ld_stream(const int* p) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// Block-wide fixed-order reduction of NV per-thread values; thread q < NV
+// writes the CTA partial to out[q].
+template <int NV>
+__device__ __forceinline__ void block_reduce_store(const double (&v)[NV], double* out) {
+  __shared__ double red[kThreads / 32][NV];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const double x = warp_sum(v[q]);
+    if (lane == 0) red[w][q] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double acc = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kThreads / 32; ++ww) acc += red[ww][threadIdx.x];
+    out[threadIdx.x] = acc;
+  }
+}
+
+// Last-CTA-done finalisation: the CTA that takes the last ticket sums the
+// grid's partial rows [gridDim.x][NV] in a fixed order and writes out[q]
+// for q < nout.  Resets the ticket for the next launch.
+template <int NV>
+__device__ __forceinline__ void ticket_finalize(const double* partials, unsigned* counter, double* out, int nout) {
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int q = w; q < nout; q += kThreads / 32) {
+    double acc = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(partials + (size_t)b * NV + q);
+    acc = warp_sum(acc);
+    if (lane == 0) out[q] = acc;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// gam[s] for the factored projector; executed by thread 0, result in smem.
+__device__ __forceinline__ void gamma_serial(const double* bsum, double scale, const ProjDesc& pd, double* gam) {
+  double pi = 0.0;
+  for (int s = 0; s < pd.h; ++s) {
+    const double c = scale * bsum[s] * pd.isb[s];
+    gam[s] = c;
+    pi = fma(pd.uh[s], c, pi);
+  }
+  for (int s = 0; s < pd.h; ++s) gam[s] = (gam[s] - pd.uh[s] * pi) * pd.isb[s];
+}
+
+__device__ __forceinline__ void add_group(double (&acc)[kHB], int g, double v) {
+#pragma unroll
+  for (int q = 0; q < kHB; ++q)
+    if (q == g) acc[q] += v;
+}
+
+// Philox4x32-10 (Salmon et al. SC'11), device implementation.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+  const unsigned M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k.x += W0;
+      k.y += W1;
+    }
+    const unsigned hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    const unsigned hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+__device__ __forceinline__ double philox_uniform(uint64_t seed, unsigned c0, unsigned c1, unsigned c2, unsigned c3) {
+  const uint4 x = philox4x32_10(make_uint4(c0, c1, c2, c3), make_uint2((unsigned)seed, (unsigned)(seed >> 32)));
+  return ((double)(x.x >> 5) * 67108864.0 + (double)(x.y >> 6)) / 9007199254740992.0;
+}
+
+
+}  // namespace sfz

@@ -13,111 +13,18 @@
 // All reductions are two-stage with a fixed partition and fixed order (no
 // floating-point atomics), so results are bitwise reproducible per GPU.
 #include "kernels.cuh"
+#include "device_common.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 
 namespace sfz {
 
-// ----------------------------------------------------------------------------
-// helpers
-// ----------------------------------------------------------------------------
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// streaming (read-once) loads: bypass L1 allocation, read-only path
-__device__ __forceinline__ int ld_stream(const int* p) {
-  int v;
-  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ double ld_stream(const double* p) {
-  double v;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-
-// Block-wide fixed-order reduction of NV per-thread values; thread q < NV
-// writes the CTA partial to out[q].
-template <int NV>
-__device__ __forceinline__ void block_reduce_store(const double (&v)[NV], double* out) {
-  __shared__ double red[kThreads / 32][NV];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    const double x = warp_sum(v[q]);
-    if (lane == 0) red[w][q] = x;
-  }
-  __syncthreads();
-  if (threadIdx.x < NV) {
-    double acc = 0.0;
-#pragma unroll
-    for (int ww = 0; ww < kThreads / 32; ++ww) acc += red[ww][threadIdx.x];
-    out[threadIdx.x] = acc;
-  }
-}
-
-// Last-CTA-done finalisation: the CTA that takes the last ticket sums the
-// grid's partial rows [gridDim.x][NV] in a fixed order and writes out[q]
-// for q < nout.  Resets the ticket for the next launch.
-template <int NV>
-__device__ __forceinline__ void ticket_finalize(const double* partials, unsigned* counter, double* out, int nout) {
-  __shared__ unsigned s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1) ? 1u : 0u;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int q = w; q < nout; q += kThreads / 32) {
-    double acc = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(partials + (size_t)b * NV + q);
-    acc = warp_sum(acc);
-    if (lane == 0) out[q] = acc;
-  }
-  if (threadIdx.x == 0) *counter = 0u;
-}
-
-// gam[s] for the factored projector; executed by thread 0, result in smem.
-__device__ __forceinline__ void gamma_serial(const double* bsum, double scale, const ProjDesc& pd, double* gam) {
-  double pi = 0.0;
-  for (int s = 0; s < pd.h; ++s) {
-    const double c = scale * bsum[s] * pd.isb[s];
-    gam[s] = c;
-    pi = fma(pd.uh[s], c, pi);
-  }
-  for (int s = 0; s < pd.h; ++s) gam[s] = (gam[s] - pd.uh[s] * pi) * pd.isb[s];
-}
-
-__device__ __forceinline__ void add_group(double (&acc)[kHB], int g, double v) {
-#pragma unroll
-  for (int q = 0; q < kHB; ++q)
-    if (q == g) acc[q] += v;
-}
-
-// Philox4x32-10 (Salmon et al. SC'11), device implementation.
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
-  const unsigned M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    if (r > 0) {
-      k.x += W0;
-      k.y += W1;
-    }
-    const unsigned hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
-    const unsigned hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-  }
-  return c;
-}
-__device__ __forceinline__ double philox_uniform(uint64_t seed, unsigned c0, unsigned c1, unsigned c2, unsigned c3) {
-  const uint4 x = philox4x32_10(make_uint4(c0, c1, c2, c3), make_uint2((unsigned)seed, (unsigned)(seed >> 32)));
-  return ((double)(x.x >> 5) * 67108864.0 + (double)(x.y >> 6)) / 9007199254740992.0;
-}
+static std::atomic<long long> g_nlaunch{0};
+static inline void bump() { g_nlaunch.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_nlaunch.load(); }
+void bump_launch() { bump(); }
 
 static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
@@ -449,18 +356,35 @@ __global__ void k_reduce_cols(const double* __restrict__ partials, int G, int J,
   }
 }
 
+// v_{j+1} = r / beta, p = P v_{j+1} (factored), B^T v_{j+1} = B^T r / beta.
+// beta = sqrt(|r|^2) is taken from device memory (no host round trip); block 0
+// records T entries alpha_j = c1[j] + c2[j], beta_j and flags a breakdown
+// (beta <= bd_tol: invariant subspace, handled by the host at the next sync).
 template <bool NORM>
 __global__ void __launch_bounds__(kThreads) k_normalize(GraphDev g, ProjDesc pd, const double* __restrict__ r,
-                                                        double beta, const double* bsum_r, double* __restrict__ v,
-                                                        double* bsum_v, double* __restrict__ p) {
+                                                        NormArgs na, double* __restrict__ v, double* bsum_v,
+                                                        double* __restrict__ p) {
   __shared__ double gam[256];
-  const double inv = 1.0 / beta;
-  if (threadIdx.x == 0) gamma_serial(bsum_r, inv, pd, gam);
-  if (blockIdx.x == 0)
-    for (int s = threadIdx.x; s < pd.h; s += blockDim.x) bsum_v[s] = bsum_r[s] * inv;
+  __shared__ double s_inv;
+  if (threadIdx.x == 0) {
+    double beta = na.beta_host > 0 ? na.beta_host : sqrt(na.nb[0]);
+    if (na.alpha_dev) {
+      if (blockIdx.x == 0) {
+        na.alpha_dev[na.j] = na.c1[na.j] + na.c2[na.j];
+        na.beta_dev[na.j] = beta;
+        if (!(beta > na.bd_tol)) atomicOr(na.flag, 1);
+      }
+    }
+    if (!(beta > na.bd_tol)) beta = 1.0;  // breakdown: column is garbage, rolled back by the host
+    s_inv = 1.0 / beta;
+    gamma_serial(na.nb + 1, s_inv, pd, gam);
+  }
   __syncthreads();
+  const double inv = s_inv;
+  if (blockIdx.x == 0)
+    for (int s = threadIdx.x; s < pd.h; s += blockDim.x) bsum_v[s] = na.nb[1 + s] * inv;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
-    const double vi = r[i] / beta;
+    const double vi = r[i] * inv;
     v[i] = vi;
     const double gi = gam[g.grp[i]];
     p[i] = NORM ? fma(-g.s[i], gi, vi) : vi - gi;
@@ -533,26 +457,33 @@ static int stream_grid(int n) { return std::max(1, std::min(cdiv(n, kThreads), n
 static int reduce_grid(int n) { return std::max(1, std::min(cdiv(n, 4 * kThreads), num_sms_cached() * 2)); }
 
 void launch_validate_csr(const GraphDev& g, int check_sym, int* flags, cudaStream_t st) {
+  bump();
   k_validate<<<stream_grid(g.n), kThreads, 0, st>>>(g, check_sym, flags);
 }
 void launch_degrees(const GraphDev& g, double* d, int* flags, cudaStream_t st) {
+  bump();
   k_degrees<<<stream_grid(g.n), kThreads, 0, st>>>(g, d, flags);
 }
 void launch_inv_sqrt(const double* d, double* s, int n, cudaStream_t st) {
+  bump();
   k_inv_sqrt<<<stream_grid(n), kThreads, 0, st>>>(d, s, n);
 }
 void launch_scale_values(const int* rp, const int* ci, double* vv, const double* s, int n, cudaStream_t st) {
+  bump();
   k_scale_values<<<stream_grid(n), kThreads, 0, st>>>(rp, ci, vv, s, n);
 }
 void launch_sigma(const GraphDev& g, double* partials, unsigned* counter, double* out, cudaStream_t st) {
+  bump();
   k_sigma<<<reduce_grid(g.n), kThreads, 0, st>>>(g, partials, counter, out);
 }
 void launch_group_check(const int32_t* groups, int n, int h, uint8_t* grp, int* flags, cudaStream_t st) {
+  bump();
   k_group_check<<<stream_grid(n), kThreads, 0, st>>>(groups, n, h, grp, flags);
 }
 
 void launch_gsum(const GraphDev& g, const double* x, int g_base, double* partials, unsigned* counter, double* bsum,
                  cudaStream_t st) {
+  bump();
   // bsum points at the h-array base; groups [g_base, g_base+16) are written
   const int G = reduce_grid(g.n);
   const int nout = kHB;  // caller guarantees room for kHB entries past g_base
@@ -563,6 +494,7 @@ void launch_gsum(const GraphDev& g, const double* x, int g_base, double* partial
 }
 void launch_project(const GraphDev& g, const ProjDesc& pd, const double* x, const double* bsum, double scale,
                     double* p, cudaStream_t st) {
+  bump();
   if (g.normalized)
     k_project<true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, x, bsum, scale, p);
   else
@@ -571,6 +503,7 @@ void launch_project(const GraphDev& g, const ProjDesc& pd, const double* x, cons
 
 void launch_finish(const GraphDev& g, const ProjDesc& pd, const double* t, const double* bsum_t,
                    const double* bsum_w, double sigma, double* y, cudaStream_t st) {
+  bump();
   if (g.normalized)
     k_finish<true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_w, sigma, y);
   else
@@ -587,6 +520,7 @@ static void spmv_vs(const GraphDev& g, const int* row_split, int grid, const dou
 }
 void launch_spmv(const GraphDev& g, int vs, const int* row_split, int grid, const double* p, double* t,
                  double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
+  bump();
   switch (vs) {
     case 2: spmv_vs<2>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
     case 4: spmv_vs<4>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
@@ -615,6 +549,7 @@ static void sweep_n(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, i
   else sweep_m<MODE, false>(g, pd, a, grid, st);
 }
 void launch_sweep(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  bump();
   switch (mode) {
     case 0: sweep_n<0>(g, pd, a, grid, st); break;
     case 1: sweep_n<1>(g, pd, a, grid, st); break;
@@ -624,16 +559,19 @@ void launch_sweep(int mode, const GraphDev& g, const ProjDesc& pd, const SweepAr
 }
 void launch_reduce_cols(const double* partials, int G, int J, double* out, cudaStream_t st) {
   if (J <= 0) return;
+  bump();
   k_reduce_cols<<<J, 128, 0, st>>>(partials, G, J, out);
 }
-void launch_normalize(const GraphDev& g, const ProjDesc& pd, const double* r, double beta, const double* bsum_r,
-                      double* vout, double* bsum_v, double* p, cudaStream_t st) {
+void launch_normalize(const GraphDev& g, const ProjDesc& pd, const double* r, const NormArgs& na, double* vout,
+                      double* bsum_v, double* p, cudaStream_t st) {
+  bump();
   if (g.normalized)
-    k_normalize<true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, r, beta, bsum_r, vout, bsum_v, p);
+    k_normalize<true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, r, na, vout, bsum_v, p);
   else
-    k_normalize<false><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, r, beta, bsum_r, vout, bsum_v, p);
+    k_normalize<false><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, r, na, vout, bsum_v, p);
 }
 void launch_random(double* x, int n, uint64_t seed, unsigned c1, unsigned stream, cudaStream_t st) {
+  bump();
   k_random<<<stream_grid(n), kThreads, 0, st>>>(x, n, seed, c1, stream);
 }
 
@@ -646,22 +584,15 @@ static void ritz_pc(const double* V, long long ld, int n, int m, const double* Y
     attr_set = true;
   }
   const int grid = std::max(1, std::min(cdiv(n, 64), num_sms_cached() * 2));
+  bump();
   k_ritz<PC><<<grid, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
 }
 void launch_ritz(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout, cudaStream_t st) {
-  // column tiles so that the Y tile fits the shared-memory budget
-  const int max_cols = std::max(1, std::min(4 * 32, (int)((96 * 1024) / (sizeof(double) * std::max(m, 1)))));
-  for (int c0 = 0; c0 < p; c0 += max_cols) {
-    const int pc = std::min(max_cols, p - c0);
-    const double* Yt = Y + (size_t)c0 * m;
-    double* Vo = Vout + (long long)c0 * ld;
-    if (pc <= 32) ritz_pc<8>(V, ld, n, m, Yt, pc, Vo, st);
-    else if (pc <= 64) ritz_pc<16>(V, ld, n, m, Yt, pc, Vo, st);
-    else ritz_pc<32>(V, ld, n, m, Yt, pc, Vo, st);
-  }
+  launch_ritz_rb(V, ld, n, m, Y, p, Vout, st);
 }
 void launch_resid(const double* y, const double* x, double theta, int n, double* partials, unsigned* counter,
                   double* out, cudaStream_t st) {
+  bump();
   k_resid<<<reduce_grid(n), kThreads, 0, st>>>(y, x, theta, n, partials, counter, out);
 }
 

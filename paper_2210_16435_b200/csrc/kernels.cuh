@@ -76,12 +76,34 @@ struct SweepArgs {
   double* norm_bsum;   // mode 2 output: [0] = |r''|^2, [1..17) = B^T r''
 };
 int sweep_grid(int n, int num_sms);
+long long launch_count();  // kernels launched by this process so far
 void launch_sweep(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st);
+// TMA-fed persistent sweeps (krylov.cu); J <= 192, grid <= #SMs
+extern int g_tma_use2d;  // 1: 2-D tensor-map TMA per chunk (default); 0: one 1-D bulk copy per column
+bool sweep_tma_ok(int J);  // also the J limit of the smem-staged sweeps
+int sweep_smem_grid(int n, int J, int num_sms);
+void launch_sweep_smem(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid,
+                       cudaStream_t st);
+int sweep_tma_grid(int n, int num_sms);
+void launch_sweep_tma(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st);
+void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout,
+                    cudaStream_t st);
 // out[l] = sum_b partials[b*J + l], fixed order
 void launch_reduce_cols(const double* partials, int G, int J, double* out, cudaStream_t st);
 // v = r / beta -> vout ; bsum_v = bsum_r / beta ; p = v - s o gam(bsum_v)
-void launch_normalize(const GraphDev& g, const ProjDesc& pd, const double* r, double beta, const double* bsum_r,
-                      double* vout, double* bsum_v, double* p, cudaStream_t st);
+struct NormArgs {
+  const double* nb;   // [0] = |r|^2, [1..1+h) = B^T r
+  double beta_host;   // > 0: use this beta instead of sqrt(nb[0])
+  double bd_tol;      // beta <= bd_tol -> breakdown flag
+  int j;              // Lanczos index: records alpha_dev[j], beta_dev[j]
+  const double* c1;   // CGS coefficients (alpha_j = c1[j] + c2[j])
+  const double* c2;
+  double* alpha_dev;  // nullptr: do not record
+  double* beta_dev;
+  int* flag;
+};
+void launch_normalize(const GraphDev& g, const ProjDesc& pd, const double* r, const NormArgs& na, double* vout,
+                      double* bsum_v, double* p, cudaStream_t st);
 // x_i = u_i - 1/2, u = Philox4x32-10(key=seed, ctr=(i, c1, stream, 0))
 void launch_random(double* x, int n, uint64_t seed, unsigned c1, unsigned stream, cudaStream_t st);
 // Vout[:, c] = sum_l V[:, l] Y[l, c]   (c < p, l < m), Y column-major m x p on device

@@ -1,0 +1,520 @@
+// libsfairsc — TMA-fed reorthogonalisation sweeps and the Ritz GEMM (sm_100a).
+//
+// Sweeps (the dominant per-step cost at large k):
+// a persistent CTA per SM walks 64-row chunks of the Krylov basis V
+// (column-major, ld = ldv).  For each chunk, warp 0 issues one 1-D bulk copy
+// (cp.async.bulk, the TMA engine) per basis column plus one for the vector
+// chunk into a 2-stage shared-memory ring guarded by mbarriers
+// (complete_tx), so the basis is streamed from HBM exactly once per sweep and
+// both the update r' = r - V c and the dots V^T r' of the fused CGS2 sweep
+// read it from shared memory.
+//
+// Ritz GEMM (A10): Vout = V Y, register-blocked fp64 FMA (8 rows x 4 cols per
+// thread, 128 x 64 CTA tiles, k-chunks of 16 staged in shared memory).
+#include "device_common.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+
+namespace sfz {
+
+namespace {
+
+constexpr int kR = 64;       // rows per chunk
+constexpr int kMaxStages = 8;                // smem ring depth (runtime: as many as fit)
+constexpr int kTmaMaxJ = 192;
+constexpr size_t kRingBytes = 200 * 1024;    // dynamic shared memory budget for the ring
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tensor2d_g2s(void* dst, const CUtensorMap* tmap, int x, int y, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// issue chunk `c` into stage buffer `buf` (warp 0): one 2-D tensor copy of the
+// (64 rows x J columns) basis box + one 1-D copy of the vector chunk, or (use2d
+// == 0) one 1-D copy per column.
+// stage layout (doubles): [J][kR] basis | x[kR] | s[kR] | grp[kR bytes, padded to 128 B]
+// (every stage starts 128-byte aligned: required by the 2-D tensor copy destination)
+__host__ __device__ __forceinline__ size_t stage_doubles(int J) { return (size_t)(J + 2) * kR + 16; }
+
+__device__ __forceinline__ void issue_chunk(const SweepArgs& a, const GraphDev& g, bool need_sg, const CUtensorMap* tmap,
+                                            int use2d, int c, double* buf, unsigned long long* bar, int lane) {
+  const int J = a.J;
+  const long long row0 = (long long)c * kR;
+  const bool with_s = need_sg && g.normalized;
+  unsigned bytes = (unsigned)((J + 1) * kR * sizeof(double));
+  if (need_sg) bytes += kR;                                   // group ids
+  if (with_s) bytes += kR * sizeof(double);                   // s = d^{-1/2}
+  if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+  __syncwarp();
+  if (lane == 1 && need_sg) {
+    bulk_g2s(buf + (size_t)(J + 2) * kR, g.grp + row0, kR, bar);
+    if (with_s) bulk_g2s(buf + (size_t)(J + 1) * kR, g.s + row0, kR * sizeof(double), bar);
+  }
+  if (use2d) {
+    if (lane == 0) {
+      tensor2d_g2s(buf, tmap, (int)row0, 0, bar);
+      bulk_g2s(buf + (size_t)J * kR, a.xin + row0, kR * sizeof(double), bar);
+    }
+    return;
+  }
+  for (int l = lane; l <= J; l += 32) {
+    const double* src = (l < J) ? a.V + (long long)l * a.ld + row0 : a.xin + row0;
+    bulk_g2s(buf + (size_t)l * kR, src, kR * sizeof(double), bar);
+  }
+}
+
+}  // namespace
+
+// MODE 0: r = t - s o gam_g, dots V^T r ; 1: r' = r - V c, dots V^T r' ;
+// 2: r'' = r - V c, |r''|^2 and B^T r'' (ticket) ; 3: dots V^T x.
+template <int MODE, int MAXCW, bool NORM>
+__global__ void __launch_bounds__(kThreads, 1) k_sweep_tma(GraphDev g, ProjDesc pd, SweepArgs a, int kStages,
+                                                                 const __grid_constant__ CUtensorMap tmap, int use2d) {
+  extern __shared__ __align__(128) double dsm[];  // [kStages][(J+1) * kR]
+  __shared__ __align__(8) unsigned long long bars[kMaxStages];
+  __shared__ double coef[kTmaMaxJ];
+  __shared__ double red[4][kR];
+  __shared__ double rs[kR];
+  __shared__ double gam[256];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int n = g.n, J = a.J;
+  const int nchunks = (n + kR - 1) / kR;
+  const size_t stage_elems = stage_doubles(J);
+  constexpr bool kNeedSG = (MODE == 0 || MODE == 2);
+
+  if (MODE == 1 || MODE == 2)
+    for (int l = tid; l < J; l += kThreads) coef[l] = a.coef[l];
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (MODE == 0) {
+      __shared__ double gw[256];
+      gamma_serial(a.bsum_t, 1.0, pd, gam);
+      gamma_serial(a.bsum_w, 1.0, pd, gw);
+      for (int s = 0; s < pd.h; ++s) gam[s] = gam[s] - a.sigma * gw[s];
+    }
+  }
+  __syncthreads();
+
+  // chunks of this CTA: c = blockIdx.x + it * gridDim.x
+  const int my_chunks = (nchunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  if (w == 0) {
+    for (int it = 0; it < kStages && it < my_chunks; ++it)
+      issue_chunk(a, g, kNeedSG, &tmap, use2d, blockIdx.x + it * gridDim.x, dsm + it * stage_elems, &bars[it], lane);
+  }
+
+  double colacc[MAXCW];
+#pragma unroll
+  for (int cc = 0; cc < MAXCW; ++cc) colacc[cc] = 0.0;
+  double gacc[kHB];
+#pragma unroll
+  for (int q = 0; q < kHB; ++q) gacc[q] = 0.0;
+  double nrm = 0.0;
+
+  for (int it = 0; it < my_chunks; ++it) {
+    const int c = blockIdx.x + it * gridDim.x;
+    const int st = it % kStages;
+    const double* buf = dsm + st * stage_elems;
+    mbar_wait(&bars[st], (unsigned)((it / kStages) & 1));
+    const double* xs = buf + (size_t)J * kR;  // vector chunk
+    const double* ss = xs + kR;                 // s chunk (normalized, modes 0/2)
+    const uint8_t* gs = reinterpret_cast<const uint8_t*>(ss + kR);  // group ids (modes 0/2)
+    const int row0 = c * kR;
+
+    // ---- phase 1: row-wise work ----
+    if (MODE == 1 || MODE == 2) {
+      const int i = tid % kR, cg = tid / kR;  // 4 column groups
+      double part = 0.0;
+      for (int l = cg; l < J; l += 4) part = fma(buf[(size_t)l * kR + i], coef[l], part);
+      red[cg][i] = part;
+      __syncthreads();
+      if (tid < kR) {
+        const int gi = row0 + tid;
+        double x = 0.0;
+        if (gi < n) {
+          x = xs[tid] - (((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid]);
+          a.xout[gi] = x;
+          if (MODE == 2) {
+            nrm = fma(x, x, nrm);
+            add_group(gacc, gs[tid], NORM ? ss[tid] * x : x);
+          }
+        }
+        rs[tid] = x;
+      }
+    } else if (MODE == 0) {
+      if (tid < kR) {
+        const int gi = row0 + tid;
+        double x = 0.0;
+        if (gi < n) {
+          x = NORM ? fma(-ss[tid], gam[gs[tid]], xs[tid]) : xs[tid] - gam[gs[tid]];
+          a.xout[gi] = x;
+        }
+        rs[tid] = x;
+      }
+    } else {  // MODE 3
+      if (tid < kR) rs[tid] = (row0 + tid < n) ? xs[tid] : 0.0;
+    }
+    __syncthreads();
+
+    // ---- phase 2: dots V[chunk, l]^T r  (lane-level partials) ----
+    if (MODE != 2) {
+      const double r0 = rs[lane], r1 = rs[lane + 32];
+#pragma unroll
+      for (int cc = 0; cc < MAXCW; ++cc) {
+        const int l = w + cc * (kThreads / 32);
+        if (l < J) {
+          const double* col = buf + (size_t)l * kR;
+          colacc[cc] = fma(col[lane], r0, colacc[cc]);
+          colacc[cc] = fma(col[lane + 32], r1, colacc[cc]);
+        }
+      }
+    }
+    __syncthreads();  // stage `st` fully consumed
+    if (w == 0 && it + kStages < my_chunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_chunk(a, g, kNeedSG, &tmap, use2d, blockIdx.x + (it + kStages) * gridDim.x, dsm + st * stage_elems,
+                  &bars[st], lane);
+    }
+  }
+
+  if (MODE != 2) {
+#pragma unroll
+    for (int cc = 0; cc < MAXCW; ++cc) {
+      const int l = w + cc * (kThreads / 32);
+      if (l < J) {
+        const double s = warp_sum(colacc[cc]);
+        if (lane == 0) a.partials[(size_t)blockIdx.x * J + l] = s;
+      }
+    }
+  } else {
+    double v[1 + kHB];
+    v[0] = nrm;
+#pragma unroll
+    for (int q = 0; q < kHB; ++q) v[1 + q] = gacc[q];
+    block_reduce_store<1 + kHB>(v, a.partials + (size_t)blockIdx.x * (1 + kHB));
+    ticket_finalize<1 + kHB>(a.partials, a.counter, a.norm_bsum, 1 + min(pd.h, kHB));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory-staged sweeps for the dots-type modes (0: finish + dots,
+// 1: update + dots, 3: dots).  Each CTA walks 64-row chunks; phase A loads the
+// chunk of the J basis columns with plain coalesced loads (4 column groups x
+// 64 rows; ~J/4 independent loads in flight per thread) into shared memory
+// (mode 1 also forms the update partials on the fly); phase B forms the dots
+// from shared memory, so every basis element is read from HBM exactly once.
+// Several CTAs per SM overlap one CTA's loads with another's dots.
+// ---------------------------------------------------------------------------
+template <int MODE, int MAXCW, bool NORM>
+__global__ void __launch_bounds__(kThreads) k_sweep_smem(GraphDev g, ProjDesc pd, SweepArgs a) {
+  extern __shared__ __align__(16) double Vs[];  // [J][kR]
+  __shared__ double coef[kTmaMaxJ];
+  __shared__ double red[4][kR];
+  __shared__ double rs[kR];
+  __shared__ double gam[256];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int n = g.n, J = a.J;
+  const long long ld = a.ld;
+  if (MODE == 1)
+    for (int l = tid; l < J; l += kThreads) coef[l] = a.coef[l];
+  if (MODE == 0 && tid == 0) {
+    __shared__ double gw[256];
+    gamma_serial(a.bsum_t, 1.0, pd, gam);
+    gamma_serial(a.bsum_w, 1.0, pd, gw);
+    for (int s = 0; s < pd.h; ++s) gam[s] = gam[s] - a.sigma * gw[s];
+  }
+  __syncthreads();
+  const int nchunks = (n + kR - 1) / kR;
+  const int c0 = (int)((long long)nchunks * blockIdx.x / gridDim.x);
+  const int c1 = (int)((long long)nchunks * (blockIdx.x + 1) / gridDim.x);
+  double colacc[MAXCW];
+#pragma unroll
+  for (int cc = 0; cc < MAXCW; ++cc) colacc[cc] = 0.0;
+  const int i = tid % kR, cg = tid / kR;
+  for (int c = c0; c < c1; ++c) {
+    const long long row0 = (long long)c * kR;
+    // ---- phase A: stage V[chunk, 0:J] (and the mode-1 update partials) ----
+    {
+      const double* __restrict__ vp = a.V + row0 + i;
+      double part = 0.0;
+      int l = cg;
+      for (; l + 12 < J; l += 16) {
+        const double v0 = vp[(long long)l * ld], v1 = vp[(long long)(l + 4) * ld];
+        const double v2 = vp[(long long)(l + 8) * ld], v3 = vp[(long long)(l + 12) * ld];
+        Vs[l * kR + i] = v0;
+        Vs[(l + 4) * kR + i] = v1;
+        Vs[(l + 8) * kR + i] = v2;
+        Vs[(l + 12) * kR + i] = v3;
+        if (MODE == 1) {
+          part = fma(v0, coef[l], part);
+          part = fma(v1, coef[l + 4], part);
+          part = fma(v2, coef[l + 8], part);
+          part = fma(v3, coef[l + 12], part);
+        }
+      }
+      for (; l < J; l += 4) {
+        const double v0 = vp[(long long)l * ld];
+        Vs[l * kR + i] = v0;
+        if (MODE == 1) part = fma(v0, coef[l], part);
+      }
+      if (MODE == 1) red[cg][i] = part;
+    }
+    if (MODE == 1) __syncthreads();
+    if (tid < kR) {
+      const long long gi = row0 + tid;
+      double x = 0.0;
+      if (gi < n) {
+        if (MODE == 0) {
+          x = NORM ? fma(-g.s[gi], gam[g.grp[gi]], a.xin[gi]) : a.xin[gi] - gam[g.grp[gi]];
+          a.xout[gi] = x;
+        } else if (MODE == 1) {
+          x = a.xin[gi] - (((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid]);
+          a.xout[gi] = x;
+        } else {
+          x = a.xin[gi];
+        }
+      }
+      rs[tid] = x;
+    }
+    __syncthreads();
+    // ---- phase B: dots from shared memory ----
+    const double r0 = rs[lane], r1 = rs[lane + 32];
+#pragma unroll
+    for (int cc = 0; cc < MAXCW; ++cc) {
+      const int l = w + cc * (kThreads / 32);
+      if (l < J) {
+        colacc[cc] = fma(Vs[l * kR + lane], r0, colacc[cc]);
+        colacc[cc] = fma(Vs[l * kR + lane + 32], r1, colacc[cc]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int cc = 0; cc < MAXCW; ++cc) {
+    const int l = w + cc * (kThreads / 32);
+    if (l < J) {
+      const double s = warp_sum(colacc[cc]);
+      if (lane == 0) a.partials[(size_t)blockIdx.x * J + l] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Ritz GEMM  Vout[:, c] = sum_l V[:, l] Y[l, c]
+// ---------------------------------------------------------------------------
+template <int TN>
+__global__ void __launch_bounds__(kThreads) k_ritz_rb(const double* __restrict__ V, long long ld, int n, int m,
+                                                      const double* __restrict__ Y, int p, double* __restrict__ Vout) {
+  constexpr int TM = 128, KC = 16, CPT = TN / 16;
+  __shared__ double As[KC][TM];
+  __shared__ double Bs[KC][TN];
+  const int col0 = blockIdx.x * TN;
+  const long long row0 = (long long)blockIdx.y * TM;
+  const int tid = threadIdx.x;
+  const int rg = tid % 16, cg = tid / 16;
+  double acc[8][CPT];
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc[q][c] = 0.0;
+  for (int k0 = 0; k0 < m; k0 += KC) {
+    for (int e = tid; e < KC * TM; e += kThreads) {
+      const int kk = e / TM, r = e % TM;
+      const int l = k0 + kk;
+      const long long i = row0 + r;
+      As[kk][r] = (l < m && i < n) ? V[(long long)l * ld + i] : 0.0;
+    }
+    for (int e = tid; e < KC * TN; e += kThreads) {
+      const int kk = e / TN, cc = e % TN;
+      const int l = k0 + kk, c = col0 + cc;
+      Bs[kk][cc] = (l < m && c < p) ? Y[(size_t)c * m + l] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      double av[8], bv[CPT];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) av[q] = As[kk][rg + 16 * q];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) bv[c] = Bs[kk][cg * CPT + c];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[q][c] = fma(av[q], bv[c], acc[q][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int col = col0 + cg * CPT + c;
+    if (col >= p) continue;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const long long i = row0 + rg + 16 * q;
+      if (i < n) Vout[(long long)col * ld + i] = acc[q][c];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+void bump_launch();
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// tensor map over V viewed as 2-D [J columns][ld rows] (fp64), box {64 rows, J columns}
+static bool encode_basis_map(const SweepArgs& a, CUtensorMap* m) {
+  auto fn = get_encode();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)a.ld, (cuuint64_t)a.J};
+  cuuint64_t strides[1] = {(cuuint64_t)a.ld * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)kR, (cuuint32_t)a.J};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(a.V), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_tma_use2d = 1;
+
+template <int MODE, int MAXCW, bool NORM>
+static void tma_launch(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  const size_t stage = stage_doubles(a.J) * sizeof(double);
+  const int stages = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, kRingBytes / stage));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep_tma<MODE, MAXCW, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(kRingBytes, 2 * stage_doubles(kTmaMaxJ) * sizeof(double)));
+    attr = true;
+  }
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  int use2d = g_tma_use2d && encode_basis_map(a, &tmap);
+  k_sweep_tma<MODE, MAXCW, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap, use2d);
+}
+
+template <int MODE, bool NORM>
+static void tma_m(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  if (a.J <= 64) tma_launch<MODE, 8, NORM>(g, pd, a, grid, st);
+  else if (a.J <= 128) tma_launch<MODE, 16, NORM>(g, pd, a, grid, st);
+  else tma_launch<MODE, 24, NORM>(g, pd, a, grid, st);
+}
+template <int MODE>
+static void tma_n(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  if (g.normalized) tma_m<MODE, true>(g, pd, a, grid, st);
+  else tma_m<MODE, false>(g, pd, a, grid, st);
+}
+
+template <int MODE, int MAXCW, bool NORM>
+static void smem_launch(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep_smem<MODE, MAXCW, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((size_t)kTmaMaxJ * kR * sizeof(double)));
+    attr = true;
+  }
+  k_sweep_smem<MODE, MAXCW, NORM><<<grid, kThreads, (size_t)a.J * kR * sizeof(double), st>>>(g, pd, a);
+}
+template <int MODE, bool NORM>
+static void smem_m(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  if (a.J <= 64) smem_launch<MODE, 8, NORM>(g, pd, a, grid, st);
+  else if (a.J <= 128) smem_launch<MODE, 16, NORM>(g, pd, a, grid, st);
+  else smem_launch<MODE, 24, NORM>(g, pd, a, grid, st);
+}
+template <int MODE>
+static void smem_n(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  if (g.normalized) smem_m<MODE, true>(g, pd, a, grid, st);
+  else smem_m<MODE, false>(g, pd, a, grid, st);
+}
+// grid: as many CTAs per SM as shared memory allows (<= 8), at most one chunk each
+int sweep_smem_grid(int n, int J, int num_sms) {
+  const size_t smem = (size_t)std::max(J, 1) * kR * sizeof(double) + 8 * 1024;
+  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / smem));
+  return std::max(1, std::min((n + kR - 1) / kR, num_sms * per_sm));
+}
+void launch_sweep_smem(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid,
+                       cudaStream_t st) {
+  bump_launch();
+  switch (mode) {
+    case 0: smem_n<0>(g, pd, a, grid, st); break;
+    case 1: smem_n<1>(g, pd, a, grid, st); break;
+    default: smem_n<3>(g, pd, a, grid, st); break;
+  }
+}
+
+bool sweep_tma_ok(int J) { return J >= 1 && J <= kTmaMaxJ; }
+int sweep_tma_grid(int n, int num_sms) { return std::max(1, std::min((n + kR - 1) / kR, num_sms)); }
+
+void launch_sweep_tma(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  bump_launch();
+  switch (mode) {
+    case 0: tma_n<0>(g, pd, a, grid, st); break;
+    case 1: tma_n<1>(g, pd, a, grid, st); break;
+    case 2: tma_n<2>(g, pd, a, grid, st); break;
+    default: tma_n<3>(g, pd, a, grid, st); break;
+  }
+}
+
+void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout,
+                    cudaStream_t st) {
+  if (p <= 0 || n <= 0) return;
+  bump_launch();
+  if (p <= 32) {
+    dim3 grid((p + 31) / 32, (n + 127) / 128);
+    k_ritz_rb<32><<<grid, kThreads, 0, st>>>(V, ld, n, m, Y, p, Vout);
+  } else {
+    dim3 grid((p + 63) / 64, (n + 127) / 128);
+    k_ritz_rb<64><<<grid, kThreads, 0, st>>>(V, ld, n, m, Y, p, Vout);
+  }
+}
+
+}  // namespace sfz

@@ -84,7 +84,9 @@ def _load():
         "sfairsc_laplacian": (C.c_int, [P, P, P, C.c_int32]),
         "sfairsc_get_info": (C.c_int, [P, C.POINTER(Info)]),
         "sfairsc_profile_enable": (C.c_int, [P, C.c_int32]),
-        "sfairsc_profile_read": (C.c_int, [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+        "sfairsc_profile_read": (C.c_int, [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_double)]),
+        "sfairsc_launch_count": (C.c_int64, []),
         "sfairsc_profile_reset": (C.c_int, [P]),
         "sfairsc_destroy": (None, [P]),
         "sfairsc_last_error": (C.c_char_p, []),
@@ -279,9 +281,15 @@ def profile_read(ctx: Context) -> dict:
     for name, kind in PROFILE_KINDS.items():
         ms = C.c_double()
         cnt = C.c_int64()
-        _check(_lib.sfairsc_profile_read(ctx.handle, kind, C.byref(ms), C.byref(cnt)))
-        out[name] = {"ms": ms.value, "launches": cnt.value}
+        by = C.c_double()
+        _check(_lib.sfairsc_profile_read(ctx.handle, kind, C.byref(ms), C.byref(cnt), C.byref(by)))
+        out[name] = {"ms": ms.value, "launches": cnt.value, "alg_bytes": by.value}
     return out
+
+
+def launch_count() -> int:
+    """Kernels launched by libsfairsc in this process."""
+    return int(_lib.sfairsc_launch_count())
 
 
 def host_symeig(A: np.ndarray):

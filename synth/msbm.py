@@ -41,6 +41,17 @@ import numpy as np
 _DENSE_PAIR_LIMIT = 30_000  # n at or below which every vertex pair is drawn
 
 
+def _sorted_unique(x: np.ndarray) -> np.ndarray:
+    """np.unique for int64 keys via sort (numpy's hash path is slow at 1e8)."""
+    x = np.sort(x)
+    if len(x) == 0:
+        return x
+    keep = np.empty(len(x), dtype=bool)
+    keep[0] = True
+    np.not_equal(x[1:], x[:-1], out=keep[1:])
+    return x[keep]
+
+
 def _rng(seed: int, stream: int) -> np.random.Generator:
     return np.random.default_rng(np.random.SeedSequence([int(seed), int(stream)]))
 
@@ -172,7 +183,7 @@ def _sample_sparse(n, cell, Pcell, seed):
         keep = u != v
         u, v = u[keep], v[keep]
         key = np.minimum(u, v) * n + np.maximum(u, v)
-        have = np.unique(np.concatenate([have, key]))
+        have = _sorted_unique(np.concatenate([have, key]))
         cnt = np.bincount(pair_id(cell[have // n].astype(np.int64), cell[have % n].astype(np.int64)),
                           minlength=len(A))
         need = M - cnt
@@ -187,9 +198,13 @@ def _to_csr(n, keys, w):
     u = keys // n
     v = keys % n
     k2 = np.concatenate([u * n + v, v * n + u])
-    idx = np.argsort(k2, kind="stable")
-    k2 = k2[idx]
-    val = np.concatenate([w, w])[idx]
+    if np.all(w == w[0]) if len(w) else True:
+        k2.sort()
+        val = np.full(len(k2), w[0] if len(w) else 1.0)
+    else:
+        idx = np.argsort(k2, kind="stable")
+        k2 = k2[idx]
+        val = np.concatenate([w, w])[idx]
     rows = k2 // n
     col = (k2 % n).astype(np.int32)
     row_ptr = np.zeros(n + 1, dtype=np.int64)
@@ -215,7 +230,7 @@ def _repair_isolated(n, keys, clusters, seed):
             pool = np.setdiff1d(np.arange(n), [vtx])
         o = int(pool[rng.integers(0, len(pool))])
         extra.append(min(o, vtx) * n + max(o, vtx))
-    keys = np.unique(np.concatenate([keys, np.asarray(extra, np.int64)]))
+    keys = _sorted_unique(np.concatenate([keys, np.asarray(extra, np.int64)]))
     return keys, len(iso)
 
 
