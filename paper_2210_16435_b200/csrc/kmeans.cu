@@ -1,9 +1,482 @@
-// placeholder: replaced by the GPU k-means (reading R16)
+// libsfairsc — k-means on the rows of H (Alg. 3 step 4), reading R16:
+// k-means++ seeding with Philox4x32-10 draws (key = seed, counter (t, r, 8, 0)),
+// Lloyd iterations (assignment ties -> lowest index; stop when no label
+// changes or 300 iterations), an empty cluster is re-seeded at the point
+// farthest from its assigned centroid, best of 10 restarts by WCSS.
+// Rows h_i = s_i X[i, :] (normalized, H = D^{-1/2} X) or X[i, :], read in place
+// from the column-major eigenvector block.  Squared distances are summed
+// over dimensions in index order without FMA contraction (same arithmetic
+// as the oracle's definition).  All reductions are fixed-order.
 #include "sfairsc.h"
-#include "kernels.cuh"
+#include "device_common.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <vector>
+
 namespace sfz {
+
+cudaStream_t ctx_stream(sfairsc_ctx* c);
+int ctx_n(sfairsc_ctx* c);
+int ctx_k(sfairsc_ctx* c);
+const double* ctx_X(sfairsc_ctx* c, long long* ld);
+const double* ctx_s(sfairsc_ctx* c);
+int ctx_num_sms(sfairsc_ctx* c);
+void** ctx_km(sfairsc_ctx* c, void (**freer)(void*));
+void ctx_set_km_free(sfairsc_ctx* c, void (*f)(void*));
 sfairsc_status ctx_fail(sfairsc_status st, const char* msg);
-sfairsc_status kmeans_run(sfairsc_ctx*, uint64_t, int32_t*, int32_t, double*) {
-  return ctx_fail(SFAIRSC_E_STATE, "embed_kmeans not built yet");
+void ctx_prof_begin(sfairsc_ctx* c, cudaEvent_t* a);
+void ctx_prof_end(sfairsc_ctx* c, int kind, cudaEvent_t a);
+void bump_launch();
+
+namespace {
+
+constexpr int kBlk = 1024;     // D2 prefix blocks
+constexpr int kMaxDim = 64;    // k <= 64 handled in registers
+constexpr int kKmStream = 8;   // Philox stream of the k-means draws
+
+__device__ __forceinline__ double hval(const double* X, long long ld, const double* s, int i, int d) {
+  const double x = X[(long long)d * ld + i];
+  return s ? s[i] * x : x;
 }
+
+// squared distance, dimensions in order, no FMA contraction
+template <int DP>
+__device__ __forceinline__ double sqdist(const double (&h)[DP], const double* mu, int dim) {
+  double acc = 0.0;
+#pragma unroll
+  for (int d = 0; d < DP; ++d)
+    if (d < dim) {
+      const double t = __dsub_rn(h[d], mu[d]);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+    }
+  return acc;
 }
+
+template <int DP>
+__device__ __forceinline__ void load_row(const double* X, long long ld, const double* s, int i, int dim, double (&h)[DP]) {
+#pragma unroll
+  for (int d = 0; d < DP; ++d) h[d] = d < dim ? hval(X, ld, s, i, d) : 0.0;
+}
+
+// D2_i = (init ? inf : D2_i) min |h_i - center|^2 ; per-block sums of D2 (fixed 1024-element blocks)
+template <int DP>
+__global__ void __launch_bounds__(256) k_d2(const double* X, long long ld, const double* s, int n, int dim,
+                                            const double* center, int init, double* D2, double* blocksum) {
+  __shared__ double red[256 / 32];
+  const int b = blockIdx.x;
+  double part = 0.0;
+  for (int q = 0; q < kBlk / 256; ++q) {
+    const int i = b * kBlk + q * 256 + threadIdx.x;
+    if (i < n) {
+      double h[DP];
+      load_row<DP>(X, ld, s, i, dim, h);
+      double v = sqdist<DP>(h, center, dim);
+      if (!init) v = fmin(v, D2[i]);
+      D2[i] = v;
+      part += v;  // order irrelevant for the block sum's use (search), but fixed
+    }
+  }
+  part = warp_sum(part);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 256 / 32; ++w) t += red[w];
+    blocksum[b] = t;
+  }
+}
+
+// smallest i in block b with (running prefix from `base`) > target, sequential
+__global__ void k_select_in_block(const double* D2, int b, int n, double base, double target, int* out) {
+  if (threadIdx.x != 0) return;
+  double cum = base;
+  int last_pos = -1;
+  const int i0 = b * kBlk, i1 = min(n, i0 + kBlk);
+  for (int i = i0; i < i1; ++i) {
+    const double v = D2[i];
+    cum += v;
+    if (v > 0) last_pos = i;
+    if (cum > target) {
+      *out = i;
+      return;
+    }
+  }
+  *out = last_pos >= 0 ? last_pos : i1 - 1;
+}
+
+__global__ void k_gather_row(const double* X, long long ld, const double* s, int i, int dim, double* out) {
+  for (int d = threadIdx.x; d < dim; d += blockDim.x) out[d] = hval(X, ld, s, i, d);
+}
+
+template <int DP>
+__global__ void __launch_bounds__(256) k_assign(const double* X, long long ld, const double* s, int n, int dim, int K,
+                                                const double* mu, const int* old_labels, int* labels, double* dist,
+                                                int* changes) {
+  extern __shared__ double smu[];
+  for (int e = threadIdx.x; e < K * dim; e += blockDim.x) smu[e] = mu[e];
+  __syncthreads();
+  int ch = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double h[DP];
+    load_row<DP>(X, ld, s, i, dim, h);
+    double best = 0.0;
+    int bl = 0;
+    for (int c = 0; c < K; ++c) {
+      const double v = sqdist<DP>(h, smu + c * dim, dim);
+      if (c == 0 || v < best) {
+        best = v;
+        bl = c;
+      }
+    }
+    if (old_labels && old_labels[i] != bl) ++ch;
+    labels[i] = bl;
+    dist[i] = best;
+  }
+  if (changes) {
+    ch = __reduce_add_sync(0xffffffffu, ch);
+    if ((threadIdx.x & 31) == 0 && ch) atomicAdd(changes, ch);  // integer: order-independent
+  }
+}
+
+// dist_i = |h_i - mu_{label_i}|^2
+template <int DP>
+__global__ void __launch_bounds__(256) k_dist_own(const double* X, long long ld, const double* s, int n, int dim,
+                                                  const double* mu, const int* labels, double* dist) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double h[DP];
+    load_row<DP>(X, ld, s, i, dim, h);
+    dist[i] = sqdist<DP>(h, mu + labels[i] * dim, dim);
+  }
+}
+
+// per-CTA cluster sums and counts: partials[b][K*dim + K]; 4 warps, each with a
+// private shared accumulator filled in row order, combined in fixed order.
+__global__ void __launch_bounds__(128) k_centroid_partials(const double* X, long long ld, const double* s, int n,
+                                                           int dim, int K, const int* labels, double* partials) {
+  extern __shared__ double acc[];  // [4][K*dim + K]
+  const int W = K * dim + K;
+  for (int e = threadIdx.x; e < 4 * W; e += blockDim.x) acc[e] = 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long i0 = (long long)n * blockIdx.x / gridDim.x, i1 = (long long)n * (blockIdx.x + 1) / gridDim.x;
+  const long long j0 = i0 + (i1 - i0) * w / 4, j1 = i0 + (i1 - i0) * (w + 1) / 4;
+  double* a = acc + (size_t)w * W;
+  for (long long i = j0; i < j1; ++i) {
+    const int l = labels[i];
+    for (int d = lane; d < dim; d += 32) a[l * dim + d] += hval(X, ld, s, (int)i, d);
+    if (lane == 0) a[K * dim + l] += 1.0;
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < W; e += blockDim.x)
+    partials[(size_t)blockIdx.x * W + e] = ((acc[e] + acc[W + e]) + acc[2 * W + e]) + acc[3 * W + e];
+}
+
+__global__ void k_means_div(const double* sums, int K, int dim, double* mu) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * dim; e += gridDim.x * blockDim.x) {
+    const double cnt = sums[K * dim + e / dim];
+    if (cnt > 0) mu[e] = sums[e] / cnt;
+  }
+}
+
+// per-block (max value, lowest index) of dist excluding `used` indices
+__global__ void k_argmax(const double* dist, int n, const int* used, int nused, double* bval, int* bidx) {
+  __shared__ double sv[256];
+  __shared__ int si[256];
+  double best = -1.0;
+  int bi = n;
+  const int i0 = blockIdx.x * kBlk, i1 = min(n, i0 + kBlk);
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    bool ex = false;
+    for (int u = 0; u < nused; ++u) ex |= (used[u] == i);
+    const double v = ex ? -1.0 : dist[i];
+    if (v > best || (v == best && i < bi)) {
+      best = v;
+      bi = i;
+    }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      const double v = sv[threadIdx.x + st];
+      const int ii = si[threadIdx.x + st];
+      if (v > sv[threadIdx.x] || (v == sv[threadIdx.x] && ii < si[threadIdx.x])) {
+        sv[threadIdx.x] = v;
+        si[threadIdx.x] = ii;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bval[blockIdx.x] = sv[0];
+    bidx[blockIdx.x] = si[0];
+  }
+}
+
+__global__ void k_sum_blocks(const double* x, int n, double* blocksum) {
+  __shared__ double red[8];
+  double part = 0.0;
+  const int i0 = blockIdx.x * kBlk, i1 = min(n, i0 + kBlk);
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) part += x[i];
+  part = warp_sum(part);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    blocksum[blockIdx.x] = t;
+  }
+}
+
+// Philox4x32-10 on the host (the library's own copy; the oracle has another)
+inline void philox_host(unsigned c[4], unsigned k0, unsigned k1) {
+  const unsigned M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const unsigned long long p0 = (unsigned long long)M0 * c[0], p1 = (unsigned long long)M1 * c[2];
+    const unsigned hi0 = (unsigned)(p0 >> 32), lo0 = (unsigned)p0, hi1 = (unsigned)(p1 >> 32), lo1 = (unsigned)p1;
+    const unsigned n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+  }
+}
+inline double uniform_host(uint64_t seed, unsigned c0, unsigned c1, unsigned c2) {
+  unsigned c[4] = {c0, c1, c2, 0u};
+  philox_host(c, (unsigned)seed, (unsigned)(seed >> 32));
+  return ((double)(c[0] >> 5) * 67108864.0 + (double)(c[1] >> 6)) / 9007199254740992.0;
+}
+
+struct KmBuf {
+  int n = 0, K = 0, G = 0, nblk = 0;
+  double *D2 = nullptr, *bsum = nullptr, *mu = nullptr, *dist = nullptr, *partials = nullptr, *sums = nullptr;
+  double* bval = nullptr;
+  int *lab = nullptr, *lab2 = nullptr, *best = nullptr, *idx = nullptr, *changes = nullptr, *bidx = nullptr,
+      *used = nullptr;
+};
+void km_free(void* p) {
+  KmBuf* b = static_cast<KmBuf*>(p);
+  void* ptrs[] = {b->D2, b->bsum, b->mu, b->dist, b->partials, b->sums, b->bval, b->lab, b->lab2, b->best, b->idx,
+                  b->changes, b->bidx, b->used};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  delete b;
+}
+
+#define KCU(expr)                                                         \
+  do {                                                                    \
+    cudaError_t e_ = (expr);                                              \
+    if (e_ != cudaSuccess) return ctx_fail(SFAIRSC_E_CUDA, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TRY_(e)                      \
+  do {                               \
+    sfairsc_status s_ = (e);         \
+    if (s_ != SFAIRSC_OK) return s_; \
+  } while (0)
+
+template <int DP>
+struct KM {
+  const double* X;
+  long long ld;
+  const double* s;
+  int n, dim, K, sms;
+  cudaStream_t st;
+  KmBuf* b;
+
+  int grid_rows() const { return std::max(1, std::min((n + 255) / 256, sms * 8)); }
+
+  sfairsc_status seed_centers(uint64_t seed, int r, std::vector<double>& hb) {
+    const double u0 = uniform_host(seed, 0u, (unsigned)r, (unsigned)kKmStream);
+    int idx = std::min((int)std::floor(u0 * n), n - 1);
+    for (int t = 0; t < K; ++t) {
+      if (t > 0) {
+        KCU(cudaMemcpyAsync(hb.data(), b->bsum, sizeof(double) * b->nblk, cudaMemcpyDeviceToHost, st));
+        KCU(cudaStreamSynchronize(st));
+        double total = 0.0;
+        for (int q = 0; q < b->nblk; ++q) total += hb[q];
+        const double u = uniform_host(seed, (unsigned)t, (unsigned)r, (unsigned)kKmStream);
+        if (total > 0) {
+          const double target = u * total;
+          double base = 0.0;
+          int bsel = b->nblk - 1;
+          for (int q = 0; q < b->nblk; ++q) {
+            if (base + hb[q] > target) {
+              bsel = q;
+              break;
+            }
+            base += hb[q];
+          }
+          bump_launch();
+          k_select_in_block<<<1, 32, 0, st>>>(b->D2, bsel, n, base, target, b->idx);
+          int hidx = 0;
+          KCU(cudaMemcpyAsync(&hidx, b->idx, sizeof(int), cudaMemcpyDeviceToHost, st));
+          KCU(cudaStreamSynchronize(st));
+          idx = hidx;
+        } else {
+          idx = std::min((int)std::floor(u * n), n - 1);
+        }
+      }
+      bump_launch();
+      k_gather_row<<<1, 64, 0, st>>>(X, ld, s, idx, dim, b->mu + (size_t)t * dim);
+      bump_launch();
+      k_d2<DP><<<b->nblk, 256, 0, st>>>(X, ld, s, n, dim, b->mu + (size_t)t * dim, t == 0, b->D2, b->bsum);
+    }
+    KCU(cudaGetLastError());
+    return SFAIRSC_OK;
+  }
+
+  sfairsc_status means(const int* lab) {
+    const int W = K * dim + K;
+    bump_launch();
+    k_centroid_partials<<<b->G, 128, 4 * W * sizeof(double), st>>>(X, ld, s, n, dim, K, lab, b->partials);
+    launch_reduce_cols(b->partials, b->G, W, b->sums, st);
+    bump_launch();
+    k_means_div<<<std::max(1, (K * dim + 255) / 256), 256, 0, st>>>(b->sums, K, dim, b->mu);
+    KCU(cudaGetLastError());
+    return SFAIRSC_OK;
+  }
+
+  sfairsc_status run(uint64_t seed, int restarts, int max_iters, double* best_wcss) {
+    std::vector<double> hb(std::max(b->nblk, K) + 8);
+    std::vector<double> counts(K);
+    std::vector<int> bidx(b->nblk);
+    std::vector<double> bval(b->nblk);
+    const size_t mu_smem = (size_t)K * dim * sizeof(double);
+    *best_wcss = std::numeric_limits<double>::infinity();
+    for (int r = 0; r < restarts; ++r) {
+      TRY_(seed_centers(seed, r, hb));
+      bump_launch();
+      k_assign<DP><<<grid_rows(), 256, mu_smem, st>>>(X, ld, s, n, dim, K, b->mu, nullptr, b->lab, b->dist, nullptr);
+      int* lab = b->lab;
+      int* lab_new = b->lab2;
+      for (int it = 0; it < max_iters; ++it) {
+        TRY_(means(lab));
+        KCU(cudaMemcpyAsync(counts.data(), b->sums + (size_t)K * dim, sizeof(double) * K, cudaMemcpyDeviceToHost, st));
+        KCU(cudaStreamSynchronize(st));
+        bool any_empty = false;
+        for (int c2 = 0; c2 < K; ++c2) any_empty |= counts[c2] == 0;
+        if (any_empty) {  // re-seed empty clusters at the farthest points (increasing c)
+          bump_launch();
+          k_dist_own<DP><<<grid_rows(), 256, 0, st>>>(X, ld, s, n, dim, b->mu, lab, b->dist);
+          std::vector<int> used;
+          for (int c2 = 0; c2 < K; ++c2) {
+            if (counts[c2] != 0) continue;
+            if (!used.empty())
+              KCU(cudaMemcpyAsync(b->used, used.data(), sizeof(int) * used.size(), cudaMemcpyHostToDevice, st));
+            bump_launch();
+            k_argmax<<<b->nblk, 256, 0, st>>>(b->dist, n, b->used, (int)used.size(), b->bval, b->bidx);
+            KCU(cudaMemcpyAsync(bval.data(), b->bval, sizeof(double) * b->nblk, cudaMemcpyDeviceToHost, st));
+            KCU(cudaMemcpyAsync(bidx.data(), b->bidx, sizeof(int) * b->nblk, cudaMemcpyDeviceToHost, st));
+            KCU(cudaStreamSynchronize(st));
+            double bv = -2.0;
+            int bi = n;
+            for (int q = 0; q < b->nblk; ++q)
+              if (bval[q] > bv || (bval[q] == bv && bidx[q] < bi)) {
+                bv = bval[q];
+                bi = bidx[q];
+              }
+            used.push_back(bi);
+            bump_launch();
+            k_gather_row<<<1, 64, 0, st>>>(X, ld, s, bi, dim, b->mu + (size_t)c2 * dim);
+          }
+        }
+        KCU(cudaMemsetAsync(b->changes, 0, sizeof(int), st));
+        bump_launch();
+        k_assign<DP><<<grid_rows(), 256, mu_smem, st>>>(X, ld, s, n, dim, K, b->mu, lab, lab_new, b->dist, b->changes);
+        int ch = 0;
+        KCU(cudaMemcpyAsync(&ch, b->changes, sizeof(int), cudaMemcpyDeviceToHost, st));
+        KCU(cudaStreamSynchronize(st));
+        if (ch == 0) break;
+        std::swap(lab, lab_new);
+      }
+      // final centroids of the final labels, WCSS
+      TRY_(means(lab));
+      bump_launch();
+      k_dist_own<DP><<<grid_rows(), 256, 0, st>>>(X, ld, s, n, dim, b->mu, lab, b->dist);
+      bump_launch();
+      k_sum_blocks<<<b->nblk, 256, 0, st>>>(b->dist, n, b->bsum);
+      KCU(cudaMemcpyAsync(hb.data(), b->bsum, sizeof(double) * b->nblk, cudaMemcpyDeviceToHost, st));
+      KCU(cudaStreamSynchronize(st));
+      double wcss = 0.0;
+      for (int q = 0; q < b->nblk; ++q) wcss += hb[q];
+      if (wcss < *best_wcss) {
+        *best_wcss = wcss;
+        KCU(cudaMemcpyAsync(b->best, lab, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    KCU(cudaStreamSynchronize(st));
+    return SFAIRSC_OK;
+  }
+};
+
+}  // namespace
+
+sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, int32_t memspace, double* objective) {
+  const int n = ctx_n(ctx), K = ctx_k(ctx);
+  long long ld = 0;
+  const double* X = ctx_X(ctx, &ld);
+  const double* s = ctx_s(ctx);
+  const int dim = K;
+  if (dim > kMaxDim) return ctx_fail(SFAIRSC_E_INVALID_ARG, "embed_kmeans supports k <= 64");
+  cudaStream_t st = ctx_stream(ctx);
+  void (*fr)(void*) = nullptr;
+  void** slot = ctx_km(ctx, &fr);
+  KmBuf* b = static_cast<KmBuf*>(*slot);
+  if (!b || b->n != n || b->K != K) {
+    if (b) km_free(b);
+    b = new KmBuf();
+    *slot = b;
+    ctx_set_km_free(ctx, km_free);
+    b->n = n;
+    b->K = K;
+    b->nblk = (n + kBlk - 1) / kBlk;
+    b->G = std::max(1, std::min(ctx_num_sms(ctx) * 2, (n + 1023) / 1024));
+    const int W = K * dim + K;
+    KCU(cudaMalloc(&b->D2, sizeof(double) * n));
+    KCU(cudaMalloc(&b->bsum, sizeof(double) * b->nblk));
+    KCU(cudaMalloc(&b->mu, sizeof(double) * K * dim));
+    KCU(cudaMalloc(&b->dist, sizeof(double) * n));
+    KCU(cudaMalloc(&b->partials, sizeof(double) * (size_t)b->G * W));
+    KCU(cudaMalloc(&b->sums, sizeof(double) * W));
+    KCU(cudaMalloc(&b->bval, sizeof(double) * b->nblk));
+    KCU(cudaMalloc(&b->lab, sizeof(int) * n));
+    KCU(cudaMalloc(&b->lab2, sizeof(int) * n));
+    KCU(cudaMalloc(&b->best, sizeof(int) * n));
+    KCU(cudaMalloc(&b->idx, sizeof(int) * 4));
+    KCU(cudaMalloc(&b->changes, sizeof(int) * 4));
+    KCU(cudaMalloc(&b->bidx, sizeof(int) * b->nblk));
+    KCU(cudaMalloc(&b->used, sizeof(int) * (K + 1)));
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_centroid_partials, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+  }
+  cudaEvent_t ev;
+  ctx_prof_begin(ctx, &ev);
+  double wcss = 0.0;
+  sfairsc_status stt;
+  const int sms = ctx_num_sms(ctx);
+  if (dim <= 8) stt = KM<8>{X, ld, s, n, dim, K, sms, st, b}.run(seed, 10, 300, &wcss);
+  else if (dim <= 16) stt = KM<16>{X, ld, s, n, dim, K, sms, st, b}.run(seed, 10, 300, &wcss);
+  else if (dim <= 32) stt = KM<32>{X, ld, s, n, dim, K, sms, st, b}.run(seed, 10, 300, &wcss);
+  else stt = KM<64>{X, ld, s, n, dim, K, sms, st, b}.run(seed, 10, 300, &wcss);
+  ctx_prof_end(ctx, 8, ev);
+  if (stt != SFAIRSC_OK) return stt;
+  KCU(cudaMemcpyAsync(labels_out, b->best, sizeof(int) * n,
+                      memspace == SFAIRSC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  KCU(cudaStreamSynchronize(st));
+  if (objective) *objective = wcss;
+  return SFAIRSC_OK;
+}
+
+}  // namespace sfz

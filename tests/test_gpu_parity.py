@@ -199,3 +199,57 @@ def test_errors(gpu_lib):
         lib.sfairsc_embed_kmeans(ctx, 1)
     assert e.value.name == "E_STATE"
     ctx.close()
+
+
+# --- Alg. 3 step 4: k-means on H (reading R16) ---------------------------------
+
+def _kmeans_parity(lib, g, k, normalized, tol, H_oracle, seed=2024):
+    from oracle.kmeans import kmeans
+    from oracle.metrics import ari, balance, hungarian_match
+    ctx = _ctx(lib, g, k, normalized)
+    lib.sfairsc_eigs(ctx, k, tol)
+    lab_gpu, wcss_gpu = lib.sfairsc_embed_kmeans(ctx, seed)
+    ctx.close()
+    ref = kmeans(H_oracle, k, seed)
+    a = ari(ref.labels, lab_gpu)
+    assert a >= 0.99, a
+    perm = hungarian_match(ref.labels, lab_gpu, k)
+    b_ref = balance(ref.labels, g.groups, k, g.h)
+    b_gpu = balance(perm[lab_gpu], g.groups, k, g.h)
+    assert np.abs(b_ref - b_gpu).max() <= 1e-3
+    return a, lab_gpu, ref
+
+
+def test_kmeans_config1_vs_oracle(gpu_lib):
+    g, cfg = baseline_config(1)
+    dense = fairsc.fairsc_dense(g.dense(), g.groups, g.h, cfg["k_eig"], cfg["normalized"])
+    _kmeans_parity(gpu_lib, g, cfg["k_eig"], cfg["normalized"], cfg["tol"], dense.H)
+
+
+def test_kmeans_normalized_random_vs_oracle(gpu_lib):
+    g = random_graph(600, 3, p=0.02, seed=31, weights="uniform")
+    dense = fairsc.fairsc_dense(g.dense(), g.groups, 3, 6, True)
+    _kmeans_parity(gpu_lib, g, 6, True, 1e-10, dense.H)
+
+
+def test_kmeans_planted_recovers_truth(gpu_lib):
+    from oracle.metrics import ari
+    g = planted_cliques(5, 8, 4, seed=3)
+    ctx = _ctx(gpu_lib, g, 5, True)
+    gpu_lib.sfairsc_eigs(ctx, 5, 1e-10)
+    lab, wcss = gpu_lib.sfairsc_embed_kmeans(ctx, 7)
+    ctx.close()
+    assert ari(lab, g.clusters) == 1.0
+    assert wcss < 1e-20
+
+
+def test_kmeans_device_labels_and_determinism(gpu_lib):
+    import torch
+    g, cfg = baseline_config(1)
+    ctx = _ctx(gpu_lib, g, 5, False)
+    gpu_lib.sfairsc_eigs(ctx, 5, 1e-10)
+    a, w1 = gpu_lib.sfairsc_embed_kmeans(ctx, 99)
+    b = torch.empty(g.n, dtype=torch.int32, device="cuda:0")
+    _, w2 = gpu_lib.sfairsc_embed_kmeans(ctx, 99, labels=b)
+    ctx.close()
+    assert np.array_equal(a, b.cpu().numpy()) and w1 == w2
