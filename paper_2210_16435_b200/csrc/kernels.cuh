@@ -79,7 +79,8 @@ int sweep_grid(int n, int num_sms);
 long long launch_count();  // kernels launched by this process so far
 void launch_sweep(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st);
 // TMA-fed persistent sweeps (krylov.cu); J <= 192, grid <= #SMs
-extern int g_tma_use2d;  // 1: 2-D tensor-map TMA per chunk (default); 0: one 1-D bulk copy per column
+extern int g_tma_use2d;
+extern int g_ritz_kind;  // 1: DMMA (fp64 tensor cores, default), 0: register-blocked FMA  // 1: 2-D tensor-map TMA per chunk (default); 0: one 1-D bulk copy per column
 bool sweep_tma_ok(int J);  // also the J limit of the smem-staged sweeps
 int sweep_smem_grid(int n, int J, int num_sms);
 void launch_sweep_smem(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid,

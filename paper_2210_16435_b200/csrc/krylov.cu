@@ -392,6 +392,76 @@ __global__ void __launch_bounds__(kThreads) k_ritz_rb(const double* __restrict__
 }
 
 // ---------------------------------------------------------------------------
+// Ritz GEMM on the fp64 tensor cores: DMMA mma.sync.m8n8k4.f64.
+// CTA tile 128 rows x 64 columns, 8 warps as 4 (rows) x 2 (cols), each warp a
+// 32 x 32 block = 4 x 4 DMMA tiles (32 fp64 accumulators per lane).  K staged
+// through shared memory in chunks of 16 with bank-conflict-free strides
+// (stride = 4 mod 16 doubles).  Fragment layouts (PTX m8n8k4 .f64):
+//   A(8x4, row):  a = A[lane>>2][lane&3];   B(4x8, col): b = B[lane&3][lane>>2];
+//   C(8x8):       c_i = C[lane>>2][2*(lane&3) + i].
+// ---------------------------------------------------------------------------
+constexpr int kDM = 128, kDN = 64, kDK = 16, kAS = kDM + 4, kBS = kDN + 4;
+
+__global__ void __launch_bounds__(kThreads) k_ritz_dmma(const double* __restrict__ V, long long ld, int n, int m,
+                                                        const double* __restrict__ Y, int p,
+                                                        double* __restrict__ Vout) {
+  __shared__ double As[kDK][kAS];
+  __shared__ double Bs[kDK][kBS];
+  const int col0 = blockIdx.x * kDN;
+  const long long row0 = (long long)blockIdx.y * kDM;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wr = w & 3, wc = w >> 2;  // warp tile origin: rows wr*32, cols wc*32
+  const int gq = lane >> 2, tq = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int k0 = 0; k0 < m; k0 += kDK) {
+    for (int e = tid; e < kDK * kDM; e += kThreads) {
+      const int kk = e / kDM, r = e % kDM;
+      const int l = k0 + kk;
+      const long long i = row0 + r;
+      As[kk][r] = (l < m && i < n) ? V[(long long)l * ld + i] : 0.0;
+    }
+    for (int e = tid; e < kDK * kDN; e += kThreads) {
+      const int kk = e / kDN, cc = e % kDN;
+      const int l = k0 + kk, c = col0 + cc;
+      Bs[kk][cc] = (l < m && c < p) ? Y[(size_t)c * m + l] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < kDK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) af[a] = As[ks + tq][wr * 32 + a * 8 + gq];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = Bs[ks + tq][wc * 32 + b * 8 + gq];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                       : "d"(af[a]), "d"(bf[b]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const long long i = row0 + wr * 32 + a * 8 + gq;
+    if (i >= n) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int col = col0 + wc * 32 + b * 8 + 2 * tq + q;
+        if (col < p) Vout[(long long)col * ld + i] = acc[a][b][q];
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 void bump_launch();
@@ -504,10 +574,17 @@ void launch_sweep_tma(int mode, const GraphDev& g, const ProjDesc& pd, const Swe
   }
 }
 
+int g_ritz_kind = 1;  // 1: DMMA tensor cores, 0: register-blocked FMA
+
 void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout,
                     cudaStream_t st) {
   if (p <= 0 || n <= 0) return;
   bump_launch();
+  if (g_ritz_kind == 1) {
+    dim3 grid((p + kDN - 1) / kDN, (n + kDM - 1) / kDM);
+    k_ritz_dmma<<<grid, kThreads, 0, st>>>(V, ld, n, m, Y, p, Vout);
+    return;
+  }
   if (p <= 32) {
     dim3 grid((p + 31) / 32, (n + 127) / 128);
     k_ritz_rb<32><<<grid, kThreads, 0, st>>>(V, ld, n, m, Y, p, Vout);
