@@ -195,18 +195,16 @@ __global__ void __launch_bounds__(kThreads) k_finish(GraphDev g, ProjDesc pd, co
 // normalized: t_i = p_i - sum_j (s_i w_ij s_j) p_j ; unnormalized: d_i p_i - sum_j w_ij p_j
 // ----------------------------------------------------------------------------
 template <int VS, bool NORM>
-__global__ void __launch_bounds__(kThreads) k_spmv(GraphDev g, const int* __restrict__ row_split,
-                                                   const double* __restrict__ p, double* __restrict__ t,
-                                                   double* partials, unsigned* counter, double* bsum_t, int nout) {
+__global__ void __launch_bounds__(kThreads, 6) k_spmv(GraphDev g, const int* __restrict__ row_split,
+                                                      const double* __restrict__ p, double* __restrict__ t,
+                                                      double* partials, unsigned* counter, double* bsum_t, int nout) {
   constexpr int NG = kThreads / VS;
   const int r0 = row_split[blockIdx.x], r1 = row_split[blockIdx.x + 1];
   const int lane = threadIdx.x % VS, gid = threadIdx.x / VS;
   const int* __restrict__ rp = g.rp;
   const int* __restrict__ ci = g.ci;
   const double* __restrict__ vv = g.vv;
-  double acc[kHB];
-#pragma unroll
-  for (int q = 0; q < kHB; ++q) acc[q] = 0.0;
+  // main loop: t only (group-sum accumulators are not live here -> fewer registers, more warps)
   for (int base = r0; base < r1; base += NG) {
     const int row = base + gid;
     const bool valid = row < r1;
@@ -231,10 +229,17 @@ __global__ void __launch_bounds__(kThreads) k_spmv(GraphDev g, const int* __rest
     for (int o = VS / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (valid && lane == 0) {
       const double pi = __ldg(p + row);
-      const double ti = (NORM ? pi : __ldg(g.dg + row) * pi) - sum;
-      t[row] = ti;
-      add_group(acc, g.grp[row], NORM ? g.s[row] * ti : ti);
+      t[row] = (NORM ? pi : __ldg(g.dg + row) * pi) - sum;
     }
+  }
+  // epilogue: B^T t over this CTA's rows (re-read from L2, fixed order)
+  __syncthreads();
+  double acc[kHB];
+#pragma unroll
+  for (int q = 0; q < kHB; ++q) acc[q] = 0.0;
+  for (int row = r0 + threadIdx.x; row < r1; row += kThreads) {
+    const double ti = __ldcg(t + row);
+    add_group(acc, g.grp[row], NORM ? g.s[row] * ti : ti);
   }
   block_reduce_store<kHB>(acc, partials + (size_t)blockIdx.x * kHB);
   ticket_finalize<kHB>(partials, counter, bsum_t, nout);

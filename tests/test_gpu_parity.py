@@ -253,3 +253,61 @@ def test_kmeans_device_labels_and_determinism(gpu_lib):
     _, w2 = gpu_lib.sfairsc_embed_kmeans(ctx, 99, labels=b)
     ctx.close()
     assert np.array_equal(a, b.cpu().numpy()) and w1 == w2
+
+
+# --- BASELINE configs 3 and 4 ------------------------------------------------------
+
+def test_eigs_config3_reduced_vs_tier_s(gpu_lib):
+    """Config 3 law (unnormalized, h=5, k=20, U(0.5,1.5) weights) at n = 50,000
+    against the Tier S oracle (ARPACK on the paper's matrix-free operator)."""
+    g, cfg = baseline_config(3, n=50_000)
+    k = cfg["k_eig"]
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, False)
+    ref = sfairsc_cpu.sfairsc_arpack(op, k, tol=1e-12, seed=3)
+    gap = ref.evals[k] - ref.evals[k - 1]
+    _check_eigs(gpu_lib, g, k, False, cfg["tol"], ref_evals=ref.evals[:k], ref_X=ref.X, gap=gap)
+
+
+def _full_size_properties(lib, c, n_sample=3):
+    """Full BASELINE size in the launch configuration bench.py times: the GPU
+    solve (device-resident CSR) checked by properties that hold at any size
+    and by oracle applies of sampled eigenvectors (Tier S, one by one)."""
+    import torch
+    g, cfg = baseline_config(c)
+    k = cfg["k_eig"]
+    dev = torch.device("cuda:0")
+    t = lambda a: torch.from_numpy(a).to(dev)
+    ctx = lib.sfairsc_build_operator(t(g.row_ptr), t(g.col), t(g.val), t(g.groups.astype(np.int32)), k,
+                                     cfg["normalized"], h=g.h)
+    Xd = torch.empty((k, g.n), dtype=torch.float64, device=dev)
+    ev, _, st = lib.sfairsc_eigs(ctx, k, cfg["tol"], evecs=Xd)
+    ctx.close()
+    X = Xd.T.cpu().numpy()
+    del Xd
+    sigma = st["sigma"]
+    assert st["converged"] == 1 and st["max_resid_rel"] <= 1e-9
+    assert np.all(np.diff(ev) >= -1e-12 * sigma) and ev[-1] < sigma
+    assert abs(ev[0]) <= 1e-12 * sigma  # lambda_1 = 0 (F^T 1 = 0, SURVEY §0)
+    assert np.abs(X.T @ X - np.eye(k)).max() <= 1e-11  # orthonormal
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, cfg["normalized"])
+    assert op.sigma == pytest.approx(sigma, rel=1e-14)
+    assert np.linalg.norm(op.C.T @ X) <= 1e-10 * np.linalg.norm(X)  # fair: C^T X = 0
+    one = np.sqrt(op.d) if cfg["normalized"] else np.ones(g.n)
+    # the lambda = 0 eigenvector is D^{1/2} 1 (normalized) / 1: it lies in span(X)
+    assert subspace_sin(X, one[:, None]) <= 1e-8
+    rng = np.random.default_rng(c)
+    for i in sorted(rng.choice(k, size=n_sample, replace=False)):
+        r = op.apply(X[:, i]) - ev[i] * X[:, i]  # oracle apply (P:803), one vector at a time
+        assert np.linalg.norm(r) / sigma <= 1e-9, (i, np.linalg.norm(r) / sigma)
+        rq = X[:, i] @ op.apply(X[:, i])
+        assert abs(rq - ev[i]) <= 1e-8 * abs(ev[i]) + 1e-12 * sigma
+    return ev, st
+
+
+def test_config3_full_size_properties(gpu_lib):
+    _full_size_properties(gpu_lib, 3)
+
+
+def test_config4_full_size_properties(gpu_lib):
+    ev, st = _full_size_properties(gpu_lib, 4, n_sample=2)
+    assert st["steps"] > 0
