@@ -90,6 +90,9 @@ typedef struct {
   void *cuda_stream;      /* cudaStream_t to run on (e.g. torch.cuda.current_stream()); NULL: library-created */
   int32_t check_symmetry; /* 1 (default): verify W == W^T at build (one O(nnz log deg) pass) */
   int32_t spmv_vector;    /* 0: auto; else lanes per row in the SpMV (2,4,8,16,32) */
+  int32_t block_size;     /* Lanczos block size b: 1 = single-vector thick-restart Lanczos; 2 or 4 = block
+                             thick-restart Lanczos (SpMM on b interleaved vectors, block CGS2, CholQR2;
+                             requires h <= 16); 0 = auto (DESIGN.md §Block Lanczos) */
 } sfairsc_opts;
 
 typedef struct {

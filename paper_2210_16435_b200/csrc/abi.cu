@@ -1,7 +1,6 @@
 // libsfairsc — C ABI (include/sfairsc.h): context, operator build (A0-A3),
 // operator apply (A4-A6), thick-restart Lanczos driver (A7-A11).
-#include "sfairsc.h"
-#include "kernels.cuh"
+#include "ctx.h"
 
 #include <cuda_runtime.h>
 
@@ -18,6 +17,8 @@
 
 namespace sfz {
 void symeig(int m, std::vector<double>& A, std::vector<double>& evals);
+sfairsc_status eigs_block(sfairsc_ctx* c, int k, double tol, double* evals_out, double* evecs_out,
+                          int evecs_memspace, sfairsc_stats* stats);
 sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, int32_t memspace, double* objective);
 }  // namespace sfz
 
@@ -25,7 +26,7 @@ using namespace sfz;
 
 static thread_local std::string g_err;
 
-static sfairsc_status fail(sfairsc_status st, const char* fmt, ...) {
+sfairsc_status sfz::fail(sfairsc_status st, const char* fmt, ...) {
   char buf[1024];
   va_list ap;
   va_start(ap, fmt);
@@ -35,134 +36,6 @@ static sfairsc_status fail(sfairsc_status st, const char* fmt, ...) {
   return st;
 }
 
-#define CU(expr)                                                                                        \
-  do {                                                                                                  \
-    cudaError_t e_ = (expr);                                                                            \
-    if (e_ != cudaSuccess)                                                                              \
-      return fail(e_ == cudaErrorMemoryAllocation ? SFAIRSC_E_OOM : SFAIRSC_E_CUDA, "%s: %s (%s:%d)", \
-                  #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                                    \
-  } while (0)
-
-#define CHECK_LAUNCH() CU(cudaGetLastError())
-#define TRY(expr)                              \
-  do {                                         \
-    sfairsc_status s_ = (expr);                \
-    if (s_ != SFAIRSC_OK) return s_;           \
-  } while (0)
-
-// --------------------------------------------------------------------------
-// per-kernel event timing (sfairsc_profile_*)
-// --------------------------------------------------------------------------
-struct Prof {
-  bool on = false;
-  struct Pending {
-    int kind;
-    cudaEvent_t a, b;
-    double bytes;
-  };
-  std::vector<Pending> pending;
-  std::vector<cudaEvent_t> pool;
-  double total_ms[10] = {};
-  int64_t launches[10] = {};
-  double bytes[10] = {};
-  cudaEvent_t get() {
-    if (pool.empty()) {
-      cudaEvent_t e;
-      cudaEventCreate(&e);
-      return e;
-    }
-    cudaEvent_t e = pool.back();
-    pool.pop_back();
-    return e;
-  }
-  void resolve() {
-    for (auto& p : pending) {
-      cudaEventSynchronize(p.b);
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, p.a, p.b);
-      total_ms[p.kind] += ms;
-      launches[p.kind] += 1;
-      bytes[p.kind] += p.bytes;
-      pool.push_back(p.a);
-      pool.push_back(p.b);
-    }
-    pending.clear();
-  }
-  ~Prof() {
-    for (auto& p : pending) {
-      cudaEventDestroy(p.a);
-      cudaEventDestroy(p.b);
-    }
-    for (auto e : pool) cudaEventDestroy(e);
-  }
-};
-
-enum { K_SPMV = 0, K_DOTS = 1, K_UPDDOT = 2, K_UPDNORM = 3, K_NORMALIZE = 4, K_RITZ = 5, K_PROJ = 6, K_FINISH = 7,
-       K_KMEANS = 8, K_OTHER = 9 };
-
-struct sfairsc_ctx {
-  int device = 0, num_sms = 148;
-  cudaStream_t st = nullptr;
-  bool own_stream = false;
-  int n = 0, nnz = 0, h = 1, k_build = 1;
-  bool normalized = false;
-  long long ldv = 0;
-  int vs = 8, spmv_grid = 1, sgrid = 1;
-  double sigma = 0.0, tol_cap = 1e-10;
-  uint64_t seed = 0x5F41C5EEDull;
-  int m = 20, keep = 0, max_restarts = 100000;
-  int check_symmetry = 1;
-  int debug = 0;
-  int sweep_kind = 2;  // 0 register sweeps, 1 smem-staged, 2 TMA 2-D tensor (default), 3 TMA 1-D (env SFAIRSC_SWEEP)
-  int tma_mode2 = 0;   // update+norm sweep: register kernel (measured faster); env SFAIRSC_TMA_MODE2=1: TMA
-  // device buffers
-  int *rp = nullptr, *ci = nullptr, *row_split = nullptr;
-  double *vv = nullptr, *dg = nullptr, *s = nullptr;
-  uint8_t* grp = nullptr;
-  double *isb = nullptr, *uh = nullptr;
-  double* partials = nullptr;
-  size_t partials_cnt = 0;
-  unsigned* counters = nullptr;
-  double *bs_w = nullptr, *bs_t = nullptr, *bs_v = nullptr, *nb = nullptr, *scal = nullptr;
-  double *c1 = nullptr, *c2 = nullptr;
-  double *vp = nullptr, *vt = nullptr, *vr = nullptr, *vy = nullptr;
-  double *V = nullptr, *Vb = nullptr, *Ydev = nullptr, *X = nullptr;
-  double *talpha = nullptr, *tbeta = nullptr;  // Lanczos T entries recorded on device
-  int* flags = nullptr;
-  double* hp = nullptr;  // pinned host staging (4 KB)
-  // results
-  bool have_eigs = false;
-  int k_eigs = 0;
-  std::vector<double> evals;
-  std::vector<int32_t> groups_host;
-  std::vector<int64_t> group_count;
-  sfairsc_stats last{};
-  double t_build = 0.0;
-  Prof prof;
-  // kmeans scratch (allocated lazily by kmeans.cu)
-  void* km = nullptr;
-  void (*km_free)(void*) = nullptr;
-
-  GraphDev g() const {
-    GraphDev G;
-    G.n = n;
-    G.nnz = nnz;
-    G.rp = rp;
-    G.ci = ci;
-    G.vv = vv;
-    G.dg = dg;
-    G.s = s;
-    G.grp = grp;
-    G.normalized = normalized;
-    return G;
-  }
-  ProjDesc pd() const { return ProjDesc{h, isb, uh}; }
-  // algorithmic bytes: one read/write of each operand
-  double vb() const { return 8.0 * n; }                      // one fp64 n-vector
-  double sgb() const { return (normalized ? 8.0 * n : 0.0) + 1.0 * n; }  // s (normalized) + group ids
-  double csr_bytes() const { return 12.0 * nnz + 4.0 * (n + 1); }
-  int gpasses() const { return (h + kHB - 1) / kHB; }
-};
 
 // accessors used by kmeans.cu
 namespace sfz {
@@ -186,26 +59,6 @@ void ctx_prof_end(sfairsc_ctx* c, int kind, cudaEvent_t a);
 sfairsc_status ctx_fail(sfairsc_status st, const char* msg) { return fail(st, "%s", msg); }
 }  // namespace sfz
 
-// profiling wrappers
-struct ProfScope {
-  sfairsc_ctx* c;
-  int kind;
-  double bytes;
-  cudaEvent_t a = nullptr;
-  ProfScope(sfairsc_ctx* c_, int kind_, double bytes_ = 0.0) : c(c_), kind(kind_), bytes(bytes_) {
-    if (c->prof.on) {
-      a = c->prof.get();
-      cudaEventRecord(a, c->st);
-    }
-  }
-  ~ProfScope() {
-    if (c->prof.on) {
-      cudaEvent_t b = c->prof.get();
-      cudaEventRecord(b, c->st);
-      c->prof.pending.push_back({kind, a, b, bytes});
-    }
-  }
-};
 namespace sfz {
 void ctx_prof_begin(sfairsc_ctx* c, cudaEvent_t* a) {
   *a = nullptr;
@@ -233,7 +86,8 @@ static void free_ctx(sfairsc_ctx* c) {
   if (c->km && c->km_free) c->km_free(c->km);
   void* ptrs[] = {c->rp, c->ci, c->row_split, c->vv, c->dg, c->s, c->grp, c->isb, c->uh, c->partials, c->counters,
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
-                  c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta};
+                  c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta,
+                  c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hp) cudaFreeHost(c->hp);
@@ -241,7 +95,7 @@ static void free_ctx(sfairsc_ctx* c) {
   delete c;
 }
 
-static double now_s() {
+double sfz::now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
@@ -260,6 +114,7 @@ extern "C" void sfairsc_default_opts(sfairsc_opts* o) {
   o->cuda_stream = nullptr;
   o->check_symmetry = 1;
   o->spmv_vector = 0;
+  o->block_size = 0;
 }
 
 extern "C" const char* sfairsc_last_error(void) { return g_err.c_str(); }
@@ -292,7 +147,7 @@ static void gsum_all(sfairsc_ctx* c, const double* x, double* bsum) {
 }
 
 // y = L^sigma x on device vectors (4 kernels; A4-A6)
-static sfairsc_status apply_dev(sfairsc_ctx* c, const double* x, double* y) {
+sfairsc_status sfz::apply_dev(sfairsc_ctx* c, const double* x, double* y) {
   {
     ProfScope ps(c, K_PROJ, c->gpasses() * (c->vb() + c->sgb()) + 2 * c->vb() + c->sgb());
     gsum_all(c, x, c->bs_w);
@@ -309,6 +164,28 @@ static sfairsc_status apply_dev(sfairsc_ctx* c, const double* x, double* y) {
     launch_finish(c->g(), c->pd(), c->vt, c->bs_t, c->bs_w, c->sigma, y, c->st);
   }
   CHECK_LAUNCH();
+  return SFAIRSC_OK;
+}
+
+
+// max_i ||L^sigma x_i - theta_i x_i|| / sigma over the k columns of X (A11), k fresh applies
+sfairsc_status sfz::true_residuals(sfairsc_ctx* c, const double* theta, int k, double* max_out) {
+  std::vector<double> res(k);
+  for (int i = 0; i < k; ++i) {
+    const double* xi = c->X + (long long)i * c->ldv;
+    TRY(apply_dev(c, xi, c->vy));
+    launch_resid(c->vy, xi, theta[i], c->n, c->partials, c->counters + 4, c->scal + 8 + i % 64, c->st);
+    CHECK_LAUNCH();
+    if (i % 64 == 63 || i == k - 1) {
+      const int base = i - i % 64;
+      CU(cudaMemcpyAsync(c->hp, c->scal + 8, sizeof(double) * (i - base + 1), cudaMemcpyDeviceToHost, c->st));
+      CU(cudaStreamSynchronize(c->st));
+      for (int q = base; q <= i; ++q) res[q] = std::sqrt(c->hp[q - base]) / c->sigma;
+    }
+  }
+  double mx = 0.0;
+  for (int i = 0; i < k; ++i) mx = std::max(mx, res[i]);
+  *max_out = mx;
   return SFAIRSC_OK;
 }
 
@@ -382,6 +259,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   if (getenv("SFAIRSC_SWEEP")) c->sweep_kind = atoi(getenv("SFAIRSC_SWEEP"));
   if (getenv("SFAIRSC_TMA_MODE2")) c->tma_mode2 = atoi(getenv("SFAIRSC_TMA_MODE2"));
   if (getenv("SFAIRSC_RITZ")) sfz::g_ritz_kind = atoi(getenv("SFAIRSC_RITZ"));
+  if (getenv("SFAIRSC_SPMV")) sfz::g_spmv_kind = atoi(getenv("SFAIRSC_SPMV"));
   if (c->sweep_kind == 3) {  // TMA with one 1-D copy per column (A/B only)
     sfz::g_tma_use2d = 0;
     c->sweep_kind = 2;
@@ -416,6 +294,26 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   c->m = m;
   c->keep = opts.keep > 0 ? opts.keep : k + (m - k) / 2;
   c->keep = std::max(std::min(c->keep, m - 1), std::min(k, m - 1));
+  // block Lanczos sizing: m + b <= kBMaxJ, m + b <= dim null(C^T) = n - h + 1, keep >= k, (m - keep) % b == 0
+  c->bsz = opts.block_size > 0 ? opts.block_size : 1;
+  if (c->bsz != 1 && c->bsz != 2 && c->bsz != 4)
+    return bail(fail(SFAIRSC_E_INVALID_ARG, "block_size must be 0, 1, 2 or 4"));
+  if (hh > kHB) c->bsz = 1;  // the fused block epilogues carry at most kHB group sums
+  if (c->bsz > 1) {
+    const int b = c->bsz;
+    int mb = opts.max_basis > 0 ? opts.max_basis : std::max(2 * k + 10, 20);
+    mb = std::min(mb, kBMaxJ - b);
+    mb = std::min(mb, n - hh + 1 - b);
+    if (mb < k + b) {
+      c->bsz = 1;  // too small for a block basis: single-vector Lanczos
+    } else {
+      int kp = opts.keep > 0 ? opts.keep : k + (mb - k) / 2;
+      kp = std::max(k, std::min(kp, mb - b));
+      mb = kp + b * ((mb - kp) / b);
+      c->m = m = mb;
+      c->keep = kp;
+    }
+  }
 
   // device allocations
   CUB(dalloc(&c->rp, n + 1));
@@ -440,8 +338,8 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     CUB(dalloc(p, 512));
     CUB(cudaMemset(*p, 0, 512 * sizeof(double)));
   }
-  CUB(dalloc(&c->c1, kMaxJ));
-  CUB(dalloc(&c->c2, kMaxJ));
+  CUB(dalloc(&c->c1, 4 * kMaxJ));
+  CUB(dalloc(&c->c2, 4 * kMaxJ));
   for (double** p : {&c->vp, &c->vt, &c->vr, &c->vy}) {
     CUB(dalloc(p, c->ldv));
     CUB(cudaMemsetAsync(*p, 0, c->ldv * sizeof(double), c->st));
@@ -555,15 +453,29 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     CUB(cudaMemcpyAsync(c->uh, uh.data(), sizeof(double) * hh, cudaMemcpyHostToDevice, c->st));
   }
   // Krylov basis (double-buffered for thick restarts) and eigenvector block
-  CUB(dalloc(&c->V, (size_t)(m + 1) * c->ldv));
-  CUB(dalloc(&c->Vb, (size_t)(m + 1) * c->ldv));
-  CUB(cudaMemsetAsync(c->V, 0, sizeof(double) * (m + 1) * c->ldv, c->st));
-  CUB(cudaMemsetAsync(c->Vb, 0, sizeof(double) * (m + 1) * c->ldv, c->st));
+  const int vcols = m + std::max(1, c->bsz);
+  CUB(dalloc(&c->V, (size_t)vcols * c->ldv));
+  CUB(dalloc(&c->Vb, (size_t)vcols * c->ldv));
+  CUB(cudaMemsetAsync(c->V, 0, sizeof(double) * vcols * c->ldv, c->st));
+  CUB(cudaMemsetAsync(c->Vb, 0, sizeof(double) * vcols * c->ldv, c->st));
   CUB(dalloc(&c->Ydev, (size_t)(m + 1) * (m + 1)));
   CUB(dalloc(&c->talpha, m + 1));
   CUB(dalloc(&c->tbeta, m + 1));
   CUB(dalloc(&c->X, (size_t)k * c->ldv));
   CUB(cudaMemsetAsync(c->X, 0, sizeof(double) * k * c->ldv, c->st));
+  if (c->bsz > 1) {  // block Lanczos buffers (m + bsz basis columns: V/Vb above hold m + 1 <= m + bsz)
+    const int nbz = c->bsz;
+    for (double** p : {&c->bP, &c->bT, &c->bR}) {
+      CUB(dalloc(p, (size_t)c->ldv * nbz));
+      CUB(cudaMemsetAsync(*p, 0, sizeof(double) * c->ldv * nbz, c->st));
+    }
+    c->ldT = m + nbz;
+    CUB(dalloc(&c->Tdev, (size_t)c->ldT * c->ldT));
+    CUB(cudaMemsetAsync(c->Tdev, 0, sizeof(double) * c->ldT * c->ldT, c->st));
+    CUB(dalloc(&c->g2, 64));
+    CUB(dalloc(&c->bflags, kMaxJ + 8));
+    CUB(cudaMemsetAsync(c->bflags, 0, sizeof(int) * (kMaxJ + 8), c->st));
+  }
   CUB(cudaStreamSynchronize(c->st));
   c->t_build = now_s() - t0;
   *out = c;
@@ -812,6 +724,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
   if (!(tol > 0)) return fail(SFAIRSC_E_INVALID_ARG, "tol must be > 0");
   if (evecs_out && evecs_memspace != SFAIRSC_MEM_HOST && evecs_memspace != SFAIRSC_MEM_DEVICE)
     return fail(SFAIRSC_E_INVALID_ARG, "memspace");
+  if (c->bsz > 1) return eigs_block(c, k, tol, evals_out, evecs_out, evecs_memspace, stats);
   c->have_eigs = false;
   Lanczos L;
   L.c = c;
@@ -952,23 +865,8 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
 
   // ---- A11: true residuals with k fresh applies ----
   double max_resid = 0.0;
-  {
-    std::vector<double> res(k);
-    for (int i = 0; i < k; ++i) {
-      const double* xi = c->X + (long long)i * c->ldv;
-      TRY(apply_dev(c, xi, c->vy));
-      launch_resid(c->vy, xi, theta[i], n, c->partials, c->counters + 4, c->scal + 8 + i % 64, c->st);
-      CHECK_LAUNCH();
-      if (i % 64 == 63 || i == k - 1) {
-        const int base = i - i % 64;
-        CU(cudaMemcpyAsync(c->hp, c->scal + 8, sizeof(double) * (i - base + 1), cudaMemcpyDeviceToHost, c->st));
-        CU(cudaStreamSynchronize(c->st));
-        for (int q = base; q <= i; ++q) res[q] = std::sqrt(c->hp[q - base]) / c->sigma;
-      }
-    }
-    L.applies += k;
-    for (int i = 0; i < k; ++i) max_resid = std::max(max_resid, res[i]);
-  }
+  TRY(true_residuals(c, theta.data(), k, &max_resid));
+  L.applies += k;
   if (c->prof.on) c->prof.resolve();
   c->evals.assign(theta.begin(), theta.begin() + k);
   c->k_eigs = k;

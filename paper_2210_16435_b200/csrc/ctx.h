@@ -1,0 +1,178 @@
+// Internal: the context behind the opaque sfairsc_ctx handle, shared by the
+// library's host translation units (abi.cu, lanczos_block.cu).  Not part of the C ABI.
+#pragma once
+#include "sfairsc.h"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+using sfz::GraphDev;
+using sfz::ProjDesc;
+using sfz::kHB;
+
+// --------------------------------------------------------------------------
+// per-kernel event timing (sfairsc_profile_*)
+// --------------------------------------------------------------------------
+struct Prof {
+  bool on = false;
+  struct Pending {
+    int kind;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  double total_ms[10] = {};
+  int64_t launches[10] = {};
+  double bytes[10] = {};
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void resolve() {
+    for (auto& p : pending) {
+      cudaEventSynchronize(p.b);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, p.a, p.b);
+      total_ms[p.kind] += ms;
+      launches[p.kind] += 1;
+      bytes[p.kind] += p.bytes;
+      pool.push_back(p.a);
+      pool.push_back(p.b);
+    }
+    pending.clear();
+  }
+  ~Prof() {
+    for (auto& p : pending) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+enum { K_SPMV = 0, K_DOTS = 1, K_UPDDOT = 2, K_UPDNORM = 3, K_NORMALIZE = 4, K_RITZ = 5, K_PROJ = 6, K_FINISH = 7,
+       K_KMEANS = 8, K_OTHER = 9 };
+
+struct sfairsc_ctx {
+  int device = 0, num_sms = 148;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  int n = 0, nnz = 0, h = 1, k_build = 1;
+  bool normalized = false;
+  long long ldv = 0;
+  int vs = 8, spmv_grid = 1, sgrid = 1;
+  double sigma = 0.0, tol_cap = 1e-10;
+  uint64_t seed = 0x5F41C5EEDull;
+  int m = 20, keep = 0, max_restarts = 100000;
+  int check_symmetry = 1;
+  int debug = 0;
+  int sweep_kind = 2;  // 0 register sweeps, 1 smem-staged, 2 TMA 2-D tensor (default), 3 TMA 1-D (env SFAIRSC_SWEEP)
+  int tma_mode2 = 0;   // update+norm sweep: register kernel (measured faster); env SFAIRSC_TMA_MODE2=1: TMA
+  // device buffers
+  int *rp = nullptr, *ci = nullptr, *row_split = nullptr;
+  double *vv = nullptr, *dg = nullptr, *s = nullptr;
+  uint8_t* grp = nullptr;
+  double *isb = nullptr, *uh = nullptr;
+  double* partials = nullptr;
+  size_t partials_cnt = 0;
+  unsigned* counters = nullptr;
+  double *bs_w = nullptr, *bs_t = nullptr, *bs_v = nullptr, *nb = nullptr, *scal = nullptr;
+  double *c1 = nullptr, *c2 = nullptr;
+  double *vp = nullptr, *vt = nullptr, *vr = nullptr, *vy = nullptr;
+  double *V = nullptr, *Vb = nullptr, *Ydev = nullptr, *X = nullptr;
+  double *talpha = nullptr, *tbeta = nullptr;  // Lanczos T entries recorded on device
+  int* flags = nullptr;
+  double* hp = nullptr;  // pinned host staging (4 KB)
+  // block Lanczos (lanczos_block.cu); bsz = 1: the single-vector path above
+  int bsz = 1;
+  double *bP = nullptr, *bT = nullptr, *bR = nullptr;  // interleaved ldv x bsz blocks
+  double *Tdev = nullptr, *g2 = nullptr;                // projected matrix (ldT = m + bsz), CholQR Gram
+  int ldT = 0;
+  int* bflags = nullptr;                                // per-step breakdown flags
+  // results
+  bool have_eigs = false;
+  int k_eigs = 0;
+  std::vector<double> evals;
+  std::vector<int32_t> groups_host;
+  std::vector<int64_t> group_count;
+  sfairsc_stats last{};
+  double t_build = 0.0;
+  Prof prof;
+  // kmeans scratch (allocated lazily by kmeans.cu)
+  void* km = nullptr;
+  void (*km_free)(void*) = nullptr;
+
+  GraphDev g() const {
+    GraphDev G;
+    G.n = n;
+    G.nnz = nnz;
+    G.rp = rp;
+    G.ci = ci;
+    G.vv = vv;
+    G.dg = dg;
+    G.s = s;
+    G.grp = grp;
+    G.normalized = normalized;
+    return G;
+  }
+  ProjDesc pd() const { return ProjDesc{h, isb, uh}; }
+  // algorithmic bytes: one read/write of each operand
+  double vb() const { return 8.0 * n; }                      // one fp64 n-vector
+  double sgb() const { return (normalized ? 8.0 * n : 0.0) + 1.0 * n; }  // s (normalized) + group ids
+  double csr_bytes() const { return 12.0 * nnz + 4.0 * (n + 1); }
+  int gpasses() const { return (h + kHB - 1) / kHB; }
+};
+
+
+namespace sfz {
+sfairsc_status fail(sfairsc_status st, const char* fmt, ...);
+sfairsc_status apply_dev(sfairsc_ctx* c, const double* x, double* y);  // y = L^sigma x (device vectors)
+sfairsc_status true_residuals(sfairsc_ctx* c, const double* theta, int k, double* max_out);  // over X
+double now_s();
+}
+
+// profiling scope: one event pair around a launch group (sfairsc_profile_*)
+struct ProfScope {
+  sfairsc_ctx* c;
+  int kind;
+  double bytes;
+  cudaEvent_t a = nullptr;
+  ProfScope(sfairsc_ctx* c_, int kind_, double bytes_ = 0.0) : c(c_), kind(kind_), bytes(bytes_) {
+    if (c->prof.on) {
+      a = c->prof.get();
+      cudaEventRecord(a, c->st);
+    }
+  }
+  ~ProfScope() {
+    if (c->prof.on) {
+      cudaEvent_t b = c->prof.get();
+      cudaEventRecord(b, c->st);
+      c->prof.pending.push_back({kind, a, b, bytes});
+    }
+  }
+};
+
+#define CU(expr)                                                                                        \
+  do {                                                                                                  \
+    cudaError_t e_ = (expr);                                                                            \
+    if (e_ != cudaSuccess)                                                                              \
+      return sfz::fail(e_ == cudaErrorMemoryAllocation ? SFAIRSC_E_OOM : SFAIRSC_E_CUDA, "%s: %s (%s:%d)", \
+                       #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                               \
+  } while (0)
+
+#define CHECK_LAUNCH() CU(cudaGetLastError())
+#define TRY(expr)                              \
+  do {                                         \
+    sfairsc_status s_ = (expr);                \
+    if (s_ != SFAIRSC_OK) return s_;           \
+  } while (0)

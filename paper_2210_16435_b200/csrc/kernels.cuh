@@ -80,6 +80,7 @@ long long launch_count();  // kernels launched by this process so far
 void launch_sweep(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st);
 // TMA-fed persistent sweeps (krylov.cu); J <= 192, grid <= #SMs
 extern int g_tma_use2d;
+extern int g_spmv_kind;
 extern int g_ritz_kind;  // 1: DMMA (fp64 tensor cores, default), 0: register-blocked FMA  // 1: 2-D tensor-map TMA per chunk (default); 0: one 1-D bulk copy per column
 bool sweep_tma_ok(int J);  // also the J limit of the smem-staged sweeps
 int sweep_smem_grid(int n, int J, int num_sms);
@@ -113,6 +114,51 @@ void launch_ritz(const double* V, long long ld, int n, int m, const double* Y, i
 // out = |y - theta x|^2 (ticket reduced)
 void launch_resid(const double* y, const double* x, double theta, int n, double* partials, unsigned* counter,
                   double* out, cudaStream_t st);
+
+// ---- block Krylov kernels (block.cu) ---------------------------------
+// NB in {1, 2, 4}; blocks of NB n-vectors are interleaved (row-major, ldv rows x NB).
+constexpr int kBMaxJ = 192;  // max basis columns of a block sweep (TMA box + smem ring)
+struct BlockSweepArgs {
+  const double* V;     // basis, column-major, ld
+  long long ld;
+  int J;               // columns of V swept (0 allowed)
+  const double* xin;   // interleaved block in (mode 0: T = L P)
+  double* xout;        // interleaved block out (modes 0, 1, 2)
+  const double* coef;  // [J][NB] (modes 1, 2)
+  const double* bsum_t;  // [NB][kHB] B^T T   (mode 0)
+  const double* bsum_w;  // [NB][kHB] B^T W   (mode 0, W = current basis block)
+  double sigma;
+  double* partials;    // [grid][J*NB] dots, or [grid][NB*(NB+kHB)] (mode 2)
+  unsigned* counter;
+  double* out;         // mode 2: [c*(NB+kHB) + j]: Gram row c (j < NB), B^T r_c (j = NB + s)
+};
+struct BlockQRArgs {
+  const double* nbo;   // mode-2 sweep output (Gram, B^T R)
+  const double* g2;    // Gram after pass 1 (NB*NB) or nullptr (single pass)
+  int J;               // first new basis column (= nv, columns orthogonalised against)
+  double* T;           // projected matrix (column-major, ldT) or nullptr (no record)
+  int ldT;
+  const double* c1;    // [nv][NB] CGS coefficients (pass 1, pass 2 may be nullptr)
+  const double* c2;
+  double* bs_v;        // out: B^T Q, [NB][kHB]
+  int* flag;           // breakdown flag
+  double bd_tol;       // absolute pivot tolerance
+  double rel_tol;      // relative pivot tolerance (ill-conditioned block)
+};
+void launch_spmm(const GraphDev& g, int nb, int vs, const int* split, int grid, const double* p, double* t,
+                 double* partials, unsigned* counter, double* bsum_t, cudaStream_t st);
+int bsweep_grid(int n);
+void launch_bsweep(int mode, int nb, const GraphDev& g, const ProjDesc& pd, const BlockSweepArgs& a, int grid,
+                   cudaStream_t st);
+void launch_bqr1(int nb, int n, double* R, const double* nbo, double* partials, unsigned* counter, double* g2,
+                 cudaStream_t st);
+void launch_bqr2(int nb, const GraphDev& g, const ProjDesc& pd, const double* R, const BlockQRArgs& qa, double* V,
+                 long long ld, double* p, cudaStream_t st);
+void launch_bgsum(int nb, const GraphDev& g, const double* x, double* partials, unsigned* counter, double* out,
+                  cudaStream_t st);
+void launch_bproject(int nb, const GraphDev& g, const ProjDesc& pd, const double* x, const double* bsum, double* y,
+                     cudaStream_t st);
+void launch_brandom(double* x, int n, int nb, uint64_t seed, unsigned c1, unsigned stream, cudaStream_t st);
 
 // ---- k-means ----------------------------------------------------------------------
 void launch_build_rows(const double* X, long long ldx, int n, int k, const double* s, double* H, cudaStream_t st);

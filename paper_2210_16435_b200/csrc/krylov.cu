@@ -12,9 +12,7 @@
 // Ritz GEMM (A10): Vout = V Y, register-blocked fp64 FMA (8 rows x 4 cols per
 // thread, 128 x 64 CTA tiles, k-chunks of 16 staged in shared memory).
 #include "device_common.cuh"
-
-#include <cuda.h>
-#include <cudaTypedefs.h>
+#include "tma.cuh"
 
 #include <algorithm>
 #include <atomic>
@@ -28,41 +26,6 @@ constexpr int kR = 64;       // rows per chunk
 constexpr int kMaxStages = 8;                // smem ring depth (runtime: as many as fit)
 constexpr int kTmaMaxJ = 192;
 constexpr size_t kRingBytes = 200 * 1024;    // dynamic shared memory budget for the ring
-
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void tensor2d_g2s(void* dst, const CUtensorMap* tmap, int x, int y, unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_addr(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_addr(bar))
-      : "memory");
-}
 
 // issue chunk `c` into stage buffer `buf` (warp 0): one 2-D tensor copy of the
 // (64 rows x J columns) basis box + one 1-D copy of the vector chunk, or (use2d
@@ -480,19 +443,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// tensor map over V viewed as 2-D [J columns][ld rows] (fp64), box {64 rows, J columns}
-static bool encode_basis_map(const SweepArgs& a, CUtensorMap* m) {
+bool encode_colmajor_map(const double* base, long long ld, int cols, int box_rows, CUtensorMap* m) {
   auto fn = get_encode();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)a.ld, (cuuint64_t)a.J};
-  cuuint64_t strides[1] = {(cuuint64_t)a.ld * sizeof(double)};
-  cuuint32_t box[2] = {(cuuint32_t)kR, (cuuint32_t)a.J};
+  if (!fn || cols < 1 || cols > 256) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)cols};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(a.V), dims, strides, box, estr,
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+// tensor map over V viewed as 2-D [J columns][ld rows] (fp64), box {64 rows, J columns}
+static bool encode_basis_map(const SweepArgs& a, CUtensorMap* m) { return encode_colmajor_map(a.V, a.ld, a.J, kR, m); }
 
 int g_tma_use2d = 1;
 

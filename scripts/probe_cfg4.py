@@ -22,6 +22,10 @@ ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--restarts", type=int, default=2)
 ap.add_argument("--applies", type=int, default=20)
 ap.add_argument("--vs", type=int, default=0)
+ap.add_argument("--bsz", type=int, default=1)
+ap.add_argument("--m", type=int, default=0)
+ap.add_argument("--keep", type=int, default=0)
+ap.add_argument("--skip-apply", action="store_true")
 args = ap.parse_args()
 
 t = time.time()
@@ -32,8 +36,8 @@ rp, ci, vv = (torch.from_numpy(a).to(dev) for a in (g.row_ptr, g.col, g.val))
 gr = torch.from_numpy(g.groups.astype(np.int32)).to(dev)
 k = cfg["k_eig"]
 ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, cfg["normalized"], h=g.h, max_restarts=args.restarts,
-                                 spmv_vector=args.vs)
-out = {"n": g.n, "nnz": g.nnz, "info": ctx.info()}
+                                 spmv_vector=args.vs, block_size=args.bsz, max_basis=args.m, keep=args.keep)
+out = {"n": g.n, "nnz": g.nnz, "info": ctx.info(), "bsz": args.bsz}
 # apply-only
 x = torch.randn((4, g.n), dtype=torch.float64, device=dev)
 y = torch.empty_like(x)
