@@ -82,8 +82,8 @@ typedef struct {
 /* Options of the extended build.  sfairsc_default_opts() fills defaults. */
 typedef struct {
   double sigma_override;  /* <= 0: sigma = ||L||_1; > 0: use this shift (must exceed lambda_k, Prop. 3.4) */
-  int32_t max_basis;      /* Lanczos basis size m; 0: max(2k+10, 20), capped at n */
-  int32_t keep;           /* Ritz vectors kept at a thick restart; 0: k + (m-k)/2 */
+  int32_t max_basis;      /* Lanczos basis size m; 0: min(192, max(2k+10, 3k, 20)) (SPEC S:342 suggests 2k+10), capped at n */
+  int32_t keep;           /* Ritz vectors kept at a thick restart; 0: k + 3(m-k)/5 (block: k + (m-k)/2) */
   int32_t max_restarts;   /* 0: 100000 */
   uint64_t start_seed;    /* Philox key for the Lanczos start / breakdown vectors */
   double tol_eff_cap;     /* residual target = min(tol, tol_eff_cap) * sigma; <= 0: 1e-10 (reading R7) */
@@ -93,6 +93,9 @@ typedef struct {
   int32_t block_size;     /* Lanczos block size b: 1 = single-vector thick-restart Lanczos; 2 or 4 = block
                              thick-restart Lanczos (SpMM on b interleaved vectors, block CGS2, CholQR2;
                              requires h <= 16); 0 = auto (DESIGN.md §Block Lanczos) */
+  int32_t reorth;         /* single-vector full reorthogonalisation: 1 = CGS2 (three basis sweeps per step),
+                             2 = lagged single sweep (one basis sweep per step, DESIGN.md §Single-sweep Lanczos;
+                             needs h <= 16, k < m <= min(192, n-h)); 0 = auto (2 where allowed, else 1) */
 } sfairsc_opts;
 
 typedef struct {

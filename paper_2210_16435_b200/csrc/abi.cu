@@ -19,6 +19,8 @@ namespace sfz {
 void symeig(int m, std::vector<double>& A, std::vector<double>& evals);
 sfairsc_status eigs_block(sfairsc_ctx* c, int k, double tol, double* evals_out, double* evecs_out,
                           int evecs_memspace, sfairsc_stats* stats);
+sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out, double* evecs_out,
+                           int evecs_memspace, sfairsc_stats* stats);
 sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, int32_t memspace, double* objective);
 }  // namespace sfz
 
@@ -87,7 +89,7 @@ static void free_ctx(sfairsc_ctx* c) {
   void* ptrs[] = {c->rp, c->ci, c->row_split, c->vv, c->dg, c->s, c->grp, c->isb, c->uh, c->partials, c->counters,
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
                   c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta,
-                  c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags};
+                  c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags, c->Hdev, c->sdev, c->lz, c->partials2, c->dd};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hp) cudaFreeHost(c->hp);
@@ -115,6 +117,7 @@ extern "C" void sfairsc_default_opts(sfairsc_opts* o) {
   o->check_symmetry = 1;
   o->spmv_vector = 0;
   o->block_size = 0;
+  o->reorth = 0;
 }
 
 extern "C" const char* sfairsc_last_error(void) { return g_err.c_str(); }
@@ -286,13 +289,15 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   }
   c->ldv = ((long long)n + 255) / 256 * 256;
   // Krylov basis size (SPEC S:342 default), capped so that v_{m+1} exists
-  int m = opts.max_basis > 0 ? opts.max_basis : std::max(2 * k + 10, 20);
+  // default basis: m = max(2k + 10, 3k, 20) (SPEC S:342 suggests 2k + 10; 3k measured faster at config 4,
+  // profiles/r1_exp), keep k + 3(m - k)/5 Ritz vectors per thick restart
+  int m = opts.max_basis > 0 ? opts.max_basis : std::min(192, std::max(std::max(2 * k + 10, 3 * k), 20));
   m = std::min(m, kMaxJ - 1);
   m = std::min(m, std::max(n - 1, 1));
   m = std::max(m, std::min(k + 1, n));
   if (m > n) m = n;
   c->m = m;
-  c->keep = opts.keep > 0 ? opts.keep : k + (m - k) / 2;
+  c->keep = opts.keep > 0 ? opts.keep : k + 3 * (m - k) / 5;
   c->keep = std::max(std::min(c->keep, m - 1), std::min(k, m - 1));
   // block Lanczos sizing: m + b <= kBMaxJ, m + b <= dim null(C^T) = n - h + 1, keep >= k, (m - keep) % b == 0
   c->bsz = opts.block_size > 0 ? opts.block_size : 1;
@@ -314,6 +319,11 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
       c->keep = kp;
     }
   }
+  // single-vector reorthogonalisation: 0 auto (= lagged single sweep), 1 CGS2 (three sweeps), 2 lagged
+  if (opts.reorth < 0 || opts.reorth > 2) return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth must be 0, 1 or 2"));
+  c->lagged = c->bsz == 1 && opts.reorth != 1 && hh <= kHB && m <= 192 && m <= n - hh && m > k;
+  if (opts.reorth == 2 && !c->lagged)
+    return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth=2 needs block_size 1, h <= 16 and k < m <= min(192, n-h)"));
 
   // device allocations
   CUB(dalloc(&c->rp, n + 1));
@@ -463,6 +473,17 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   CUB(dalloc(&c->tbeta, m + 1));
   CUB(dalloc(&c->X, (size_t)k * c->ldv));
   CUB(cudaMemsetAsync(c->X, 0, sizeof(double) * k * c->ldv, c->st));
+  if (c->lagged) {
+    c->ldT = m + 2;
+    CUB(dalloc(&c->Hdev, (size_t)c->ldT * c->ldT));
+    CUB(dalloc(&c->sdev, m + 2));
+    CUB(dalloc(&c->lz, 16));
+    CUB(cudaMemsetAsync(c->lz, 0, sizeof(double) * 16, c->st));
+    CUB(dalloc(&c->partials2, (size_t)c->num_sms * (kHB + 1) + 64));
+    CUB(dalloc(&c->dd, kMaxJ + 8));
+    CUB(dalloc(&c->bflags, kMaxJ + 8));
+    CUB(cudaMemsetAsync(c->bflags, 0, sizeof(int) * (kMaxJ + 8), c->st));
+  }
   if (c->bsz > 1) {  // block Lanczos buffers (m + bsz basis columns: V/Vb above hold m + 1 <= m + bsz)
     const int nbz = c->bsz;
     for (double** p : {&c->bP, &c->bT, &c->bR}) {
@@ -725,6 +746,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
   if (evecs_out && evecs_memspace != SFAIRSC_MEM_HOST && evecs_memspace != SFAIRSC_MEM_DEVICE)
     return fail(SFAIRSC_E_INVALID_ARG, "memspace");
   if (c->bsz > 1) return eigs_block(c, k, tol, evals_out, evecs_out, evecs_memspace, stats);
+  if (c->lagged) return eigs_lagged(c, k, tol, evals_out, evecs_out, evecs_memspace, stats);
   c->have_eigs = false;
   Lanczos L;
   L.c = c;

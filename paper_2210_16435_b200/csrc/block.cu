@@ -71,6 +71,9 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
   const int* __restrict__ rp = g.rp;
   const int* __restrict__ ci = g.ci;
   const double* __restrict__ vv = g.vv;
+  double ptacc[NB];  // p^T t (lane-0 rows)
+#pragma unroll
+  for (int c = 0; c < NB; ++c) ptacc[c] = 0.0;
   for (int base = r0; base < r1; base += NG) {
     const int row = base + gid;
     const bool valid = row < r1;
@@ -107,23 +110,35 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
       ld_row<NB>(p, row, pi);
       const double di = NORM ? 1.0 : __ldg(g.dg + row);
 #pragma unroll
-      for (int c = 0; c < NB; ++c) t[(size_t)row * NB + c] = fma(di, pi[c], -acc[c]);
+      for (int c = 0; c < NB; ++c) {
+        const double tc = fma(di, pi[c], -acc[c]);
+        t[(size_t)row * NB + c] = tc;
+        ptacc[c] = fma(pi[c], tc, ptacc[c]);
+      }
     }
   }
-  // epilogue: B^T t over this CTA's rows (fixed order), one vector at a time
+  // epilogue: B^T t and p^T t over this CTA's rows (fixed order), one vector at a time;
+  // out layout: bsum_t[c * kBT + s] = (B^T t_c)_s (s < kHB), bsum_t[c * kBT + kHB] = p_c^T t_c
 #pragma unroll 1
   for (int c = 0; c < NB; ++c) {
     __syncthreads();
-    double gacc[kHB];
+    double gacc[kBT];
 #pragma unroll
-    for (int q = 0; q < kHB; ++q) gacc[q] = 0.0;
+    for (int q = 0; q < kBT; ++q) gacc[q] = 0.0;
     for (int row = r0 + threadIdx.x; row < r1; row += kThreads) {
       const double ti = __ldcg(t + (size_t)row * NB + c);
-      add_group(gacc, g.grp[row], NORM ? g.s[row] * ti : ti);
+      const double v = NORM ? g.s[row] * ti : ti;
+      const int gg = g.grp[row];
+#pragma unroll
+      for (int q = 0; q < kHB; ++q)
+        if (q == gg) gacc[q] += v;
     }
-    block_reduce_store<kHB>(gacc, partials + ((size_t)blockIdx.x * NB + c) * kHB);
+#pragma unroll
+    for (int cc = 0; cc < NB; ++cc)
+      if (cc == c) gacc[kHB] = ptacc[cc];
+    block_reduce_store<kBT>(gacc, partials + ((size_t)blockIdx.x * NB + c) * kBT);
   }
-  ticket_finalize<NB * kHB>(partials, counter, bsum_t, NB * kHB);
+  ticket_finalize<NB * kBT>(partials, counter, bsum_t, NB * kBT);
 }
 
 // ----------------------------------------------------------------------------
@@ -178,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bsweep(GraphDev g, ProjDesc pd,
   }
   if (MODE == 0 && tid < NB) {  // thread c: gam_c = gamma(B^T t_c) - sigma gamma(B^T w_c)
     double gw[kHB];
-    gamma_serial(a.bsum_t + tid * kHB, 1.0, pd, gam[tid]);
+    gamma_serial(a.bsum_t + tid * kBT, 1.0, pd, gam[tid]);
     gamma_serial(a.bsum_w + tid * kHB, 1.0, pd, gw);
     for (int s = 0; s < pd.h; ++s) gam[tid][s] -= a.sigma * gw[s];
   }
@@ -445,8 +460,10 @@ __global__ void __launch_bounds__(kThreads) k_bqr2(GraphDev g, ProjDesc pd, cons
       }
     for (int c = 0; c < NB; ++c) gamma_serial(btq[c], 1.0, pd, gam[c]);
     if (blockIdx.x == 0) {
+      // the basis block is P q: B^T (P q) = B^T q - beta o gam (so that gamma(B^T w) = 0 in the next finish)
       for (int c = 0; c < NB; ++c)
-        for (int s = 0; s < kHB; ++s) qa.bs_v[c * kHB + s] = btq[c][s];
+        for (int s = 0; s < kHB; ++s)
+          qa.bs_v[c * kHB + s] = s < pd.h ? btq[c][s] - gam[c][s] / (pd.isb[s] * pd.isb[s]) : 0.0;
       if (qa.T) {
         const int nv = qa.J;  // expanded block = columns [nv - NB, nv)
         for (int c = 0; c < NB; ++c)
@@ -474,8 +491,9 @@ __global__ void __launch_bounds__(kThreads) k_bqr2(GraphDev g, ProjDesc pd, cons
       double s = 0.0;
 #pragma unroll
       for (int c2 = 0; c2 <= c; ++c2) s = fma(r[c2], Ui[c2][c], s);
-      V[(long long)(qa.J + c) * ld + i] = s;
-      p[(size_t)i * NB + c] = fma(-si, gam[c][gi], s);
+      const double pc = fma(-si, gam[c][gi], s);  // P q: the basis stays in range(P) to rounding
+      V[(long long)(qa.J + c) * ld + i] = pc;
+      p[(size_t)i * NB + c] = pc;
     }
   }
 }

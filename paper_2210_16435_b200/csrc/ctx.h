@@ -99,6 +99,9 @@ struct sfairsc_ctx {
   double *Tdev = nullptr, *g2 = nullptr;                // projected matrix (ldT = m + bsz), CholQR Gram
   int ldT = 0;
   int* bflags = nullptr;                                // per-step breakdown flags
+  // single-sweep (lagged) Lanczos (lanczos1.cu); uses ldT = m + 2 for H
+  bool lagged = false;
+  double *Hdev = nullptr, *sdev = nullptr, *lz = nullptr, *partials2 = nullptr, *dd = nullptr;
   // results
   bool have_eigs = false;
   int k_eigs = 0;

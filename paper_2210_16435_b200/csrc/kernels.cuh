@@ -9,6 +9,7 @@ namespace sfz {
 constexpr int kThreads = 256;  // CTA size of every streaming kernel
 constexpr int kHB = 16;        // group sums fused per kernel (h > 16: extra gsum passes)
 constexpr int kMaxJ = 512;     // max Krylov basis columns handled by the sweep kernels
+constexpr int kBT = kHB + 1;   // per-vector stride of the SpMV epilogue output: B^T t (kHB) and p^T t
 
 // Factored projector coefficients (DESIGN.md §Factored projector).
 //   b_s   = sum_{i in V_s} s_i x_i          (B^T x, B = [s o g_1 ... s o g_h])
@@ -49,7 +50,7 @@ void launch_gsum(const GraphDev& g, const double* x, int g_base, double* partial
 // p = x - s o gam(bsum, scale)_g
 void launch_project(const GraphDev& g, const ProjDesc& pd, const double* x, const double* bsum, double scale,
                     double* p, cudaStream_t st);
-// t = L p ; bsum_t[0..16) = B^T t (fused epilogue)
+// t = L p ; bsum_t[0..16) = B^T t, bsum_t[16] = p^T t (fused epilogue)
 void launch_spmv(const GraphDev& g, int vs, const int* row_split, int grid, const double* p, double* t,
                  double* partials, unsigned* counter, double* bsum_t, cudaStream_t st);
 // y = t - s o (gam_t - sigma gam_w)_g ;  optional dot w^T y -> *dot
@@ -125,7 +126,7 @@ struct BlockSweepArgs {
   const double* xin;   // interleaved block in (mode 0: T = L P)
   double* xout;        // interleaved block out (modes 0, 1, 2)
   const double* coef;  // [J][NB] (modes 1, 2)
-  const double* bsum_t;  // [NB][kHB] B^T T   (mode 0)
+  const double* bsum_t;  // [NB][kBT] B^T T (+ P^T T)   (mode 0)
   const double* bsum_w;  // [NB][kHB] B^T W   (mode 0, W = current basis block)
   double sigma;
   double* partials;    // [grid][J*NB] dots, or [grid][NB*(NB+kHB)] (mode 2)

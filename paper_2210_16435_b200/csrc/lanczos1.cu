@@ -1,0 +1,727 @@
+// libsfairsc — single-sweep thick-restart Lanczos (A7-A11 with ONE pass over
+// the Krylov basis per step).  Alg. 3 step 3 needs the k smallest
+// eigenpairs of L^sigma; the paper uses eigs and names
+// "orthonormalization of basis vectors" (O(nk^2)) as a main cost.
+//
+// Full reorthogonalisation is kept, but delayed by one step (the "lagged"
+// vector of low-synchronisation Gram-Schmidt): step j works with v~_j whose
+// projections s = V_j^T v~_j on the basis were measured by the previous pass.
+//   coef   (1 CTA): mu = sqrt(|v~|^2 - |s|^2); the previous column of the
+//                   projected matrix H absorbs the correction (H += s b~^T);
+//                   from z = V_j^T A v~_j = H^T s + mu^2 b~ (no pass needed)
+//                   and zeta = v~^T A v~ (SpMV epilogue) it forms the
+//                   coefficients of the corrected v_j = (v~ - V s)/mu and of
+//                   w = A v_j - V_j c - alpha v_j = y/mu - kappa v~ - V_j g.
+//   spmv   t = L P v~ (epilogue B^T t, p~^T t)                          (A5)
+//   update ONE TMA-fed sweep over V_j: writes v_j (basis column j) and w,
+//          and accumulates the dots [V_j, v_j]^T w (next step's s), |w|^2,
+//          B^T w                                                      (A6-A9)
+//   norm   v~_{j+1} = p~ = P (w/|w|), s_{j+1} = dots/|w|               (A4, A9)
+// The relation A V_j = V_j H_j + v_j b^T holds to rounding for the
+// coefficients actually used, so the Rayleigh-Ritz matrix sym(H) is exact
+// whatever way c was computed; v_j is orthogonal to V_j to O(eps) because
+// v~_j's own loss is only O(eps sigma / beta) (it came out of a projected
+// recurrence) and one measured projection removes it.  scripts/proto_lagged.py
+// is the same algorithm in numpy.
+#include "ctx.h"
+#include "device_common.cuh"
+#include "tma.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <vector>
+
+namespace sfz {
+
+void symeig(int m, std::vector<double>& A, std::vector<double>& evals);
+void bump_launch();
+
+namespace {
+constexpr int kR = 64;
+constexpr int kMaxStages = 8;
+constexpr size_t kRingBytes = 200 * 1024;
+constexpr int kLMaxJ = 191;  // basis columns swept (+1 new column in the dots: <= 192)
+
+// scalar slots of the device state `lz`
+enum { LZ_OMEGA = 0, LZ_PNORM2 = 1, LZ_AY = 2, LZ_AV = 3, LZ_MU = 4, LZ_INVMU = 5, LZ_BETA = 6 };
+}  // namespace
+
+struct LzDev {
+  double* H;       // (ldH x ldH) column-major; A V_j = V_j H[:j,:j] + v~_j H[j,:j] (lagged)
+  int ldH;
+  double* s;       // V_j^T v~_j (j entries)
+  double* lz;      // scalars (LZ_*)
+  double* cs;      // s / mu        (update coefficients of v_j)
+  double* cg;      // g             (update coefficients of w)
+  const double* bs_t;  // B^T t [kHB], p~^T t at [kHB]
+  const double* bs_v;  // B^T v~ [kHB]
+  int* flag;       // breakdown flag of this step
+  double sigma;
+  double bd_tol;
+};
+
+// ---------------------------------------------------------------------------
+// coefficient step (one CTA)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_lz_coef(LzDev d, int j) {
+  __shared__ double ss[kLMaxJ + 1], bt[kLMaxJ + 1], u[kLMaxJ + 1], v[kLMaxJ + 1], red[kThreads / 32][3];
+  __shared__ double sh_mu, sh_alpha, sh_kappa;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int ld = d.ldH;
+  for (int l = tid; l < j; l += kThreads) {
+    ss[l] = d.s[l];
+    bt[l] = d.H[(size_t)l * ld + j];  // row j: b~
+  }
+  __syncthreads();
+  // |s|^2, b~ . s
+  double a0 = 0.0, a1 = 0.0;
+  for (int l = tid; l < j; l += kThreads) {
+    a0 = fma(ss[l], ss[l], a0);
+    a1 = fma(bt[l], ss[l], a1);
+  }
+  a0 = warp_sum(a0);
+  a1 = warp_sum(a1);
+  if (lane == 0) {
+    red[w][0] = a0;
+    red[w][1] = a1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s2 = 0.0, bs = 0.0;
+    for (int q = 0; q < kThreads / 32; ++q) {
+      s2 += red[q][0];
+      bs += red[q][1];
+    }
+    const double omega = d.lz[LZ_OMEGA];
+    double mu2 = omega - s2;
+    int bad = 0;
+    if (!(mu2 > 1e-12 * omega)) {  // v~ (numerically) inside span(V_j): breakdown
+      bad = 2;
+      mu2 = 1.0;
+    }
+    sh_mu = sqrt(mu2);
+    red[0][2] = bs;
+    *d.flag = bad;
+  }
+  __syncthreads();
+  const double mu = sh_mu, bts = red[0][2];
+  // H[:j,:j] += s b~^T ; H[j,:j] = mu b~   (column c of H gets s * b~_c)
+  for (int e = tid; e < j * j; e += kThreads) {
+    const int c = e / j, r = e % j;
+    if (bt[c] != 0.0) d.H[(size_t)c * ld + r] = fma(ss[r], bt[c], d.H[(size_t)c * ld + r]);
+  }
+  __syncthreads();
+  for (int l = tid; l < j; l += kThreads) d.H[(size_t)l * ld + j] = mu * bt[l];
+  // u = H_j s (rows), v = H_j^T s (columns)
+  for (int l = tid; l < j; l += kThreads) {
+    double au = 0.0, av = 0.0;
+    for (int i = 0; i < j; ++i) {
+      au = fma(d.H[(size_t)i * ld + l], ss[i], au);
+      av = fma(d.H[(size_t)l * ld + i], ss[i], av);
+    }
+    u[l] = au;
+    v[l] = av;
+  }
+  __syncthreads();
+  // z = v + mu^2 b~ ; zeta = p~^T t + sigma (omega - |p~|^2)
+  a0 = 0.0;
+  a1 = 0.0;
+  for (int l = tid; l < j; l += kThreads) {
+    const double z = fma(mu * mu, bt[l], v[l]);
+    a0 = fma(ss[l], z, a0);      // s.z
+    a1 = fma(ss[l], u[l], a1);   // s.H s
+  }
+  a0 = warp_sum(a0);
+  a1 = warp_sum(a1);
+  __syncthreads();
+  if (lane == 0) {
+    red[w][0] = a0;
+    red[w][1] = a1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double sz = 0.0, shs = 0.0;
+    for (int q = 0; q < kThreads / 32; ++q) {
+      sz += red[q][0];
+      shs += red[q][1];
+    }
+    const double omega = d.lz[LZ_OMEGA];
+    const double zeta = d.bs_t[kHB] + d.sigma * (omega - d.lz[LZ_PNORM2]);
+    const double alpha = (zeta - 2.0 * sz + shs) / (mu * mu);
+    const double kappa = (alpha + bts) / mu;
+    sh_alpha = alpha;
+    sh_kappa = kappa;
+    d.H[(size_t)j * ld + j] = alpha;
+    d.lz[LZ_AY] = 1.0 / mu;
+    d.lz[LZ_AV] = -kappa;
+    d.lz[LZ_MU] = mu;
+    d.lz[LZ_INVMU] = 1.0 / mu;
+  }
+  __syncthreads();
+  const double kappa = sh_kappa;
+  for (int l = tid; l < j; l += kThreads) {
+    const double z = fma(mu * mu, bt[l], v[l]);
+    const double c = (z - u[l]) / mu;
+    d.H[(size_t)j * ld + l] = c;                  // column j: c
+    d.cs[l] = ss[l] / mu;                         // v_j = v~/mu - V (s/mu)
+    d.cg[l] = u[l] / mu + c - kappa * ss[l];      // w = y/mu - kappa v~ - V g
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the one sweep: v_j, w, dots [V_j, v_j]^T w, |w|^2, B^T w
+// stage (doubles): [J][kR] basis | v~[kR] | t[kR] | s[kR] | grp bytes (pad 128 B)
+// ---------------------------------------------------------------------------
+struct LzSweepArgs {
+  const double* V;
+  long long ld;
+  int J;
+  const double* vt;   // v~
+  const double* t;    // L p~
+  double* vj_out;     // V column J
+  double* w_out;
+  const double* cs;
+  const double* cg;
+  const double* lz;
+  const double* bs_t;
+  const double* bs_v;
+  double sigma;
+  double* partials;   // [grid][J+1]
+  double* partials2;  // [grid][1+kHB]
+  unsigned* counter;
+  double* nb;         // out: |w|^2, B^T w
+};
+
+__host__ __device__ constexpr size_t lz_stage_doubles(int J) { return (size_t)(J + 3) * kR + 16; }
+
+__device__ __forceinline__ void lz_issue(const LzSweepArgs& a, const GraphDev& g, const CUtensorMap* tmap, int c,
+                                         double* buf, unsigned long long* bar, int lane) {
+  const int J = a.J;
+  const long long row0 = (long long)c * kR;
+  unsigned bytes = (unsigned)((J + 2) * kR * sizeof(double)) + kR;
+  if (g.normalized) bytes += kR * sizeof(double);
+  if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+  __syncwarp();
+  if (lane == 0) {
+    if (J > 0) tensor2d_g2s(buf, tmap, (int)row0, 0, bar);
+    bulk_g2s(buf + (size_t)J * kR, a.vt + row0, kR * sizeof(double), bar);
+    bulk_g2s(buf + (size_t)(J + 1) * kR, a.t + row0, kR * sizeof(double), bar);
+  } else if (lane == 1) {
+    bulk_g2s(buf + (size_t)(J + 3) * kR, g.grp + row0, kR, bar);
+    if (g.normalized) bulk_g2s(buf + (size_t)(J + 2) * kR, g.s + row0, kR * sizeof(double), bar);
+  }
+}
+
+template <int MAXCW, bool NORM>
+__global__ void __launch_bounds__(kThreads, 1) k_lz_update(GraphDev g, ProjDesc pd, LzSweepArgs a, int kStages,
+                                                            const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) double dsm[];
+  __shared__ __align__(8) unsigned long long bars[kMaxStages];
+  __shared__ double cs[kLMaxJ + 1], cg[kLMaxJ + 1];
+  __shared__ double red[2][4][kR];
+  __shared__ double rw[kR], rv[kR];
+  __shared__ double gam[kHB];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int n = g.n, J = a.J;
+  const int nchunks = (n + kR - 1) / kR;
+  const size_t stage_elems = lz_stage_doubles(J);
+  for (int l = tid; l < J; l += kThreads) {
+    cs[l] = a.cs[l];
+    cg[l] = a.cg[l];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    double gw[kHB];
+    gamma_serial(a.bs_t, 1.0, pd, gam);  // y = t - s o (gam(B^T t) - sigma gam(B^T v~))_g
+    gamma_serial(a.bs_v, 1.0, pd, gw);
+    for (int s = 0; s < pd.h; ++s) gam[s] -= a.sigma * gw[s];
+  }
+  __syncthreads();
+  const double ay = a.lz[LZ_AY], av = a.lz[LZ_AV], invmu = a.lz[LZ_INVMU];
+  const int my_chunks = (nchunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  if (w == 0)
+    for (int it = 0; it < kStages && it < my_chunks; ++it)
+      lz_issue(a, g, &tmap, blockIdx.x + it * gridDim.x, dsm + it * stage_elems, &bars[it], lane);
+
+  double colacc[MAXCW];
+#pragma unroll
+  for (int cc = 0; cc < MAXCW; ++cc) colacc[cc] = 0.0;
+  double v2[1 + kHB];
+#pragma unroll
+  for (int q = 0; q < 1 + kHB; ++q) v2[q] = 0.0;
+
+  for (int it = 0; it < my_chunks; ++it) {
+    const int c = blockIdx.x + it * gridDim.x;
+    const int st = it % kStages;
+    const double* buf = dsm + st * stage_elems;
+    mbar_wait(&bars[st], (unsigned)((it / kStages) & 1));
+    const double* vts = buf + (size_t)J * kR;
+    const double* ts = vts + kR;
+    const double* ssc = ts + kR;
+    const uint8_t* gs = reinterpret_cast<const uint8_t*>(ssc + kR);
+    const long long row0 = (long long)c * kR;
+    {
+      const int i = tid % kR, cgp = tid / kR;
+      double ps = 0.0, pg = 0.0;
+      for (int l = cgp; l < J; l += 4) {
+        const double vv = buf[(size_t)l * kR + i];
+        ps = fma(vv, cs[l], ps);
+        pg = fma(vv, cg[l], pg);
+      }
+      red[0][cgp][i] = ps;
+      red[1][cgp][i] = pg;
+    }
+    __syncthreads();
+    if (tid < kR) {
+      const long long gi = row0 + tid;
+      double wv = 0.0, vj = 0.0;
+      if (gi < n) {
+        const double sumS = ((red[0][0][tid] + red[0][1][tid]) + red[0][2][tid]) + red[0][3][tid];
+        const double sumG = ((red[1][0][tid] + red[1][1][tid]) + red[1][2][tid]) + red[1][3][tid];
+        const double vti = vts[tid];
+        vj = fma(vti, invmu, -sumS);
+        const int gg = gs[tid];
+        const double y = NORM ? fma(-ssc[tid], gam[gg], ts[tid]) : ts[tid] - gam[gg];
+        wv = fma(ay, y, fma(av, vti, -sumG));
+        a.vj_out[gi] = vj;
+        a.w_out[gi] = wv;
+        v2[0] = fma(wv, wv, v2[0]);
+        const double sv = NORM ? ssc[tid] * wv : wv;
+#pragma unroll
+        for (int q = 0; q < kHB; ++q)
+          if (q == gg) v2[1 + q] += sv;
+      }
+      rw[tid] = wv;
+      rv[tid] = vj;
+    }
+    __syncthreads();
+    {
+      const double r0 = rw[lane], r1 = rw[lane + 32];
+#pragma unroll
+      for (int cc = 0; cc < MAXCW; ++cc) {
+        const int l = w + cc * (kThreads / 32);
+        if (l <= J) {
+          const double* col = (l < J) ? buf + (size_t)l * kR : rv;
+          colacc[cc] = fma(col[lane + 32], r1, fma(col[lane], r0, colacc[cc]));
+        }
+      }
+    }
+    __syncthreads();
+    if (w == 0 && it + kStages < my_chunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      lz_issue(a, g, &tmap, blockIdx.x + (it + kStages) * gridDim.x, dsm + st * stage_elems, &bars[st], lane);
+    }
+  }
+#pragma unroll
+  for (int cc = 0; cc < MAXCW; ++cc) {
+    const int l = w + cc * (kThreads / 32);
+    const double s = warp_sum(colacc[cc]);
+    if (lane == 0 && l <= J) a.partials[(size_t)blockIdx.x * (J + 1) + l] = s;
+  }
+  block_reduce_store<1 + kHB>(v2, a.partials2 + (size_t)blockIdx.x * (1 + kHB));
+  ticket_finalize<1 + kHB>(a.partials2, a.counter, a.nb, 1 + min(pd.h, kHB));
+}
+
+// ---------------------------------------------------------------------------
+// normalise: v~ = w/|w|, p~ = P v~, B^T v~, s = dots/|w|, |p~|^2, H row j+1
+// ---------------------------------------------------------------------------
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) k_lz_norm(GraphDev g, ProjDesc pd, const double* __restrict__ w,
+                                                      const double* nb, const double* dots, int nd, LzDev d, int jrow,
+                                                      double* __restrict__ vt, double* __restrict__ p, double* bs_v) {
+  __shared__ double gam[kHB];
+  __shared__ double s_inv;
+  if (threadIdx.x == 0) {
+    double beta = sqrt(nb[0]);
+    if (!(beta > d.bd_tol)) {
+      if (blockIdx.x == 0) atomicOr(d.flag, 1);
+      beta = 1.0;
+    }
+    s_inv = 1.0 / beta;
+    gamma_serial(nb + 1, s_inv, pd, gam);
+    if (blockIdx.x == 0) {
+      // v~ = P (w / |w|): the lagged vector is kept in range(P) (no drift out of null(C^T));
+      // B^T v~ = B^T w/|w| - beta o gam,  |v~|^2 = |w|^2/|w|^2 - sum_s beta_s gam_s^2
+      double q2 = 0.0;
+      for (int s = 0; s < pd.h; ++s) {
+        const double bet = 1.0 / (pd.isb[s] * pd.isb[s]);
+        bs_v[s] = nb[1 + s] * s_inv - bet * gam[s];
+        q2 += bet * gam[s] * gam[s];
+      }
+      const double omega = nb[0] * s_inv * s_inv - q2;
+      d.lz[LZ_OMEGA] = omega;
+      d.lz[LZ_PNORM2] = omega;
+      d.lz[LZ_BETA] = beta;
+    }
+  }
+  __syncthreads();
+  const double inv = s_inv;
+  if (blockIdx.x == 0) {
+    for (int l = threadIdx.x; l < nd; l += blockDim.x) d.s[l] = dots[l] * inv;
+    if (jrow >= 0)  // row jrow of H: b~ = beta e_{jrow-1}
+      for (int l = threadIdx.x; l < jrow; l += blockDim.x)
+        d.H[(size_t)l * d.ldH + jrow] = (l == jrow - 1) ? 1.0 / inv : 0.0;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const double vi = w[i] * inv;
+    const double gi = gam[g.grp[i]];
+    const double pi = NORM ? fma(-g.s[i], gi, vi) : vi - gi;
+    vt[i] = pi;
+    p[i] = pi;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static int lz_sgrid(int n) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return std::max(1, std::min((n + kThreads - 1) / kThreads, sms * 8));
+}
+
+template <int MAXCW, bool NORM>
+static void lz_update_launch(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st) {
+  const size_t stage = lz_stage_doubles(a.J) * sizeof(double);
+  const int stages = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, kRingBytes / stage));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_lz_update<MAXCW, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(kRingBytes, 2 * lz_stage_doubles(kLMaxJ) * sizeof(double)));
+    attr = true;
+  }
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  if (a.J > 0) encode_colmajor_map(a.V, a.ld, a.J, kR, &tmap);
+  k_lz_update<MAXCW, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap);
+}
+template <bool NORM>
+static void lz_update_m(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st) {
+  if (a.J + 1 <= 64) lz_update_launch<8, NORM>(g, pd, a, grid, st);
+  else if (a.J + 1 <= 128) lz_update_launch<16, NORM>(g, pd, a, grid, st);
+  else lz_update_launch<24, NORM>(g, pd, a, grid, st);
+}
+
+// ---------------------------------------------------------------------------
+// driver
+// ---------------------------------------------------------------------------
+namespace {
+struct Lagged {
+  sfairsc_ctx* c;
+  int m, keep, k;
+  int64_t applies = 0, steps = 0, restarts = 0, breakdowns = 0;
+  unsigned inject = 0;
+  double bd_tol = 0.0;
+
+  LzDev dev(int j) const {
+    LzDev d{};
+    d.H = c->Hdev;
+    d.ldH = c->ldT;
+    d.s = c->sdev;
+    d.lz = c->lz;
+    d.cs = c->c1;
+    d.cg = c->c2;
+    d.bs_t = c->bs_t;
+    d.bs_v = c->bs_v;
+    d.flag = c->bflags + j;
+    d.sigma = c->sigma;
+    d.bd_tol = bd_tol;
+    return d;
+  }
+
+  void norm(const double* w, const double* dots, int nd, int jrow, int flag_idx) {
+    ProfScope ps(c, K_NORMALIZE, 3 * c->vb() + c->sgb());
+    LzDev d = dev(flag_idx);
+    bump_launch();
+    if (c->normalized)
+      k_lz_norm<true><<<lz_sgrid(c->n), kThreads, 0, c->st>>>(c->g(), c->pd(), w, c->nb, dots, nd, d, jrow, c->vr,
+                                                              c->vp, c->bs_v);
+    else
+      k_lz_norm<false><<<lz_sgrid(c->n), kThreads, 0, c->st>>>(c->g(), c->pd(), w, c->nb, dots, nd, d, jrow, c->vr,
+                                                               c->vp, c->bs_v);
+  }
+
+  // one Lanczos step at column j (A5-A9)
+  sfairsc_status step(int j) {
+    {
+      ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
+      launch_spmm(c->g(), 1, c->vs, c->row_split, c->spmv_grid, c->vp, c->vt, c->partials, c->counters + 1, c->bs_t,
+                  c->st);  // epilogue: B^T t and p~^T t (bs_t[kHB])
+    }
+    {
+      ProfScope ps(c, K_OTHER, 0.0);
+      bump_launch();
+      k_lz_coef<<<1, kThreads, 0, c->st>>>(dev(j), j);
+    }
+    {
+      ProfScope ps(c, K_UPDDOT, (j + 4) * c->vb() + c->sgb());
+      LzSweepArgs a{};
+      a.V = c->V;
+      a.ld = c->ldv;
+      a.J = j;
+      a.vt = c->vr;
+      a.t = c->vt;
+      a.vj_out = c->V + (long long)j * c->ldv;
+      a.w_out = c->vy;
+      a.cs = c->c1;
+      a.cg = c->c2;
+      a.lz = c->lz;
+      a.bs_t = c->bs_t;
+      a.bs_v = c->bs_v;
+      a.sigma = c->sigma;
+      a.partials = c->partials;
+      a.partials2 = c->partials2;
+      a.counter = c->counters + 6;
+      a.nb = c->nb;
+      const int G = sweep_tma_grid(c->n, c->num_sms);
+      bump_launch();
+      if (c->normalized) lz_update_m<true>(c->g(), c->pd(), a, G, c->st);
+      else lz_update_m<false>(c->g(), c->pd(), a, G, c->st);
+      launch_reduce_cols(c->partials, G, j + 1, c->dd, c->st);
+    }
+    norm(c->vy, c->dd, j + 1, j + 1, j);
+    CHECK_LAUNCH();
+    applies++;
+    steps++;
+    return SFAIRSC_OK;
+  }
+
+  // v~_j = random vector, projected, CGS2 (twice) against V[:, 0:j], normalised; s = 0, no coupling
+  sfairsc_status random_start(int j) {
+    const GraphDev g = c->g();
+    for (int attempt = 0; attempt < 5; ++attempt) {
+      launch_random(c->vt, c->n, c->seed, 4096u + inject++, 7u, c->st);
+      for (int gb = 0; gb < c->h; gb += kHB) launch_gsum(g, c->vt, gb, c->partials, c->counters + 3, c->bs_w, c->st);
+      launch_project(g, c->pd(), c->vt, c->bs_w, 1.0, c->vy, c->st);
+      // CGS2 twice with the three-sweep kernels (mode 3 dots, mode 1 update+dots, mode 2 update+norm)
+      for (int rep = 0; rep < (j > 0 ? 2 : 1); ++rep) {
+        SweepArgs a{};
+        a.V = c->V;
+        a.ld = c->ldv;
+        a.J = j;
+        a.xin = c->vy;
+        a.xout = c->vy;
+        a.bsum_t = c->bs_t;
+        a.bsum_w = c->bs_v;
+        a.sigma = c->sigma;
+        a.partials = c->partials;
+        a.counter = c->counters + 2;
+        a.norm_bsum = c->nb;
+        if (j > 0) {
+          launch_sweep(3, g, c->pd(), a, c->sgrid, c->st);
+          launch_reduce_cols(c->partials, c->sgrid, j, c->c1, c->st);
+          a.coef = c->c1;
+          launch_sweep(1, g, c->pd(), a, c->sgrid, c->st);
+          launch_reduce_cols(c->partials, c->sgrid, j, c->c2, c->st);
+        }
+        a.coef = c->c2;
+        launch_sweep(2, g, c->pd(), a, c->sgrid, c->st);
+        if (c->h > kHB)
+          for (int gb = kHB; gb < c->h; gb += kHB)
+            launch_gsum(g, c->vy, gb, c->partials, c->counters + 3, c->nb + 1, c->st);
+      }
+      CU(cudaMemsetAsync(c->bflags + kMaxJ, 0, sizeof(int), c->st));
+      norm(c->vy, nullptr, 0, -1, kMaxJ);
+      CU(cudaMemsetAsync(c->sdev, 0, sizeof(double) * (j + 1), c->st));
+      // no coupling of the injected vector to the basis: H row j = 0
+      std::vector<double> zero(std::max(j, 1), 0.0);
+      if (j > 0)
+        CU(cudaMemcpy2DAsync(c->Hdev + j, sizeof(double) * c->ldT, zero.data(), sizeof(double), sizeof(double), j,
+                             cudaMemcpyHostToDevice, c->st));
+      int flag = 0;
+      CU(cudaMemcpyAsync(c->hp, c->bflags + kMaxJ, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+      CU(cudaStreamSynchronize(c->st));
+      std::memcpy(&flag, c->hp, sizeof(int));
+      if (!flag) return SFAIRSC_OK;
+    }
+    return fail(SFAIRSC_E_NO_CONVERGENCE, "could not generate a random vector outside the Krylov basis");
+  }
+};
+}  // namespace
+
+sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out, double* evecs_out,
+                           int evecs_memspace, sfairsc_stats* stats) {
+  const double t0 = now_s();
+  c->have_eigs = false;
+  Lagged L;
+  L.c = c;
+  L.m = c->m;
+  L.k = k;
+  L.keep = c->keep;
+  const int m = L.m, keep = L.keep, n = c->n, ldH = c->ldT;
+  const double tol_eff = std::min(tol, c->tol_cap);
+  const double target = tol_eff * c->sigma;
+  L.bd_tol = std::min(1e-12, 0.01 * tol_eff) * c->sigma;
+  CU(cudaMemsetAsync(c->Hdev, 0, sizeof(double) * ldH * ldH, c->st));
+  CU(cudaMemsetAsync(c->bflags, 0, sizeof(int) * (kMaxJ + 8), c->st));
+  TRY(L.random_start(0));
+  int j = 0, jsync = 0;
+  bool converged = false;
+  std::vector<double> theta, Y, Hh((size_t)ldH * ldH), sh(m + 2);
+  double gap = std::numeric_limits<double>::quiet_NaN();
+  double max_resid = std::numeric_limits<double>::infinity();
+  for (;;) {
+    while (j < m) TRY(L.step(j++));
+    // ---- sync ----
+    CU(cudaMemcpyAsync(Hh.data(), c->Hdev, sizeof(double) * ldH * ldH, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(sh.data(), c->sdev, sizeof(double) * m, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(c->hp, c->lz, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(c->hp + 8, c->bflags, sizeof(int) * (m + 1), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    if (c->prof.on) c->prof.resolve();
+    int jb = -1;
+    {
+      const int* fl = reinterpret_cast<const int*>(c->hp + 8);
+      for (int q = jsync; q < m; ++q)
+        if (fl[q]) {
+          jb = q;
+          break;
+        }
+    }
+    if (jb >= 0) {
+      // flag 2 (coef): v~_jb numerically inside span(V_jb): columns 0..jb-1 valid, new v~_jb.
+      // flag 1 (norm): |w| <= bd_tol, span(V_{jb+1}) invariant: columns 0..jb valid, new v~_{jb+1}.
+      const int* fl = reinterpret_cast<const int*>(c->hp + 8);
+      const int jn = (fl[jb] & 2) ? jb : jb + 1;
+      if (c->debug) fprintf(stderr, "[sfairsc] lagged breakdown at step %d (flag %d)\n", jb, fl[jb]);
+      L.breakdowns++;
+      CU(cudaMemsetAsync(c->bflags, 0, sizeof(int) * (kMaxJ + 8), c->st));
+      TRY(L.random_start(jn));
+      j = jn;
+      jsync = j;
+      continue;
+    }
+    // ---- Rayleigh-Ritz on sym(H_m + s b~^T) ----
+    const double om = c->hp[LZ_OMEGA];
+    double s2 = 0.0;
+    for (int l = 0; l < m; ++l) s2 += sh[l] * sh[l];
+    double mu = std::sqrt(std::max(om - s2, 0.0));
+    if (!(mu > 0.0)) mu = 1.0;
+    std::vector<double> bt(m), A((size_t)m * m);
+    for (int l = 0; l < m; ++l) bt[l] = Hh[(size_t)l * ldH + m];
+    for (int r = 0; r < m; ++r)
+      for (int q = 0; q < m; ++q) {
+        const double hrq = Hh[(size_t)q * ldH + r] + sh[r] * bt[q];
+        const double hqr = Hh[(size_t)r * ldH + q] + sh[q] * bt[r];
+        A[(size_t)r * m + q] = 0.5 * (hrq + hqr);
+      }
+    Y = A;
+    symeig(m, Y, theta);
+    double maxres = 0.0;
+    std::vector<double> bY(m, 0.0);
+    for (int i = 0; i < m; ++i) {
+      double acc = 0.0;
+      for (int l = 0; l < m; ++l) acc += bt[l] * Y[(size_t)l * m + i];
+      bY[i] = mu * acc;  // b = mu b~ : coupling of Ritz vector i to v_m
+    }
+    for (int i = 0; i < k; ++i) maxres = std::max(maxres, std::fabs(bY[i]));
+    if (k < m) gap = theta[k] - theta[k - 1];
+    converged = maxres <= target;
+    if (c->debug)
+      fprintf(stderr, "[sfairsc] lagged RR restarts=%lld steps=%lld maxres=%g target=%g theta_k=%.17g mu=%g\n",
+              (long long)L.restarts, (long long)L.steps, maxres, target, theta[k - 1], mu);
+    if (converged || L.restarts >= c->max_restarts) {
+      std::vector<double> Yc((size_t)m * k);
+      for (int cc = 0; cc < k; ++cc)
+        for (int l = 0; l < m; ++l) Yc[(size_t)cc * m + l] = Y[(size_t)l * m + cc];
+      CU(cudaMemcpyAsync(c->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, c->st));
+      {
+        ProfScope ps(c, K_RITZ, (double)(m + k) * c->vb());
+        launch_ritz(c->V, c->ldv, n, m, c->Ydev, k, c->X, c->st);
+      }
+      CHECK_LAUNCH();
+      break;
+    }
+    // ---- thick restart: [V_m Y_keep, v_m], v_m = (v~ - V_m s)/mu as one GEMM with v~ in column m ----
+    CU(cudaMemcpyAsync(c->V + (long long)m * c->ldv, c->vr, sizeof(double) * c->ldv, cudaMemcpyDeviceToDevice,
+                       c->st));
+    const int me = m + 1, pe = keep + 1;
+    std::vector<double> Yc((size_t)me * pe, 0.0);
+    for (int cc = 0; cc < keep; ++cc)
+      for (int l = 0; l < m; ++l) Yc[(size_t)cc * me + l] = Y[(size_t)l * m + cc];
+    for (int l = 0; l < m; ++l) Yc[(size_t)keep * me + l] = -sh[l] / mu;
+    Yc[(size_t)keep * me + m] = 1.0 / mu;
+    CU(cudaMemcpyAsync(c->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, c->st));
+    {
+      ProfScope ps(c, K_RITZ, (double)(me + pe) * c->vb());
+      launch_ritz(c->V, c->ldv, n, me, c->Ydev, pe, c->Vb, c->st);
+    }
+    CHECK_LAUNCH();
+    std::swap(c->V, c->Vb);
+    // state at j = keep: v~ = v_m exactly (s = 0), coupling row b~ = (b Y)_i for the kept vectors
+    std::fill(Hh.begin(), Hh.end(), 0.0);
+    for (int i = 0; i < keep; ++i) {
+      Hh[(size_t)i * ldH + i] = theta[i];
+      Hh[(size_t)i * ldH + keep] = bY[i];
+    }
+    CU(cudaMemcpyAsync(c->Hdev, Hh.data(), sizeof(double) * ldH * ldH, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemsetAsync(c->sdev, 0, sizeof(double) * (m + 2), c->st));
+    {
+      // v~ <- column keep; p~ = P v~; B^T v~; omega, |p~|^2 via the normalise kernel (|v|^2 and B^T v first)
+      SweepArgs a{};
+      a.V = c->V;
+      a.ld = c->ldv;
+      a.J = 0;
+      a.xin = c->V + (long long)keep * c->ldv;
+      a.xout = c->vy;
+      a.bsum_t = c->bs_t;
+      a.bsum_w = c->bs_v;
+      a.partials = c->partials;
+      a.counter = c->counters + 2;
+      a.norm_bsum = c->nb;
+      launch_sweep(2, c->g(), c->pd(), a, c->sgrid, c->st);  // J = 0: copy + |v|^2 + B^T v
+      if (c->h > kHB)
+        for (int gb = kHB; gb < c->h; gb += kHB)
+          launch_gsum(c->g(), c->vy, gb, c->partials, c->counters + 3, c->nb + 1, c->st);
+      L.norm(c->vy, nullptr, 0, -1, kMaxJ);
+    }
+    CHECK_LAUNCH();
+    j = keep;
+    jsync = keep;
+    L.restarts++;
+  }
+
+  TRY(true_residuals(c, theta.data(), k, &max_resid));
+  L.applies += k;
+  if (c->prof.on) c->prof.resolve();
+  c->evals.assign(theta.begin(), theta.begin() + k);
+  c->k_eigs = k;
+  c->have_eigs = true;
+  for (int i = 0; i < k; ++i) evals_out[i] = theta[i];
+  if (evecs_out) {
+    const cudaMemcpyKind kind = evecs_memspace == SFAIRSC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CU(cudaMemcpy2DAsync(evecs_out, sizeof(double) * n, c->X, sizeof(double) * c->ldv, sizeof(double) * n, k, kind,
+                         c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
+  sfairsc_stats S{};
+  S.applies = L.applies;
+  S.steps = L.steps;
+  S.restarts = L.restarts;
+  S.breakdowns = L.breakdowns;
+  S.sigma = c->sigma;
+  S.max_resid_rel = max_resid;
+  S.gap_est = gap;
+  S.t_build_s = c->t_build;
+  S.t_eigs_s = now_s() - t0;
+  S.converged = converged ? 1 : 0;
+  S.basis_size = m;
+  S.kept = keep;
+  c->last = S;
+  if (stats) *stats = S;
+  if (!converged) return fail(SFAIRSC_E_NO_CONVERGENCE, "no convergence after %lld restarts", (long long)L.restarts);
+  if (theta[k - 1] >= c->sigma * (1.0 - 1e-8))
+    return fail(SFAIRSC_E_SHIFT_TOO_SMALL, "lambda_k=%g >= sigma(1-1e-8)=%g (Prop. 3.4)", theta[k - 1], c->sigma);
+  return SFAIRSC_OK;
+}
+
+}  // namespace sfz

@@ -48,7 +48,7 @@ class Opts(C.Structure):
     _fields_ = [("sigma_override", C.c_double), ("max_basis", C.c_int32), ("keep", C.c_int32),
                 ("max_restarts", C.c_int32), ("start_seed", C.c_uint64), ("tol_eff_cap", C.c_double),
                 ("cuda_stream", C.c_void_p), ("check_symmetry", C.c_int32), ("spmv_vector", C.c_int32),
-                ("block_size", C.c_int32)]
+                ("block_size", C.c_int32), ("reorth", C.c_int32)]
 
 
 class Stats(C.Structure):

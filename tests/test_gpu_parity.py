@@ -79,8 +79,13 @@ def test_operator_device_tensors(gpu_lib):
     ctx.close()
 
 
-def _check_eigs(lib, g, k, normalized, tol, dense=None, ref_evals=None, ref_X=None, gap=None):
-    ctx = _ctx(lib, g, k, normalized)
+# eigensolver variants of the C ABI (sfairsc_opts): the default (single-sweep lagged
+# reorthogonalisation where allowed), three-sweep CGS2, and block Lanczos with b = 2
+SOLVERS = {"default": {}, "cgs2": {"reorth": 1}, "block2": {"block_size": 2}}
+
+
+def _check_eigs(lib, g, k, normalized, tol, dense=None, ref_evals=None, ref_X=None, gap=None, **kw):
+    ctx = _ctx(lib, g, k, normalized, **kw)
     ev, Xt, st = lib.sfairsc_eigs(ctx, k, tol)
     X = Xt.T
     sigma = st["sigma"]
@@ -105,28 +110,31 @@ def _check_eigs(lib, g, k, normalized, tol, dense=None, ref_evals=None, ref_X=No
     return ev, X, st
 
 
-def test_eigs_config1_vs_dense_fairsc(gpu_lib):
+@pytest.mark.parametrize("solver", list(SOLVERS))
+def test_eigs_config1_vs_dense_fairsc(gpu_lib, solver):
     g, cfg = baseline_config(1)
     dense = fairsc.fairsc_dense(g.dense(), g.groups, g.h, cfg["k_eig"], cfg["normalized"])
-    _check_eigs(gpu_lib, g, cfg["k_eig"], cfg["normalized"], cfg["tol"], dense=dense)
+    _check_eigs(gpu_lib, g, cfg["k_eig"], cfg["normalized"], cfg["tol"], dense=dense, **SOLVERS[solver])
 
 
 @pytest.mark.parametrize("n,h,normalized,k,seed", [(200, 2, True, 4, 1), (513, 5, False, 6, 2),
                                                    (400, 3, True, 8, 3), (300, 1, False, 5, 4),
                                                    (1500, 20, True, 5, 5)])
-def test_eigs_random_vs_dense(gpu_lib, n, h, normalized, k, seed):
+@pytest.mark.parametrize("solver", list(SOLVERS))
+def test_eigs_random_vs_dense(gpu_lib, n, h, normalized, k, seed, solver):
     g = random_graph(n, h, p=min(0.5, 8.0 / n), seed=seed, weights="uniform")
     dense = fairsc.fairsc_dense(g.dense(), g.groups, h, k, normalized)
-    _check_eigs(gpu_lib, g, k, normalized, 1e-10, dense=dense)
+    _check_eigs(gpu_lib, g, k, normalized, 1e-10, dense=dense, **SOLVERS[solver])
 
 
+@pytest.mark.parametrize("solver", list(SOLVERS))
 @pytest.mark.parametrize("normalized", [False, True])
-def test_eigs_planted_cliques_closed_form(gpu_lib, normalized):
+def test_eigs_planted_cliques_closed_form(gpu_lib, normalized, solver):
     """Disconnected planted graph (P-closed-1): spec = {0^k, m or m/(m-1)},
     eigenspace span{1_{C_l}} (D^{1/2} 1_{C_l}).  Exercises Lanczos breakdown."""
     k, m, h = 4, 6, 3
     g = planted_cliques(k, m, h, seed=7)
-    ev, X, st = _check_eigs(gpu_lib, g, k, normalized, 1e-10, ref_evals=np.zeros(k))
+    ev, X, st = _check_eigs(gpu_lib, g, k, normalized, 1e-10, ref_evals=np.zeros(k), **SOLVERS[solver])
     d = np.diff(g.row_ptr).astype(float)
     E = np.zeros((g.n, k))
     E[np.arange(g.n), g.clusters] = 1.0
@@ -149,13 +157,20 @@ def test_eigs_deterministic(gpu_lib):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
-def test_eigs_config2_vs_tier_s(gpu_lib):
+@pytest.fixture(scope="module")
+def config2_ref():
     g, cfg = baseline_config(2)
     k = cfg["k_eig"]
     op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, True)
-    ref = sfairsc_cpu.sfairsc_arpack(op, k, tol=1e-13, seed=2)
+    return g, cfg, sfairsc_cpu.sfairsc_arpack(op, k, tol=1e-13, seed=2)
+
+
+@pytest.mark.parametrize("solver", list(SOLVERS))
+def test_eigs_config2_vs_tier_s(gpu_lib, config2_ref, solver):
+    g, cfg, ref = config2_ref
+    k = cfg["k_eig"]
     gap = ref.evals[k] - ref.evals[k - 1]
-    _check_eigs(gpu_lib, g, k, True, cfg["tol"], ref_evals=ref.evals[:k], ref_X=ref.X, gap=gap)
+    _check_eigs(gpu_lib, g, k, True, cfg["tol"], ref_evals=ref.evals[:k], ref_X=ref.X, gap=gap, **SOLVERS[solver])
 
 
 # --- error vocabulary ----------------------------------------------------------
