@@ -263,6 +263,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   if (getenv("SFAIRSC_TMA_MODE2")) c->tma_mode2 = atoi(getenv("SFAIRSC_TMA_MODE2"));
   if (getenv("SFAIRSC_RITZ")) sfz::g_ritz_kind = atoi(getenv("SFAIRSC_RITZ"));
   if (getenv("SFAIRSC_SPMV")) sfz::g_spmv_kind = atoi(getenv("SFAIRSC_SPMV"));
+  if (getenv("SFAIRSC_LZ_SWEEP")) sfz::g_lz_sweep = atoi(getenv("SFAIRSC_LZ_SWEEP"));
   if (c->sweep_kind == 3) {  // TMA with one 1-D copy per column (A/B only)
     sfz::g_tma_use2d = 0;
     c->sweep_kind = 2;

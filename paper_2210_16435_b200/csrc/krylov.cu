@@ -425,6 +425,115 @@ __global__ void __launch_bounds__(kThreads) k_ritz_dmma(const double* __restrict
 }
 
 // ---------------------------------------------------------------------------
+// Ritz GEMM v2 (default): Vout = V Y on the fp64 tensor cores (DMMA
+// m8n8k4), CTA tile 128 rows x 128 columns so V is streamed once for p <= 128,
+// 8 warps as 4 (rows) x 2 (cols), each 32 x 64 = 4 x 8 DMMA tiles.  The V
+// tile (16 columns x 128 rows) arrives by cp.async into a double-buffered
+// shared-memory ring; the Y tile (column-major m x p, 16 k x 128 cols) is
+// register-staged and stored transposed.  Shared-memory row stride 136
+// doubles (= 8 mod 16): every fragment load is 2 wavefronts (conflict-free).
+// ---------------------------------------------------------------------------
+constexpr int kGM = 128, kGN = 128, kGK = 16, kGS = 136;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __restrict__ V, long long ld, int n, int m,
+                                                            const double* __restrict__ Y, int p,
+                                                            double* __restrict__ Vout) {
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;                      // [2][kGK][kGS]
+  double* Bs = gsm + 2 * kGK * kGS;      // [2][kGK][kGS]
+  const int col0 = blockIdx.x * kGN;
+  const long long row0 = (long long)blockIdx.y * kGM;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wr = w & 3, wc = w >> 2;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int nk = (m + kGK - 1) / kGK;
+  // B staging: thread -> (col = tid / 2, 8 consecutive k starting at (tid & 1) * 8)
+  const int bcol = tid >> 1, bk0 = (tid & 1) * 8;
+  double breg[8];
+  auto load_a = [&](int buf, int k0) {
+    double* dst = As + buf * kGK * kGS;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * kThreads;     // 16 columns x 64 pairs of rows
+      const int kk = e >> 6, r2 = e & 63;
+      const int l = k0 + kk;
+      const double* src = V + (long long)min(l, m - 1) * ld + row0 + 2 * r2;
+      cp_async16(dst + kk * kGS + 2 * r2, src, l < m ? 16 : 0);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto load_b = [&](int k0) {
+    const int c = col0 + bcol;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int l = k0 + bk0 + q;
+      breg[q] = (c < p && l < m) ? __ldg(Y + (size_t)c * m + l) : 0.0;
+    }
+  };
+  auto store_b = [&](int buf) {
+    double* dst = Bs + buf * kGK * kGS;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[(bk0 + q) * kGS + bcol] = breg[q];
+  };
+  double acc[4][8][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  load_a(0, 0);
+  load_b(0);
+  store_b(0);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) {
+      load_a(buf ^ 1, (kt + 1) * kGK);
+      load_b((kt + 1) * kGK);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* A = As + buf * kGK * kGS;
+    const double* B = Bs + buf * kGK * kGS;
+#pragma unroll
+    for (int ks = 0; ks < kGK; ks += 4) {
+      double af[4], bf[8];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) af[a] = A[(ks + tq) * kGS + wr * 32 + a * 8 + gq];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) bf[b] = B[(ks + tq) * kGS + wc * 64 + b * 8 + gq];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                       : "d"(af[a]), "d"(bf[b]));
+    }
+    if (kt + 1 < nk) store_b(buf ^ 1);  // buffer buf^1 was last read in iteration kt-1 (synced below)
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const long long i = row0 + wr * 32 + a * 8 + gq;
+    if (i >= n) continue;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int col = col0 + wc * 64 + b * 8 + 2 * tq + q;
+        if (col < p) Vout[(long long)col * ld + i] = acc[a][b][q];
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 void bump_launch();
@@ -539,12 +648,23 @@ void launch_sweep_tma(int mode, const GraphDev& g, const ProjDesc& pd, const Swe
   }
 }
 
-int g_ritz_kind = 1;  // 1: DMMA tensor cores, 0: register-blocked FMA
+int g_ritz_kind = 2;  // 2: DMMA 128x128 tiles, cp.async ring (default); 1: DMMA 128x64; 0: register-blocked FMA
 
 void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout,
                     cudaStream_t st) {
   if (p <= 0 || n <= 0) return;
   bump_launch();
+  if (g_ritz_kind == 2 && ld % 2 == 0 && ld >= (long long)((n + kGM - 1) / kGM) * kGM) {
+    static bool attr = false;
+    const int smem = 4 * kGK * kGS * (int)sizeof(double);
+    if (!attr) {
+      cudaFuncSetAttribute(k_ritz_dmma2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    dim3 grid((p + kGN - 1) / kGN, (n + kGM - 1) / kGM);
+    k_ritz_dmma2<<<grid, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
+    return;
+  }
   if (g_ritz_kind == 1) {
     dim3 grid((p + kDN - 1) / kDN, (n + kDM - 1) / kDM);
     k_ritz_dmma<<<grid, kThreads, 0, st>>>(V, ld, n, m, Y, p, Vout);
