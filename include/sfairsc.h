@@ -45,6 +45,7 @@ extern "C" {
 #endif
 
 typedef struct sfairsc_ctx sfairsc_ctx; /* opaque; owns all device memory */
+typedef struct sfairsc_comm sfairsc_comm; /* opaque NCCL communicator of a row-partitioned job */
 
 typedef enum {
   SFAIRSC_OK = 0,
@@ -96,6 +97,12 @@ typedef struct {
   int32_t reorth;         /* single-vector full reorthogonalisation: 1 = CGS2 (three basis sweeps per step),
                              2 = lagged single sweep (one basis sweep per step, DESIGN.md §Single-sweep Lanczos;
                              needs h <= 16, k < m <= min(192, n-h)); 0 = auto (2 where allowed, else 1) */
+  struct sfairsc_comm *comm; /* NULL: single GPU.  Else row-partitioned across the communicator's ranks
+                             (SURVEY §8(e)): each rank passes its contiguous row block of W (row_offset,
+                             n_rows, global n_cols; blocks tile [0, n) in rank order) and the groups of its
+                             rows; h must be given; evecs/labels/apply vectors hold the rank's rows */
+  int32_t virtual_parts;  /* > 1 (test/emulation): split the full W into this many nnz-balanced row blocks
+                             inside one process and GPU and run the row-partitioned solver over them */
 } sfairsc_opts;
 
 typedef struct {
@@ -192,6 +199,15 @@ sfairsc_status sfairsc_profile_reset(sfairsc_ctx *ctx);
  * symmetric; evals[m] ascending; evecs (m x m row-major, column c = vector c,
  * may be NULL).  Returns 0 on success.  Exported so tests can pin it on CPU. */
 int sfairsc_host_symeig(int32_t m, const double *A, double *evals, double *evecs);
+
+/* Multi-GPU bootstrap: rank 0 calls sfairsc_comm_unique_id and
+ * broadcasts the 128 bytes (e.g. with torch.distributed); every rank then calls
+ * sfairsc_comm_init with its rank, the rank count and its CUDA device.  NCCL
+ * (libnccl.so.2) is loaded at run time; SFAIRSC_E_NCCL if it is missing or fails. */
+sfairsc_status sfairsc_comm_unique_id(uint8_t id_out[128]);
+sfairsc_status sfairsc_comm_init(const uint8_t id[128], int32_t rank, int32_t nranks, int32_t device,
+                                 sfairsc_comm **out);
+void sfairsc_comm_destroy(sfairsc_comm *comm);
 
 void sfairsc_destroy(sfairsc_ctx *ctx);
 const char *sfairsc_last_error(void);

@@ -22,7 +22,7 @@ INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(PKG, "build")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsfairsc.so")
-SOURCES = ["kernels.cu", "krylov.cu", "block.cu", "abi.cu", "lanczos_block.cu", "lanczos1.cu", "kmeans.cu", "symeig.cpp"]
+SOURCES = ["kernels.cu", "krylov.cu", "block.cu", "abi.cu", "lanczos_block.cu", "lanczos1.cu", "dist.cu", "kmeans.cu", "symeig.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]
@@ -67,7 +67,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 print(log, file=sys.stderr)
     if force or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-lpthread", "-ldl",
-               "-Xlinker", "--no-undefined"]
+               "-ldl", "-Xlinker", "--no-undefined"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -21,6 +21,14 @@ sfairsc_status eigs_block(sfairsc_ctx* c, int k, double tol, double* evals_out, 
                           int evecs_memspace, sfairsc_stats* stats);
 sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out, double* evecs_out,
                            int evecs_memspace, sfairsc_stats* stats);
+sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* groups, int hh,
+                          const std::vector<int64_t>& cnt_local, const sfairsc_opts& opts);
+sfairsc_status dist_eigs(sfairsc_ctx* c, int k, double tol, double* evals_out, double* evecs_out, int evecs_memspace,
+                         sfairsc_stats* stats);
+sfairsc_status dist_apply(sfairsc_ctx* c, const double* x, double* y);
+sfairsc_status dist_kmeans(sfairsc_ctx* c, uint64_t seed, int32_t* labels_out, int32_t memspace, double* objective);
+long long dist_local_rows(const sfairsc_ctx* c);
+void dist_free(DistCtx* D);
 sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, int32_t memspace, double* objective);
 }  // namespace sfz
 
@@ -85,6 +93,7 @@ static cudaError_t dalloc(T** p, size_t count) {
 
 static void free_ctx(sfairsc_ctx* c) {
   if (!c) return;
+  if (c->dist) dist_free(c->dist);
   if (c->km && c->km_free) c->km_free(c->km);
   void* ptrs[] = {c->rp, c->ci, c->row_split, c->vv, c->dg, c->s, c->grp, c->isb, c->uh, c->partials, c->counters,
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
@@ -118,6 +127,8 @@ extern "C" void sfairsc_default_opts(sfairsc_opts* o) {
   o->spmv_vector = 0;
   o->block_size = 0;
   o->reorth = 0;
+  o->comm = nullptr;
+  o->virtual_parts = 0;
 }
 
 extern "C" const char* sfairsc_last_error(void) { return g_err.c_str(); }
@@ -211,39 +222,48 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   if (opts_in) opts = *opts_in;
   if (W->memspace != SFAIRSC_MEM_HOST && W->memspace != SFAIRSC_MEM_DEVICE)
     return fail(SFAIRSC_E_INVALID_ARG, "bad memspace");
-  if (W->n_rows != W->n_cols) return fail(SFAIRSC_E_DIM_MISMATCH, "n_rows != n_cols (multi-GPU row blocks not built)");
-  if (W->row_offset != 0) return fail(SFAIRSC_E_INVALID_ARG, "row_offset must be 0 on a single GPU");
-  if (W->n_rows < 1 || W->n_rows >= (1LL << 31) - 1024) return fail(SFAIRSC_E_INVALID_ARG, "n out of range");
+  // row-partitioned: NCCL ranks pass their own contiguous row block; virtual parts: the full matrix
+  const bool is_nccl = opts.comm != nullptr;
+  const bool is_dist = is_nccl || opts.virtual_parts > 1;
+  if (opts.virtual_parts < 0 || opts.virtual_parts > 64) return fail(SFAIRSC_E_INVALID_ARG, "virtual_parts in [0, 64]");
+  if (!is_nccl && W->n_rows != W->n_cols) return fail(SFAIRSC_E_DIM_MISMATCH, "n_rows != n_cols (row blocks need opts.comm)");
+  if (!is_nccl && W->row_offset != 0) return fail(SFAIRSC_E_INVALID_ARG, "row_offset must be 0 without opts.comm");
+  if (is_nccl && (W->row_offset < 0 || W->row_offset + W->n_rows > W->n_cols || W->n_rows < 1))
+    return fail(SFAIRSC_E_DIM_MISMATCH, "row block [row_offset, row_offset + n_rows) outside [0, n_cols)");
+  if (is_nccl && h < 1) return fail(SFAIRSC_E_INVALID_ARG, "h must be given (> 0) for a row-partitioned build");
+  if (W->n_cols < 1 || W->n_cols >= (1LL << 31) - 1024) return fail(SFAIRSC_E_INVALID_ARG, "n out of range");
   if (W->nnz < 0 || W->nnz >= (1LL << 31) - 1) return fail(SFAIRSC_E_INVALID_ARG, "nnz out of int32 range");
   if (W->nnz > 0 && (!W->col_idx || !W->values)) return fail(SFAIRSC_E_INVALID_ARG, "null CSR arrays");
   if (!W->row_ptr) return fail(SFAIRSC_E_INVALID_ARG, "null row_ptr");
   if (k < 1) return fail(SFAIRSC_E_INVALID_ARG, "k must be >= 1");
   if (h < 0 || h > 255) return fail(SFAIRSC_E_INVALID_ARG, "h must be in [0, 255]");
-  const int n = (int)W->n_rows, nnz = (int)W->nnz;
+  const int n = (int)W->n_cols, nnz = (int)W->nnz;  // n: global vertex count
+  const int n_rows = (int)W->n_rows;                  // rows passed (= n unless an NCCL row block)
   const bool dev_in = W->memspace == SFAIRSC_MEM_DEVICE;
 
   // groups on host: counts, inferred h, range check
-  std::vector<int32_t> hg(n);
+  std::vector<int32_t> hg(n_rows);
   if (dev_in) {
-    cudaError_t e = cudaMemcpy(hg.data(), groups, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(hg.data(), groups, sizeof(int32_t) * n_rows, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(SFAIRSC_E_CUDA, "groups copy: %s", cudaGetErrorString(e));
   } else {
-    std::memcpy(hg.data(), groups, sizeof(int32_t) * n);
+    std::memcpy(hg.data(), groups, sizeof(int32_t) * n_rows);
   }
   int hh = h;
   if (hh == 0) {
     int mx = -1;
-    for (int i = 0; i < n; ++i) mx = std::max(mx, hg[i]);
+    for (int i = 0; i < n_rows; ++i) mx = std::max(mx, hg[i]);
     hh = mx + 1;
     if (hh < 1 || hh > 255) return fail(SFAIRSC_E_INVALID_ARG, "inferred h out of range");
   }
   std::vector<int64_t> cnt(hh, 0);
-  for (int i = 0; i < n; ++i) {
+  for (int i = 0; i < n_rows; ++i) {
     if (hg[i] < 0 || hg[i] >= hh) return fail(SFAIRSC_E_INVALID_ARG, "group id %d out of [0,%d) at vertex %d", hg[i], hh, i);
     cnt[hg[i]]++;
   }
-  for (int s = 0; s < hh; ++s)
-    if (cnt[s] == 0) return fail(SFAIRSC_E_EMPTY_GROUP, "group %d is empty (P:152)", s);
+  if (!is_nccl)  // a rank's row block may miss a group: checked globally in dist_build
+    for (int s = 0; s < hh; ++s)
+      if (cnt[s] == 0) return fail(SFAIRSC_E_EMPTY_GROUP, "group %d is empty (P:152)", s);
   if ((int64_t)k > (int64_t)n - hh + 1) return fail(SFAIRSC_E_K_TOO_LARGE, "k=%d > n-h+1=%lld", k, (long long)n - hh + 1);
 
   sfairsc_ctx* c = new sfairsc_ctx();
@@ -325,6 +345,20 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   c->lagged = c->bsz == 1 && opts.reorth != 1 && hh <= kHB && m <= 192 && m <= n - hh && m > k;
   if (opts.reorth == 2 && !c->lagged)
     return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth=2 needs block_size 1, h <= 16 and k < m <= min(192, n-h)"));
+  if (is_dist) {  // row-partitioned single-sweep Lanczos (dist.cu)
+    if (!c->lagged) return bail(fail(SFAIRSC_E_INVALID_ARG, "row-partitioned builds need h <= 16, block_size 1, reorth 0/2"));
+    {
+      const double mean_deg = (double)W->nnz / std::max(1, n_rows);
+      int vs = 2;
+      while (vs < 32 && vs * 4 <= mean_deg) vs *= 2;
+      c->vs = opts.spmv_vector > 0 ? opts.spmv_vector : vs;
+    }
+    sfairsc_status ds = dist_build(c, W, groups, hh, cnt, opts);
+    if (ds != SFAIRSC_OK) return bail(ds);
+    c->t_build = now_s() - t0;
+    *out = c;
+    return SFAIRSC_OK;
+  }
 
   // device allocations
   CUB(dalloc(&c->rp, n + 1));
@@ -518,6 +552,25 @@ static sfairsc_status vec_io(sfairsc_ctx* c, const double* x, double* y, int32_t
                              sfairsc_status (*op)(sfairsc_ctx*, const double*, double*)) {
   if (!c || !x || !y || nvec < 0) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
   if (memspace != SFAIRSC_MEM_HOST && memspace != SFAIRSC_MEM_DEVICE) return fail(SFAIRSC_E_INVALID_ARG, "memspace");
+  if (c->dist) {  // row-partitioned: vectors hold this process's rows; only the operator apply is offered
+    if (op != apply_dev) return fail(SFAIRSC_E_INVALID_ARG, "only sfairsc_apply is available on a row-partitioned context");
+    const long long nl = dist_local_rows(c);
+    double *dx = nullptr, *dy = nullptr;
+    CU(cudaMalloc(&dx, sizeof(double) * std::max(nl, 1LL)));
+    CU(cudaMalloc(&dy, sizeof(double) * std::max(nl, 1LL)));
+    sfairsc_status rs = SFAIRSC_OK;
+    const cudaMemcpyKind kin = memspace == SFAIRSC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const cudaMemcpyKind kout = memspace == SFAIRSC_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    for (int v = 0; v < nvec && rs == SFAIRSC_OK; ++v) {
+      cudaMemcpyAsync(dx, x + (size_t)v * nl, sizeof(double) * nl, kin, c->st);
+      rs = dist_apply(c, dx, dy);
+      if (rs == SFAIRSC_OK) cudaMemcpyAsync(y + (size_t)v * nl, dy, sizeof(double) * nl, kout, c->st);
+    }
+    cudaStreamSynchronize(c->st);
+    cudaFree(dx);
+    cudaFree(dy);
+    return rs;
+  }
   const size_t nb = sizeof(double) * c->n;
   for (int v = 0; v < nvec; ++v) {
     const double* xv = x + (size_t)v * c->n;
@@ -747,6 +800,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
   if (evecs_out && evecs_memspace != SFAIRSC_MEM_HOST && evecs_memspace != SFAIRSC_MEM_DEVICE)
     return fail(SFAIRSC_E_INVALID_ARG, "memspace");
   if (c->bsz > 1) return eigs_block(c, k, tol, evals_out, evecs_out, evecs_memspace, stats);
+  if (c->dist) return dist_eigs(c, k, tol, evals_out, evecs_out, evecs_memspace, stats);
   if (c->lagged) return eigs_lagged(c, k, tol, evals_out, evecs_out, evecs_memspace, stats);
   c->have_eigs = false;
   Lanczos L;
@@ -927,6 +981,7 @@ extern "C" sfairsc_status sfairsc_embed_kmeans(sfairsc_ctx* c, uint64_t seed, in
   if (!c || !labels_out) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
   if (!c->have_eigs) return fail(SFAIRSC_E_STATE, "sfairsc_eigs must succeed before sfairsc_embed_kmeans");
   if (memspace != SFAIRSC_MEM_HOST && memspace != SFAIRSC_MEM_DEVICE) return fail(SFAIRSC_E_INVALID_ARG, "memspace");
+  if (c->dist) return dist_kmeans(c, seed, labels_out, memspace, objective_out);
   return kmeans_run(c, seed, labels_out, memspace, objective_out);
 }
 

@@ -63,8 +63,9 @@ __device__ __forceinline__ void ld_row(const double* __restrict__ p, int c, doub
 // ----------------------------------------------------------------------------
 template <int VS, int NB, bool NORM>
 __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __restrict__ row_split,
-                                                   const double* __restrict__ p, double* __restrict__ t,
-                                                   double* partials, unsigned* counter, double* bsum_t) {
+                                                   const double* __restrict__ p, const double* __restrict__ p_self,
+                                                   double* __restrict__ t, double* partials, unsigned* counter,
+                                                   double* bsum_t) {
   constexpr int NG = kThreads / VS, U = 4;
   const int r0 = row_split[blockIdx.x], r1 = row_split[blockIdx.x + 1];
   const int lane = threadIdx.x % VS, gid = threadIdx.x / VS;
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
       for (int o = VS / 2; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
     if (valid && lane == 0) {
       double pi[NB];
-      ld_row<NB>(p, row, pi);
+      ld_row<NB>(p_self, row, pi);  // own rows (row-partitioned: this part's segment of the gathered p)
       const double di = NORM ? 1.0 : __ldg(g.dg + row);
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
@@ -557,31 +558,32 @@ static int sgrid(int n) { return std::max(1, std::min((n + kThreads - 1) / kThre
 static int rgrid(int n) { return std::max(1, std::min((n + 4 * kThreads - 1) / (4 * kThreads), n_sms() * 2)); }
 
 template <int VS, int NB>
-static void spmm_vs(const GraphDev& g, const int* split, int grid, const double* p, double* t, double* partials,
-                    unsigned* counter, double* bsum_t, cudaStream_t st) {
+static void spmm_vs(const GraphDev& g, const int* split, int grid, const double* p, const double* ps, double* t,
+                    double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
   if (g.normalized)
-    k_spmm<VS, NB, true><<<grid, kThreads, 0, st>>>(g, split, p, t, partials, counter, bsum_t);
+    k_spmm<VS, NB, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
   else
-    k_spmm<VS, NB, false><<<grid, kThreads, 0, st>>>(g, split, p, t, partials, counter, bsum_t);
+    k_spmm<VS, NB, false><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
 }
 template <int NB>
-static void spmm_nb(const GraphDev& g, int vs, const int* split, int grid, const double* p, double* t,
-                    double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
+static void spmm_nb(const GraphDev& g, int vs, const int* split, int grid, const double* p, const double* ps,
+                    double* t, double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
   switch (vs) {
-    case 2: spmm_vs<2, NB>(g, split, grid, p, t, partials, counter, bsum_t, st); break;
-    case 4: spmm_vs<4, NB>(g, split, grid, p, t, partials, counter, bsum_t, st); break;
-    case 8: spmm_vs<8, NB>(g, split, grid, p, t, partials, counter, bsum_t, st); break;
-    case 16: spmm_vs<16, NB>(g, split, grid, p, t, partials, counter, bsum_t, st); break;
-    default: spmm_vs<32, NB>(g, split, grid, p, t, partials, counter, bsum_t, st); break;
+    case 2: spmm_vs<2, NB>(g, split, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    case 4: spmm_vs<4, NB>(g, split, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    case 8: spmm_vs<8, NB>(g, split, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    case 16: spmm_vs<16, NB>(g, split, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    default: spmm_vs<32, NB>(g, split, grid, p, ps, t, partials, counter, bsum_t, st); break;
   }
 }
 void launch_spmm(const GraphDev& g, int nb, int vs, const int* split, int grid, const double* p, double* t,
-                 double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
+                 double* partials, unsigned* counter, double* bsum_t, cudaStream_t st, const double* p_self) {
   bump_launch();
+  const double* ps = p_self ? p_self : p;
   switch (nb) {
-    case 1: spmm_nb<1>(g, vs, split, grid, p, t, partials, counter, bsum_t, st); break;
-    case 2: spmm_nb<2>(g, vs, split, grid, p, t, partials, counter, bsum_t, st); break;
-    default: spmm_nb<4>(g, vs, split, grid, p, t, partials, counter, bsum_t, st); break;
+    case 1: spmm_nb<1>(g, vs, split, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    case 2: spmm_nb<2>(g, vs, split, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    default: spmm_nb<4>(g, vs, split, grid, p, ps, t, partials, counter, bsum_t, st); break;
   }
 }
 

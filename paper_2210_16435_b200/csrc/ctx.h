@@ -9,6 +9,9 @@
 #include <string>
 #include <vector>
 
+namespace sfz {
+struct DistCtx;  // row-partitioned state (dist.cu)
+}
 using sfz::GraphDev;
 using sfz::ProjDesc;
 using sfz::kHB;
@@ -102,6 +105,8 @@ struct sfairsc_ctx {
   // single-sweep (lagged) Lanczos (lanczos1.cu); uses ldT = m + 2 for H
   bool lagged = false;
   double *Hdev = nullptr, *sdev = nullptr, *lz = nullptr, *partials2 = nullptr, *dd = nullptr;
+  // row-partitioned contexts: all device state lives in dist
+  sfz::DistCtx* dist = nullptr;
   // results
   bool have_eigs = false;
   int k_eigs = 0;

@@ -524,8 +524,6 @@ static void spmv_vs(const GraphDev& g, const int* row_split, int grid, const dou
     k_spmv<VS, false><<<grid, kThreads, 0, st>>>(g, row_split, p, t, partials, counter, bsum_t, kHB);
 }
 int g_spmv_kind = 1;  // 1: predicated 4-deep gather kernel (block.cu k_spmm<VS,1>), 0: k_spmv (A/B, env SFAIRSC_SPMV)
-void launch_spmm(const GraphDev& g, int nb, int vs, const int* split, int grid, const double* p, double* t,
-                 double* partials, unsigned* counter, double* bsum_t, cudaStream_t st);
 void launch_spmv(const GraphDev& g, int vs, const int* row_split, int grid, const double* p, double* t,
                  double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
   if (g_spmv_kind == 1) {

@@ -147,8 +147,10 @@ struct BlockQRArgs {
   double bd_tol;       // absolute pivot tolerance
   double rel_tol;      // relative pivot tolerance (ill-conditioned block)
 };
+// p: the gathered vector indexed by ci; p_self (nullptr: p): this part's own rows (diagonal term)
 void launch_spmm(const GraphDev& g, int nb, int vs, const int* split, int grid, const double* p, double* t,
-                 double* partials, unsigned* counter, double* bsum_t, cudaStream_t st);
+                 double* partials, unsigned* counter, double* bsum_t, cudaStream_t st,
+                 const double* p_self = nullptr);
 int bsweep_grid(int n);
 void launch_bsweep(int mode, int nb, const GraphDev& g, const ProjDesc& pd, const BlockSweepArgs& a, int grid,
                    cudaStream_t st);

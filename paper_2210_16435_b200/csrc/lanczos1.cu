@@ -26,6 +26,7 @@
 #include "ctx.h"
 #include "device_common.cuh"
 #include "tma.cuh"
+#include "lanczos1.h"
 
 #include <algorithm>
 #include <cmath>
@@ -45,23 +46,9 @@ constexpr int kMaxStages = 8;
 constexpr size_t kRingBytes = 214 * 1024;
 constexpr int kLMaxJ = 191;  // basis columns swept (+1 new column in the dots: <= 192)
 
-// scalar slots of the device state `lz`
-enum { LZ_OMEGA = 0, LZ_PNORM2 = 1, LZ_AY = 2, LZ_AV = 3, LZ_MU = 4, LZ_INVMU = 5, LZ_BETA = 6 };
 }  // namespace
 
-struct LzDev {
-  double* H;       // (ldH x ldH) column-major; A V_j = V_j H[:j,:j] + v~_j H[j,:j] (lagged)
-  int ldH;
-  double* s;       // V_j^T v~_j (j entries)
-  double* lz;      // scalars (LZ_*)
-  double* cs;      // s / mu        (update coefficients of v_j)
-  double* cg;      // g             (update coefficients of w)
-  const double* bs_t;  // B^T t [kHB], p~^T t at [kHB]
-  const double* bs_v;  // B^T v~ [kHB]
-  int* flag;       // breakdown flag of this step
-  double sigma;
-  double bd_tol;
-};
+
 
 // ---------------------------------------------------------------------------
 // coefficient step (one CTA)
@@ -176,25 +163,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_coef(LzDev d, int j) {
 // the one sweep: v_j, w, dots [V_j, v_j]^T w, |w|^2, B^T w
 // stage (doubles): [J][kR] basis | v~[kR] | t[kR] | s[kR] | grp bytes (pad 128 B)
 // ---------------------------------------------------------------------------
-struct LzSweepArgs {
-  const double* V;
-  long long ld;
-  int J;
-  const double* vt;   // v~
-  const double* t;    // L p~
-  double* vj_out;     // V column J
-  double* w_out;
-  const double* cs;
-  const double* cg;
-  const double* lz;
-  const double* bs_t;
-  const double* bs_v;
-  double sigma;
-  double* partials;   // [grid][J+1]
-  double* partials2;  // [grid][1+kHB]
-  unsigned* counter;
-  double* nb;         // out: |w|^2, B^T w
-};
+
 
 __host__ __device__ constexpr size_t lz_stage_doubles(int J) { return (size_t)(J + 3) * kR + 16; }
 
@@ -579,6 +548,24 @@ static void lz_update_m(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs
   if (a.J + 1 <= 64) lz_update_launch<8, NORM>(g, pd, a, grid, st);
   else if (a.J + 1 <= 128) lz_update_launch<16, NORM>(g, pd, a, grid, st);
   else lz_update_launch<24, NORM>(g, pd, a, grid, st);
+}
+
+void launch_lz_coef(const LzDev& d, int j, cudaStream_t st) {
+  bump_launch();
+  k_lz_coef<<<1, kThreads, 0, st>>>(d, j);
+}
+void launch_lz_update(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st) {
+  bump_launch();
+  if (g.normalized) lz_update_m<true>(g, pd, a, grid, st);
+  else lz_update_m<false>(g, pd, a, grid, st);
+}
+void launch_lz_norm(const GraphDev& g, const ProjDesc& pd, const double* w, const double* nb, const double* dots,
+                    int nd, const LzDev& d, int jrow, double* vt, double* p, double* bs_v, cudaStream_t st) {
+  bump_launch();
+  if (g.normalized)
+    k_lz_norm<true><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v);
+  else
+    k_lz_norm<false><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,53 @@
+// Single-sweep (lagged) Lanczos kernels (lanczos1.cu), shared with the
+// row-partitioned driver (dist.cu).  Internal, not part of the C ABI.
+#pragma once
+#include "kernels.cuh"
+
+namespace sfz {
+
+// scalar slots of the device state `lz`
+enum { LZ_OMEGA = 0, LZ_PNORM2 = 1, LZ_AY = 2, LZ_AV = 3, LZ_MU = 4, LZ_INVMU = 5, LZ_BETA = 6 };
+
+struct LzDev {
+  double* H;       // (ldH x ldH) column-major; A V_j = V_j H[:j,:j] + v~_j H[j,:j] (lagged)
+  int ldH;
+  double* s;       // V_j^T v~_j (j entries)
+  double* lz;      // scalars (LZ_*)
+  double* cs;      // s / mu        (update coefficients of v_j)
+  double* cg;      // g             (update coefficients of w)
+  const double* bs_t;  // B^T t [kHB], p~^T t at [kHB]
+  const double* bs_v;  // B^T v~ [kHB]
+  int* flag;       // breakdown flag of this step
+  double sigma;
+  double bd_tol;
+};
+
+struct LzSweepArgs {
+  const double* V;
+  long long ld;
+  int J;
+  const double* vt;   // v~
+  const double* t;    // L p~
+  double* vj_out;     // V column J
+  double* w_out;
+  const double* cs;
+  const double* cg;
+  const double* lz;
+  const double* bs_t;
+  const double* bs_v;
+  double sigma;
+  double* partials;   // [grid][J+1]
+  double* partials2;  // [grid][1+kHB]
+  unsigned* counter;
+  double* nb;         // out: |w|^2, B^T w
+};
+
+// coefficient step (one CTA): reads s, H, lz, bs_t[kHB] = p~^T t; writes H column j, cs, cg, lz
+void launch_lz_coef(const LzDev& d, int j, cudaStream_t st);
+// the one basis sweep of step J = a.J (TMA-fed): v_J, w, partial dots -> a.partials, |w|^2 and B^T w -> a.nb
+void launch_lz_update(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st);
+// v~ = p~ = P(w/|w|) -> vt, p; s = dots/|w| (nd entries); H row jrow (jrow >= 0); B^T v~ -> bs_v
+void launch_lz_norm(const GraphDev& g, const ProjDesc& pd, const double* w, const double* nb, const double* dots,
+                    int nd, const LzDev& d, int jrow, double* vt, double* p, double* bs_v, cudaStream_t st);
+
+}  // namespace sfz

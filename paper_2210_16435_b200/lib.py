@@ -48,7 +48,8 @@ class Opts(C.Structure):
     _fields_ = [("sigma_override", C.c_double), ("max_basis", C.c_int32), ("keep", C.c_int32),
                 ("max_restarts", C.c_int32), ("start_seed", C.c_uint64), ("tol_eff_cap", C.c_double),
                 ("cuda_stream", C.c_void_p), ("check_symmetry", C.c_int32), ("spmv_vector", C.c_int32),
-                ("block_size", C.c_int32), ("reorth", C.c_int32)]
+                ("block_size", C.c_int32), ("reorth", C.c_int32), ("comm", C.c_void_p),
+                ("virtual_parts", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -93,6 +94,9 @@ def _load():
         "sfairsc_last_error": (C.c_char_p, []),
         "sfairsc_version": (C.c_char_p, []),
         "sfairsc_host_symeig": (C.c_int, [C.c_int32, P, P, P]),
+        "sfairsc_comm_unique_id": (C.c_int, [P]),
+        "sfairsc_comm_init": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
+        "sfairsc_comm_destroy": (None, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -136,6 +140,8 @@ def default_opts(**kw) -> Opts:
     for k, v in kw.items():
         if k == "cuda_stream" and v is not None and not isinstance(v, int):
             v = v.cuda_stream  # torch.cuda.Stream
+        if k == "comm" and isinstance(v, Comm):
+            v = v.handle.value
         setattr(o, k, v)
     return o
 
@@ -177,7 +183,8 @@ class Context:
 
 
 def sfairsc_build_operator(row_ptr, col_idx, values, groups, k: int, normalized: bool, h: int = 0,
-                           opts: Opts | None = None, **opt_kw) -> Context:
+                           opts: Opts | None = None, n_global: int | None = None, row_offset: int = 0,
+                           **opt_kw) -> Context:
     """Build the operator from CSR arrays (numpy host arrays or CUDA tensors;
     all four in the same memspace).  See include/sfairsc.h."""
     rp, ms = _ptr(row_ptr, np.int32)
@@ -188,7 +195,8 @@ def sfairsc_build_operator(row_ptr, col_idx, values, groups, k: int, normalized:
         raise ValueError("row_ptr, col_idx, values and groups must share one memspace")
     n = len(row_ptr) - 1
     nnz = len(col_idx)
-    csr = CSR(n, n, nnz, 0, rp, ci, vv, ms)
+    # a rank of a row-partitioned job passes its row block [row_offset, row_offset + n) of the n_global rows
+    csr = CSR(n, n if n_global is None else int(n_global), nnz, int(row_offset), rp, ci, vv, ms)
     if opts is None and opt_kw:
         opts = default_opts(**opt_kw)
     out = C.c_void_p()
@@ -301,3 +309,76 @@ def host_symeig(A: np.ndarray):
     V = np.zeros((m, m))
     _check(_lib.sfairsc_host_symeig(m, A.ctypes.data, ev.ctypes.data, V.ctypes.data))
     return ev, V
+
+
+# --- multi-GPU (row-partitioned) ---------------------------------------
+
+class Comm:
+    """An NCCL communicator of the row-partitioned solver (sfairsc_comm)."""
+
+    def __init__(self, uid: bytes, rank: int, nranks: int, device: int):
+        if len(uid) != 128:
+            raise ValueError("unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(_lib.sfairsc_comm_init(C.cast(buf, C.c_void_p), rank, nranks, device, C.byref(h)))
+        self.handle = h
+        self.rank, self.nranks, self.device = rank, nranks, device
+
+    def close(self):
+        if self.handle:
+            _lib.sfairsc_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(_lib.sfairsc_comm_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def comm_from_torch(device: int, group=None) -> Comm:
+    """Bootstrap over an initialised torch.distributed process group: rank 0
+    creates the NCCL unique id, every rank receives it by broadcast and joins."""
+    import torch.distributed as dist
+    rank, ws = dist.get_rank(group), dist.get_world_size(group)
+    uid = broadcast_uid(comm_unique_id() if rank == 0 else None, group)
+    return Comm(uid, rank, ws, device)
+
+
+def broadcast_uid(uid: bytes | None, group=None) -> bytes:
+    """Rank 0's 128-byte NCCL unique id, delivered to every rank of `group`."""
+    import torch.distributed as dist
+    obj = [uid if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    if not isinstance(obj[0], (bytes, bytearray)) or len(obj[0]) != 128:
+        raise RuntimeError("bad unique id broadcast")
+    return bytes(obj[0])
+
+
+def partition_rows(row_ptr: np.ndarray, nparts: int) -> np.ndarray:
+    """Contiguous row blocks balanced by nnz + 4 per row (the library's own
+    rule for virtual parts): cuts[q] <= rows of part q < cuts[q+1]."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    n = len(row_ptr) - 1
+    w = row_ptr + 4 * np.arange(n + 1, dtype=np.int64)
+    tot = int(w[-1])
+    cuts = np.zeros(nparts + 1, dtype=np.int64)
+    cuts[-1] = n
+    for q in range(1, nparts):
+        cuts[q] = max(cuts[q - 1], int(np.searchsorted(w, tot * q // nparts, side="left")))
+    return cuts
+
+
+def row_block(row_ptr, col_idx, values, groups, r0: int, r1: int):
+    """The CSR rows [r0, r1) of W (global column indices kept) and their groups."""
+    a, b = int(row_ptr[r0]), int(row_ptr[r1])
+    rp = (np.asarray(row_ptr[r0:r1 + 1], dtype=np.int64) - a).astype(np.int32)
+    return rp, np.ascontiguousarray(col_idx[a:b]), np.ascontiguousarray(values[a:b]), \
+        np.ascontiguousarray(np.asarray(groups[r0:r1], dtype=np.int32))
