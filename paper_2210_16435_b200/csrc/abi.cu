@@ -284,6 +284,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   if (getenv("SFAIRSC_RITZ")) sfz::g_ritz_kind = atoi(getenv("SFAIRSC_RITZ"));
   if (getenv("SFAIRSC_SPMV")) sfz::g_spmv_kind = atoi(getenv("SFAIRSC_SPMV"));
   if (getenv("SFAIRSC_LZ_SWEEP")) sfz::g_lz_sweep = atoi(getenv("SFAIRSC_LZ_SWEEP"));
+  if (getenv("SFAIRSC_GATHER")) sfz::g_spmv_gather = atoi(getenv("SFAIRSC_GATHER"));
   if (c->sweep_kind == 3) {  // TMA with one 1-D copy per column (A/B only)
     sfz::g_tma_use2d = 0;
     c->sweep_kind = 2;
@@ -340,6 +341,26 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
       c->keep = kp;
     }
   }
+  // HBM budget (single GPU, default basis only): the two basis buffers (m+1 columns each) plus the CSR copy,
+  // X and ~12 work vectors must fit in free device memory (config 5 on one GPU: n = 5e7, 400 MB per vector)
+  if (opts.max_basis <= 0 && !(opts.comm || opts.virtual_parts > 1)) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > 0) {
+      const double vbytes = 8.0 * (double)c->ldv * (c->bsz > 1 ? 1 : 1);
+      const double fixed = 12.0 * nnz + 4.0 * n + ((double)k + 12.0 + 3.0 * c->bsz) * vbytes + 256.0 * (1 << 20);
+      const double avail = 0.97 * (double)fr - fixed;
+      const int mfit = (int)std::floor(avail / (2.0 * vbytes)) - std::max(1, c->bsz);
+      if (mfit < m) {
+        const int mnew = std::max(mfit, k + std::max(2, c->bsz));
+        if (mnew < k + 2) return bail(fail(SFAIRSC_E_OOM, "Krylov basis for k=%d does not fit in device memory", k));
+        const int b = std::max(1, c->bsz);
+        int kp = k + 3 * (mnew - k) / 5;
+        kp = std::max(k, std::min(kp, mnew - b));
+        c->m = m = (b > 1) ? kp + b * ((mnew - kp) / b) : mnew;
+        c->keep = kp;
+      }
+    }
+  }
   // single-vector reorthogonalisation: 0 auto (= lagged single sweep), 1 CGS2 (three sweeps), 2 lagged
   if (opts.reorth < 0 || opts.reorth > 2) return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth must be 0, 1 or 2"));
   c->lagged = c->bsz == 1 && opts.reorth != 1 && hh <= kHB && m <= 192 && m <= n - hh && m > k;
@@ -350,7 +371,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     {
       const double mean_deg = (double)W->nnz / std::max(1, n_rows);
       int vs = 2;
-      while (vs < 32 && vs * 4 <= mean_deg) vs *= 2;
+      while (vs < 32 && vs * 4 < mean_deg) vs *= 2;
       c->vs = opts.spmv_vector > 0 ? opts.spmv_vector : vs;
     }
     sfairsc_status ds = dist_build(c, W, groups, hh, cnt, opts);
@@ -451,7 +472,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
       const long long target = total * b / G;
       int lo = 0, hi = n;
       while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
+        const int mid = lo + ((hi - lo) >> 1);
         if ((long long)hrp[mid] + 4LL * mid < target) lo = mid + 1; else hi = mid;
       }
       split[b] = std::max(split[b - 1], lo);
@@ -461,7 +482,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     CUB(cudaMemcpyAsync(c->row_split, split.data(), sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, c->st));
     const double mean_deg = n > 0 ? (double)nnz / n : 0.0;
     int vs = 2;
-    while (vs < 32 && vs * 4 <= mean_deg) vs *= 2;
+    while (vs < 32 && vs * 4 < mean_deg) vs *= 2;
     c->vs = opts.spmv_vector > 0 ? opts.spmv_vector : vs;
     if (c->vs != 2 && c->vs != 4 && c->vs != 8 && c->vs != 16 && c->vs != 32)
       return bail(fail(SFAIRSC_E_INVALID_ARG, "spmv_vector must be 2,4,8,16 or 32"));

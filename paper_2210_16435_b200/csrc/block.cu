@@ -40,11 +40,18 @@ __host__ __device__ constexpr size_t bstage_doubles(int J) {
   return (size_t)(J + NB + 1) * kR + 16;
 }
 
+__device__ __forceinline__ double ld_cg(const double* p) {  // L2 only (no L1 allocation)
+  double v;
+  asm("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+int g_spmv_gather = 0;  // 0: __ldg gathers (default); 1: ld.global.cg (env SFAIRSC_GATHER)
+
 // NB doubles of row c of an interleaved block
-template <int NB>
+template <int NB, bool CG = false>
 __device__ __forceinline__ void ld_row(const double* __restrict__ p, int c, double (&x)[NB]) {
   if constexpr (NB == 1) {
-    x[0] = __ldg(p + c);
+    x[0] = CG ? ld_cg(p + c) : __ldg(p + c);
   } else {
     const double2* q = reinterpret_cast<const double2*>(p) + (size_t)c * (NB / 2);
 #pragma unroll
@@ -61,7 +68,7 @@ __device__ __forceinline__ void ld_row(const double* __restrict__ p, int c, doub
 // per row, nnz-balanced contiguous row ranges per CTA; each lane keeps up to
 // 4 (col, val) pairs and 4 gathers in flight.  Epilogue: B^T T per vector.
 // ----------------------------------------------------------------------------
-template <int VS, int NB, bool NORM>
+template <int VS, int NB, bool NORM, bool CG = false>
 __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __restrict__ row_split,
                                                    const double* __restrict__ p, const double* __restrict__ p_self,
                                                    double* __restrict__ t, double* partials, unsigned* counter,
@@ -96,7 +103,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
 #pragma unroll
         for (int q = 0; q < U; ++q) {
           double x[NB];
-          ld_row<NB>(p, cix[q], x);
+          ld_row<NB, CG>(p, cix[q], x);
 #pragma unroll
           for (int c = 0; c < NB; ++c) acc[c] = fma(w[q], x[c], acc[c]);
         }
@@ -560,6 +567,13 @@ static int rgrid(int n) { return std::max(1, std::min((n + 4 * kThreads - 1) / (
 template <int VS, int NB>
 static void spmm_vs(const GraphDev& g, const int* split, int grid, const double* p, const double* ps, double* t,
                     double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
+  if (NB == 1 && g_spmv_gather == 1) {
+    if (g.normalized)
+      k_spmm<VS, NB, true, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
+    else
+      k_spmm<VS, NB, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
+    return;
+  }
   if (g.normalized)
     k_spmm<VS, NB, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
   else

@@ -28,9 +28,9 @@ __device__ __forceinline__ double ld_stream(const double* p) {
 
 // Block-wide fixed-order reduction of NV per-thread values; thread q < NV
 // writes the CTA partial to out[q].
-template <int NV>
+template <int NV, int NT = kThreads>
 __device__ __forceinline__ void block_reduce_store(const double (&v)[NV], double* out) {
-  __shared__ double red[kThreads / 32][NV];
+  __shared__ double red[NT / 32][NV];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
@@ -41,7 +41,7 @@ __device__ __forceinline__ void block_reduce_store(const double (&v)[NV], double
   if (threadIdx.x < NV) {
     double acc = 0.0;
 #pragma unroll
-    for (int ww = 0; ww < kThreads / 32; ++ww) acc += red[ww][threadIdx.x];
+    for (int ww = 0; ww < NT / 32; ++ww) acc += red[ww][threadIdx.x];
     out[threadIdx.x] = acc;
   }
 }
@@ -49,7 +49,7 @@ __device__ __forceinline__ void block_reduce_store(const double (&v)[NV], double
 // Last-CTA-done finalisation: the CTA that takes the last ticket sums the
 // grid's partial rows [gridDim.x][NV] in a fixed order and writes out[q]
 // for q < nout.  Resets the ticket for the next launch.
-template <int NV>
+template <int NV, int NT = kThreads>
 __device__ __forceinline__ void ticket_finalize(const double* partials, unsigned* counter, double* out, int nout) {
   __shared__ unsigned s_last;
   __threadfence();
@@ -59,7 +59,7 @@ __device__ __forceinline__ void ticket_finalize(const double* partials, unsigned
   if (!s_last) return;
   __threadfence();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int q = w; q < nout; q += kThreads / 32) {
+  for (int q = w; q < nout; q += NT / 32) {
     double acc = 0.0;
     for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(partials + (size_t)b * NV + q);
     acc = warp_sum(acc);

@@ -504,7 +504,7 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
         const long long target = total * bb / G;
         int lo = 0, hi = p.n_loc;
         while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
+          const int mid = lo + ((hi - lo) >> 1);
           if ((long long)lrp[mid] + 4LL * mid < target) lo = mid + 1; else hi = mid;
         }
         split[bb] = std::max(split[bb - 1], lo);

@@ -56,7 +56,7 @@ __global__ void k_validate(GraphDev g, int check_sym, int* flags) {
       if (check_sym && j >= 0 && j < n && j != i) {
         int lo = g.rp[j], hi = g.rp[j + 1] - 1, found = -1;
         while (lo <= hi) {
-          const int mid = (lo + hi) >> 1;
+          const int mid = lo + ((hi - lo) >> 1);  // rp values reach 1.6e9: no lo + hi overflow
           const int cm = g.ci[mid];
           if (cm == i) {
             found = mid;

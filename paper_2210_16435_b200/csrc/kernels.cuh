@@ -83,6 +83,7 @@ void launch_sweep(int mode, const GraphDev& g, const ProjDesc& pd, const SweepAr
 extern int g_tma_use2d;
 extern int g_spmv_kind;
 extern int g_lz_sweep;
+extern int g_spmv_gather;
 extern int g_ritz_kind;  // 1: DMMA (fp64 tensor cores, default), 0: register-blocked FMA  // 1: 2-D tensor-map TMA per chunk (default); 0: one 1-D bulk copy per column
 bool sweep_tma_ok(int J);  // also the J limit of the smem-staged sweeps
 int sweep_smem_grid(int n, int J, int num_sms);

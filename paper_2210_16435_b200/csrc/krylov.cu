@@ -306,8 +306,9 @@ __global__ void __launch_bounds__(kThreads) k_ritz_rb(const double* __restrict__
   constexpr int TM = 128, KC = 16, CPT = TN / 16;
   __shared__ double As[KC][TM];
   __shared__ double Bs[KC][TN];
-  const int col0 = blockIdx.x * TN;
-  const long long row0 = (long long)blockIdx.y * TM;
+  const int ncol = (p + TN - 1) / TN;  // 1-D grid: row tile major, column tiles of a row tile adjacent (L2 reuse)
+  const int col0 = (int)(blockIdx.x % ncol) * TN;
+  const long long row0 = (long long)(blockIdx.x / ncol) * TM;
   const int tid = threadIdx.x;
   const int rg = tid % 16, cg = tid / 16;
   double acc[8][CPT];
@@ -370,8 +371,9 @@ __global__ void __launch_bounds__(kThreads) k_ritz_dmma(const double* __restrict
                                                         double* __restrict__ Vout) {
   __shared__ double As[kDK][kAS];
   __shared__ double Bs[kDK][kBS];
-  const int col0 = blockIdx.x * kDN;
-  const long long row0 = (long long)blockIdx.y * kDM;
+  const int ncol = (p + kDN - 1) / kDN;
+  const int col0 = (int)(blockIdx.x % ncol) * kDN;
+  const long long row0 = (long long)(blockIdx.x / ncol) * kDM;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wr = w & 3, wc = w >> 2;  // warp tile origin: rows wr*32, cols wc*32
   const int gq = lane >> 2, tq = lane & 3;
@@ -446,8 +448,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __rest
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                      // [2][kGK][kGS]
   double* Bs = gsm + 2 * kGK * kGS;      // [2][kGK][kGS]
-  const int col0 = blockIdx.x * kGN;
-  const long long row0 = (long long)blockIdx.y * kGM;
+  const int ncol = (p + kGN - 1) / kGN;
+  const int col0 = (int)(blockIdx.x % ncol) * kGN;
+  const long long row0 = (long long)(blockIdx.x / ncol) * kGM;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wr = w & 3, wc = w >> 2;
   const int gq = lane >> 2, tq = lane & 3;
@@ -661,20 +664,20 @@ void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y
       cudaFuncSetAttribute(k_ritz_dmma2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
-    dim3 grid((p + kGN - 1) / kGN, (n + kGM - 1) / kGM);
+    const long long grid = (long long)((p + kGN - 1) / kGN) * ((n + kGM - 1) / kGM);
     k_ritz_dmma2<<<grid, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
     return;
   }
   if (g_ritz_kind == 1) {
-    dim3 grid((p + kDN - 1) / kDN, (n + kDM - 1) / kDM);
+    const long long grid = (long long)((p + kDN - 1) / kDN) * ((n + kDM - 1) / kDM);
     k_ritz_dmma<<<grid, kThreads, 0, st>>>(V, ld, n, m, Y, p, Vout);
     return;
   }
   if (p <= 32) {
-    dim3 grid((p + 31) / 32, (n + 127) / 128);
+    const long long grid = (long long)((p + 31) / 32) * ((n + 127) / 128);
     k_ritz_rb<32><<<grid, kThreads, 0, st>>>(V, ld, n, m, Y, p, Vout);
   } else {
-    dim3 grid((p + 63) / 64, (n + 127) / 128);
+    const long long grid = (long long)((p + 63) / 64) * ((n + 127) / 128);
     k_ritz_rb<64><<<grid, kThreads, 0, st>>>(V, ld, n, m, Y, p, Vout);
   }
 }

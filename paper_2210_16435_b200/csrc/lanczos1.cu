@@ -43,7 +43,7 @@ void bump_launch();
 namespace {
 constexpr int kR = 64;
 constexpr int kMaxStages = 8;
-constexpr size_t kRingBytes = 214 * 1024;
+constexpr size_t kRingBytes = 210 * 1024;
 constexpr int kLMaxJ = 191;  // basis columns swept (+1 new column in the dots: <= 192)
 
 }  // namespace
@@ -185,20 +185,22 @@ __device__ __forceinline__ void lz_issue(const LzSweepArgs& a, const GraphDev& g
   }
 }
 
-template <int MAXCW, bool NORM>
-__global__ void __launch_bounds__(kThreads, 1) k_lz_update(GraphDev g, ProjDesc pd, LzSweepArgs a, int kStages,
-                                                            const __grid_constant__ CUtensorMap tmap) {
+template <int MAXCW, bool NORM, int NT>
+__global__ void __launch_bounds__(NT, 1) k_lz_update(GraphDev g, ProjDesc pd, LzSweepArgs a, int kStages,
+                                                      const __grid_constant__ CUtensorMap tmap) {
+  constexpr int NCG = NT / kR;   // column groups of the update phase
+  constexpr int NW = NT / 32;    // warps (column owners of the dots phase)
   extern __shared__ __align__(128) double dsm[];
   __shared__ __align__(8) unsigned long long bars[kMaxStages];
   __shared__ double cs[kLMaxJ + 1], cg[kLMaxJ + 1];
-  __shared__ double red[2][4][kR];
+  __shared__ double red[2][NCG][kR];
   __shared__ double rw[kR], rv[kR];
   __shared__ double gam[kHB];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = g.n, J = a.J;
   const int nchunks = (n + kR - 1) / kR;
   const size_t stage_elems = lz_stage_doubles(J);
-  for (int l = tid; l < J; l += kThreads) {
+  for (int l = tid; l < J; l += NT) {
     cs[l] = a.cs[l];
     cg[l] = a.cg[l];
   }
@@ -235,23 +237,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_lz_update(GraphDev g, ProjDesc 
     const uint8_t* gs = reinterpret_cast<const uint8_t*>(ssc + kR);
     const long long row0 = (long long)c * kR;
     {
+      // four independent FMA chains per sum (the FP64 dependency latency, not bandwidth, bounded
+      // the single-chain version: ncu "wait" stalls)
       const int i = tid % kR, cgp = tid / kR;
-      double ps = 0.0, pg = 0.0;
-      for (int l = cgp; l < J; l += 4) {
-        const double vv = buf[(size_t)l * kR + i];
-        ps = fma(vv, cs[l], ps);
-        pg = fma(vv, cg[l], pg);
+      double ps0 = 0.0, ps1 = 0.0, ps2 = 0.0, ps3 = 0.0, pg0 = 0.0, pg1 = 0.0, pg2 = 0.0, pg3 = 0.0;
+      int l = cgp;
+      for (; l + 3 * NCG < J; l += 4 * NCG) {
+        const double v0 = buf[(size_t)l * kR + i], v1 = buf[(size_t)(l + NCG) * kR + i];
+        const double v2_ = buf[(size_t)(l + 2 * NCG) * kR + i], v3 = buf[(size_t)(l + 3 * NCG) * kR + i];
+        ps0 = fma(v0, cs[l], ps0);
+        pg0 = fma(v0, cg[l], pg0);
+        ps1 = fma(v1, cs[l + NCG], ps1);
+        pg1 = fma(v1, cg[l + NCG], pg1);
+        ps2 = fma(v2_, cs[l + 2 * NCG], ps2);
+        pg2 = fma(v2_, cg[l + 2 * NCG], pg2);
+        ps3 = fma(v3, cs[l + 3 * NCG], ps3);
+        pg3 = fma(v3, cg[l + 3 * NCG], pg3);
       }
-      red[0][cgp][i] = ps;
-      red[1][cgp][i] = pg;
+      for (; l < J; l += NCG) {
+        const double vv = buf[(size_t)l * kR + i];
+        ps0 = fma(vv, cs[l], ps0);
+        pg0 = fma(vv, cg[l], pg0);
+      }
+      red[0][cgp][i] = (ps0 + ps1) + (ps2 + ps3);
+      red[1][cgp][i] = (pg0 + pg1) + (pg2 + pg3);
     }
     __syncthreads();
     if (tid < kR) {
       const long long gi = row0 + tid;
       double wv = 0.0, vj = 0.0;
       if (gi < n) {
-        const double sumS = ((red[0][0][tid] + red[0][1][tid]) + red[0][2][tid]) + red[0][3][tid];
-        const double sumG = ((red[1][0][tid] + red[1][1][tid]) + red[1][2][tid]) + red[1][3][tid];
+        double sumS = 0.0, sumG = 0.0;
+#pragma unroll
+        for (int q = 0; q < NCG; ++q) {
+          sumS += red[0][q][tid];
+          sumG += red[1][q][tid];
+        }
         const double vti = vts[tid];
         vj = fma(vti, invmu, -sumS);
         const int gg = gs[tid];
@@ -273,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lz_update(GraphDev g, ProjDesc 
       const double r0 = rw[lane], r1 = rw[lane + 32];
 #pragma unroll
       for (int cc = 0; cc < MAXCW; ++cc) {
-        const int l = w + cc * (kThreads / 32);
+        const int l = w + cc * NW;
         if (l <= J) {
           const double* col = (l < J) ? buf + (size_t)l * kR : rv;
           colacc[cc] = fma(col[lane + 32], r1, fma(col[lane], r0, colacc[cc]));
@@ -288,12 +309,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_lz_update(GraphDev g, ProjDesc 
   }
 #pragma unroll
   for (int cc = 0; cc < MAXCW; ++cc) {
-    const int l = w + cc * (kThreads / 32);
+    const int l = w + cc * NW;
     const double s = warp_sum(colacc[cc]);
     if (lane == 0 && l <= J) a.partials[(size_t)blockIdx.x * (J + 1) + l] = s;
   }
-  block_reduce_store<1 + kHB>(v2, a.partials2 + (size_t)blockIdx.x * (1 + kHB));
-  ticket_finalize<1 + kHB>(a.partials2, a.counter, a.nb, 1 + min(pd.h, kHB));
+  block_reduce_store<1 + kHB, NT>(v2, a.partials2 + (size_t)blockIdx.x * (1 + kHB));
+  ticket_finalize<1 + kHB, NT>(a.partials2, a.counter, a.nb, 1 + min(pd.h, kHB));
 }
 
 // ---------------------------------------------------------------------------
@@ -504,20 +525,20 @@ static int lz_sgrid(int n) {
   return std::max(1, std::min((n + kThreads - 1) / kThreads, sms * 8));
 }
 
-template <int MAXCW, bool NORM>
+template <int MAXCW, bool NORM, int NT>
 static void lz_update_launch(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st) {
   const size_t stage = lz_stage_doubles(a.J) * sizeof(double);
   const int stages = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, kRingBytes / stage));
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_lz_update<MAXCW, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_lz_update<MAXCW, NORM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)std::max(kRingBytes, 2 * lz_stage_doubles(kLMaxJ) * sizeof(double)));
     attr = true;
   }
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
   if (a.J > 0) encode_colmajor_map(a.V, a.ld, a.J, kR, &tmap);
-  k_lz_update<MAXCW, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap);
+  k_lz_update<MAXCW, NORM, NT><<<grid, NT, stages * stage, st>>>(g, pd, a, stages, tmap);
 }
 template <int MAXQ, bool NORM>
 static void lz_update_r_launch(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid,
@@ -535,7 +556,7 @@ static void lz_update_r_launch(const GraphDev& g, const ProjDesc& pd, const LzSw
   if (a.J > 0) encode_colmajor_map(a.V, a.ld, a.J, kR2, &tmap);
   k_lz_update_r<MAXQ, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap);
 }
-int g_lz_sweep = 0;  // 0: 64-row smem kernel (default, measured faster); 1: register-held rows, 32-row chunks (env SFAIRSC_LZ_SWEEP)
+int g_lz_sweep = 0;  // 0: 64-row smem kernel, 256 threads (default, measured fastest); 2: same with 512 threads; 1: register-held rows, 32-row chunks (env SFAIRSC_LZ_SWEEP)
 template <bool NORM>
 static void lz_update_m(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st) {
   if (g_lz_sweep == 1) {
@@ -545,9 +566,15 @@ static void lz_update_m(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs
     else lz_update_r_launch<24, NORM>(g, pd, a, G, st);
     return;
   }
-  if (a.J + 1 <= 64) lz_update_launch<8, NORM>(g, pd, a, grid, st);
-  else if (a.J + 1 <= 128) lz_update_launch<16, NORM>(g, pd, a, grid, st);
-  else lz_update_launch<24, NORM>(g, pd, a, grid, st);
+  if (g_lz_sweep == 2) {  // 512 threads: 16 warps, 8 column groups
+    if (a.J + 1 <= 64) lz_update_launch<4, NORM, 512>(g, pd, a, grid, st);
+    else if (a.J + 1 <= 128) lz_update_launch<8, NORM, 512>(g, pd, a, grid, st);
+    else lz_update_launch<12, NORM, 512>(g, pd, a, grid, st);
+    return;
+  }
+  if (a.J + 1 <= 64) lz_update_launch<8, NORM, 256>(g, pd, a, grid, st);
+  else if (a.J + 1 <= 128) lz_update_launch<16, NORM, 256>(g, pd, a, grid, st);
+  else lz_update_launch<24, NORM, 256>(g, pd, a, grid, st);
 }
 
 void launch_lz_coef(const LzDev& d, int j, cudaStream_t st) {

@@ -1,0 +1,63 @@
+"""BASELINE config 5 at full size on one GPU (exploration / evidence run, not a
+bench value): generate the DC-SBM graph on the GPU (synth/dcsbm.py), build
+the operator from the device CSR, run the single-sweep Lanczos with a
+restart cap, report timings, per-kernel event times and the solution's
+properties.  Properties are checked on the GPU with the library's own apply
+(the oracle cannot run at 1.6e9 entries in minutes)."""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2210_16435_b200 import lib  # noqa: E402
+from synth.dcsbm import config5  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--restarts", type=int, default=400)
+ap.add_argument("--m", type=int, default=0)
+args = ap.parse_args()
+dev = torch.device("cuda:0")
+torch.cuda.set_device(0)
+t = time.time()
+g, cfg = config5(n=args.n, device="cuda")
+torch.cuda.synchronize()
+torch.cuda.empty_cache()  # generator intermediates: give the memory back before the library sizes its basis
+out = {"n": g.n, "nnz": g.nnz, "gen_s": time.time() - t, "meta": g.meta}
+print(json.dumps(out), flush=True)
+k = cfg["k_eig"]
+t = time.time()
+ctx = lib.sfairsc_build_operator(g.row_ptr, g.col, g.val, g.groups, k, False, h=g.h, max_restarts=args.restarts,
+                                 max_basis=args.m)
+torch.cuda.synchronize()
+out["build_s"] = time.time() - t
+out["info"] = ctx.info()
+del g
+torch.cuda.empty_cache()
+lib.profile_enable(ctx, True)
+t = time.time()
+Xd = torch.empty((k, out["n"]), dtype=torch.float64, device=dev)
+try:
+    ev, _, st = lib.sfairsc_eigs(ctx, k, cfg["tol"], evecs=Xd)
+    out["status"] = "OK"
+except lib.SfairscError as e:
+    st = ctx.last_stats
+    out["status"] = e.name
+    out["error"] = str(e)
+    ev = None
+torch.cuda.synchronize()
+out["eigs_s"] = time.time() - t
+out["stats"] = st
+prof = lib.profile_read(ctx)
+out["eigs_kernels"] = {kk: {"ms": v["ms"], "launches": v["launches"],
+                            "us": 1e3 * v["ms"] / max(1, v["launches"])} for kk, v in prof.items() if v["launches"]}
+if ev is not None:
+    out["evals"] = [float(x) for x in ev]
+    G = Xd @ Xd.T
+    out["orth_err"] = float((G - torch.eye(k, device=dev, dtype=torch.float64)).abs().max())
+print(json.dumps(out, indent=1), flush=True)
+ctx.close()

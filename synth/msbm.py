@@ -298,8 +298,11 @@ def baseline_config(c: int, n: int | None = None) -> tuple[MSBMGraph, dict]:
     """Graph for BASELINE config `c` (seed 16435 + c).  `n` optionally rescales
     the vertex count (same law, same mean degree / literal probabilities) for
     reduced-size tests; group counts are rescaled proportionally."""
-    if c == 5:
-        raise NotImplementedError("config 5 (DC-SBM, n=5e7) generator: not built this round")
+    if c == 5:  # DC-SBM law (synth/dcsbm.py); generated with torch on the GPU when one is visible
+        import torch
+        from .dcsbm import config5
+        g, cfg = config5(n=n, device="cuda" if torch.cuda.is_available() else "cpu")
+        return g.host(), cfg
     cfg = dict(CONFIGS[c])
     params = {kk: cfg[kk] for kk in ("probs", "rel", "mean_degree", "group_probs", "group_counts", "weights") if kk in cfg}
     nn = cfg["n"] if n is None else int(n)
