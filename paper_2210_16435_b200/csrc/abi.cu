@@ -98,7 +98,7 @@ static void free_ctx(sfairsc_ctx* c) {
   void* ptrs[] = {c->rp, c->ci, c->row_split, c->vv, c->dg, c->s, c->grp, c->isb, c->uh, c->partials, c->counters,
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
                   c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta,
-                  c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags, c->Hdev, c->sdev, c->lz, c->partials2, c->dd};
+                  c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags, c->Hdev, c->sdev, c->lz, c->partials2, c->dd, c->rpb};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hp) cudaFreeHost(c->hp);
@@ -169,8 +169,7 @@ sfairsc_status sfz::apply_dev(sfairsc_ctx* c, const double* x, double* y) {
   }
   {
     ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
-    launch_spmv(c->g(), c->vs, c->row_split, c->spmv_grid, c->vp, c->vt, c->partials, c->counters + 1, c->bs_t,
-                c->st);
+    ctx_spmv(c, c->vp, c->vt);
   }
   if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
   {
@@ -181,6 +180,20 @@ sfairsc_status sfz::apply_dev(sfairsc_ctx* c, const double* x, double* y) {
   return SFAIRSC_OK;
 }
 
+
+void sfz::ctx_spmv(sfairsc_ctx* c, const double* p, double* t) {
+  if (c->nblk <= 1) {
+    launch_spmm(c->g(), 1, c->vs, c->row_split, c->spmv_grid, p, t, c->partials, c->counters + 1, c->bs_t, c->st);
+    return;
+  }
+  for (int b = 0; b < c->nblk; ++b) {  // p restricted to block b (8n/nblk bytes) stays in L2 while W_b streams
+    GraphDev g = c->g();
+    g.rp = c->rpb + (size_t)b * (c->n + 1);
+    const int cmode = (b == 0) ? 1 : (b + 1 < c->nblk ? 2 : 3);
+    launch_spmv_colblock(g, c->vs_blk, c->row_split, c->spmv_grid, p, t, c->partials, c->counters + 1, c->bs_t, cmode,
+                         c->st);
+  }
+}
 
 // max_i ||L^sigma x_i - theta_i x_i|| / sigma over the k columns of X (A11), k fresh applies
 sfairsc_status sfz::true_residuals(sfairsc_ctx* c, const double* theta, int k, double* max_out) {
@@ -459,6 +472,51 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   CUB(cudaStreamSynchronize(c->st));
   c->sigma = opts.sigma_override > 0 ? opts.sigma_override : hsig;
 
+  // column blocking (single GPU, single-vector solvers): when 8n bytes of the gathered vector exceed what
+  // L2 keeps across the CSR stream (~48 MB), the SpMV runs per column block on a block-major copy of W
+  {
+    const double pbytes = 8.0 * n;
+    const double blk_bytes = getenv("SFAIRSC_COLBLK_MB") ? atof(getenv("SFAIRSC_COLBLK_MB")) * 1048576.0 : 48.0 * 1048576.0;
+    if (c->bsz == 1 && pbytes > 1.34 * blk_bytes && nnz > 0) {
+      const int nb = (int)std::ceil(pbytes / blk_bytes);
+      const int cb = (n + nb - 1) / nb;
+      int* cnt = nullptr;
+      CUB(dalloc(&cnt, (size_t)nb * n));
+      launch_colblk_starts(c->rp, c->ci, n, nb, cb, cnt, c->st);
+      std::vector<int32_t> hc((size_t)nb * n);
+      CUB(cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * hc.size(), cudaMemcpyDeviceToHost, c->st));
+      CUB(cudaStreamSynchronize(c->st));
+      cudaFree(cnt);
+      std::vector<int32_t> hr((size_t)nb * (n + 1));
+      long long base = 0;
+      for (int b = 0; b < nb; ++b) {
+        int32_t* r = hr.data() + (size_t)b * (n + 1);
+        const int32_t* q = hc.data() + (size_t)b * n;
+        r[0] = (int32_t)base;
+        for (int i = 0; i < n; ++i) r[i + 1] = r[i] + q[i];
+        base = r[n];
+      }
+      if (base != nnz) return bail(fail(SFAIRSC_E_CUDA, "column blocking lost entries (%lld vs %d)", base, nnz));
+      CUB(dalloc(&c->rpb, hr.size()));
+      CUB(cudaMemcpyAsync(c->rpb, hr.data(), sizeof(int32_t) * hr.size(), cudaMemcpyHostToDevice, c->st));
+      int* ci2 = nullptr;
+      double* vv2 = nullptr;
+      CUB(dalloc(&ci2, nnz));
+      CUB(dalloc(&vv2, nnz));
+      launch_colblk_scatter(c->rp, c->ci, c->vv, n, nb, c->rpb, ci2, vv2, c->st);
+      CUB(cudaGetLastError());
+      CUB(cudaStreamSynchronize(c->st));
+      cudaFree(c->ci);
+      cudaFree(c->vv);
+      c->ci = ci2;
+      c->vv = vv2;
+      c->nblk = nb;
+      const double mdb = (double)nnz / n / nb;
+      int vsb = 2;
+      while (vsb < 32 && vsb * 4 < mdb) vsb *= 2;
+      c->vs_blk = vsb;
+    }
+  }
   // A3: factored basis of range(C): beta_s = sum_{V_s} s_i^2, u_s = |V_s| beta_s^{-1/2}
   c->sgrid = sweep_grid(n, c->num_sms);
   // SpMV partition: CTA b owns rows with cumulative (nnz + 4 rows) weight in [b, b+1)/G
@@ -619,7 +677,7 @@ static sfairsc_status project_dev(sfairsc_ctx* c, const double* x, double* y) {
 
 static sfairsc_status lap_dev(sfairsc_ctx* c, const double* x, double* y) {
   ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
-  launch_spmv(c->g(), c->vs, c->row_split, c->spmv_grid, x, y, c->partials, c->counters + 1, c->bs_t, c->st);
+  ctx_spmv(c, x, y);
   CHECK_LAUNCH();
   return SFAIRSC_OK;
 }
@@ -854,8 +912,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
     // (no host synchronisation inside the expansion; breakdowns are detected at the next sync)
     {
       ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
-      launch_spmv(c->g(), c->vs, c->row_split, c->spmv_grid, c->vp, c->vt, c->partials, c->counters + 1, c->bs_t,
-                  c->st);
+      ctx_spmv(c, c->vp, c->vt);
     }
     if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
     TRY(L.cgs2(j + 1, true));

@@ -68,11 +68,14 @@ __device__ __forceinline__ void ld_row(const double* __restrict__ p, int c, doub
 // per row, nnz-balanced contiguous row ranges per CTA; each lane keeps up to
 // 4 (col, val) pairs and 4 gathers in flight.  Epilogue: B^T T per vector.
 // ----------------------------------------------------------------------------
+// cmode (column-blocked SpMV for a gathered vector too large for L2, config 5):
+//   0 whole matrix (write t, epilogue); 1 first column block (write t); 2 middle (t -= W_b p);
+//   3 last (t -= W_b p, epilogue).  g.rp is then the block's row offsets into the block-major CSR.
 template <int VS, int NB, bool NORM, bool CG = false>
 __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __restrict__ row_split,
                                                    const double* __restrict__ p, const double* __restrict__ p_self,
                                                    double* __restrict__ t, double* partials, unsigned* counter,
-                                                   double* bsum_t) {
+                                                   double* bsum_t, int cmode = 0) {
   constexpr int NG = kThreads / VS, U = 4;
   const int r0 = row_split[blockIdx.x], r1 = row_split[blockIdx.x + 1];
   const int lane = threadIdx.x % VS, gid = threadIdx.x / VS;
@@ -119,12 +122,13 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
       const double di = NORM ? 1.0 : __ldg(g.dg + row);
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
-        const double tc = fma(di, pi[c], -acc[c]);
+        const double tc = cmode < 2 ? fma(di, pi[c], -acc[c]) : t[(size_t)row * NB + c] - acc[c];
         t[(size_t)row * NB + c] = tc;
         ptacc[c] = fma(pi[c], tc, ptacc[c]);
       }
     }
   }
+  if (cmode == 1 || cmode == 2) return;  // partial column block: no epilogue
   // epilogue: B^T t and p^T t over this CTA's rows (fixed order), one vector at a time;
   // out layout: bsum_t[c * kBT + s] = (B^T t_c)_s (s < kHB), bsum_t[c * kBT + kHB] = p_c^T t_c
 #pragma unroll 1
@@ -566,7 +570,7 @@ static int rgrid(int n) { return std::max(1, std::min((n + 4 * kThreads - 1) / (
 
 template <int VS, int NB>
 static void spmm_vs(const GraphDev& g, const int* split, int grid, const double* p, const double* ps, double* t,
-                    double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
+                    double* partials, unsigned* counter, double* bsum_t, cudaStream_t st, int cmode = 0) {
   if (NB == 1 && g_spmv_gather == 1) {
     if (g.normalized)
       k_spmm<VS, NB, true, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
@@ -575,9 +579,65 @@ static void spmm_vs(const GraphDev& g, const int* split, int grid, const double*
     return;
   }
   if (g.normalized)
-    k_spmm<VS, NB, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
+    k_spmm<VS, NB, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t, cmode);
   else
-    k_spmm<VS, NB, false><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
+    k_spmm<VS, NB, false><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t, cmode);
+}
+void launch_spmv_colblock(const GraphDev& g, int vs, const int* split, int grid, const double* p, double* t,
+                          double* partials, unsigned* counter, double* bsum_t, int cmode, cudaStream_t st) {
+  bump_launch();
+  switch (vs) {
+    case 2: spmm_vs<2, 1>(g, split, grid, p, p, t, partials, counter, bsum_t, st, cmode); break;
+    case 4: spmm_vs<4, 1>(g, split, grid, p, p, t, partials, counter, bsum_t, st, cmode); break;
+    case 8: spmm_vs<8, 1>(g, split, grid, p, p, t, partials, counter, bsum_t, st, cmode); break;
+    case 16: spmm_vs<16, 1>(g, split, grid, p, p, t, partials, counter, bsum_t, st, cmode); break;
+    default: spmm_vs<32, 1>(g, split, grid, p, p, t, partials, counter, bsum_t, st, cmode); break;
+  }
+}
+// column blocking of the CSR (block-major copy): per row, the start of each column block (cols sorted)
+__global__ void k_colblk_starts(const int* __restrict__ rp, const int* __restrict__ ci, int n, int nblk, int cb,
+                                int* __restrict__ cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int a = rp[i], b = rp[i + 1];
+    int prev = a;
+    for (int q = 1; q <= nblk; ++q) {
+      int pos = b;
+      if (q < nblk) {  // first entry with col >= q * cb
+        int lo = prev, hi = b;
+        const long long bound = (long long)q * cb;
+        while (lo < hi) {
+          const int mid = lo + ((hi - lo) >> 1);
+          if (ci[mid] < bound) lo = mid + 1; else hi = mid;
+        }
+        pos = lo;
+      }
+      cnt[(size_t)(q - 1) * n + i] = pos - prev;
+      prev = pos;
+    }
+  }
+}
+__global__ void k_colblk_scatter(const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vv,
+                                 int n, int nblk, const int* __restrict__ rpb, int* __restrict__ ci2,
+                                 double* __restrict__ vv2) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int src = rp[i];
+    for (int q = 0; q < nblk; ++q) {
+      const int d0 = rpb[(size_t)q * (n + 1) + i], d1 = rpb[(size_t)q * (n + 1) + i + 1];
+      for (int e = d0; e < d1; ++e, ++src) {
+        ci2[e] = ci[src];
+        vv2[e] = vv[src];
+      }
+    }
+  }
+}
+void launch_colblk_starts(const int* rp, const int* ci, int n, int nblk, int cb, int* cnt, cudaStream_t st) {
+  bump_launch();
+  k_colblk_starts<<<sgrid(n), kThreads, 0, st>>>(rp, ci, n, nblk, cb, cnt);
+}
+void launch_colblk_scatter(const int* rp, const int* ci, const double* vv, int n, int nblk, const int* rpb, int* ci2,
+                           double* vv2, cudaStream_t st) {
+  bump_launch();
+  k_colblk_scatter<<<sgrid(n), kThreads, 0, st>>>(rp, ci, vv, n, nblk, rpb, ci2, vv2);
 }
 template <int NB>
 static void spmm_nb(const GraphDev& g, int vs, const int* split, int grid, const double* p, const double* ps,

@@ -105,6 +105,10 @@ struct sfairsc_ctx {
   // single-sweep (lagged) Lanczos (lanczos1.cu); uses ldT = m + 2 for H
   bool lagged = false;
   double *Hdev = nullptr, *sdev = nullptr, *lz = nullptr, *partials2 = nullptr, *dd = nullptr;
+  // column-blocked CSR (the gathered vector exceeds L2, e.g. config 5): block-major copy of the CSR,
+  // rpb[b*(n+1) + i] = start of row i in column block b; nblk = 1: plain CSR
+  int nblk = 1, vs_blk = 2;
+  int* rpb = nullptr;
   // row-partitioned contexts: all device state lives in dist
   sfz::DistCtx* dist = nullptr;
   // results
@@ -146,6 +150,8 @@ namespace sfz {
 sfairsc_status fail(sfairsc_status st, const char* fmt, ...);
 sfairsc_status apply_dev(sfairsc_ctx* c, const double* x, double* y);  // y = L^sigma x (device vectors)
 sfairsc_status true_residuals(sfairsc_ctx* c, const double* theta, int k, double* max_out);  // over X
+// t = L p (+ B^T t, p^T t into bs_t) through the plain or the column-blocked CSR
+void ctx_spmv(sfairsc_ctx* c, const double* p, double* t);
 double now_s();
 }
 

@@ -638,8 +638,7 @@ struct Lagged {
   sfairsc_status step(int j) {
     {
       ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
-      launch_spmm(c->g(), 1, c->vs, c->row_split, c->spmv_grid, c->vp, c->vt, c->partials, c->counters + 1, c->bs_t,
-                  c->st);  // epilogue: B^T t and p~^T t (bs_t[kHB])
+      ctx_spmv(c, c->vp, c->vt);  // epilogue: B^T t and p~^T t (bs_t[kHB])
     }
     {
       ProfScope ps(c, K_OTHER, 0.0);

@@ -36,6 +36,7 @@ ctx = lib.sfairsc_build_operator(g.row_ptr, g.col, g.val, g.groups, k, False, h=
 torch.cuda.synchronize()
 out["build_s"] = time.time() - t
 out["info"] = ctx.info()
+groups_dev = g.groups.to(torch.int64)
 del g
 torch.cuda.empty_cache()
 lib.profile_enable(ctx, True)
@@ -59,5 +60,13 @@ if ev is not None:
     out["evals"] = [float(x) for x in ev]
     G = Xd @ Xd.T
     out["orth_err"] = float((G - torch.eye(k, device=dev, dtype=torch.float64)).abs().max())
+    # fairness F^T X = 0 (unnormalized: C = F = G - 1 z^T, first h-1 columns), computed independently in torch
+    h = out["info"]["h"]
+    n = out["n"]
+    cnt = torch.bincount(groups_dev, minlength=h).to(torch.float64)
+    gs = torch.zeros((h, k), dtype=torch.float64, device=dev).index_add_(0, groups_dev, Xd.T)
+    FtX = gs[: h - 1] - (cnt[: h - 1, None] / n) * Xd.sum(dim=1)[None, :]
+    out["FtX_rel"] = float(FtX.norm() / Xd.norm())
+    out["lambda1_rel"] = abs(out["evals"][0]) / st["sigma"]
 print(json.dumps(out, indent=1), flush=True)
 ctx.close()

@@ -326,3 +326,25 @@ def test_config3_full_size_properties(gpu_lib):
 def test_config4_full_size_properties(gpu_lib):
     ev, st = _full_size_properties(gpu_lib, 4, n_sample=2)
     assert st["steps"] > 0
+
+
+# --- column-blocked SpMV (the config-5 path: gathered vector larger than L2) ------------------
+
+@pytest.mark.parametrize("normalized", [False, True])
+def test_column_blocked_spmv_matches_oracle(gpu_lib, normalized, monkeypatch):
+    """Force the block-major CSR (normally chosen for n > ~8M) on a small graph:
+    SpMV, L^sigma and the eigensolve must equal the oracle as for the plain CSR."""
+    monkeypatch.setenv("SFAIRSC_COLBLK_MB", "0.003")  # 3 KB column blocks -> several blocks at n ~ 1000
+    g = random_graph(1031, 5, p=0.02, seed=21, weights="uniform")
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, normalized)
+    ctx = _ctx(gpu_lib, g, 6, normalized)
+    monkeypatch.delenv("SFAIRSC_COLBLK_MB")
+    x = np.random.default_rng(5).standard_normal((2, g.n))
+    tol = 1e-13 * op.sigma * np.abs(x).max()
+    assert np.abs(gpu_lib.sfairsc_laplacian(ctx, np.ascontiguousarray(x[0])) - op.Ln @ x[0]).max() <= tol
+    assert np.abs(gpu_lib.sfairsc_apply(ctx, x) - np.stack([op.apply(v) for v in x])).max() <= tol
+    ev, Xt, st = gpu_lib.sfairsc_eigs(ctx, 6, 1e-10)
+    ctx.close()
+    dense = fairsc.fairsc_dense(g.dense(), g.groups, g.h, 6, normalized)
+    assert st["converged"] == 1 and st["max_resid_rel"] <= 1e-9
+    assert np.all(np.abs(ev - dense.evals[:6]) <= 1e-8 * np.abs(dense.evals[:6]) + 1e-12 * st["sigma"])
