@@ -4,7 +4,8 @@
 * count matrix M = G^T H (Eq. mz, P:193-203);
 * adjusted Rand index (Hubert & Arabie) — permutation invariant;
 * Hungarian matching of cluster labels (scipy linear_sum_assignment);
-* largest principal angle between subspaces, sine form (reading R9).
+* largest principal angle between subspaces, sine form (reading R9);
+* error rate of a clustering (Eq. err).
 """
 from __future__ import annotations
 
@@ -65,3 +66,19 @@ def subspace_sin(Xa, Xb):
     Qb, _ = np.linalg.qr(Xb)
     R = Qb - Qa @ (Qa.T @ Qb)
     return float(np.linalg.norm(R, 2))
+
+
+def error_rate(truth, labels, k):
+    """Err(H^ - H) = (1/n) min_{J in Pi_k} ||H^ J - H||_F^2 (Eq. err, P:911-918):
+    H, H^ are the n x k cluster indicator matrices; the minimising permutation is
+    the assignment maximising the agreement (the squared Frobenius distance of
+    indicator matrices is 2 (n - agreement)).  Note this is twice the proportion
+    of misclustered vertices (reading R17)."""
+    truth = np.asarray(truth)
+    labels = np.asarray(labels)
+    n = len(truth)
+    tab = np.zeros((k, k), dtype=np.int64)
+    np.add.at(tab, (labels, truth), 1)
+    r, c = linear_sum_assignment(-tab)
+    agree = int(tab[r, c].sum())
+    return 2.0 * (n - agree) / n

@@ -9,8 +9,8 @@ App. B.1.2, with the five BASELINE.json configurations as
 concrete parameterisations, plus the small structured
 graphs the oracle pins use (disjoint cliques, P-closed-1 in SURVEY §8(c)).
 """
-from .msbm import (MSBMGraph, msbm, baseline_config, planted_cliques,
+from .msbm import (MSBMGraph, msbm, baseline_config, exp1_msbm, planted_cliques,
                    random_graph, CONFIGS)
 
-__all__ = ["MSBMGraph", "msbm", "baseline_config", "planted_cliques",
+__all__ = ["MSBMGraph", "msbm", "baseline_config", "exp1_msbm", "planted_cliques",
            "random_graph", "CONFIGS"]

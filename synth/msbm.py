@@ -315,6 +315,20 @@ def baseline_config(c: int, n: int | None = None) -> tuple[MSBMGraph, dict]:
     return g, cfg
 
 
+def exp1_msbm(n, h, *, k=5, seed=0) -> MSBMGraph:
+    """The paper's Experiment-1 / Fig. 8 m-SBM: k = 5
+    fair planted clusters, h equal groups, a,b,c,d = (10, 7, 4, 1) (log n / n)^(2/3)
+    with the paper's letters (b: different cluster / same group, c: same
+    cluster / different group, Eq. p-msbm), unit weights (the
+    caption gives no alpha, beta; reading R11).  §8(f) N3."""
+    base = (np.log(n) / n) ** (2.0 / 3.0)
+    probs = tuple(float(x * base) for x in (10, 7, 4, 1))
+    counts = np.full(h, n // h, dtype=np.int64)
+    counts[: n - counts.sum()] += 1
+    return msbm(n, h, k, seed=seed, probs=probs, group_counts=tuple(int(c) for c in counts), weights="unit",
+                letters="paper", name=f"exp1-h{h}")
+
+
 def planted_cliques(k, m, h, seed=0, shuffle=True) -> MSBMGraph:
     """k disjoint complete graphs K_m, each holding every group in exact
     proportion m/h (SURVEY §8(c) P-closed-1).  Unit weights."""

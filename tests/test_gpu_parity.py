@@ -348,3 +348,50 @@ def test_column_blocked_spmv_matches_oracle(gpu_lib, normalized, monkeypatch):
     dense = fairsc.fairsc_dense(g.dense(), g.groups, g.h, 6, normalized)
     assert st["converged"] == 1 and st["max_resid_rel"] <= 1e-9
     assert np.all(np.abs(ev - dense.evals[:6]) <= 1e-8 * np.abs(dense.evals[:6]) + 1e-12 * st["sigma"])
+
+
+# --- BASELINE config 5 (DC-SBM, reading R20) ---------------------------------------
+
+def test_eigs_config5_reduced_vs_tier_s(gpu_lib):
+    """Config 5 law (unnormalized, h=8, k=64, Pareto(2.5) degree propensities,
+    Dirichlet(2) cluster sizes) at n = 20,000 against the Tier S oracle (ARPACK
+    on the paper's matrix-free operator).  The full-size (n = 5e7) solve is an
+    evidence run (scripts/run_cfg5.py, profiles/) — ARPACK cannot finish there."""
+    from synth.dcsbm import config5
+    g, cfg = config5(n=20_000, device="cuda")
+    g = g.host()
+    k = cfg["k_eig"]
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, False)
+    ref = sfairsc_cpu.sfairsc_arpack(op, k, tol=1e-12, seed=5, ncv=160)
+    gap = ref.evals[k] - ref.evals[k - 1]
+    _check_eigs(gpu_lib, g, k, False, cfg["tol"], ref_evals=ref.evals[:k], ref_X=ref.X, gap=gap)
+
+
+# --- §8(f) N3: the paper's Experiment-1 m-SBM (fair vs unconstrained SC) ---------------------
+
+@pytest.mark.parametrize("h", [2, 5])
+def test_exp1_fair_recovers_planted_sc_fails(gpu_lib, h):
+    """Fig. 8 setting: with a,b,c,d = (10,7,4,1)(log n/n)^(2/3)
+    group membership dominates the edges, so SC (Alg. 1, h = 1) splits by group while
+    s-FairSC recovers the fair planted clusters; the error rate (Eq. err) of the GPU
+    clustering equals the oracle's (dense FairSC + oracle k-means) on the same graph."""
+    from oracle.kmeans import kmeans
+    from oracle.metrics import error_rate
+    from synth import exp1_msbm
+    n, k = 3000, 5
+    g = exp1_msbm(n, h, seed=3)
+    ctx = _ctx(gpu_lib, g, k, True)
+    gpu_lib.sfairsc_eigs(ctx, k, 1e-10)
+    lab_fair, _ = gpu_lib.sfairsc_embed_kmeans(ctx, 11)
+    ctx.close()
+    ctx = gpu_lib.sfairsc_build_operator(g.row_ptr, g.col, g.val, np.zeros(n, np.int32), k, True, h=1)
+    gpu_lib.sfairsc_eigs(ctx, k, 1e-10)
+    lab_sc, _ = gpu_lib.sfairsc_embed_kmeans(ctx, 11)
+    ctx.close()
+    err_fair = error_rate(g.clusters, lab_fair, k)
+    err_sc = error_rate(g.clusters, lab_sc, k)
+    dense = fairsc.fairsc_dense(g.dense(), g.groups, h, k, True)
+    err_or = error_rate(g.clusters, kmeans(dense.H, k, 11).labels, k)
+    assert err_fair <= 0.05, err_fair
+    assert err_sc >= 0.3, err_sc
+    assert abs(err_fair - err_or) <= 2.0 / n * 5  # a handful of borderline vertices at most

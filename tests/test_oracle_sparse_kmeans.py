@@ -137,3 +137,24 @@ def test_balance_example_b2_and_hungarian():
     other = perm[labels]
     m = hungarian_match(labels, other, 3)
     assert np.array_equal(m[other], labels)
+
+
+def test_error_rate_definition():
+    """Eq. err: (1/n) min_J ||H^ J - H||_F^2 — brute force over all
+    k! permutations on small cases, and the closed values 0 and 2/n."""
+    import itertools
+    from oracle.metrics import error_rate
+    rng = np.random.default_rng(0)
+    for trial in range(20):
+        n, k = 12, 3
+        t = rng.integers(0, k, n)
+        l = rng.integers(0, k, n)
+        H = np.eye(k)[t]
+        Hh = np.eye(k)[l]
+        best = min(np.sum((Hh @ np.eye(k)[list(p)] - H) ** 2) for p in itertools.permutations(range(k))) / n
+        assert error_rate(t, l, k) == pytest.approx(best)
+    t = np.array([0, 0, 1, 1, 2, 2])
+    assert error_rate(t, (t + 1) % 3, 3) == 0.0  # relabelled: no error
+    l = t.copy()
+    l[0] = 1
+    assert error_rate(t, l, 3) == pytest.approx(2.0 / 6)
