@@ -63,10 +63,13 @@ if ev is not None:
     # fairness F^T X = 0 (unnormalized: C = F = G - 1 z^T, first h-1 columns), computed independently in torch
     h = out["info"]["h"]
     n = out["n"]
+    # per-group pairwise (tree) sums, not atomics: the check's own rounding stays ~log(n) eps
     cnt = torch.bincount(groups_dev, minlength=h).to(torch.float64)
-    gs = torch.zeros((h, k), dtype=torch.float64, device=dev).index_add_(0, groups_dev, Xd.T)
-    FtX = gs[: h - 1] - (cnt[: h - 1, None] / n) * Xd.sum(dim=1)[None, :]
+    tot = Xd.sum(dim=1)
+    FtX = torch.stack([Xd[:, groups_dev == s_].sum(dim=1) - (cnt[s_] / n) * tot for s_ in range(h - 1)])
     out["FtX_rel"] = float(FtX.norm() / Xd.norm())
+    Fnorm = float(torch.sqrt(cnt[: h - 1] * (1 - cnt[: h - 1] / n)).max())  # ~ |F|_2 (diagonal-dominant F^T F)
+    out["FtX_normwise"] = out["FtX_rel"] / Fnorm
     out["lambda1_rel"] = abs(out["evals"][0]) / st["sigma"]
 print(json.dumps(out, indent=1), flush=True)
 ctx.close()
