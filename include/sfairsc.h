@@ -83,8 +83,8 @@ typedef struct {
 /* Options of the extended build.  sfairsc_default_opts() fills defaults. */
 typedef struct {
   double sigma_override;  /* <= 0: sigma = ||L||_1; > 0: use this shift (must exceed lambda_k, Prop. 3.4) */
-  int32_t max_basis;      /* Lanczos basis size m; 0: min(192, max(2k+10, 3k, 20)) (SPEC S:342 suggests 2k+10), capped at n */
-  int32_t keep;           /* Ritz vectors kept at a thick restart; 0: k + 3(m-k)/5 (block: k + (m-k)/2) */
+  int32_t max_basis;      /* Lanczos basis size m; 0: min(192, max(2k+10, 3.4k, 20)) (SPEC S:342 suggests 2k+10), capped at n and to fit HBM */
+  int32_t keep;           /* Ritz vectors kept at a thick restart; 0: k + (m-k)/4 (block: k + (m-k)/2) */
   int32_t max_restarts;   /* 0: 100000 */
   uint64_t start_seed;    /* Philox key for the Lanczos start / breakdown vectors */
   double tol_eff_cap;     /* residual target = min(tol, tol_eff_cap) * sigma; <= 0: 1e-10 (reading R7) */

@@ -324,15 +324,15 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   }
   c->ldv = ((long long)n + 255) / 256 * 256;
   // Krylov basis size (SPEC S:342 default), capped so that v_{m+1} exists
-  // default basis: m = max(2k + 10, 3k, 20) (SPEC S:342 suggests 2k + 10; 3k measured faster at config 4,
-  // profiles/r1_exp), keep k + 3(m - k)/5 Ritz vectors per thick restart
-  int m = opts.max_basis > 0 ? opts.max_basis : std::min(192, std::max(std::max(2 * k + 10, 3 * k), 20));
+  // default basis: m = max(2k + 10, 3.4k, 20) (SPEC S:342 suggests 2k + 10; 3.4k measured fastest at config 4,
+  // profiles/r1_exp/cfg4_restart_scan.json), keep k + (m - k)/4 Ritz vectors per thick restart
+  int m = opts.max_basis > 0 ? opts.max_basis : std::min(192, std::max(std::max(2 * k + 10, 17 * k / 5), 20));
   m = std::min(m, kMaxJ - 1);
   m = std::min(m, std::max(n - 1, 1));
   m = std::max(m, std::min(k + 1, n));
   if (m > n) m = n;
   c->m = m;
-  c->keep = opts.keep > 0 ? opts.keep : k + 3 * (m - k) / 5;
+  c->keep = opts.keep > 0 ? opts.keep : k + (m - k) / 4;
   c->keep = std::max(std::min(c->keep, m - 1), std::min(k, m - 1));
   // block Lanczos sizing: m + b <= kBMaxJ, m + b <= dim null(C^T) = n - h + 1, keep >= k, (m - keep) % b == 0
   c->bsz = opts.block_size > 0 ? opts.block_size : 1;
@@ -367,7 +367,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
         const int mnew = std::max(mfit, k + std::max(2, c->bsz));
         if (mnew < k + 2) return bail(fail(SFAIRSC_E_OOM, "Krylov basis for k=%d does not fit in device memory", k));
         const int b = std::max(1, c->bsz);
-        int kp = k + 3 * (mnew - k) / 5;
+        int kp = opts.keep > 0 ? opts.keep : k + (mnew - k) / 4;
         kp = std::max(k, std::min(kp, mnew - b));
         c->m = m = (b > 1) ? kp + b * ((mnew - kp) / b) : mnew;
         c->keep = kp;
