@@ -71,11 +71,11 @@ __device__ __forceinline__ void ld_row(const double* __restrict__ p, int c, doub
 // cmode (column-blocked SpMV for a gathered vector too large for L2, config 5):
 //   0 whole matrix (write t, epilogue); 1 first column block (write t); 2 middle (t -= W_b p);
 //   3 last (t -= W_b p, epilogue).  g.rp is then the block's row offsets into the block-major CSR.
-template <int VS, int NB, bool NORM, bool CG = false>
+template <int VS, int NB, bool NORM, bool CG = false, int cmode = 0>
 __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __restrict__ row_split,
                                                    const double* __restrict__ p, const double* __restrict__ p_self,
                                                    double* __restrict__ t, double* partials, unsigned* counter,
-                                                   double* bsum_t, int cmode = 0) {
+                                                   double* bsum_t) {
   constexpr int NG = kThreads / VS, U = 4;
   const int r0 = row_split[blockIdx.x], r1 = row_split[blockIdx.x + 1];
   const int lane = threadIdx.x % VS, gid = threadIdx.x / VS;
@@ -122,13 +122,15 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
       const double di = NORM ? 1.0 : __ldg(g.dg + row);
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
-        const double tc = cmode < 2 ? fma(di, pi[c], -acc[c]) : t[(size_t)row * NB + c] - acc[c];
+        double tc;
+        if constexpr (cmode < 2) tc = fma(di, pi[c], -acc[c]);
+        else tc = t[(size_t)row * NB + c] - acc[c];
         t[(size_t)row * NB + c] = tc;
         ptacc[c] = fma(pi[c], tc, ptacc[c]);
       }
     }
   }
-  if (cmode == 1 || cmode == 2) return;  // partial column block: no epilogue
+  if constexpr (cmode == 1 || cmode == 2) return;  // partial column block: no epilogue
   // epilogue: B^T t and p^T t over this CTA's rows (fixed order), one vector at a time;
   // out layout: bsum_t[c * kBT + s] = (B^T t_c)_s (s < kHB), bsum_t[c * kBT + kHB] = p_c^T t_c
 #pragma unroll 1
@@ -578,10 +580,16 @@ static void spmm_vs(const GraphDev& g, const int* split, int grid, const double*
       k_spmm<VS, NB, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
     return;
   }
-  if (g.normalized)
-    k_spmm<VS, NB, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t, cmode);
-  else
-    k_spmm<VS, NB, false><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t, cmode);
+#define SPMM_CM(CM)                                                                                              \
+  if (g.normalized) k_spmm<VS, NB, true, false, CM><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
+  else k_spmm<VS, NB, false, false, CM><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
+  switch (cmode) {
+    case 0: SPMM_CM(0) break;
+    case 1: SPMM_CM(1) break;
+    case 2: SPMM_CM(2) break;
+    default: SPMM_CM(3) break;
+  }
+#undef SPMM_CM
 }
 void launch_spmv_colblock(const GraphDev& g, int vs, const int* split, int grid, const double* p, double* t,
                           double* partials, unsigned* counter, double* bsum_t, int cmode, cudaStream_t st) {
