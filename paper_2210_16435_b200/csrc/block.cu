@@ -592,14 +592,16 @@ static void spmm_vs(const GraphDev& g, const int* split, int grid, const double*
 #undef SPMM_CM
 }
 void launch_spmv_colblock(const GraphDev& g, int vs, const int* split, int grid, const double* p, double* t,
-                          double* partials, unsigned* counter, double* bsum_t, int cmode, cudaStream_t st) {
+                          double* partials, unsigned* counter, double* bsum_t, int cmode, cudaStream_t st,
+                          const double* p_self) {
   bump_launch();
+  const double* ps = p_self ? p_self : p;
   switch (vs) {
-    case 2: spmm_vs<2, 1>(g, split, grid, p, p, t, partials, counter, bsum_t, st, cmode); break;
-    case 4: spmm_vs<4, 1>(g, split, grid, p, p, t, partials, counter, bsum_t, st, cmode); break;
-    case 8: spmm_vs<8, 1>(g, split, grid, p, p, t, partials, counter, bsum_t, st, cmode); break;
-    case 16: spmm_vs<16, 1>(g, split, grid, p, p, t, partials, counter, bsum_t, st, cmode); break;
-    default: spmm_vs<32, 1>(g, split, grid, p, p, t, partials, counter, bsum_t, st, cmode); break;
+    case 2: spmm_vs<2, 1>(g, split, grid, p, ps, t, partials, counter, bsum_t, st, cmode); break;
+    case 4: spmm_vs<4, 1>(g, split, grid, p, ps, t, partials, counter, bsum_t, st, cmode); break;
+    case 8: spmm_vs<8, 1>(g, split, grid, p, ps, t, partials, counter, bsum_t, st, cmode); break;
+    case 16: spmm_vs<16, 1>(g, split, grid, p, ps, t, partials, counter, bsum_t, st, cmode); break;
+    default: spmm_vs<32, 1>(g, split, grid, p, ps, t, partials, counter, bsum_t, st, cmode); break;
   }
 }
 // column blocking of the CSR (block-major copy): per row, the start of each column block (cols sorted)

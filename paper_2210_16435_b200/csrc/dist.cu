@@ -255,6 +255,10 @@ struct DistPart {
   uint8_t* grp = nullptr;
   double *isb = nullptr, *uh = nullptr;
   int spmv_grid = 1, vs = 8;
+  // owner-segment column blocks (P_total > 1): block b = the columns owned by part b (n_max entries of the
+  // gathered vector, L2-sized); rpb[b*(n_loc+1) + i] = start of row i in block b of the block-major CSR
+  int nblk = 1, vs_blk = 2;
+  int* rpb = nullptr;
   double *vr = nullptr, *vy = nullptr, *vt = nullptr;  // v~ (lagged), w, t
   double *V = nullptr, *Vb = nullptr, *X = nullptr;
   double *partials = nullptr, *partials2 = nullptr;
@@ -294,6 +298,8 @@ struct DistCtx {
   double* s_full = nullptr;       // gathered s (normalized), P_total * n_max
   std::vector<DistPart> parts;
   double** ptr_tab = nullptr;     // device table of per-part buffer pointers (virtual reductions)
+  cudaStream_t cst = nullptr;     // NCCL stream: the all-gather overlaps the own-block SpMV
+  cudaEvent_t ev_ready = nullptr, ev_gathered = nullptr;
   // replicated Lanczos state (one copy per process)
   double *H = nullptr, *sv = nullptr, *lz = nullptr, *cs = nullptr, *cg = nullptr, *Ydev = nullptr;
   int ldH = 0;
@@ -330,11 +336,45 @@ static sfairsc_status allgather_full(DistCtx* D, cudaStream_t st, double* full) 
   return SFAIRSC_OK;  // virtual parts share `full`; one rank: nothing to gather
 }
 
+// t = L p~ for every part with the halo exchange: the own column block first, overlapped with the NCCL
+// all-gather of the other parts' segments on the communication stream, then the remote blocks (cmode:
+// 1 first, 2 middle, 3 last incl. the B^T t / p^T t epilogue).  Without blocking (one part): the plain SpMV.
+static sfairsc_status dist_spmv(DistCtx* D, sfairsc_ctx* c, cudaStream_t st) {
+  const bool nccl_multi = D->comm && D->comm->nranks > 1;
+  if (nccl_multi) {  // p~ segment written on st; start the all-gather on cst
+    CU(cudaEventRecord(D->ev_ready, st));
+    CU(cudaStreamWaitEvent(D->cst, D->ev_ready, 0));
+    NC(nccl().AllGather(D->p_full + (size_t)D->comm->rank * D->n_max, D->p_full, D->n_max, ncclDouble,
+                        D->comm->comm, D->cst));
+    CU(cudaEventRecord(D->ev_gathered, D->cst));
+  }
+  for (auto& p : D->parts) {
+    const double* pself = D->p_full + (size_t)p.q * D->n_max;
+    if (p.nblk <= 1) {
+      if (nccl_multi) CU(cudaStreamWaitEvent(st, D->ev_gathered, 0));
+      launch_spmm(p.g(c->normalized), 1, p.vs, p.row_split, p.spmv_grid, D->p_full, p.vt, p.partials,
+                  p.counters + 1, p.bs_t(), st, pself);
+      continue;
+    }
+    for (int idx = 0; idx < p.nblk; ++idx) {
+      const int b = idx == 0 ? p.q : (idx <= p.q ? idx - 1 : idx);  // own block, then the others in order
+      if (idx == 1 && nccl_multi) CU(cudaStreamWaitEvent(st, D->ev_gathered, 0));
+      GraphDev g = p.g(c->normalized);
+      g.rp = p.rpb + (size_t)b * (p.n_loc + 1);
+      const int cmode = idx == 0 ? 1 : (idx + 1 < p.nblk ? 2 : 3);
+      launch_spmv_colblock(g, p.vs_blk, p.row_split, p.spmv_grid, D->p_full, p.vt, p.partials, p.counters + 1,
+                           p.bs_t(), cmode, st, pself);
+    }
+  }
+  CU(cudaGetLastError());
+  return SFAIRSC_OK;
+}
+
 void dist_free(DistCtx* D) {
   if (!D) return;
   for (auto& p : D->parts) {
     void* ptrs[] = {p.rp, p.ci, p.row_split, p.vv, p.dg, p.s, p.grp, p.isb, p.uh, p.vr, p.vy, p.vt, p.V, p.Vb, p.X,
-                    p.partials, p.partials2, p.counters, p.small, p.flags};
+                    p.partials, p.partials2, p.counters, p.small, p.flags, p.rpb};
     for (void* x : ptrs)
       if (x) cudaFree(x);
   }
@@ -343,6 +383,9 @@ void dist_free(DistCtx* D) {
   for (void* x : ptrs)
     if (x) cudaFree(x);
   if (D->hp) cudaFreeHost(D->hp);
+  if (D->cst) cudaStreamDestroy(D->cst);
+  if (D->ev_ready) cudaEventDestroy(D->ev_ready);
+  if (D->ev_gathered) cudaEventDestroy(D->ev_gathered);
   if (D->km) {
     // shadow context: owns nothing but its k-means scratch
     D->km->X = nullptr;
@@ -554,6 +597,52 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
   CU(cudaMemcpyAsync(&hsig, D->parts[0].scal(), sizeof(double), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   c->sigma = opts.sigma_override > 0 ? opts.sigma_override : hsig;
+  // owner-segment column blocking (P_total > 1): block-major copy of each part's CSR
+  if (D->P_total > 1) {
+    for (auto& p : D->parts) {
+      if (p.nnz_loc == 0) continue;
+      const int nb = D->P_total, nl = p.n_loc;
+      int* cnt = nullptr;
+      CU(dal(&cnt, (size_t)nb * nl));
+      launch_colblk_starts(p.rp, p.ci, nl, nb, D->n_max, cnt, st);
+      std::vector<int32_t> hc((size_t)nb * nl), hr((size_t)nb * (nl + 1));
+      CU(cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * hc.size(), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      cudaFree(cnt);
+      long long base = 0;
+      for (int b = 0; b < nb; ++b) {
+        int32_t* r = hr.data() + (size_t)b * (nl + 1);
+        const int32_t* q = hc.data() + (size_t)b * nl;
+        r[0] = (int32_t)base;
+        for (int i = 0; i < nl; ++i) r[i + 1] = r[i] + q[i];
+        base = r[nl];
+      }
+      if (base != p.nnz_loc) return fail(SFAIRSC_E_CUDA, "column blocking lost entries");
+      CU(dal(&p.rpb, hr.size()));
+      CU(cudaMemcpyAsync(p.rpb, hr.data(), sizeof(int32_t) * hr.size(), cudaMemcpyHostToDevice, st));
+      int* ci2 = nullptr;
+      double* vv2 = nullptr;
+      CU(dal(&ci2, p.nnz_loc));
+      CU(dal(&vv2, p.nnz_loc));
+      launch_colblk_scatter(p.rp, p.ci, p.vv, nl, nb, p.rpb, ci2, vv2, st);
+      CU(cudaGetLastError());
+      CU(cudaStreamSynchronize(st));
+      cudaFree(p.ci);
+      cudaFree(p.vv);
+      p.ci = ci2;
+      p.vv = vv2;
+      p.nblk = nb;
+      const double mdb = (double)p.nnz_loc / std::max(1, nl) / nb;
+      int vsb = 2;
+      while (vsb < 32 && vsb * 4 < mdb) vsb *= 2;
+      p.vs_blk = vsb;
+    }
+    if (D->comm) {
+      CU(cudaStreamCreateWithFlags(&D->cst, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&D->ev_ready, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&D->ev_gathered, cudaEventDisableTiming));
+    }
+  }
   // A3: factored projector; group counts and beta_s = sum_{V_s} s_i^2 summed over parts
   std::vector<double> beta(hh), cntg(hh);
   {
@@ -653,12 +742,9 @@ struct DistLanczos {
   }
 
   sfairsc_status step(int j) {
-    TRY(allgather_full(D, st(), D->p_full));
     {
       ProfScope ps(c, K_SPMV, 0.0);
-      for (auto& p : D->parts)
-        launch_spmm(p.g(c->normalized), 1, p.vs, p.row_split, p.spmv_grid, D->p_full, p.vt, p.partials,
-                    p.counters + 1, p.bs_t(), st(), pseg(p));
+      TRY(dist_spmv(D, c, st()));  // all-gather of p~ overlapped with the own-block SpMV
       TRY(allreduce(D, st(), kBT, [](const DistPart& p) { return p.bs_t(); }));
     }
     launch_lz_coef(dev(D->parts[0], j), j, st());
@@ -790,10 +876,7 @@ struct DistLanczos {
       TRY(allreduce(D, st(), kHB, [](const DistPart& p) { return p.bs_w(); }));
       for (auto& p : D->parts)
         launch_project(p.g(c->normalized), pd(p), p.X + (long long)i * p.ldv, p.bs_w(), 1.0, pseg(p), st());
-      TRY(allgather_full(D, st(), D->p_full));
-      for (auto& p : D->parts)
-        launch_spmm(p.g(c->normalized), 1, p.vs, p.row_split, p.spmv_grid, D->p_full, p.vt, p.partials,
-                    p.counters + 1, p.bs_t(), st(), pseg(p));
+      TRY(dist_spmv(D, c, st()));
       TRY(allreduce(D, st(), kBT, [](const DistPart& p) { return p.bs_t(); }));
       for (auto& p : D->parts) {
         launch_finish(p.g(c->normalized), pd(p), p.vt, p.bs_t(), p.bs_w(), c->sigma, p.vy, st());
@@ -989,10 +1072,7 @@ sfairsc_status dist_apply(sfairsc_ctx* c, const double* x, double* y) {
   }
   TRY(allreduce(D, st, kHB, [](const DistPart& p) { return p.bs_w(); }));
   for (auto& p : D->parts) launch_project(p.g(c->normalized), L.pd(p), p.vr, p.bs_w(), 1.0, L.pseg(p), st);
-  TRY(allgather_full(D, st, D->p_full));
-  for (auto& p : D->parts)
-    launch_spmm(p.g(c->normalized), 1, p.vs, p.row_split, p.spmv_grid, D->p_full, p.vt, p.partials, p.counters + 1,
-                p.bs_t(), st, L.pseg(p));
+  TRY(dist_spmv(D, c, st));
   TRY(allreduce(D, st, kBT, [](const DistPart& p) { return p.bs_t(); }));
   off = 0;
   for (auto& p : D->parts) {

@@ -155,7 +155,8 @@ void launch_spmm(const GraphDev& g, int nb, int vs, const int* split, int grid, 
 int bsweep_grid(int n);
 // column-blocked single-vector SpMV (cmode 1 first, 2 middle, 3 last block; g.rp = the block's row offsets)
 void launch_spmv_colblock(const GraphDev& g, int vs, const int* split, int grid, const double* p, double* t,
-                          double* partials, unsigned* counter, double* bsum_t, int cmode, cudaStream_t st);
+                          double* partials, unsigned* counter, double* bsum_t, int cmode, cudaStream_t st,
+                          const double* p_self = nullptr);
 void launch_colblk_starts(const int* rp, const int* ci, int n, int nblk, int cb, int* cnt, cudaStream_t st);
 void launch_colblk_scatter(const int* rp, const int* ci, const double* vv, int n, int nblk, const int* rpb, int* ci2,
                            double* vv2, cudaStream_t st);
