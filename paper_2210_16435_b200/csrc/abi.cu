@@ -98,7 +98,8 @@ static void free_ctx(sfairsc_ctx* c) {
   void* ptrs[] = {c->rp, c->ci, c->row_split, c->vv, c->dg, c->s, c->grp, c->isb, c->uh, c->partials, c->counters,
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
                   c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta,
-                  c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags, c->Hdev, c->sdev, c->lz, c->partials2, c->dd, c->rpb};
+                  c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags, c->Hdev, c->sdev, c->lz, c->partials2, c->dd, c->rpb,
+                  c->pairP, c->pairT};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hp) cudaFreeHost(c->hp);
@@ -181,6 +182,32 @@ sfairsc_status sfz::apply_dev(sfairsc_ctx* c, const double* x, double* y) {
 }
 
 
+// y0, y1 = L^sigma x0, x1 through one SpMM of the interleaved pair (h <= 16, plain CSR); the pair
+// buffers are allocated on first use (2 interleaved n x 2 blocks)
+sfairsc_status sfz::apply_pair_dev(sfairsc_ctx* c, const double* x0, const double* x1, double* y0, double* y1) {
+  if (!c->pairP) {
+    CU(cudaMalloc(&c->pairP, sizeof(double) * 2 * c->ldv));
+    CU(cudaMalloc(&c->pairT, sizeof(double) * 2 * c->ldv));
+  }
+  {
+    ProfScope ps(c, K_PROJ, 2 * (2 * c->vb() + c->sgb()) + 2 * c->vb());
+    launch_pair_gsum(c->g(), x0, x1, c->partials, c->counters + 3, c->bs_w, c->st);
+    launch_pair_project(c->g(), c->pd(), x0, x1, c->bs_w, c->pairP, c->st);
+  }
+  {
+    ProfScope ps(c, K_SPMV, c->csr_bytes() + 4 * c->vb() + c->vb() + 1.0 * c->n);
+    launch_spmm(c->g(), 2, c->vs, c->row_split, c->spmv_grid, c->pairP, c->pairT, c->partials, c->counters + 1,
+                c->bs_t, c->st);
+  }
+  {
+    ProfScope ps(c, K_FINISH, 4 * c->vb() + c->sgb());
+    launch_pair_finish(c->g(), c->pd(), c->pairT, c->bs_t, c->bs_w, c->sigma, y0, y1, c->st);
+  }
+  CHECK_LAUNCH();
+  return SFAIRSC_OK;
+}
+static bool pair_ok(const sfairsc_ctx* c) { return c->h <= kHB && c->nblk <= 1 && !c->dist; }
+
 void sfz::ctx_spmv(sfairsc_ctx* c, const double* p, double* t) {
   if (c->nblk <= 1) {
     launch_spmm(c->g(), 1, c->vs, c->row_split, c->spmv_grid, p, t, c->partials, c->counters + 1, c->bs_t, c->st);
@@ -198,11 +225,21 @@ void sfz::ctx_spmv(sfairsc_ctx* c, const double* p, double* t) {
 // max_i ||L^sigma x_i - theta_i x_i|| / sigma over the k columns of X (A11), k fresh applies
 sfairsc_status sfz::true_residuals(sfairsc_ctx* c, const double* theta, int k, double* max_out) {
   std::vector<double> res(k);
+  if (pair_ok(c) && !c->pairY) CU(cudaMalloc(&c->pairY, sizeof(double) * c->ldv));
   for (int i = 0; i < k; ++i) {
     const double* xi = c->X + (long long)i * c->ldv;
-    TRY(apply_dev(c, xi, c->vy));
-    launch_resid(c->vy, xi, theta[i], c->n, c->partials, c->counters + 4, c->scal + 8 + i % 64, c->st);
-    CHECK_LAUNCH();
+    if (pair_ok(c) && i + 1 < k && i % 64 != 63) {  // two residuals per SpMM (the pair stays in one 64-batch)
+      const double* xj = xi + c->ldv;
+      TRY(apply_pair_dev(c, xi, xj, c->vy, c->pairY));
+      launch_resid(c->vy, xi, theta[i], c->n, c->partials, c->counters + 4, c->scal + 8 + i % 64, c->st);
+      launch_resid(c->pairY, xj, theta[i + 1], c->n, c->partials, c->counters + 4, c->scal + 8 + (i + 1) % 64, c->st);
+      CHECK_LAUNCH();
+      ++i;
+    } else {
+      TRY(apply_dev(c, xi, c->vy));
+      launch_resid(c->vy, xi, theta[i], c->n, c->partials, c->counters + 4, c->scal + 8 + i % 64, c->st);
+      CHECK_LAUNCH();
+    }
     if (i % 64 == 63 || i == k - 1) {
       const int base = i - i % 64;
       CU(cudaMemcpyAsync(c->hp, c->scal + 8, sizeof(double) * (i - base + 1), cudaMemcpyDeviceToHost, c->st));
@@ -651,7 +688,13 @@ static sfairsc_status vec_io(sfairsc_ctx* c, const double* x, double* y, int32_t
     return rs;
   }
   const size_t nb = sizeof(double) * c->n;
-  for (int v = 0; v < nvec; ++v) {
+  int v0 = 0;
+  if (op == apply_dev && pair_ok(c) && nvec >= 2 && memspace == SFAIRSC_MEM_DEVICE) {
+    for (; v0 + 1 < nvec; v0 += 2)
+      TRY(apply_pair_dev(c, x + (size_t)v0 * c->n, x + (size_t)(v0 + 1) * c->n, y + (size_t)v0 * c->n,
+                         y + (size_t)(v0 + 1) * c->n));
+  }
+  for (int v = v0; v < nvec; ++v) {
     const double* xv = x + (size_t)v * c->n;
     double* yv = y + (size_t)v * c->n;
     if (memspace == SFAIRSC_MEM_HOST) {

@@ -548,6 +548,76 @@ __global__ void __launch_bounds__(kThreads) k_bproject(GraphDev g, ProjDesc pd, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pair apply: L^sigma on two separate vectors through ONE SpMM of the
+// interleaved pair (the SpMV is bound by random L2 requests, a 16-byte pair
+// gather costs about one 8-byte gather).  Packing and unpacking are fused into
+// the projection and finish passes, so no extra vector pass is added.
+// ---------------------------------------------------------------------------
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) k_pair_gsum(GraphDev g, const double* __restrict__ x0,
+                                                        const double* __restrict__ x1, double* partials,
+                                                        unsigned* counter, double* out) {
+  const int n = g.n;
+  const int i0 = (int)((long long)n * blockIdx.x / gridDim.x), i1 = (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
+  double a0[kHB], a1[kHB];
+#pragma unroll
+  for (int q = 0; q < kHB; ++q) a0[q] = a1[q] = 0.0;
+  for (int i = i0 + threadIdx.x; i < i1; i += kThreads) {
+    const double si = NORM ? g.s[i] : 1.0;
+    const int gg = g.grp[i];
+    const double v0 = si * x0[i], v1 = si * x1[i];
+#pragma unroll
+    for (int q = 0; q < kHB; ++q)
+      if (q == gg) {
+        a0[q] += v0;
+        a1[q] += v1;
+      }
+  }
+  block_reduce_store<kHB>(a0, partials + ((size_t)blockIdx.x * 2 + 0) * kHB);
+  __syncthreads();
+  block_reduce_store<kHB>(a1, partials + ((size_t)blockIdx.x * 2 + 1) * kHB);
+  ticket_finalize<2 * kHB>(partials, counter, out, 2 * kHB);
+}
+// p[i] = (P x0, P x1)_i interleaved
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) k_pair_project(GraphDev g, ProjDesc pd, const double* __restrict__ x0,
+                                                           const double* __restrict__ x1, const double* bsum,
+                                                           double* __restrict__ p) {
+  __shared__ double gam[2][kHB];
+  if (threadIdx.x < 2) gamma_serial(bsum + threadIdx.x * kHB, 1.0, pd, gam[threadIdx.x]);
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const int gi = g.grp[i];
+    const double si = NORM ? g.s[i] : 1.0;
+    double2 v;
+    v.x = fma(-si, gam[0][gi], x0[i]);
+    v.y = fma(-si, gam[1][gi], x1[i]);
+    reinterpret_cast<double2*>(p)[i] = v;
+  }
+}
+// y_c = t_c - s o (gam(B^T t_c) - sigma gam(B^T x_c))_g, unpacked to two vectors
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) k_pair_finish(GraphDev g, ProjDesc pd, const double* __restrict__ t,
+                                                          const double* bsum_t, const double* bsum_x, double sigma,
+                                                          double* __restrict__ y0, double* __restrict__ y1) {
+  __shared__ double gam[2][kHB];
+  if (threadIdx.x < 2) {
+    double gw[kHB];
+    gamma_serial(bsum_t + threadIdx.x * kBT, 1.0, pd, gam[threadIdx.x]);
+    gamma_serial(bsum_x + threadIdx.x * kHB, 1.0, pd, gw);
+    for (int s = 0; s < pd.h; ++s) gam[threadIdx.x][s] -= sigma * gw[s];
+  }
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const int gi = g.grp[i];
+    const double si = NORM ? g.s[i] : 1.0;
+    const double2 v = reinterpret_cast<const double2*>(t)[i];
+    y0[i] = fma(-si, gam[0][gi], v.x);
+    y1[i] = fma(-si, gam[1][gi], v.y);
+  }
+}
+
 // x[i*NB + c] = u - 1/2, u = Philox4x32-10(key = seed, ctr = (i, c1 + c, stream, 0))
 __global__ void k_brandom(double* x, int n, int nb, uint64_t seed, unsigned c1, unsigned stream) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -773,6 +843,25 @@ void launch_bproject(int nb, const GraphDev& g, const ProjDesc& pd, const double
     default: BP(4) break;
   }
 #undef BP
+}
+void launch_pair_gsum(const GraphDev& g, const double* x0, const double* x1, double* partials, unsigned* counter,
+                      double* out, cudaStream_t st) {
+  bump_launch();
+  const int G = std::max(1, std::min((g.n + kThreads - 1) / kThreads, n_sms() * 4));
+  if (g.normalized) k_pair_gsum<true><<<G, kThreads, 0, st>>>(g, x0, x1, partials, counter, out);
+  else k_pair_gsum<false><<<G, kThreads, 0, st>>>(g, x0, x1, partials, counter, out);
+}
+void launch_pair_project(const GraphDev& g, const ProjDesc& pd, const double* x0, const double* x1,
+                         const double* bsum, double* p, cudaStream_t st) {
+  bump_launch();
+  if (g.normalized) k_pair_project<true><<<sgrid(g.n), kThreads, 0, st>>>(g, pd, x0, x1, bsum, p);
+  else k_pair_project<false><<<sgrid(g.n), kThreads, 0, st>>>(g, pd, x0, x1, bsum, p);
+}
+void launch_pair_finish(const GraphDev& g, const ProjDesc& pd, const double* t, const double* bsum_t,
+                        const double* bsum_x, double sigma, double* y0, double* y1, cudaStream_t st) {
+  bump_launch();
+  if (g.normalized) k_pair_finish<true><<<sgrid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_x, sigma, y0, y1);
+  else k_pair_finish<false><<<sgrid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_x, sigma, y0, y1);
 }
 void launch_brandom(double* x, int n, int nb, uint64_t seed, unsigned c1, unsigned stream, cudaStream_t st) {
   bump_launch();

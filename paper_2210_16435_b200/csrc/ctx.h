@@ -109,6 +109,7 @@ struct sfairsc_ctx {
   // rpb[b*(n+1) + i] = start of row i in column block b; nblk = 1: plain CSR
   int nblk = 1, vs_blk = 2;
   int* rpb = nullptr;
+  double *pairP = nullptr, *pairT = nullptr, *pairY = nullptr;  // pair apply (lazily allocated)
   // row-partitioned contexts: all device state lives in dist
   sfz::DistCtx* dist = nullptr;
   // results
@@ -152,6 +153,7 @@ sfairsc_status apply_dev(sfairsc_ctx* c, const double* x, double* y);  // y = L^
 sfairsc_status true_residuals(sfairsc_ctx* c, const double* theta, int k, double* max_out);  // over X
 // t = L p (+ B^T t, p^T t into bs_t) through the plain or the column-blocked CSR
 void ctx_spmv(sfairsc_ctx* c, const double* p, double* t);
+sfairsc_status apply_pair_dev(sfairsc_ctx* c, const double* x0, const double* x1, double* y0, double* y1);
 double now_s();
 }
 

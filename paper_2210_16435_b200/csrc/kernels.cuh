@@ -171,6 +171,14 @@ void launch_bgsum(int nb, const GraphDev& g, const double* x, double* partials, 
 void launch_bproject(int nb, const GraphDev& g, const ProjDesc& pd, const double* x, const double* bsum, double* y,
                      cudaStream_t st);
 void launch_brandom(double* x, int n, int nb, uint64_t seed, unsigned c1, unsigned stream, cudaStream_t st);
+// pair apply (two vectors through one b = 2 SpMM): out[c*kHB + s] = B^T x_c; p = (P x0, P x1) interleaved;
+// y_c = t_c - s o (gam(B^T t_c) - sigma gam(B^T x_c))_g unpacked
+void launch_pair_gsum(const GraphDev& g, const double* x0, const double* x1, double* partials, unsigned* counter,
+                      double* out, cudaStream_t st);
+void launch_pair_project(const GraphDev& g, const ProjDesc& pd, const double* x0, const double* x1,
+                         const double* bsum, double* p, cudaStream_t st);
+void launch_pair_finish(const GraphDev& g, const ProjDesc& pd, const double* t, const double* bsum_t,
+                        const double* bsum_x, double sigma, double* y0, double* y1, cudaStream_t st);
 
 // ---- k-means ----------------------------------------------------------------------
 void launch_build_rows(const double* X, long long ldx, int n, int k, const double* s, double* H, cudaStream_t st);

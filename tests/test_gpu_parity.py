@@ -395,3 +395,20 @@ def test_exp1_fair_recovers_planted_sc_fails(gpu_lib, h):
     assert err_fair <= 0.05, err_fair
     assert err_sc >= 0.3, err_sc
     assert abs(err_fair - err_or) <= 2.0 / n * 5  # a handful of borderline vertices at most
+
+
+def test_pair_apply_matches_single(gpu_lib):
+    """sfairsc_apply on several device vectors runs them in pairs through one SpMM of the
+    interleaved pair: equal to the oracle and to the one-vector path (odd count: last alone)."""
+    import torch
+    g = random_graph(1500, 4, p=0.01, seed=31, weights="uniform")
+    for normalized in (False, True):
+        op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, normalized)
+        ctx = _ctx(gpu_lib, g, 3, normalized)
+        x = torch.from_numpy(np.random.default_rng(3).standard_normal((5, g.n))).cuda()
+        y = gpu_lib.sfairsc_apply(ctx, x).cpu().numpy()
+        ref = np.stack([op.apply(v) for v in x.cpu().numpy()])
+        assert np.abs(y - ref).max() <= 1e-13 * op.sigma * float(x.abs().max())
+        y1 = np.stack([gpu_lib.sfairsc_apply(ctx, np.ascontiguousarray(v)) for v in x.cpu().numpy()])
+        assert np.abs(y - y1).max() <= 1e-13 * op.sigma * float(x.abs().max())
+        ctx.close()
