@@ -412,3 +412,24 @@ def test_pair_apply_matches_single(gpu_lib):
         y1 = np.stack([gpu_lib.sfairsc_apply(ctx, np.ascontiguousarray(v)) for v in x.cpu().numpy()])
         assert np.abs(y - y1).max() <= 1e-13 * op.sigma * float(x.abs().max())
         ctx.close()
+
+
+def test_kmeans_config2_vs_oracle(gpu_lib, config2_ref):
+    """Config 2 (normalized, n = 20,000, h = 5, k = 10): fair clustering of the GPU
+    (eigs + embed_kmeans) against the oracle's k-means on the Tier-S embedding
+    H = D^{-1/2} X (ARI >= 0.99, per-cluster balance within 1e-3; north star)."""
+    from oracle.kmeans import kmeans
+    from oracle.metrics import ari, balance, hungarian_match
+    g, cfg, ref = config2_ref
+    k = cfg["k_eig"]
+    d = np.diff(g.row_ptr).astype(float)
+    d = np.asarray(g.to_scipy().sum(axis=1)).ravel()
+    H_or = ref.X / np.sqrt(d)[:, None]
+    ctx = _ctx(gpu_lib, g, k, True)
+    gpu_lib.sfairsc_eigs(ctx, k, cfg["tol"])
+    lab, _ = gpu_lib.sfairsc_embed_kmeans(ctx, 2024)
+    ctx.close()
+    r = kmeans(H_or, k, 2024)
+    assert ari(r.labels, lab) >= 0.99
+    perm = hungarian_match(r.labels, lab, k)
+    assert np.abs(balance(r.labels, g.groups, k, g.h) - balance(perm[lab], g.groups, k, g.h)).max() <= 1e-3
