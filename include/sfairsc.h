@@ -145,6 +145,16 @@ sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr *W, const int32_t *gr
                                          int32_t k, int32_t normalized, const sfairsc_opts *opts,
                                          sfairsc_ctx **out);
 
+/* §8(f) N4 — general linear constraints C^T H = 0 with a dense constraint matrix F (n x r,
+ * column-major, 0 <= r <= 16; e.g. the random-F Laplacian of Experiment 4, or
+ * overlapping groups; P:465-490 take F as input): C = D^{-1/2} F (normalized) or F,
+ * Q = orth(C) by CholQR2 on the device (SFAIRSC_E_RANK_DEFICIENT if rank C < r), and every
+ * projector step applies P = I - Q Q^T with the dense rows of Q (Q^T x fused into the SpMV
+ * epilogue and the basis sweep, x - Q (Q^T x) into the normalisation).  F in W's memspace.
+ * Single GPU, single-sweep solver.  sfairsc_eigs / sfairsc_apply / embed_kmeans as usual. */
+sfairsc_status sfairsc_build_operator_dense(const sfairsc_csr *W, const double *F, int32_t r, int32_t k,
+                                            int32_t normalized, const sfairsc_opts *opts, sfairsc_ctx **out);
+
 /* Alg. 3 step 3: the k smallest eigenpairs of L^sigma by
  * thick-restart Lanczos with full CGS2 reorthogonalisation (replaces
  * MATLAB eigs / ARPACK).  Stops when every wanted Ritz pair has

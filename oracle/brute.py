@@ -15,8 +15,9 @@ import mpmath as mp
 import numpy as np
 
 
-def brute_fair_eig(W, groups, h, normalized, dps=50):
-    """Return (evals ascending as mpf list, X as mp.matrix n x (n-h+1))."""
+def brute_fair_eig(W, groups, h, normalized, dps=50, F=None):
+    """Return (evals ascending as mpf list, X as mp.matrix n x (n-r)), r = h-1 for
+    group fairness, or the columns of an explicit constraint matrix F (n x r)."""
     mp.mp.dps = dps
     W = [[mp.mpf(float(x)) for x in row] for row in np.asarray(W)]
     n = len(W)
@@ -30,17 +31,23 @@ def brute_fair_eig(W, groups, h, normalized, dps=50):
     for i in range(n):
         for j in range(n):
             Ln[i, j] = s[i] * L[i, j] * s[j]
-    counts = [sum(1 for g in groups if g == t) for t in range(h)]
-    if h > 1:
-        C = mp.matrix(n, h - 1)
+    if F is not None:
+        Fa = np.asarray(F, dtype=np.float64).reshape(n, -1)
+        r = Fa.shape[1]
+    else:
+        counts = [sum(1 for g in groups if g == t) for t in range(h)]
+        r = h - 1
+    if r > 0:
+        C = mp.matrix(n, r)
         for i in range(n):
-            for t in range(h - 1):
-                C[i, t] = s[i] * ((1 if groups[i] == t else 0) - mp.mpf(counts[t]) / n)
+            for t in range(r):
+                f = mp.mpf(float(Fa[i, t])) if F is not None else (1 if groups[i] == t else 0) - mp.mpf(counts[t]) / n
+                C[i, t] = s[i] * f
         Qf, _ = mp.qr(C, mode="full")
-        V = mp.matrix(n, n - h + 1)
+        V = mp.matrix(n, n - r)
         for i in range(n):
-            for j in range(n - h + 1):
-                V[i, j] = Qf[i, j + h - 1]
+            for j in range(n - r):
+                V[i, j] = Qf[i, j + r]
     else:
         V = mp.eye(n)
     Lv = V.T * Ln * V

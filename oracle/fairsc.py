@@ -88,8 +88,23 @@ def sigma_norm1(L: np.ndarray) -> float:
 
 def fairsc_dense(W: np.ndarray, groups: np.ndarray, h: int, k: int, normalized: bool,
                  extra: int = 1) -> FairSCResult:
-    """Algorithm 2 (FairSC).  Returns the k smallest eigenpairs of
-    the fair-SC problem plus `extra` further eigenvalues.
+    """Algorithm 2 with the group-fairness F of Lemma 2.1."""
+    validate(W, groups, h)
+    return fairsc_dense_F(W, fairness_matrix(groups, h), k, normalized, extra)
+
+
+def validate_W(W: np.ndarray) -> None:
+    """w_ij >= 0, w_ii = 0, W symmetric, no isolated vertex (D > 0)."""
+    if W.shape[0] != W.shape[1]:
+        raise OracleInputError("dimension mismatch")
+    if np.any(W < 0) or np.any(np.diag(W) != 0) or not np.array_equal(W, W.T) or np.any(W.sum(axis=1) <= 0):
+        raise OracleInputError("W is not a valid weighted adjacency matrix")
+
+
+def fairsc_dense_F(W: np.ndarray, F: np.ndarray, k: int, normalized: bool, extra: int = 1) -> FairSCResult:
+    """Algorithm 2 (FairSC), P:465-490, for a given constraint matrix F (n x r;
+    the paper's algorithm takes F as its input).  Returns the k smallest
+    eigenpairs of the fair-SC problem plus `extra` further eigenvalues.
 
     normalized (Alg. 2 as printed):
       1. L = D - W;  2. Z = null(F^T);  3. Q = (Z^T D Z)^{1/2};
@@ -97,11 +112,10 @@ def fairsc_dense(W: np.ndarray, groups: np.ndarray, h: int, k: int, normalized: 
       6. H = Z Q^{-1} X_M.   Comparison frame X = D^{1/2} H (R9).
     unnormalized (R1, D -> I): eigenpairs of Z^T L Z, X = H = Z Y.
     """
-    validate(W, groups, h)
+    validate_W(W)
     n = W.shape[0]
     L, d = laplacian(W)  # step 1
-    F = fairness_matrix(groups, h)
-    Z = nullspace_basis(F)  # step 2
+    Z = nullspace_basis(np.asarray(F, dtype=np.float64).reshape(n, -1))  # step 2: Z = null(F^T)
     A = Z.T @ L @ Z
     A = 0.5 * (A + A.T)
     kk = min(k + extra, Z.shape[1])
@@ -184,3 +198,27 @@ def apply_deflated(W, groups, h, normalized, w, sigma=None) -> np.ndarray:
     P = projector(constraint_matrix(W, groups, h, normalized))
     Pw = P @ w
     return P @ (Ln @ Pw) - sigma * Pw + sigma * w
+
+
+def constraint_matrix_F(W: np.ndarray, F: np.ndarray, normalized: bool) -> np.ndarray:
+    """C = D^{-1/2} F or C = F (R1) for an explicit F."""
+    if normalized:
+        return F / np.sqrt(W.sum(axis=1))[:, None]
+    return np.asarray(F, dtype=np.float64)
+
+
+def variant_evals_F(W, F, normalized) -> np.ndarray:
+    """§3.2 variant with an explicit F: eigenvalues of V^T L_n V, V = null(C^T)."""
+    V = nullspace_basis(constraint_matrix_F(W, F, normalized))
+    A = V.T @ operator_laplacian(W, normalized) @ V
+    return np.linalg.eigvalsh(0.5 * (A + A.T))
+
+
+def deflated_operator_F(W, F, normalized, sigma=None) -> tuple[np.ndarray, float]:
+    """L^sigma = P L_n P + sigma (I - P) (Eq. asigma) with P from an explicit F."""
+    Ln = operator_laplacian(W, normalized)
+    if sigma is None:
+        sigma = sigma_norm1(Ln)
+    P = projector(constraint_matrix_F(W, F, normalized))
+    A = P @ Ln @ P + sigma * (np.eye(W.shape[0]) - P)
+    return 0.5 * (A + A.T), float(sigma)

@@ -49,7 +49,7 @@ class SparseOperator:
 
 
 def build_operator(W: sp.csr_matrix, groups: np.ndarray, h: int, normalized: bool,
-                   sigma: float | None = None) -> SparseOperator:
+                   sigma: float | None = None, F: np.ndarray | None = None) -> SparseOperator:
     """Alg. 3 steps 1-2: L = D - W; L_n = D^{-1/2} L D^{-1/2}; C = D^{-1/2} F."""
     W = sp.csr_matrix(W)
     n = W.shape[0]
@@ -63,13 +63,16 @@ def build_operator(W: sp.csr_matrix, groups: np.ndarray, h: int, normalized: boo
         Ln = L
     Ln = sp.csr_matrix(Ln)
     # F = F_0(:, 1:h-1), F_0 = G - 1 z^T, z = G^T 1/n
-    counts = np.bincount(groups, minlength=h).astype(np.float64)
-    z = counts / n
-    F = np.zeros((n, max(h - 1, 0)))
-    for col in range(h - 1):
-        F[:, col] = (groups == col).astype(np.float64) - z[col]
+    if F is None:  # group fairness: F = F_0(:, 1:h-1)
+        counts = np.bincount(groups, minlength=h).astype(np.float64)
+        z = counts / n
+        F = np.zeros((n, max(h - 1, 0)))
+        for col in range(h - 1):
+            F[:, col] = (groups == col).astype(np.float64) - z[col]
+    else:  # an explicit constraint matrix (Exp. 4's random F)
+        F = np.asarray(F, dtype=np.float64).reshape(n, -1)
     C = s[:, None] * F
-    cho = sla.cho_factor(C.T @ C) if h > 1 else None
+    cho = sla.cho_factor(C.T @ C) if C.shape[1] > 0 else None
     if sigma is None:
         sigma = float(abs(Ln).sum(axis=0).max())  # ||L_n||_1, max column sum
     return SparseOperator(n, Ln, C, cho, float(sigma), d, normalized)

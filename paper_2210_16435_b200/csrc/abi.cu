@@ -99,7 +99,7 @@ static void free_ctx(sfairsc_ctx* c) {
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
                   c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta,
                   c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags, c->Hdev, c->sdev, c->lz, c->partials2, c->dd, c->rpb,
-                  c->pairP, c->pairT};
+                  c->pairP, c->pairT, c->pairY, c->Qr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hp) cudaFreeHost(c->hp);
@@ -206,7 +206,7 @@ sfairsc_status sfz::apply_pair_dev(sfairsc_ctx* c, const double* x0, const doubl
   CHECK_LAUNCH();
   return SFAIRSC_OK;
 }
-static bool pair_ok(const sfairsc_ctx* c) { return c->h <= kHB && c->nblk <= 1 && !c->dist; }
+static bool pair_ok(const sfairsc_ctx* c) { return c->h <= kHB && c->nblk <= 1 && !c->dist && !c->Qr; }
 
 void sfz::ctx_spmv(sfairsc_ctx* c, const double* p, double* t) {
   if (c->nblk <= 1) {
@@ -652,6 +652,127 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   c->t_build = now_s() - t0;
   *out = c;
 #undef CUB
+  return SFAIRSC_OK;
+}
+
+// §8(f) N4: general constraints C^T H = 0 with a dense F (n x r).  Builds the operator with the group
+// machinery switched off (h = 1: P = I), then forms Q = orth(C), C = D^{-1/2} F (normalized) or F, by
+// CholQR2 and switches every projector kernel to the dense rows of Q.
+extern "C" sfairsc_status sfairsc_build_operator_dense(const sfairsc_csr* W, const double* F, int32_t r, int32_t k,
+                                                       int32_t normalized, const sfairsc_opts* opts_in,
+                                                       sfairsc_ctx** out) {
+  if (!W || !out || (r > 0 && !F)) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
+  if (r < 0 || r > kHB) return fail(SFAIRSC_E_INVALID_ARG, "r must be in [0, %d]", kHB);
+  *out = nullptr;
+  sfairsc_opts opts;
+  sfairsc_default_opts(&opts);
+  if (opts_in) opts = *opts_in;
+  if (opts.comm || opts.virtual_parts > 1) return fail(SFAIRSC_E_INVALID_ARG, "dense constraints: single GPU only");
+  if (opts.block_size > 1 || opts.reorth == 1)
+    return fail(SFAIRSC_E_INVALID_ARG, "dense constraints use the single-sweep solver (block_size 0/1, reorth 0/2)");
+  const long long n = W->n_rows;
+  if (n < 2 || (long long)k > n - r) return fail(SFAIRSC_E_K_TOO_LARGE, "k=%d > n - r = %lld", k, n - r);
+  opts.block_size = 1;
+  opts.reorth = 2;
+  if (opts.max_basis <= 0) {
+    int m = std::min(192, std::max(std::max(2 * k + 10, 17 * k / 5), 20));
+    opts.max_basis = (int)std::min<long long>(m, n - r - 1);
+  }
+  std::vector<int32_t> zeros((size_t)n, 0);
+  int32_t* gz = zeros.data();
+  int32_t* gzd = nullptr;
+  if (W->memspace == SFAIRSC_MEM_DEVICE) {
+    CU(cudaMalloc(&gzd, sizeof(int32_t) * n));
+    CU(cudaMemset(gzd, 0, sizeof(int32_t) * n));
+    gz = gzd;
+  }
+  sfairsc_ctx* c = nullptr;
+  sfairsc_status st0 = sfairsc_build_operator_ex(W, gz, 1, k, normalized, &opts, &c);
+  if (gzd) cudaFree(gzd);
+  if (st0 != SFAIRSC_OK) return st0;
+  if (r == 0) {
+    *out = c;
+    return SFAIRSC_OK;
+  }
+  auto bail = [&](sfairsc_status s) {
+    sfairsc_destroy(c);
+    return s;
+  };
+  const int ni = (int)n;
+  c->qr = r;
+  c->ldq = (r + 1) / 2 * 2;  // 16-byte rows for the TMA bulk copies
+  double *Cd = nullptr, *Q1 = nullptr, *G = nullptr, *Ud = nullptr;
+  auto cleanup = [&]() {
+    if (Cd) cudaFree(Cd);
+    if (Q1) cudaFree(Q1);
+    if (G) cudaFree(G);
+    if (Ud) cudaFree(Ud);
+  };
+#define CUD(expr)                                                                                       \
+  do {                                                                                                  \
+    cudaError_t e_ = (expr);                                                                            \
+    if (e_ != cudaSuccess) {                                                                            \
+      cleanup();                                                                                        \
+      return bail(fail(e_ == cudaErrorMemoryAllocation ? SFAIRSC_E_OOM : SFAIRSC_E_CUDA, "%s: %s", #expr, \
+                       cudaGetErrorString(e_)));                                                        \
+    }                                                                                                   \
+  } while (0)
+  CUD(cudaMalloc(&Cd, sizeof(double) * (size_t)n * r));
+  CUD(cudaMemcpyAsync(Cd, F, sizeof(double) * (size_t)n * r,
+                      W->memspace == SFAIRSC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+  if (c->normalized) launch_scale_rows(Cd, n, ni, r, c->s, c->st);  // C = D^{-1/2} F
+  CUD(cudaMalloc(&Q1, sizeof(double) * (size_t)c->ldv * c->ldq));
+  CUD(cudaMemsetAsync(Q1, 0, sizeof(double) * (size_t)c->ldv * c->ldq, c->st));
+  CUD(cudaMalloc(&c->Qr, sizeof(double) * (size_t)c->ldv * c->ldq));
+  CUD(cudaMemsetAsync(c->Qr, 0, sizeof(double) * (size_t)c->ldv * c->ldq, c->st));
+  CUD(cudaMalloc(&G, sizeof(double) * r * r));
+  CUD(cudaMalloc(&Ud, sizeof(double) * r * r));
+  std::vector<double> Gh(r * r), U(r * r), Ui(r * r);
+  double maxdiag0 = 0.0;
+  for (int pass = 0; pass < 2; ++pass) {  // CholQR2: C -> Q1 -> Q
+    const double* Min = pass == 0 ? Cd : Q1;
+    const long long rs = pass == 0 ? 1 : c->ldq, cs = pass == 0 ? n : 1;
+    CUD(cudaMemsetAsync(G, 0, sizeof(double) * r * r, c->st));
+    launch_gram_pairs(Min, rs, cs, ni, r, G, c->st);
+    CUD(cudaMemcpyAsync(Gh.data(), G, sizeof(double) * r * r, cudaMemcpyDeviceToHost, c->st));
+    CUD(cudaStreamSynchronize(c->st));
+    for (int a = 0; a < r; ++a)
+      for (int b = 0; b < a; ++b) Gh[a * r + b] = Gh[b * r + a];
+    if (pass == 0)
+      for (int a = 0; a < r; ++a) maxdiag0 = std::max(maxdiag0, Gh[a * r + a]);
+    // Cholesky G = U^T U (U upper); rank check on the first pass (Lemma 2.1(i) for group F)
+    std::fill(U.begin(), U.end(), 0.0);
+    for (int j = 0; j < r; ++j) {
+      double d = Gh[j * r + j];
+      for (int q = 0; q < j; ++q) d -= U[q * r + j] * U[q * r + j];
+      if (!(d > (pass == 0 ? 1e-24 * maxdiag0 : 0.25))) {
+        cleanup();
+        return bail(fail(SFAIRSC_E_RANK_DEFICIENT, "constraint matrix C has (numerical) rank < r = %d", r));
+      }
+      U[j * r + j] = std::sqrt(d);
+      for (int i = j + 1; i < r; ++i) {
+        double v = Gh[j * r + i];
+        for (int q = 0; q < j; ++q) v -= U[q * r + j] * U[q * r + i];
+        U[j * r + i] = v / U[j * r + j];
+      }
+    }
+    std::fill(Ui.begin(), Ui.end(), 0.0);
+    for (int j = 0; j < r; ++j) {
+      Ui[j * r + j] = 1.0 / U[j * r + j];
+      for (int i = j - 1; i >= 0; --i) {
+        double v = 0.0;
+        for (int q = i + 1; q <= j; ++q) v += U[i * r + q] * Ui[q * r + j];
+        Ui[i * r + j] = -v / U[i * r + i];
+      }
+    }
+    CUD(cudaMemcpyAsync(Ud, Ui.data(), sizeof(double) * r * r, cudaMemcpyHostToDevice, c->st));
+    launch_rows_times_upper(Min, rs, cs, ni, r, Ud, pass == 0 ? Q1 : c->Qr, c->ldq, c->st);
+    CUD(cudaGetLastError());
+    CUD(cudaStreamSynchronize(c->st));
+  }
+  cleanup();
+#undef CUD
+  *out = c;
   return SFAIRSC_OK;
 }
 

@@ -71,7 +71,7 @@ __device__ __forceinline__ void ld_row(const double* __restrict__ p, int c, doub
 // cmode (column-blocked SpMV for a gathered vector too large for L2, config 5):
 //   0 whole matrix (write t, epilogue); 1 first column block (write t); 2 middle (t -= W_b p);
 //   3 last (t -= W_b p, epilogue).  g.rp is then the block's row offsets into the block-major CSR.
-template <int VS, int NB, bool NORM, bool CG = false, int cmode = 0>
+template <int VS, int NB, bool NORM, bool CG = false, int cmode = 0, bool DQ = false>
 __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __restrict__ row_split,
                                                    const double* __restrict__ p, const double* __restrict__ p_self,
                                                    double* __restrict__ t, double* partials, unsigned* counter,
@@ -141,11 +141,18 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
     for (int q = 0; q < kBT; ++q) gacc[q] = 0.0;
     for (int row = r0 + threadIdx.x; row < r1; row += kThreads) {
       const double ti = __ldcg(t + (size_t)row * NB + c);
-      const double v = NORM ? g.s[row] * ti : ti;
-      const int gg = g.grp[row];
+      if constexpr (DQ) {  // dense projector: Q^T t
+        const double* qr = g.Q + (size_t)row * g.ldq;
 #pragma unroll
-      for (int q = 0; q < kHB; ++q)
-        if (q == gg) gacc[q] += v;
+        for (int q = 0; q < kHB; ++q)
+          if (q < g.qr) gacc[q] = fma(qr[q], ti, gacc[q]);
+      } else {
+        const double v = NORM ? g.s[row] * ti : ti;
+        const int gg = g.grp[row];
+#pragma unroll
+        for (int q = 0; q < kHB; ++q)
+          if (q == gg) gacc[q] += v;
+      }
     }
 #pragma unroll
     for (int cc = 0; cc < NB; ++cc)
@@ -643,7 +650,7 @@ static int rgrid(int n) { return std::max(1, std::min((n + 4 * kThreads - 1) / (
 template <int VS, int NB>
 static void spmm_vs(const GraphDev& g, const int* split, int grid, const double* p, const double* ps, double* t,
                     double* partials, unsigned* counter, double* bsum_t, cudaStream_t st, int cmode = 0) {
-  if (NB == 1 && g_spmv_gather == 1) {
+  if (NB == 1 && g_spmv_gather == 1 && !g.Q) {
     if (g.normalized)
       k_spmm<VS, NB, true, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
     else
@@ -651,7 +658,10 @@ static void spmm_vs(const GraphDev& g, const int* split, int grid, const double*
     return;
   }
 #define SPMM_CM(CM)                                                                                              \
-  if (g.normalized) k_spmm<VS, NB, true, false, CM><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
+  if (NB == 1 && g.Q) {                                                                                      \
+    if (g.normalized) k_spmm<VS, NB, true, false, CM, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
+    else k_spmm<VS, NB, false, false, CM, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
+  } else if (g.normalized) k_spmm<VS, NB, true, false, CM><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
   else k_spmm<VS, NB, false, false, CM><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
   switch (cmode) {
     case 0: SPMM_CM(0) break;

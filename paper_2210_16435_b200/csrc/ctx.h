@@ -110,6 +110,9 @@ struct sfairsc_ctx {
   int nblk = 1, vs_blk = 2;
   int* rpb = nullptr;
   double *pairP = nullptr, *pairT = nullptr, *pairY = nullptr;  // pair apply (lazily allocated)
+  // dense constraint basis (§8(f) N4, sfairsc_build_operator_dense): Q n x qr row-major (ldq); nullptr: groups
+  double* Qr = nullptr;
+  int qr = 0, ldq = 0;
   // row-partitioned contexts: all device state lives in dist
   sfz::DistCtx* dist = nullptr;
   // results
@@ -136,9 +139,17 @@ struct sfairsc_ctx {
     G.s = s;
     G.grp = grp;
     G.normalized = normalized;
+    G.Q = Qr;
+    G.ldq = ldq;
+    G.qr = qr;
     return G;
   }
-  ProjDesc pd() const { return ProjDesc{h, isb, uh}; }
+  ProjDesc pd() const {
+    ProjDesc P{Qr ? qr : h, isb, uh};
+    P.Q = Qr;
+    P.ldq = ldq;
+    return P;
+  }
   // algorithmic bytes: one read/write of each operand
   double vb() const { return 8.0 * n; }                      // one fp64 n-vector
   double sgb() const { return (normalized ? 8.0 * n : 0.0) + 1.0 * n; }  // s (normalized) + group ids

@@ -70,6 +70,10 @@ __device__ __forceinline__ void ticket_finalize(const double* partials, unsigned
 
 // gam[s] for the factored projector; executed by thread 0, result in smem.
 __device__ __forceinline__ void gamma_serial(const double* bsum, double scale, const ProjDesc& pd, double* gam) {
+  if (pd.Q) {  // dense orthonormal Q: the coefficients of QQ^T x are Q^T x itself
+    for (int s = 0; s < pd.h; ++s) gam[s] = scale * bsum[s];
+    return;
+  }
   double pi = 0.0;
   for (int s = 0; s < pd.h; ++s) {
     const double c = scale * bsum[s] * pd.isb[s];
@@ -83,6 +87,34 @@ __device__ __forceinline__ void add_group(double (&acc)[kHB], int g, double v) {
 #pragma unroll
   for (int q = 0; q < kHB; ++q)
     if (q == g) acc[q] += v;
+}
+
+// Projector rows.  Group mode: (QQ^T x)_i = s_i gam[g_i] and B^T x accumulates s_i x_i into group g_i.
+// Dense mode (DQ): (QQ^T x)_i = Q[i, :] . gam and Q^T x accumulates Q[i, q] x_i.
+template <bool DQ, bool NORM>
+__device__ __forceinline__ double proj_row(const GraphDev& g, long long i, const double* gam) {
+  if constexpr (DQ) {
+    const double* q = g.Q + (size_t)i * g.ldq;
+    double a = 0.0;
+#pragma unroll
+    for (int c = 0; c < kHB; ++c)
+      if (c < g.qr) a = fma(q[c], gam[c], a);
+    return a;
+  } else {
+    const double gv = gam[g.grp[i]];
+    return NORM ? g.s[i] * gv : gv;
+  }
+}
+template <bool DQ, bool NORM>
+__device__ __forceinline__ void accum_row(const GraphDev& g, long long i, double x, double (&acc)[kHB]) {
+  if constexpr (DQ) {
+    const double* q = g.Q + (size_t)i * g.ldq;
+#pragma unroll
+    for (int c = 0; c < kHB; ++c)
+      if (c < g.qr) acc[c] = fma(q[c], x, acc[c]);
+  } else {
+    add_group(acc, g.grp[i], NORM ? g.s[i] * x : x);
+  }
 }
 
 // Philox4x32-10 (Salmon et al. SC'11), device implementation.

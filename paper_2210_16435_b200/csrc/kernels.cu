@@ -143,7 +143,7 @@ __global__ void k_group_check(const int32_t* groups, int n, int h, uint8_t* grp,
 // ----------------------------------------------------------------------------
 // factored-projector kernels (A4, A6)
 // ----------------------------------------------------------------------------
-template <bool NORM>
+template <bool NORM, bool DQ = false>
 __global__ void __launch_bounds__(kThreads) k_gsum(GraphDev g, const double* __restrict__ x, int g_base,
                                                    double* partials, unsigned* counter, double* bsum, int nout) {
   double acc[kHB];
@@ -152,26 +152,34 @@ __global__ void __launch_bounds__(kThreads) k_gsum(GraphDev g, const double* __r
   const int n = g.n;
   const int i0 = (int)((long long)n * blockIdx.x / gridDim.x), i1 = (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
   for (int i = i0 + threadIdx.x; i < i1; i += kThreads) {
-    const double v = NORM ? g.s[i] * x[i] : x[i];
-    add_group(acc, (int)g.grp[i] - g_base, v);
+    if constexpr (DQ) {
+      accum_row<true, NORM>(g, i, x[i], acc);
+    } else {
+      const double v = NORM ? g.s[i] * x[i] : x[i];
+      add_group(acc, (int)g.grp[i] - g_base, v);
+    }
   }
   block_reduce_store<kHB>(acc, partials + (size_t)blockIdx.x * kHB);
   ticket_finalize<kHB>(partials, counter, bsum + g_base, nout);
 }
 
-template <bool NORM>
+template <bool NORM, bool DQ = false>
 __global__ void __launch_bounds__(kThreads) k_project(GraphDev g, ProjDesc pd, const double* __restrict__ x,
                                                       const double* bsum, double scale, double* __restrict__ p) {
   __shared__ double gam[256];
   if (threadIdx.x == 0) gamma_serial(bsum, scale, pd, gam);
   __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
-    const double gi = gam[g.grp[i]];
-    p[i] = NORM ? fma(-g.s[i], gi, x[i]) : x[i] - gi;
+    if constexpr (DQ) {
+      p[i] = x[i] - proj_row<true, NORM>(g, i, gam);
+    } else {
+      const double gi = gam[g.grp[i]];
+      p[i] = NORM ? fma(-g.s[i], gi, x[i]) : x[i] - gi;
+    }
   }
 }
 
-template <bool NORM>
+template <bool NORM, bool DQ = false>
 __global__ void __launch_bounds__(kThreads) k_finish(GraphDev g, ProjDesc pd, const double* __restrict__ t,
                                                      const double* bsum_t, const double* bsum_w, double sigma,
                                                      double* __restrict__ y) {
@@ -183,8 +191,12 @@ __global__ void __launch_bounds__(kThreads) k_finish(GraphDev g, ProjDesc pd, co
   }
   __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
-    const double gi = gt[g.grp[i]];
-    y[i] = NORM ? fma(-g.s[i], gi, t[i]) : t[i] - gi;
+    if constexpr (DQ) {
+      y[i] = t[i] - proj_row<true, NORM>(g, i, gt);
+    } else {
+      const double gi = gt[g.grp[i]];
+      y[i] = NORM ? fma(-g.s[i], gi, t[i]) : t[i] - gi;
+    }
   }
 }
 
@@ -248,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_spmv(GraphDev g, const int* __r
 // ----------------------------------------------------------------------------
 // Krylov sweeps (A7-A9)
 // ----------------------------------------------------------------------------
-template <int MODE, int MAXCW, bool NORM>
+template <int MODE, int MAXCW, bool NORM, bool DQ = false>
 __global__ void __launch_bounds__(kThreads) k_sweep(GraphDev g, ProjDesc pd, SweepArgs a) {
   __shared__ double xs[kThreads];
   __shared__ double coef[kMaxJ];
@@ -280,7 +292,8 @@ __global__ void __launch_bounds__(kThreads) k_sweep(GraphDev g, ProjDesc pd, Swe
     double x = 0.0;
     if (i < n) {
       if (MODE == 0) {
-        x = NORM ? fma(-g.s[i], gam[g.grp[i]], a.xin[i]) : a.xin[i] - gam[g.grp[i]];
+        if constexpr (DQ) x = a.xin[i] - proj_row<true, NORM>(g, i, gam);
+        else x = NORM ? fma(-g.s[i], gam[g.grp[i]], a.xin[i]) : a.xin[i] - gam[g.grp[i]];
         a.xout[i] = x;
       } else if (MODE == 3) {
         x = a.xin[i];
@@ -305,7 +318,7 @@ __global__ void __launch_bounds__(kThreads) k_sweep(GraphDev g, ProjDesc pd, Swe
         a.xout[i] = x;
         if (MODE == 2) {
           nrm = fma(x, x, nrm);
-          add_group(gacc, g.grp[i], NORM ? g.s[i] * x : x);
+          accum_row<DQ, NORM>(g, i, x, gacc);
         }
       }
     }
@@ -446,6 +459,45 @@ __global__ void __launch_bounds__(kThreads) k_resid(const double* __restrict__ y
 }
 
 // ----------------------------------------------------------------------------
+// Dense constraint basis (§8(f) N4): Q = orth(C) by CholQR2 (Gram on the device, Cholesky on the host)
+// element (i, a) of an n x r matrix at M[i * rs + a * cs]
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_gram_pairs(const double* __restrict__ M, long long rs, long long cs,
+                                                         int n, int r, double* out) {
+  const int a = blockIdx.x, b = blockIdx.y;
+  if (a > b) return;
+  double v[1] = {0.0};
+  for (int i = threadIdx.x; i < n; i += kThreads) v[0] = fma(M[i * rs + a * cs], M[i * rs + b * cs], v[0]);
+  block_reduce_store<1>(v, out + a * r + b);  // upper triangle; the host mirrors it
+}
+// rows scaled by s (C = D^{-1/2} F): F col-major (ld) in place
+__global__ void k_scale_rows(double* M, long long ld, int n, int r, const double* s) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int a = 0; a < r; ++a) M[(long long)a * ld + i] *= s[i];
+}
+// Qout[i, :] = Min[i, :] Ui (Ui upper triangular r x r row-major), Qout row-major (ldq)
+__global__ void k_rows_times_upper(const double* __restrict__ Min, long long rs, long long cs, int n, int r,
+                                   const double* __restrict__ Ui, double* __restrict__ Qout, int ldq) {
+  __shared__ double U[16 * 16];
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) U[e] = Ui[e];
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double row[16];
+    for (int a = 0; a < r; ++a) row[a] = Min[(long long)i * rs + (long long)a * cs];
+    for (int j = 0; j < ldq; ++j) {
+      double acc = 0.0;
+      if (j < r)
+        for (int l = 0; l <= j; ++l) acc = fma(row[l], U[l * r + j], acc);
+      Qout[(long long)i * ldq + j] = acc;
+    }
+  }
+}
+void launch_gram_pairs(const double* M, long long rs, long long cs, int n, int r, double* out, cudaStream_t st);
+void launch_scale_rows(double* M, long long ld, int n, int r, const double* s, cudaStream_t st);
+void launch_rows_times_upper(const double* Min, long long rs, long long cs, int n, int r, const double* Ui,
+                             double* Qout, int ldq, cudaStream_t st);
+
+// ----------------------------------------------------------------------------
 // launch wrappers
 // ----------------------------------------------------------------------------
 static int num_sms_cached() {
@@ -492,6 +544,11 @@ void launch_gsum(const GraphDev& g, const double* x, int g_base, double* partial
   // bsum points at the h-array base; groups [g_base, g_base+16) are written
   const int G = reduce_grid(g.n);
   const int nout = kHB;  // caller guarantees room for kHB entries past g_base
+  if (g.Q) {
+    if (g.normalized) k_gsum<true, true><<<G, kThreads, 0, st>>>(g, x, 0, partials, counter, bsum, nout);
+    else k_gsum<false, true><<<G, kThreads, 0, st>>>(g, x, 0, partials, counter, bsum, nout);
+    return;
+  }
   if (g.normalized)
     k_gsum<true><<<G, kThreads, 0, st>>>(g, x, g_base, partials, counter, bsum, nout);
   else
@@ -500,6 +557,11 @@ void launch_gsum(const GraphDev& g, const double* x, int g_base, double* partial
 void launch_project(const GraphDev& g, const ProjDesc& pd, const double* x, const double* bsum, double scale,
                     double* p, cudaStream_t st) {
   bump();
+  if (g.Q) {
+    if (g.normalized) k_project<true, true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, x, bsum, scale, p);
+    else k_project<false, true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, x, bsum, scale, p);
+    return;
+  }
   if (g.normalized)
     k_project<true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, x, bsum, scale, p);
   else
@@ -509,6 +571,11 @@ void launch_project(const GraphDev& g, const ProjDesc& pd, const double* x, cons
 void launch_finish(const GraphDev& g, const ProjDesc& pd, const double* t, const double* bsum_t,
                    const double* bsum_w, double sigma, double* y, cudaStream_t st) {
   bump();
+  if (g.Q) {
+    if (g.normalized) k_finish<true, true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_w, sigma, y);
+    else k_finish<false, true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_w, sigma, y);
+    return;
+  }
   if (g.normalized)
     k_finish<true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_w, sigma, y);
   else
@@ -544,6 +611,13 @@ int sweep_grid(int n, int num_sms) { return std::max(1, std::min(cdiv(n, kThread
 
 template <int MODE, bool NORM>
 static void sweep_m(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
+  if (g.Q && (MODE == 0 || MODE == 2)) {  // dense projector: the modes that touch it
+    if (a.J <= 64) k_sweep<MODE, 8, NORM, true><<<grid, kThreads, 0, st>>>(g, pd, a);
+    else if (a.J <= 128) k_sweep<MODE, 16, NORM, true><<<grid, kThreads, 0, st>>>(g, pd, a);
+    else if (a.J <= 256) k_sweep<MODE, 32, NORM, true><<<grid, kThreads, 0, st>>>(g, pd, a);
+    else k_sweep<MODE, 64, NORM, true><<<grid, kThreads, 0, st>>>(g, pd, a);
+    return;
+  }
   if (a.J <= 64)
     k_sweep<MODE, 8, NORM><<<grid, kThreads, 0, st>>>(g, pd, a);
   else if (a.J <= 128)
@@ -606,4 +680,20 @@ void launch_resid(const double* y, const double* x, double theta, int n, double*
   k_resid<<<reduce_grid(n), kThreads, 0, st>>>(y, x, theta, n, partials, counter, out);
 }
 
+}  // namespace sfz
+
+namespace sfz {
+void launch_gram_pairs(const double* M, long long rs, long long cs, int n, int r, double* out, cudaStream_t st) {
+  bump();
+  k_gram_pairs<<<dim3(r, r), kThreads, 0, st>>>(M, rs, cs, n, r, out);
+}
+void launch_scale_rows(double* M, long long ld, int n, int r, const double* s, cudaStream_t st) {
+  bump();
+  k_scale_rows<<<stream_grid(n), kThreads, 0, st>>>(M, ld, n, r, s);
+}
+void launch_rows_times_upper(const double* Min, long long rs, long long cs, int n, int r, const double* Ui,
+                             double* Qout, int ldq, cudaStream_t st) {
+  bump();
+  k_rows_times_upper<<<stream_grid(n), kThreads, 0, st>>>(Min, rs, cs, n, r, Ui, Qout, ldq);
+}
 }  // namespace sfz

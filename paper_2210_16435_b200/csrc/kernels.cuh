@@ -16,10 +16,15 @@ constexpr int kBT = kHB + 1;   // per-vector stride of the SpMV epilogue output:
 //   c_s   = scale * b_s * isb_s              (isb_s = beta_s^{-1/2}, beta_s = sum_{i in V_s} s_i^2)
 //   pi    = sum_s uh_s c_s                   (uh = u/|u|, u_s = |V_s| isb_s)
 //   gam_s = (c_s - uh_s pi) * isb_s          so that  Q Q^T x = s o gam_{g(i)}
+// Dense mode (§8(f) N4, general constraints C^T H = 0 with a dense F): Q (n x r, row-major, ld = ldq,
+// orthonormal columns spanning range(C)) replaces the group structure; h = r, QQ^T x = Q gam with
+// gam = Q^T x (gamma_serial is the identity), B^T x := Q^T x.
 struct ProjDesc {
   int h;
   const double* isb;  // device, h
   const double* uh;   // device, h
+  const double* Q = nullptr;  // dense mode: n x r row-major
+  int ldq = 0;
 };
 
 struct GraphDev {
@@ -32,6 +37,9 @@ struct GraphDev {
   const double* s;    // d^{-1/2} (normalized only; nullptr otherwise)
   const uint8_t* grp;
   bool normalized;
+  // dense projector (§8(f) N4): Q (n x qr, row-major, ld = ldq); nullptr: group-factored projector
+  const double* Q = nullptr;
+  int ldq = 0, qr = 0;
 };
 
 // ---- build-time kernels -----------------------------------------------------
@@ -179,6 +187,14 @@ void launch_pair_project(const GraphDev& g, const ProjDesc& pd, const double* x0
                          const double* bsum, double* p, cudaStream_t st);
 void launch_pair_finish(const GraphDev& g, const ProjDesc& pd, const double* t, const double* bsum_t,
                         const double* bsum_x, double sigma, double* y0, double* y1, cudaStream_t st);
+
+// ---- dense constraint basis (§8(f) N4) -----------------------------------------------
+// out[a*r + b] (a <= b) = sum_i M(i,a) M(i,b), M(i,a) = M[i*rs + a*cs] (fixed-order block reduction)
+void launch_gram_pairs(const double* M, long long rs, long long cs, int n, int r, double* out, cudaStream_t st);
+void launch_scale_rows(double* M, long long ld, int n, int r, const double* s, cudaStream_t st);
+// Qout (row-major, ldq) = M Ui, Ui upper triangular r x r (row-major, device)
+void launch_rows_times_upper(const double* Min, long long rs, long long cs, int n, int r, const double* Ui,
+                             double* Qout, int ldq, cudaStream_t st);
 
 // ---- k-means ----------------------------------------------------------------------
 void launch_build_rows(const double* X, long long ldx, int n, int k, const double* s, double* H, cudaStream_t st);

@@ -165,14 +165,20 @@ __global__ void __launch_bounds__(kThreads) k_lz_coef(LzDev d, int j) {
 // ---------------------------------------------------------------------------
 
 
-__host__ __device__ constexpr size_t lz_stage_doubles(int J) { return (size_t)(J + 3) * kR + 16; }
+// stage layout (doubles): [J][kR] basis | v~[kR] | t[kR] | projector rows: group mode s[kR] + grp bytes,
+// dense mode (§8(f) N4) Q[kR][ldq]; + 16 (128-byte pad)
+__host__ __device__ constexpr size_t lz_stage_doubles(int J, int ldq = 0) {
+  return (size_t)(J + 2) * kR + (size_t)kR * (ldq > 0 ? ldq : 1) + 16;
+}
 
+template <bool DQ>
 __device__ __forceinline__ void lz_issue(const LzSweepArgs& a, const GraphDev& g, const CUtensorMap* tmap, int c,
                                          double* buf, unsigned long long* bar, int lane) {
   const int J = a.J;
   const long long row0 = (long long)c * kR;
-  unsigned bytes = (unsigned)((J + 2) * kR * sizeof(double)) + kR;
-  if (g.normalized) bytes += kR * sizeof(double);
+  unsigned bytes = (unsigned)((J + 2) * kR * sizeof(double));
+  if constexpr (DQ) bytes += (unsigned)(kR * g.ldq * sizeof(double));
+  else bytes += kR + (g.normalized ? kR * sizeof(double) : 0);
   if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
   __syncwarp();
   if (lane == 0) {
@@ -180,12 +186,16 @@ __device__ __forceinline__ void lz_issue(const LzSweepArgs& a, const GraphDev& g
     bulk_g2s(buf + (size_t)J * kR, a.vt + row0, kR * sizeof(double), bar);
     bulk_g2s(buf + (size_t)(J + 1) * kR, a.t + row0, kR * sizeof(double), bar);
   } else if (lane == 1) {
-    bulk_g2s(buf + (size_t)(J + 3) * kR, g.grp + row0, kR, bar);
-    if (g.normalized) bulk_g2s(buf + (size_t)(J + 2) * kR, g.s + row0, kR * sizeof(double), bar);
+    if constexpr (DQ) {
+      bulk_g2s(buf + (size_t)(J + 2) * kR, g.Q + row0 * g.ldq, (unsigned)(kR * g.ldq * sizeof(double)), bar);
+    } else {
+      bulk_g2s(buf + (size_t)(J + 3) * kR, g.grp + row0, kR, bar);
+      if (g.normalized) bulk_g2s(buf + (size_t)(J + 2) * kR, g.s + row0, kR * sizeof(double), bar);
+    }
   }
 }
 
-template <int MAXCW, bool NORM, int NT>
+template <int MAXCW, bool NORM, int NT, bool DQ = false>
 __global__ void __launch_bounds__(NT, 1) k_lz_update(GraphDev g, ProjDesc pd, LzSweepArgs a, int kStages,
                                                       const __grid_constant__ CUtensorMap tmap) {
   constexpr int NCG = NT / kR;   // column groups of the update phase
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(NT, 1) k_lz_update(GraphDev g, ProjDesc pd, Lz
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = g.n, J = a.J;
   const int nchunks = (n + kR - 1) / kR;
-  const size_t stage_elems = lz_stage_doubles(J);
+  const size_t stage_elems = lz_stage_doubles(J, DQ ? g.ldq : 0);
   for (int l = tid; l < J; l += NT) {
     cs[l] = a.cs[l];
     cg[l] = a.cg[l];
@@ -217,7 +227,7 @@ __global__ void __launch_bounds__(NT, 1) k_lz_update(GraphDev g, ProjDesc pd, Lz
   const int my_chunks = (nchunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   if (w == 0)
     for (int it = 0; it < kStages && it < my_chunks; ++it)
-      lz_issue(a, g, &tmap, blockIdx.x + it * gridDim.x, dsm + it * stage_elems, &bars[it], lane);
+      lz_issue<DQ>(a, g, &tmap, blockIdx.x + it * gridDim.x, dsm + it * stage_elems, &bars[it], lane);
 
   double colacc[MAXCW];
 #pragma unroll
@@ -275,16 +285,31 @@ __global__ void __launch_bounds__(NT, 1) k_lz_update(GraphDev g, ProjDesc pd, Lz
         }
         const double vti = vts[tid];
         vj = fma(vti, invmu, -sumS);
-        const int gg = gs[tid];
-        const double y = NORM ? fma(-ssc[tid], gam[gg], ts[tid]) : ts[tid] - gam[gg];
-        wv = fma(ay, y, fma(av, vti, -sumG));
-        a.vj_out[gi] = vj;
-        a.w_out[gi] = wv;
-        v2[0] = fma(wv, wv, v2[0]);
-        const double sv = NORM ? ssc[tid] * wv : wv;
+        if constexpr (DQ) {  // dense projector rows Q[i, :] staged after t
+          const double* qr = ssc + (size_t)tid * g.ldq;
+          double pr = 0.0;
 #pragma unroll
-        for (int q = 0; q < kHB; ++q)
-          if (q == gg) v2[1 + q] += sv;
+          for (int q = 0; q < kHB; ++q)
+            if (q < g.qr) pr = fma(qr[q], gam[q], pr);
+          wv = fma(ay, ts[tid] - pr, fma(av, vti, -sumG));
+          a.vj_out[gi] = vj;
+          a.w_out[gi] = wv;
+          v2[0] = fma(wv, wv, v2[0]);
+#pragma unroll
+          for (int q = 0; q < kHB; ++q)
+            if (q < g.qr) v2[1 + q] = fma(qr[q], wv, v2[1 + q]);
+        } else {
+          const int gg = gs[tid];
+          const double y = NORM ? fma(-ssc[tid], gam[gg], ts[tid]) : ts[tid] - gam[gg];
+          wv = fma(ay, y, fma(av, vti, -sumG));
+          a.vj_out[gi] = vj;
+          a.w_out[gi] = wv;
+          v2[0] = fma(wv, wv, v2[0]);
+          const double sv = NORM ? ssc[tid] * wv : wv;
+#pragma unroll
+          for (int q = 0; q < kHB; ++q)
+            if (q == gg) v2[1 + q] += sv;
+        }
       }
       rw[tid] = wv;
       rv[tid] = vj;
@@ -304,7 +329,7 @@ __global__ void __launch_bounds__(NT, 1) k_lz_update(GraphDev g, ProjDesc pd, Lz
     __syncthreads();
     if (w == 0 && it + kStages < my_chunks) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      lz_issue(a, g, &tmap, blockIdx.x + (it + kStages) * gridDim.x, dsm + st * stage_elems, &bars[st], lane);
+      lz_issue<DQ>(a, g, &tmap, blockIdx.x + (it + kStages) * gridDim.x, dsm + st * stage_elems, &bars[st], lane);
     }
   }
 #pragma unroll
@@ -465,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lz_update_r(GraphDev g, ProjDes
 // ---------------------------------------------------------------------------
 // normalise: v~ = w/|w|, p~ = P v~, B^T v~, s = dots/|w|, |p~|^2, H row j+1
 // ---------------------------------------------------------------------------
-template <bool NORM>
+template <bool NORM, bool DQ = false>
 __global__ void __launch_bounds__(kThreads) k_lz_norm(GraphDev g, ProjDesc pd, const double* __restrict__ w,
                                                       const double* nb, const double* dots, int nd, LzDev d, int jrow,
                                                       double* __restrict__ vt, double* __restrict__ p, double* bs_v) {
@@ -484,7 +509,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_norm(GraphDev g, ProjDesc pd, c
       // B^T v~ = B^T w/|w| - beta o gam,  |v~|^2 = |w|^2/|w|^2 - sum_s beta_s gam_s^2
       double q2 = 0.0;
       for (int s = 0; s < pd.h; ++s) {
-        const double bet = 1.0 / (pd.isb[s] * pd.isb[s]);
+        const double bet = DQ ? 1.0 : 1.0 / (pd.isb[s] * pd.isb[s]);  // dense: Q^T Q = I
         bs_v[s] = nb[1 + s] * s_inv - bet * gam[s];
         q2 += bet * gam[s] * gam[s];
       }
@@ -504,8 +529,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_norm(GraphDev g, ProjDesc pd, c
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
     const double vi = w[i] * inv;
-    const double gi = gam[g.grp[i]];
-    const double pi = NORM ? fma(-g.s[i], gi, vi) : vi - gi;
+    const double pi = vi - proj_row<DQ, NORM>(g, i, gam);
     vt[i] = pi;
     p[i] = pi;
   }
@@ -525,20 +549,20 @@ static int lz_sgrid(int n) {
   return std::max(1, std::min((n + kThreads - 1) / kThreads, sms * 8));
 }
 
-template <int MAXCW, bool NORM, int NT>
+template <int MAXCW, bool NORM, int NT, bool DQ = false>
 static void lz_update_launch(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st) {
-  const size_t stage = lz_stage_doubles(a.J) * sizeof(double);
+  const size_t stage = lz_stage_doubles(a.J, DQ ? g.ldq : 0) * sizeof(double);
   const int stages = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, kRingBytes / stage));
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_lz_update<MAXCW, NORM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max(kRingBytes, 2 * lz_stage_doubles(kLMaxJ) * sizeof(double)));
+    cudaFuncSetAttribute(k_lz_update<MAXCW, NORM, NT, DQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(kRingBytes, 2 * lz_stage_doubles(kLMaxJ, DQ ? 16 : 0) * sizeof(double)));
     attr = true;
   }
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
   if (a.J > 0) encode_colmajor_map(a.V, a.ld, a.J, kR, &tmap);
-  k_lz_update<MAXCW, NORM, NT><<<grid, NT, stages * stage, st>>>(g, pd, a, stages, tmap);
+  k_lz_update<MAXCW, NORM, NT, DQ><<<grid, NT, stages * stage, st>>>(g, pd, a, stages, tmap);
 }
 template <int MAXQ, bool NORM>
 static void lz_update_r_launch(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid,
@@ -572,6 +596,12 @@ static void lz_update_m(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs
     else lz_update_launch<12, NORM, 512>(g, pd, a, grid, st);
     return;
   }
+  if (g.Q) {  // dense projector (§8(f) N4)
+    if (a.J + 1 <= 64) lz_update_launch<8, NORM, 256, true>(g, pd, a, grid, st);
+    else if (a.J + 1 <= 128) lz_update_launch<16, NORM, 256, true>(g, pd, a, grid, st);
+    else lz_update_launch<24, NORM, 256, true>(g, pd, a, grid, st);
+    return;
+  }
   if (a.J + 1 <= 64) lz_update_launch<8, NORM, 256>(g, pd, a, grid, st);
   else if (a.J + 1 <= 128) lz_update_launch<16, NORM, 256>(g, pd, a, grid, st);
   else lz_update_launch<24, NORM, 256>(g, pd, a, grid, st);
@@ -589,6 +619,11 @@ void launch_lz_update(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& 
 void launch_lz_norm(const GraphDev& g, const ProjDesc& pd, const double* w, const double* nb, const double* dots,
                     int nd, const LzDev& d, int jrow, double* vt, double* p, double* bs_v, cudaStream_t st) {
   bump_launch();
+  if (g.Q) {
+    if (g.normalized) k_lz_norm<true, true><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v);
+    else k_lz_norm<false, true><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v);
+    return;
+  }
   if (g.normalized)
     k_lz_norm<true><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v);
   else
@@ -624,14 +659,7 @@ struct Lagged {
 
   void norm(const double* w, const double* dots, int nd, int jrow, int flag_idx) {
     ProfScope ps(c, K_NORMALIZE, 3 * c->vb() + c->sgb());
-    LzDev d = dev(flag_idx);
-    bump_launch();
-    if (c->normalized)
-      k_lz_norm<true><<<lz_sgrid(c->n), kThreads, 0, c->st>>>(c->g(), c->pd(), w, c->nb, dots, nd, d, jrow, c->vr,
-                                                              c->vp, c->bs_v);
-    else
-      k_lz_norm<false><<<lz_sgrid(c->n), kThreads, 0, c->st>>>(c->g(), c->pd(), w, c->nb, dots, nd, d, jrow, c->vr,
-                                                               c->vp, c->bs_v);
+    launch_lz_norm(c->g(), c->pd(), w, c->nb, dots, nd, dev(flag_idx), jrow, c->vr, c->vp, c->bs_v, c->st);
   }
 
   // one Lanczos step at column j (A5-A9)

@@ -94,6 +94,8 @@ def _load():
         "sfairsc_last_error": (C.c_char_p, []),
         "sfairsc_version": (C.c_char_p, []),
         "sfairsc_host_symeig": (C.c_int, [C.c_int32, P, P, P]),
+        "sfairsc_build_operator_dense": (C.c_int, [C.POINTER(CSR), P, C.c_int32, C.c_int32, C.c_int32,
+                                                   C.POINTER(Opts), C.POINTER(P)]),
         "sfairsc_comm_unique_id": (C.c_int, [P]),
         "sfairsc_comm_init": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
         "sfairsc_comm_destroy": (None, [P]),
@@ -205,6 +207,34 @@ def sfairsc_build_operator(row_ptr, col_idx, values, groups, k: int, normalized:
     else:
         _check(_lib.sfairsc_build_operator_ex(C.byref(csr), gp, h, k, int(bool(normalized)), C.byref(opts),
                                               C.byref(out)))
+    return Context(out.value, n, k)
+
+
+def sfairsc_build_operator_dense(row_ptr, col_idx, values, F, k: int, normalized: bool, opts: Opts | None = None,
+                                 **opt_kw) -> Context:
+    """§8(f) N4: constraints C^T H = 0 with a dense F.  F: numpy (n, r) array (any order; passed
+    column-major) or a CUDA tensor of shape (r, n) (= F column-major); same memspace as W."""
+    rp, ms = _ptr(row_ptr, np.int32)
+    ci, _ = _ptr(col_idx, np.int32)
+    vv, _ = _ptr(values, np.float64)
+    n = len(row_ptr) - 1
+    if _is_torch(F):
+        r = int(F.shape[0]) if F.ndim == 2 else 1
+        fp, msf = _ptr(F.contiguous(), np.float64)
+        Fk = F
+    else:
+        Fk = np.asfortranarray(np.asarray(F, dtype=np.float64).reshape(n, -1))
+        r = Fk.shape[1]
+        fp, msf = Fk.ctypes.data, MEM_HOST
+    if msf != ms:
+        raise ValueError("F and W must share a memspace")
+    csr = CSR(n, n, len(col_idx), 0, rp, ci, vv, ms)
+    if opts is None:
+        opts = default_opts(**opt_kw)
+    out = C.c_void_p()
+    _check(_lib.sfairsc_build_operator_dense(C.byref(csr), fp if r > 0 else None, r, k, int(bool(normalized)),
+                                             C.byref(opts), C.byref(out)))
+    del Fk
     return Context(out.value, n, k)
 
 

@@ -352,6 +352,17 @@ def planted_cliques(k, m, h, seed=0, shuffle=True) -> MSBMGraph:
     return MSBMGraph(n, row_ptr, col, val, gr, cl, h, k, dict(name="planted_cliques", m=m, seed=seed))
 
 
+def random_laplacian(n, density, r, *, seed=0):
+    """Experiment 4's random Laplacian: a random symmetric weight matrix
+    W of prescribed sparsity `density` (uniform(0.5,1.5) weights, isolated vertices
+    repaired, R13) and a random constraint matrix F (n x r, standard normal, PCG64
+    stream 7) that "is not for group-membership information but only acts as a
+    placeholder".  Returns (graph with h = 1, F)."""
+    g = random_graph(n, 1, p=density, seed=seed, weights="uniform")
+    F = _rng(seed, 7).standard_normal((n, r))
+    return g, F
+
+
 def random_graph(n, h, *, p=0.3, seed=0, weights="uniform", group_counts=None) -> MSBMGraph:
     """Erdos-Renyi G(n,p) with random groups and (optionally) random weights;
     isolated vertices repaired (R13).  For small oracle pins."""

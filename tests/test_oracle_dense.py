@@ -249,3 +249,55 @@ def test_validation_rejects_bad_inputs():
         fairsc.fairsc_dense(bad, g.groups, 2, 2, False)
     with pytest.raises(fairsc.OracleInputError):
         fairsc.fairsc_dense(W, np.zeros(10, int), 2, 2, False)
+
+
+# --- explicit constraint matrix F (§8(f) N4; Experiment 4's random F) -------------
+
+@pytest.mark.parametrize("normalized", [False, True])
+@pytest.mark.parametrize("n,r,seed", [(9, 2, 1), (11, 3, 2), (12, 1, 3)])
+def test_dense_F_matches_bruteforce(normalized, n, r, seed):
+    """Alg. 2 with an explicit random F equals the 50-digit brute force (QR null space + Jacobi)."""
+    from oracle import brute
+    from synth import random_laplacian
+    g, F = random_laplacian(n, 0.6, r, seed=seed)
+    W = g.dense()
+    res = fairsc.fairsc_dense_F(W, F, n - r - 1, normalized, extra=0)
+    ev, _ = brute.brute_fair_eig(W, None, 1, normalized, F=F)
+    ref = np.array([float(x) for x in ev])[: n - r - 1]
+    assert np.allclose(res.evals, ref, atol=1e-13 * max(1.0, np.abs(ref).max()))
+
+
+@pytest.mark.parametrize("normalized", [False, True])
+def test_dense_F_range_invariance_variant_and_prop31(normalized):
+    """Only range(F) matters (F and F R agree); Alg. 2 = the §3.2 variant (P:509-528);
+    spec L^sigma = spec L^v U {sigma}^r (Prop. 3.1, Eq. asigma) for an explicit F."""
+    from synth import random_laplacian
+    n, r, k = 60, 4, 8
+    g, F = random_laplacian(n, 0.15, r, seed=4)
+    W = g.dense()
+    a = fairsc.fairsc_dense_F(W, F, k, normalized)
+    R = np.random.default_rng(1).standard_normal((r, r)) + 3 * np.eye(r)
+    b = fairsc.fairsc_dense_F(W, F @ R, k, normalized)
+    assert np.allclose(a.evals, b.evals, atol=1e-12)
+    var = fairsc.variant_evals_F(W, F, normalized)
+    assert np.allclose(a.evals, var[: len(a.evals)], atol=1e-12)
+    A, sigma = fairsc.deflated_operator_F(W, F, normalized)
+    full = np.sort(np.concatenate([var, np.full(r, sigma)]))
+    assert np.allclose(np.linalg.eigvalsh(A), full, atol=1e-11 * sigma)
+    # X is fair: C^T X = 0, and orthonormal in the comparison frame
+    C = fairsc.constraint_matrix_F(W, F, normalized)
+    assert np.linalg.norm(C.T @ a.X) <= 1e-12 * np.linalg.norm(C) * np.linalg.norm(a.X)
+    assert np.allclose(a.X.T @ a.X, np.eye(k), atol=1e-12)
+
+
+def test_dense_F_tier_s_matches_tier_d():
+    """Tier S (the paper's matrix-free operator with the normal-equations projector) with an
+    explicit F equals Tier D."""
+    from oracle import sfairsc_cpu
+    from synth import random_laplacian
+    g, F = random_laplacian(400, 0.03, 5, seed=6)
+    for normalized in (False, True):
+        d = fairsc.fairsc_dense_F(g.dense(), F, 6, normalized)
+        op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, 1, normalized, F=F)
+        s = sfairsc_cpu.sfairsc_arpack(op, 6, tol=1e-13, seed=1)
+        assert np.allclose(s.evals[:6], d.evals[:6], atol=1e-10 * op.sigma)
