@@ -335,6 +335,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   if (getenv("SFAIRSC_SPMV")) sfz::g_spmv_kind = atoi(getenv("SFAIRSC_SPMV"));
   if (getenv("SFAIRSC_LZ_SWEEP")) sfz::g_lz_sweep = atoi(getenv("SFAIRSC_LZ_SWEEP"));
   if (getenv("SFAIRSC_GATHER")) sfz::g_spmv_gather = atoi(getenv("SFAIRSC_GATHER"));
+  if (getenv("SFAIRSC_SPMV_PIPE")) sfz::g_spmv_pipe = atoi(getenv("SFAIRSC_SPMV_PIPE"));
   if (c->sweep_kind == 3) {  // TMA with one 1-D copy per column (A/B only)
     sfz::g_tma_use2d = 0;
     c->sweep_kind = 2;
@@ -576,6 +577,11 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     CUB(dalloc(&c->row_split, G + 1));
     CUB(cudaMemcpyAsync(c->row_split, split.data(), sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, c->st));
     const double mean_deg = n > 0 ? (double)nnz / n : 0.0;
+    {
+      int maxdeg = 0;
+      for (int i = 0; i < n; ++i) maxdeg = std::max(maxdeg, hrp[i + 1] - hrp[i]);
+      c->skewed = maxdeg > 16.0 * std::max(1.0, mean_deg);
+    }
     int vs = 2;
     while (vs < 32 && vs * 4 < mean_deg) vs *= 2;
     c->vs = opts.spmv_vector > 0 ? opts.spmv_vector : vs;

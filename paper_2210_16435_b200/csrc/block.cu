@@ -46,6 +46,7 @@ __device__ __forceinline__ double ld_cg(const double* p) {  // L2 only (no L1 al
   return v;
 }
 int g_spmv_gather = 0;  // 0: __ldg gathers (default); 1: ld.global.cg (env SFAIRSC_GATHER)
+int g_spmv_pipe = 0;    // 1: software-pipelined CSR slots (env SFAIRSC_SPMV_PIPE=1; measured equal, off by default)
 
 // NB doubles of row c of an interleaved block
 template <int NB, bool CG = false>
@@ -71,7 +72,8 @@ __device__ __forceinline__ void ld_row(const double* __restrict__ p, int c, doub
 // cmode (column-blocked SpMV for a gathered vector too large for L2, config 5):
 //   0 whole matrix (write t, epilogue); 1 first column block (write t); 2 middle (t -= W_b p);
 //   3 last (t -= W_b p, epilogue).  g.rp is then the block's row offsets into the block-major CSR.
-template <int VS, int NB, bool NORM, bool CG = false, int cmode = 0, bool DQ = false>
+template <int VS, int NB, bool NORM, bool CG = false, int cmode = 0, bool DQ = false, bool PIPE = false,
+          bool LONGR = false>
 __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __restrict__ row_split,
                                                    const double* __restrict__ p, const double* __restrict__ p_self,
                                                    double* __restrict__ t, double* partials, unsigned* counter,
@@ -85,14 +87,85 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
   double ptacc[NB];  // p^T t (lane-0 rows)
 #pragma unroll
   for (int c = 0; c < NB; ++c) ptacc[c] = 0.0;
+  // software pipeline (PIPE): the (col, val) slots of the next row group are loaded before the
+  // gathers of the current one, so the CSR stream latency overlaps the L2 gathers
+  const bool pipe = PIPE;
+  int pa = 0, pb = 0, pc[U];
+  double pw[U];
+  if (pipe) {
+    const int row = r0 + gid;
+    if (row < r1) {
+      pa = __ldg(rp + row);
+      pb = __ldg(rp + row + 1);
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int e = pa + lane + q * VS;
+      const bool ok = e < pb;
+      pc[q] = ok ? ld_stream(ci + e) : row;
+      pw[q] = ok ? ld_stream(vv + e) : 0.0;
+    }
+  }
   for (int base = r0; base < r1; base += NG) {
     const int row = base + gid;
     const bool valid = row < r1;
     double acc[NB];
 #pragma unroll
     for (int c = 0; c < NB; ++c) acc[c] = 0.0;
-    if (valid) {
-      const int a = __ldg(rp + row), b = __ldg(rp + row + 1);
+    if (pipe) {
+      const int a = pa, b = pb;
+      int cc[U];
+      double ww[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        cc[q] = pc[q];
+        ww[q] = pw[q];
+      }
+      const int nrow = row + NG;  // prefetch the next row group's first slots
+      pa = 0;
+      pb = 0;
+      if (nrow < r1) {
+        pa = __ldg(rp + nrow);
+        pb = __ldg(rp + nrow + 1);
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int e = pa + lane + q * VS;
+        const bool ok = e < pb;
+        pc[q] = ok ? ld_stream(ci + e) : nrow;
+        pw[q] = ok ? ld_stream(vv + e) : 0.0;
+      }
+      if (valid) {
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          double x[NB];
+          ld_row<NB, CG>(p, cc[q], x);
+#pragma unroll
+          for (int c = 0; c < NB; ++c) acc[c] = fma(ww[q], x[c], acc[c]);
+        }
+        for (int e0 = a + lane + U * VS; e0 < b; e0 += U * VS) {  // rows longer than U*VS
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            const int e = e0 + q * VS;
+            if (e < b) {
+              double x[NB];
+              ld_row<NB, CG>(p, ld_stream(ci + e), x);
+              const double wv = ld_stream(vv + e);
+#pragma unroll
+              for (int c = 0; c < NB; ++c) acc[c] = fma(wv, x[c], acc[c]);
+            }
+          }
+        }
+      }
+    }
+    int a = 0, b = 0;
+    if (!pipe && valid) {
+      a = __ldg(rp + row);
+      b = __ldg(rp + row + 1);
+    }
+    // LONGR (skewed degrees, config 5): rows longer than kLong slots are left to the whole warp below
+    constexpr int kLong = 8 * U * VS;
+    if (!pipe && valid && !(LONGR && b - a > kLong)) {
       for (int e0 = a + lane; e0 < b; e0 += U * VS) {
         int cix[U];
         double w[U];
@@ -116,6 +189,38 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
     for (int c = 0; c < NB; ++c)
 #pragma unroll
       for (int o = VS / 2; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    if constexpr (LONGR && NB == 1) {  // warp-per-row for the long rows of this warp, one at a time
+      const int wl = threadIdx.x & 31;
+      const bool my_long = valid && lane == 0 && (b - a > kLong);
+      unsigned m = __ballot_sync(0xffffffffu, my_long);
+      double along = 0.0;
+      while (m) {
+        const int src = __ffs(m) - 1;
+        const int la = __shfl_sync(0xffffffffu, a, src), lb = __shfl_sync(0xffffffffu, b, src);
+        double sacc = 0.0;
+        for (int e0 = la + wl; e0 < lb; e0 += 32 * U) {
+          int cix[U];
+          double w[U];
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            const int e = e0 + q * 32;
+            const bool ok = e < lb;
+            cix[q] = ok ? ld_stream(ci + e) : 0;
+            w[q] = ok ? ld_stream(vv + e) : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            double x[1];
+            ld_row<1, CG>(p, cix[q], x);
+            sacc = fma(w[q], x[0], sacc);
+          }
+        }
+        sacc = warp_sum(sacc);
+        if (wl == src) along = sacc;
+        m &= m - 1;
+      }
+      if (my_long) acc[0] = along;
+    }
     if (valid && lane == 0) {
       double pi[NB];
       ld_row<NB>(p_self, row, pi);  // own rows (row-partitioned: this part's segment of the gathered p)
@@ -657,8 +762,16 @@ static void spmm_vs(const GraphDev& g, const int* split, int grid, const double*
       k_spmm<VS, NB, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
     return;
   }
+  if (NB == 1 && cmode == 0 && !g.Q && g_spmv_pipe) {
+    if (g.normalized) k_spmm<VS, NB, true, false, 0, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
+    else k_spmm<VS, NB, false, false, 0, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
+    return;
+  }
 #define SPMM_CM(CM)                                                                                              \
-  if (NB == 1 && g.Q) {                                                                                      \
+  if (NB == 1 && g.skewed && !g.Q) {                                                                         \
+    if (g.normalized) k_spmm<VS, NB, true, false, CM, false, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
+    else k_spmm<VS, NB, false, false, CM, false, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
+  } else if (NB == 1 && g.Q) {                                                                               \
     if (g.normalized) k_spmm<VS, NB, true, false, CM, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
     else k_spmm<VS, NB, false, false, CM, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
   } else if (g.normalized) k_spmm<VS, NB, true, false, CM><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \

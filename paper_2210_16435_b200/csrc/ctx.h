@@ -108,6 +108,7 @@ struct sfairsc_ctx {
   // column-blocked CSR (the gathered vector exceeds L2, e.g. config 5): block-major copy of the CSR,
   // rpb[b*(n+1) + i] = start of row i in column block b; nblk = 1: plain CSR
   int nblk = 1, vs_blk = 2;
+  bool skewed = false;  // max degree > 16 x mean degree (config 5's Pareto degrees)
   int* rpb = nullptr;
   double *pairP = nullptr, *pairT = nullptr, *pairY = nullptr;  // pair apply (lazily allocated)
   // dense constraint basis (§8(f) N4, sfairsc_build_operator_dense): Q n x qr row-major (ldq); nullptr: groups
@@ -142,6 +143,7 @@ struct sfairsc_ctx {
     G.Q = Qr;
     G.ldq = ldq;
     G.qr = qr;
+    G.skewed = skewed;
     return G;
   }
   ProjDesc pd() const {

@@ -40,6 +40,7 @@ struct GraphDev {
   // dense projector (§8(f) N4): Q (n x qr, row-major, ld = ldq); nullptr: group-factored projector
   const double* Q = nullptr;
   int ldq = 0, qr = 0;
+  bool skewed = false;  // heavy-tailed degrees: the SpMV gives rows longer than 32 VS slots a whole warp
 };
 
 // ---- build-time kernels -----------------------------------------------------
@@ -92,6 +93,7 @@ extern int g_tma_use2d;
 extern int g_spmv_kind;
 extern int g_lz_sweep;
 extern int g_spmv_gather;
+extern int g_spmv_pipe;
 extern int g_ritz_kind;  // 1: DMMA (fp64 tensor cores, default), 0: register-blocked FMA  // 1: 2-D tensor-map TMA per chunk (default); 0: one 1-D bulk copy per column
 bool sweep_tma_ok(int J);  // also the J limit of the smem-staged sweeps
 int sweep_smem_grid(int n, int J, int num_sms);

@@ -433,3 +433,26 @@ def test_kmeans_config2_vs_oracle(gpu_lib, config2_ref):
     assert ari(r.labels, lab) >= 0.99
     perm = hungarian_match(r.labels, lab, k)
     assert np.abs(balance(r.labels, g.groups, k, g.h) - balance(perm[lab], g.groups, k, g.h)).max() <= 1e-3
+
+
+@pytest.mark.parametrize("blocked", [False, True])
+def test_skewed_degree_spmv(gpu_lib, blocked, monkeypatch):
+    """Heavy-tailed degrees (config-5 law: Pareto(2.5) propensities): rows longer than
+    32 VS slots go to a whole warp; L x and L^sigma x equal the oracle, with and
+    without the column-blocked CSR."""
+    from synth.dcsbm import config5
+    g, cfg = config5(n=30_000, device="cpu")
+    g = g.host()
+    deg = np.diff(g.row_ptr)
+    assert deg.max() > 16 * deg.mean()  # the long-row path is exercised
+    if blocked:
+        monkeypatch.setenv("SFAIRSC_COLBLK_MB", "0.05")
+    ctx = _ctx(gpu_lib, g, 4, False)
+    if blocked:
+        monkeypatch.delenv("SFAIRSC_COLBLK_MB")
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, False)
+    x = np.random.default_rng(9).standard_normal((2, g.n))
+    tol = 1e-13 * op.sigma * np.abs(x).max()
+    assert np.abs(gpu_lib.sfairsc_laplacian(ctx, np.ascontiguousarray(x[0])) - op.Ln @ x[0]).max() <= tol
+    assert np.abs(gpu_lib.sfairsc_apply(ctx, x) - np.stack([op.apply(v) for v in x])).max() <= tol
+    ctx.close()
