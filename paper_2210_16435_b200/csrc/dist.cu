@@ -259,6 +259,7 @@ struct DistPart {
   // gathered vector, L2-sized); rpb[b*(n_loc+1) + i] = start of row i in block b of the block-major CSR
   int nblk = 1, vs_blk = 2;
   int* rpb = nullptr;
+  bool skewed = false;  // heavy-tailed local degrees: long rows get a whole warp in the SpMV
   double *vr = nullptr, *vy = nullptr, *vt = nullptr;  // v~ (lagged), w, t
   double *V = nullptr, *Vb = nullptr, *X = nullptr;
   double *partials = nullptr, *partials2 = nullptr;
@@ -276,6 +277,7 @@ struct DistPart {
     G.s = s;
     G.grp = grp;
     G.normalized = normalized;
+    G.skewed = skewed;
     return G;
   }
   double* bs_t() const { return small; }
@@ -557,6 +559,11 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
       CU(cudaMemcpyAsync(p.row_split, split.data(), sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, st));
     }
     p.vs = c->vs;
+    {
+      int maxdeg = 0;
+      for (int i = 0; i < p.n_loc; ++i) maxdeg = std::max(maxdeg, lrp[i + 1] - lrp[i]);
+      p.skewed = maxdeg > 16.0 * std::max(1.0, (double)p.nnz_loc / std::max(1, p.n_loc));
+    }
     const size_t pc = std::max<size_t>((size_t)p.spmv_grid * 4 * kBT, (size_t)c->num_sms * 8 * (kMaxJ + 2));
     CU(dal(&p.partials, pc));
     CU(dal(&p.partials2, (size_t)c->num_sms * 8 * (kHB + 2)));
