@@ -456,3 +456,47 @@ def test_skewed_degree_spmv(gpu_lib, blocked, monkeypatch):
     assert np.abs(gpu_lib.sfairsc_laplacian(ctx, np.ascontiguousarray(x[0])) - op.Ln @ x[0]).max() <= tol
     assert np.abs(gpu_lib.sfairsc_apply(ctx, x) - np.stack([op.apply(v) for v in x])).max() <= tol
     ctx.close()
+
+
+# --- edge cases: the whole constrained spectrum, tiny graphs, empty input --------------------
+
+@pytest.mark.parametrize("normalized", [False, True])
+def test_eigs_full_constrained_spectrum(gpu_lib, normalized):
+    """k = n - h + 1 = dim null(C^T): every eigenpair of the fair problem (the Krylov space
+    exhausts null(C^T); the solver must stop on the invariant subspace, not fail)."""
+    g = random_graph(31, 3, p=0.3, seed=41, weights="uniform")
+    k = g.n - g.h + 1
+    dense = fairsc.fairsc_dense(g.dense(), g.groups, g.h, k, normalized, extra=0)
+    _check_eigs(gpu_lib, g, k, normalized, 1e-10, ref_evals=dense.evals[:k], ref_X=dense.X, gap=None)
+
+
+def test_eigs_tiny_graph_k1(gpu_lib):
+    """n = 4, h = 2, k = 1: the trivial pair lambda_1 = 0 only."""
+    g = random_graph(4, 2, p=1.0, seed=3, weights="unit", group_counts=(2, 2))
+    ev, X, st = _check_eigs(gpu_lib, g, 1, True, 1e-10, ref_evals=np.zeros(1))
+    assert abs(ev[0]) <= 1e-12 * st["sigma"]
+
+
+def test_empty_and_invalid_inputs(gpu_lib):
+    lib = gpu_lib
+    with pytest.raises(lib.SfairscError) as e:  # n = 0
+        lib.sfairsc_build_operator(np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0), np.zeros(0, np.int32),
+                                   1, False, h=1)
+    assert e.value.name == "E_INVALID_ARG"
+    g = random_graph(20, 2, p=0.3, seed=2)
+    with pytest.raises(lib.SfairscError) as e:  # k = 0
+        lib.sfairsc_build_operator(g.row_ptr, g.col, g.val, g.groups.astype(np.int32), 0, False)
+    assert e.value.name == "E_INVALID_ARG"
+    ctx = lib.sfairsc_build_operator(g.row_ptr, g.col, g.val, g.groups.astype(np.int32), 3, False)
+    with pytest.raises(lib.SfairscError) as e:  # eigs k above the build k
+        lib.sfairsc_eigs(ctx, 4, 1e-10)
+    assert e.value.name == "E_K_TOO_LARGE"
+    with pytest.raises(lib.SfairscError) as e:  # tol <= 0
+        lib.sfairsc_eigs(ctx, 2, 0.0)
+    assert e.value.name == "E_INVALID_ARG"
+    ctx.close()
+    col = g.col.copy()
+    col[0] = g.n + 5  # column out of range
+    with pytest.raises(lib.SfairscError) as e:
+        lib.sfairsc_build_operator(g.row_ptr, col, g.val, g.groups.astype(np.int32), 2, False)
+    assert e.value.name == "E_CSR_INVALID"
