@@ -319,7 +319,7 @@ struct DistCtx {
 static sfairsc_status allreduce(DistCtx* D, cudaStream_t st, int count, double* (*sel)(const DistPart&), bool op_max = false) {
   if (D->comm) {
     double* b = sel(D->parts[0]);
-    if (D->comm->nranks > 1) NC(nccl().AllReduce(b, b, count, ncclDouble, op_max ? ncclMax : ncclSum, D->comm->comm, st));
+    NC(nccl().AllReduce(b, b, count, ncclDouble, op_max ? ncclMax : ncclSum, D->comm->comm, st));
     return SFAIRSC_OK;
   }
   if (D->P == 1) return SFAIRSC_OK;
@@ -333,16 +333,16 @@ static sfairsc_status allreduce(DistCtx* D, cudaStream_t st, int count, double* 
   return SFAIRSC_OK;
 }
 static sfairsc_status allgather_full(DistCtx* D, cudaStream_t st, double* full) {
-  if (D->comm && D->comm->nranks > 1)
+  if (D->comm)  // (one rank: an in-place no-op, still issued so the 1-rank tests run the NCCL path)
     NC(nccl().AllGather(full + (size_t)D->comm->rank * D->n_max, full, D->n_max, ncclDouble, D->comm->comm, st));
-  return SFAIRSC_OK;  // virtual parts share `full`; one rank: nothing to gather
+  return SFAIRSC_OK;  // virtual parts share `full`
 }
 
 // t = L p~ for every part with the halo exchange: the own column block first, overlapped with the NCCL
 // all-gather of the other parts' segments on the communication stream, then the remote blocks (cmode:
 // 1 first, 2 middle, 3 last incl. the B^T t / p^T t epilogue).  Without blocking (one part): the plain SpMV.
 static sfairsc_status dist_spmv(DistCtx* D, sfairsc_ctx* c, cudaStream_t st) {
-  const bool nccl_multi = D->comm && D->comm->nranks > 1;
+  const bool nccl_multi = D->comm != nullptr;
   if (nccl_multi) {  // p~ segment written on st; start the all-gather on cst
     CU(cudaEventRecord(D->ev_ready, st));
     CU(cudaStreamWaitEvent(D->cst, D->ev_ready, 0));
@@ -429,7 +429,7 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
     CU(dal(&tmp, 2 * D->P_total));
     std::vector<double> mine = {(double)W->row_offset, (double)W->n_rows};
     CU(cudaMemcpy(tmp + 2 * D->part0, mine.data(), 2 * sizeof(double), cudaMemcpyHostToDevice));
-    if (D->P_total > 1) NC(nccl().AllGather(tmp + 2 * D->part0, tmp, 2, ncclDouble, D->comm->comm, st));
+    NC(nccl().AllGather(tmp + 2 * D->part0, tmp, 2, ncclDouble, D->comm->comm, st));
     std::vector<double> all(2 * D->P_total);
     CU(cudaMemcpyAsync(all.data(), tmp, sizeof(double) * 2 * D->P_total, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
@@ -644,17 +644,17 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
       while (vsb < 32 && vsb * 4 < mdb) vsb *= 2;
       p.vs_blk = vsb;
     }
-    if (D->comm) {
-      CU(cudaStreamCreateWithFlags(&D->cst, cudaStreamNonBlocking));
-      CU(cudaEventCreateWithFlags(&D->ev_ready, cudaEventDisableTiming));
-      CU(cudaEventCreateWithFlags(&D->ev_gathered, cudaEventDisableTiming));
-    }
+  }
+  if (D->comm) {
+    CU(cudaStreamCreateWithFlags(&D->cst, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&D->ev_ready, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&D->ev_gathered, cudaEventDisableTiming));
   }
   // A3: factored projector; group counts and beta_s = sum_{V_s} s_i^2 summed over parts
   std::vector<double> beta(hh), cntg(hh);
   {
     for (int s = 0; s < hh; ++s) cntg[s] = (double)cnt_local[s];
-    if (D->comm && D->comm->nranks > 1) {  // the caller passed only this rank's groups
+    if (D->comm) {  // the caller passed only this rank's groups
       double* t = D->parts[0].scal();
       CU(cudaMemcpyAsync(t, cntg.data(), sizeof(double) * hh, cudaMemcpyHostToDevice, st));
       TRY(allreduce(D, st, hh, [](const DistPart& p) { return p.scal(); }));
@@ -1114,7 +1114,7 @@ sfairsc_status dist_kmeans(sfairsc_ctx* c, uint64_t seed, int32_t* labels_out, i
     for (auto& p : D->parts)
       CU(cudaMemcpyAsync(gc + (size_t)p.q * D->n_max, p.X + (long long)col * p.ldv, sizeof(double) * p.n_loc,
                          cudaMemcpyDeviceToDevice, st));
-    if (D->comm && D->comm->nranks > 1)
+    if (D->comm)
       NC(nccl().AllGather(gc + (size_t)D->comm->rank * D->n_max, gc, D->n_max, ncclDouble, D->comm->comm, st));
   }
   for (int r = 0; r < D->P_total; ++r) {
