@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <vector>
@@ -604,8 +605,13 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
   CU(cudaMemcpyAsync(&hsig, D->parts[0].scal(), sizeof(double), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   c->sigma = opts.sigma_override > 0 ? opts.sigma_override : hsig;
-  // owner-segment column blocking (P_total > 1): block-major copy of each part's CSR
-  if (D->P_total > 1) {
+  // owner-segment column blocking (P_total > 1 and a gathered vector beyond the ~48 MB that L2 keeps
+  // across the CSR stream, e.g. config 5; env SFAIRSC_DIST_BLOCK=1 forces it, 0 disables): block-major
+  // copy of each part's CSR.  Smaller problems gather first and run one SpMV (a 28 MB all-gather at
+  // config 4 costs less than the extra column-block passes).
+  bool blk = 8.0 * D->P_total * D->n_max > 48.0 * 1048576.0;
+  if (getenv("SFAIRSC_DIST_BLOCK")) blk = atoi(getenv("SFAIRSC_DIST_BLOCK")) != 0;
+  if (D->P_total > 1 && blk) {
     for (auto& p : D->parts) {
       if (p.nnz_loc == 0) continue;
       const int nb = D->P_total, nl = p.n_loc;

@@ -27,6 +27,7 @@ ap.add_argument("--m", type=int, default=0)
 ap.add_argument("--keep", type=int, default=0)
 ap.add_argument("--skip-apply", action="store_true")
 ap.add_argument("--reorth", type=int, default=0)
+ap.add_argument("--vparts", type=int, default=0)
 args = ap.parse_args()
 
 t = time.time()
@@ -38,7 +39,7 @@ gr = torch.from_numpy(g.groups.astype(np.int32)).to(dev)
 k = cfg["k_eig"]
 ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, cfg["normalized"], h=g.h, max_restarts=args.restarts,
                                  spmv_vector=args.vs, block_size=args.bsz, max_basis=args.m, keep=args.keep,
-                                 reorth=args.reorth)
+                                 reorth=args.reorth, virtual_parts=args.vparts)
 out = {"n": g.n, "nnz": g.nnz, "info": ctx.info(), "bsz": args.bsz, "reorth": args.reorth}
 # apply-only
 x = torch.randn((4, g.n), dtype=torch.float64, device=dev)

@@ -23,9 +23,10 @@ def _solve(lib, g, k, normalized, tol, **kw):
     return ctx, ev, Xt.T, st, info
 
 
+@pytest.mark.parametrize("blocked", ["0", "1"])
 @pytest.mark.parametrize("parts", [2, 3])
 @pytest.mark.parametrize("case", ["cfg1", "rand_norm"])
-def test_virtual_parts_vs_dense(gpu_lib, parts, case):
+def test_virtual_parts_vs_dense(gpu_lib, parts, case, blocked, monkeypatch):
     if case == "cfg1":
         g, cfg = baseline_config(1)
         k, normalized, tol = cfg["k_eig"], cfg["normalized"], cfg["tol"]
@@ -33,7 +34,9 @@ def test_virtual_parts_vs_dense(gpu_lib, parts, case):
         g = random_graph(900, 4, p=0.015, seed=11, weights="uniform")
         k, normalized, tol = 6, True, 1e-10
     dense = fairsc.fairsc_dense(g.dense(), g.groups, g.h, k, normalized)
+    monkeypatch.setenv("SFAIRSC_DIST_BLOCK", blocked)  # owner-segment column blocks (config-5 path) or not
     ctx, ev, X, st, info = _solve(gpu_lib, g, k, normalized, tol, virtual_parts=parts)
+    monkeypatch.delenv("SFAIRSC_DIST_BLOCK")
     sigma = st["sigma"]
     assert st["converged"] == 1 and st["max_resid_rel"] <= 1e-9
     assert np.all(np.abs(ev - dense.evals[:k]) <= 1e-8 * np.abs(dense.evals[:k]) + 1e-12 * sigma)
