@@ -60,24 +60,45 @@ __device__ __forceinline__ void load_row(const double* X, long long ld, const do
   for (int d = 0; d < DP; ++d) h[d] = d < dim ? hval(X, ld, s, i, d) : 0.0;
 }
 
-// D2_i = (init ? inf : D2_i) min |h_i - center|^2 ; per-block sums of D2 (fixed 1024-element blocks)
+// D2_i = (init ? inf : D2_i) min |h_i - center|^2 ; per-block sums of D2 (fixed 1024-element blocks).
+// Each thread carries kBlk/256 = 4 rows as independent accumulation chains (each
+// still summed over d in index order) so the fp64 add latency is overlapped.
 template <int DP>
 __global__ void __launch_bounds__(256) k_d2(const double* X, long long ld, const double* s, int n, int dim,
                                             const double* center, int init, double* D2, double* blocksum) {
+  constexpr int Q = kBlk / 256;
   __shared__ double red[256 / 32];
+  __shared__ double cs[DP];
+  for (int d = threadIdx.x; d < DP; d += blockDim.x) cs[d] = d < dim ? center[d] : 0.0;
+  __syncthreads();
   const int b = blockIdx.x;
+  int i[Q];
+  double sc[Q], acc[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    i[q] = b * kBlk + q * 256 + threadIdx.x;
+    sc[q] = (s && i[q] < n) ? s[i[q]] : 1.0;
+    acc[q] = 0.0;
+  }
+#pragma unroll
+  for (int d = 0; d < DP; ++d)
+    if (d < dim) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (i[q] < n) {
+          const double x = X[(long long)d * ld + i[q]];
+          const double t = __dsub_rn(s ? __dmul_rn(sc[q], x) : x, cs[d]);
+          acc[q] = __dadd_rn(acc[q], __dmul_rn(t, t));
+        }
+    }
   double part = 0.0;
-  for (int q = 0; q < kBlk / 256; ++q) {
-    const int i = b * kBlk + q * 256 + threadIdx.x;
-    if (i < n) {
-      double h[DP];
-      load_row<DP>(X, ld, s, i, dim, h);
-      double v = sqdist<DP>(h, center, dim);
-      if (!init) v = fmin(v, D2[i]);
-      D2[i] = v;
+#pragma unroll
+  for (int q = 0; q < Q; ++q)
+    if (i[q] < n) {
+      const double v = init ? acc[q] : fmin(acc[q], D2[i[q]]);
+      D2[i[q]] = v;
       part += v;  // order irrelevant for the block sum's use (search), but fixed
     }
-  }
   part = warp_sum(part);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
   __syncthreads();
@@ -110,33 +131,109 @@ __global__ void k_gather_row(const double* X, long long ld, const double* s, int
   for (int d = threadIdx.x; d < dim; d += blockDim.x) out[d] = hval(X, ld, s, i, d);
 }
 
+__device__ __forceinline__ unsigned sptr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sptr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sptr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Assignment.  One CTA per SM, 8 warps; each warp owns 32 rows at a time (lane =
+// row) and prefetches its next 32 rows into a private shared tile with cp.async
+// while it computes the current ones from registers.  Centroids in shared memory
+// as [K][dimp] (dimp = dim rounded up to even, so a pair of dimensions is one
+// 16-byte load); four centroids are evaluated together (four independent chains,
+// each summed over d in index order) and compared in increasing index order, so
+// ties still go to the lowest index.
+// 12 warps per CTA (3 per scheduler) while their row tiles fit in shared memory, else 8
 template <int DP>
-__global__ void __launch_bounds__(256) k_assign(const double* X, long long ld, const double* s, int n, int dim, int K,
-                                                const double* mu, const int* old_labels, int* labels, double* dist,
-                                                int* changes) {
-  extern __shared__ double smu[];
-  for (int e = threadIdx.x; e < K * dim; e += blockDim.x) smu[e] = mu[e];
+constexpr int asg_warps() { return DP <= 56 ? 12 : 8; }
+inline size_t asg_smem(int K, int dim, int warps) {
+  return sizeof(double) * ((size_t)K * ((dim + 1) & ~1) + (size_t)warps * (dim + 1) * 32);
+}
+template <int DP, int kAsgU, int kAsgWarps = asg_warps<DP>()>
+__global__ void __launch_bounds__(kAsgWarps * 32) k_assign(const double* X, long long ld, const double* s, int n, int dim,
+                                                           int K, const double* mu, const int* old_labels, int* labels,
+                                                           double* dist, int* changes) {
+  extern __shared__ __align__(16) double smu[];
+  const int dimp = (dim + 1) & ~1;
+  for (int e = threadIdx.x; e < K * dimp; e += blockDim.x) {
+    const int c = e / dimp, d = e - c * dimp;
+    smu[e] = d < dim ? mu[c * dim + d] : 0.0;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* tile = smu + (size_t)K * dimp + (size_t)w * (dim + 1) * 32;  // [dim][32], then s [32]
+  const long long stride = (long long)gridDim.x * kAsgWarps * 32;
+  long long base = ((long long)blockIdx.x * kAsgWarps + w) * 32;
+  auto prefetch = [&](long long b0) {
+    const long long i = b0 + lane;
+    if (i < n) {
+      for (int d = 0; d < dim; ++d) cp_async8(tile + d * 32 + lane, X + (long long)d * ld + i);
+      if (s) cp_async8(tile + dim * 32 + lane, s + i);
+    }
+    cp_commit();
+  };
+  prefetch(base);
   __syncthreads();
   int ch = 0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  for (; base < n; base += stride) {
+    cp_wait<0>();
+    __syncwarp();
+    const long long i = base + lane;
     double h[DP];
-    load_row<DP>(X, ld, s, i, dim, h);
-    double best = 0.0;
-    int bl = 0;
-    for (int c = 0; c < K; ++c) {
-      const double v = sqdist<DP>(h, smu + c * dim, dim);
-      if (c == 0 || v < best) {
-        best = v;
-        bl = c;
-      }
+    const double sc = s ? tile[dim * 32 + lane] : 1.0;
+#pragma unroll
+    for (int d = 0; d < DP; ++d) {
+      const double x = d < dim ? tile[d * 32 + lane] : 0.0;
+      h[d] = s ? __dmul_rn(sc, x) : x;
     }
-    if (old_labels && old_labels[i] != bl) ++ch;
-    labels[i] = bl;
-    dist[i] = best;
+    __syncwarp();
+    prefetch(base + stride);
+    if (i < n) {
+      double best = 0.0;
+      int bl = 0;
+      for (int c0 = 0; c0 < K; c0 += kAsgU) {
+        double a[kAsgU];
+        const double* m[kAsgU];
+#pragma unroll
+        for (int j = 0; j < kAsgU; ++j) {
+          a[j] = 0.0;
+          m[j] = smu + min(c0 + j, K - 1) * dimp;
+        }
+#pragma unroll
+        for (int d = 0; d < DP; d += 2)
+          if (d < dim) {
+#pragma unroll
+            for (int j = 0; j < kAsgU; ++j) {
+              const double2 q = *reinterpret_cast<const double2*>(m[j] + d);
+              const double t0 = __dsub_rn(h[d], q.x);
+              a[j] = __dadd_rn(a[j], __dmul_rn(t0, t0));
+              if (d + 1 < dim) {
+                const double t1 = __dsub_rn(h[d + 1], q.y);
+                a[j] = __dadd_rn(a[j], __dmul_rn(t1, t1));
+              }
+            }
+          }
+#pragma unroll
+        for (int j = 0; j < kAsgU; ++j)
+          if (c0 + j < K && (c0 + j == 0 || a[j] < best)) {
+            best = a[j];
+            bl = c0 + j;
+          }
+      }
+      if (old_labels && old_labels[i] != bl) ++ch;
+      labels[i] = bl;
+      dist[i] = best;
+    }
   }
+  cp_wait<0>();
   if (changes) {
     ch = __reduce_add_sync(0xffffffffu, ch);
-    if ((threadIdx.x & 31) == 0 && ch) atomicAdd(changes, ch);  // integer: order-independent
+    if (lane == 0 && ch) atomicAdd(changes, ch);  // integer: order-independent
   }
 }
 
@@ -151,24 +248,82 @@ __global__ void __launch_bounds__(256) k_dist_own(const double* X, long long ld,
   }
 }
 
-// per-CTA cluster sums and counts: partials[b][K*dim + K]; 4 warps, each with a
-// private shared accumulator filled in row order, combined in fixed order.
-__global__ void __launch_bounds__(128) k_centroid_partials(const double* X, long long ld, const double* s, int n,
-                                                           int dim, int K, const int* labels, double* partials) {
-  extern __shared__ double acc[];  // [4][K*dim + K]
+// per-CTA cluster sums and counts: partials[b][K*dim + K].  One CTA per SM over a
+// contiguous row range, staged R rows at a time (cp.async, double-buffered;
+// consecutive threads read consecutive rows of a column).  Thread t owns column
+// c = t mod 64 (columns 0..dim-1 = coordinates, column dim = the count) of row
+// quarter q = t / 64 and adds that quarter's rows of each tile, in row order, into
+// the quarter's private accumulator; the four accumulators are combined in fixed
+// order.  Every sum is therefore in a fixed order, independent of timing.
+constexpr int kCpThreads = 256, kCpQ = 4;
+inline size_t cp_smem_r(int K, int dim, int R) {
+  return sizeof(double) * ((size_t)kCpQ * (K * dim + K) + 2 * (size_t)(dim + 1) * (R + 1)) + sizeof(int) * 2 * R;
+}
+inline int cp_rows(int K, int dim) {
+  int R = 128;
+  while (R > 32 && cp_smem_r(K, dim, R) > 220 * 1024) R /= 2;
+  return R;
+}
+template <int DP>
+__global__ void __launch_bounds__(kCpThreads) k_centroid_partials(const double* X, long long ld, const double* s,
+                                                                  int n, int dim, int K, int R, const int* labels,
+                                                                  double* partials) {
+  extern __shared__ double acc[];  // [kCpQ][W], tiles [2][dim + 1][R + 1] (row dim = s), labels [2][R]
+  const int RP = R + 1;             // padded column stride: lanes on consecutive columns hit different banks
   const int W = K * dim + K;
-  for (int e = threadIdx.x; e < 4 * W; e += blockDim.x) acc[e] = 0.0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* tiles = acc + (size_t)kCpQ * W;
+  int* tl = reinterpret_cast<int*>(tiles + 2 * (size_t)(dim + 1) * RP);
+  for (int e = threadIdx.x; e < kCpQ * W; e += blockDim.x) acc[e] = 0.0;
   const long long i0 = (long long)n * blockIdx.x / gridDim.x, i1 = (long long)n * (blockIdx.x + 1) / gridDim.x;
-  const long long j0 = i0 + (i1 - i0) * w / 4, j1 = i0 + (i1 - i0) * (w + 1) / 4;
-  double* a = acc + (size_t)w * W;
-  for (long long i = j0; i < j1; ++i) {
-    const int l = labels[i];
-    for (int d = lane; d < dim; d += 32) a[l * dim + d] += hval(X, ld, s, (int)i, d);
-    if (lane == 0) a[K * dim + l] += 1.0;
-    __syncwarp();
+  const int ntiles = (int)((i1 - i0 + R - 1) / R);
+  auto prefetch = [&](int t) {
+    if (t < ntiles) {
+      double* tb = tiles + (size_t)(t & 1) * (dim + 1) * RP;
+      int* lb = tl + (t & 1) * R;
+      const long long r0 = i0 + (long long)t * R;
+      const int ncol = dim + (s ? 1 : 0);
+      const int r = threadIdx.x & (R - 1), dstep = kCpThreads / R;  // R: power of two <= kCpThreads
+      if (r0 + r < i1)
+        for (int d = threadIdx.x / R; d < ncol; d += dstep)
+          cp_async8(tb + (size_t)d * RP + r, d < dim ? X + (long long)d * ld + r0 + r : s + r0 + r);
+      for (int r = threadIdx.x; r < R; r += blockDim.x)
+        if (r0 + r < i1) cp_async4(lb + r, labels + r0 + r);
+    }
+    cp_commit();
+  };
+  prefetch(0);
+  const int c = threadIdx.x & 63, q = threadIdx.x >> 6, RQ = R / kCpQ;
+  double* a = acc + (size_t)q * W;
+  for (int t = 0; t < ntiles; ++t) {
+    prefetch(t + 1);
+    cp_wait<1>();
+    __syncthreads();
+    const double* tb = tiles + (size_t)(t & 1) * (dim + 1) * RP;
+    const int* lb = tl + (t & 1) * R;
+    const int nr = (int)min((long long)R, i1 - (i0 + (long long)t * R));
+    const int ra = q * RQ, rb = min(nr, ra + RQ);
+    for (int cc = c; cc <= dim; cc += 64) {
+      // column dim is the count: value 1, address K*dim + label
+      const double* col = tb + (size_t)min(cc, dim - 1) * RP;
+      const double* sv = tb + (size_t)dim * RP;
+      const int mul = cc < dim ? dim : 1, off = cc < dim ? cc : K * dim;
+      int r = ra;
+      for (; r + 4 <= rb; r += 4) {  // operands loaded first; the four updates stay in row order
+        double v[4];
+        double* p[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          v[u] = cc < dim ? (s ? __dmul_rn(sv[r + u], col[r + u]) : col[r + u]) : 1.0;
+          p[u] = a + lb[r + u] * mul + off;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) *p[u] += v[u];
+      }
+      for (; r < rb; ++r) a[lb[r] * mul + off] += cc < dim ? (s ? __dmul_rn(sv[r], col[r]) : col[r]) : 1.0;
+    }
+    __syncthreads();
   }
+  cp_wait<0>();
   __syncthreads();
   for (int e = threadIdx.x; e < W; e += blockDim.x)
     partials[(size_t)blockIdx.x * W + e] = ((acc[e] + acc[W + e]) + acc[2 * W + e]) + acc[3 * W + e];
@@ -293,6 +448,12 @@ struct KM {
   KmBuf* b;
 
   int grid_rows() const { return std::max(1, std::min((n + 255) / 256, sms * 8)); }
+  void assign(const int* old_lab, int* new_lab, int* changes) {
+    constexpr int NW = asg_warps<DP>();
+    k_assign<DP, 4><<<grid_asg(), NW * 32, asg_smem(K, dim, NW), st>>>(X, ld, s, n, dim, K, b->mu, old_lab, new_lab,
+                                                                     b->dist, changes);
+  }
+  int grid_asg() const { return std::max(1, std::min((n + 255) / 256, sms)); }
 
   sfairsc_status seed_centers(uint64_t seed, int r, std::vector<double>& hb) {
     const double u0 = uniform_host(seed, 0u, (unsigned)r, (unsigned)kKmStream);
@@ -337,7 +498,8 @@ struct KM {
   sfairsc_status means(const int* lab) {
     const int W = K * dim + K;
     bump_launch();
-    k_centroid_partials<<<b->G, 128, 4 * W * sizeof(double), st>>>(X, ld, s, n, dim, K, lab, b->partials);
+    const int R = cp_rows(K, dim);
+    k_centroid_partials<DP><<<b->G, kCpThreads, cp_smem_r(K, dim, R), st>>>(X, ld, s, n, dim, K, R, lab, b->partials);
     launch_reduce_cols(b->partials, b->G, W, b->sums, st);
     bump_launch();
     k_means_div<<<std::max(1, (K * dim + 255) / 256), 256, 0, st>>>(b->sums, K, dim, b->mu);
@@ -350,12 +512,11 @@ struct KM {
     std::vector<double> counts(K);
     std::vector<int> bidx(b->nblk);
     std::vector<double> bval(b->nblk);
-    const size_t mu_smem = (size_t)K * dim * sizeof(double);
     *best_wcss = std::numeric_limits<double>::infinity();
     for (int r = 0; r < restarts; ++r) {
       TRY_(seed_centers(seed, r, hb));
       bump_launch();
-      k_assign<DP><<<grid_rows(), 256, mu_smem, st>>>(X, ld, s, n, dim, K, b->mu, nullptr, b->lab, b->dist, nullptr);
+      assign(nullptr, b->lab, nullptr);
       int* lab = b->lab;
       int* lab_new = b->lab2;
       for (int it = 0; it < max_iters; ++it) {
@@ -391,7 +552,7 @@ struct KM {
         }
         KCU(cudaMemsetAsync(b->changes, 0, sizeof(int), st));
         bump_launch();
-        k_assign<DP><<<grid_rows(), 256, mu_smem, st>>>(X, ld, s, n, dim, K, b->mu, lab, lab_new, b->dist, b->changes);
+        assign(lab, lab_new, b->changes);
         int ch = 0;
         KCU(cudaMemcpyAsync(&ch, b->changes, sizeof(int), cudaMemcpyDeviceToHost, st));
         KCU(cudaStreamSynchronize(st));
@@ -439,7 +600,7 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
     b->n = n;
     b->K = K;
     b->nblk = (n + kBlk - 1) / kBlk;
-    b->G = std::max(1, std::min(ctx_num_sms(ctx) * 2, (n + 1023) / 1024));
+    b->G = std::max(1, std::min(ctx_num_sms(ctx), (n + 1023) / 1024));  // one CTA per SM (shared memory)
     const int W = K * dim + K;
     KCU(cudaMalloc(&b->D2, sizeof(double) * n));
     KCU(cudaMalloc(&b->bsum, sizeof(double) * b->nblk));
@@ -457,7 +618,19 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
     KCU(cudaMalloc(&b->used, sizeof(int) * (K + 1)));
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_centroid_partials, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      auto big = [](const void* f) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); };
+      big((const void*)k_centroid_partials<8>);
+      big((const void*)k_centroid_partials<16>);
+      big((const void*)k_centroid_partials<32>);
+      big((const void*)k_centroid_partials<48>);
+      big((const void*)k_centroid_partials<56>);
+      big((const void*)k_centroid_partials<64>);
+      big((const void*)k_assign<8, 4>);
+      big((const void*)k_assign<16, 4>);
+      big((const void*)k_assign<32, 4>);
+      big((const void*)k_assign<48, 4>);
+      big((const void*)k_assign<56, 4>);
+      big((const void*)k_assign<64, 4>);
       attr = true;
     }
   }
@@ -469,6 +642,8 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
   if (dim <= 8) stt = KM<8>{X, ld, s, n, dim, K, sms, st, b}.run(seed, 10, 300, &wcss);
   else if (dim <= 16) stt = KM<16>{X, ld, s, n, dim, K, sms, st, b}.run(seed, 10, 300, &wcss);
   else if (dim <= 32) stt = KM<32>{X, ld, s, n, dim, K, sms, st, b}.run(seed, 10, 300, &wcss);
+  else if (dim <= 48) stt = KM<48>{X, ld, s, n, dim, K, sms, st, b}.run(seed, 10, 300, &wcss);
+  else if (dim <= 56) stt = KM<56>{X, ld, s, n, dim, K, sms, st, b}.run(seed, 10, 300, &wcss);
   else stt = KM<64>{X, ld, s, n, dim, K, sms, st, b}.run(seed, 10, 300, &wcss);
   ctx_prof_end(ctx, 8, ev);
   if (stt != SFAIRSC_OK) return stt;
