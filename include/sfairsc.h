@@ -126,6 +126,9 @@ typedef struct {
   int32_t h, k_build, normalized, spmv_vector;
   double sigma;
   int32_t device, num_sms;
+  int32_t unit_weights;   /* 1: every stored w_ij = 1 (no diagonal entries): the single-vector SpMV
+                             streams only column indices (normalized: gathers s o x, row sums scaled by s_i) */
+  int32_t reserved;
 } sfairsc_info;
 
 void sfairsc_default_opts(sfairsc_opts *opts);

@@ -99,7 +99,7 @@ static void free_ctx(sfairsc_ctx* c) {
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
                   c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta,
                   c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags, c->Hdev, c->sdev, c->lz, c->partials2, c->dd, c->rpb,
-                  c->pairP, c->pairT, c->pairY, c->Qr};
+                  c->pairP, c->pairT, c->pairY, c->Qr, c->vq, c->vq_lz};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hp) cudaFreeHost(c->hp);
@@ -146,6 +146,8 @@ extern "C" sfairsc_status sfairsc_get_info(const sfairsc_ctx* c, sfairsc_info* i
   info->sigma = c->sigma;
   info->device = c->device;
   info->num_sms = c->num_sms;
+  info->unit_weights = c->unit ? 1 : 0;
+  info->reserved = 0;
   return SFAIRSC_OK;
 }
 
@@ -169,7 +171,7 @@ sfairsc_status sfz::apply_dev(sfairsc_ctx* c, const double* x, double* y) {
     launch_project(c->g(), c->pd(), x, c->bs_w, 1.0, c->vp, c->st);
   }
   {
-    ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
+    ProfScope ps(c, K_SPMV, c->csr_bytes_spmv() + 3 * c->vb() + 1.0 * c->n);
     ctx_spmv(c, c->vp, c->vt);
   }
   if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
@@ -208,17 +210,28 @@ sfairsc_status sfz::apply_pair_dev(sfairsc_ctx* c, const double* x0, const doubl
 }
 static bool pair_ok(const sfairsc_ctx* c) { return c->h <= kHB && c->nblk <= 1 && !c->dist && !c->Qr; }
 
-void sfz::ctx_spmv(sfairsc_ctx* c, const double* p, double* t) {
+// set by the dense-constraint build around its inner build: the DQ SpMV streams the values
+static thread_local bool g_build_keep_values = false;
+
+void sfz::ctx_spmv(sfairsc_ctx* c, const double* p, double* t, const double* q_pre) {
+  // unit weights, normalized: gather q = s o p (the row sum is scaled by s_i in the kernel)
+  const double* pg = p;
+  if (c->unit_spmv() && c->normalized && q_pre) {
+    pg = q_pre;
+  } else if (c->unit_spmv() && c->normalized) {
+    launch_scale_vec(c->s, p, c->vq, c->n, c->st);
+    pg = c->vq;
+  }
   if (c->nblk <= 1) {
-    launch_spmm(c->g(), 1, c->vs, c->row_split, c->spmv_grid, p, t, c->partials, c->counters + 1, c->bs_t, c->st);
+    launch_spmm(c->gs(), 1, c->vs, c->row_split, c->spmv_grid, pg, t, c->partials, c->counters + 1, c->bs_t, c->st, p);
     return;
   }
   for (int b = 0; b < c->nblk; ++b) {  // p restricted to block b (8n/nblk bytes) stays in L2 while W_b streams
-    GraphDev g = c->g();
+    GraphDev g = c->gs();
     g.rp = c->rpb + (size_t)b * (c->n + 1);
     const int cmode = (b == 0) ? 1 : (b + 1 < c->nblk ? 2 : 3);
-    launch_spmv_colblock(g, c->vs_blk, c->row_split, c->spmv_grid, p, t, c->partials, c->counters + 1, c->bs_t, cmode,
-                         c->st);
+    launch_spmv_colblock(g, c->vs_blk, c->row_split, c->spmv_grid, pg, t, c->partials, c->counters + 1, c->bs_t, cmode,
+                         c->st, p);
   }
 }
 
@@ -372,6 +385,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   c->m = m;
   c->keep = opts.keep > 0 ? opts.keep : k + (m - k) / 4;
   c->keep = std::max(std::min(c->keep, m - 1), std::min(k, m - 1));
+  const int m_pref = m;  // the basis the HBM budget below may shrink (and a dropped value array may regrow)
   // block Lanczos sizing: m + b <= kBMaxJ, m + b <= dim null(C^T) = n - h + 1, keep >= k, (m - keep) % b == 0
   c->bsz = opts.block_size > 0 ? opts.block_size : 1;
   if (c->bsz != 1 && c->bsz != 2 && c->bsz != 4)
@@ -493,6 +507,15 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   if (hflags & 1) return bail(fail(SFAIRSC_E_CSR_INVALID, "CSR invalid (row_ptr/col range, unsorted or duplicate columns, or nonzero diagonal)"));
   if (hflags & 2) return bail(fail(SFAIRSC_E_NEGATIVE_WEIGHT, "negative or NaN weight (P:121)"));
   if (hflags & 4) return bail(fail(SFAIRSC_E_ASYMMETRIC, "W is not symmetric"));
+  // unit-weight pattern (every stored w_ij = 1): the single-vector SpMV needs no value stream
+  // (env SFAIRSC_UNIT=0 keeps the value-streaming kernel, for A/B measurements)
+  c->unit = nnz > 0 && !(hflags & 32) && !(getenv("SFAIRSC_UNIT") && atoi(getenv("SFAIRSC_UNIT")) == 0);
+  if (c->unit && c->normalized) {
+    CUB(dalloc(&c->vq, c->ldv));
+    CUB(dalloc(&c->vq_lz, c->ldv));
+    CUB(cudaMemsetAsync(c->vq, 0, sizeof(double) * c->ldv, c->st));
+    CUB(cudaMemsetAsync(c->vq_lz, 0, sizeof(double) * c->ldv, c->st));
+  }
   // A1: degrees d = W 1
   launch_degrees(c->g(), c->dg, c->flags, c->st);
   CUB(cudaMemcpyAsync(&hflags, c->flags, sizeof(int), cudaMemcpyDeviceToHost, c->st));
@@ -537,17 +560,36 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
       if (base != nnz) return bail(fail(SFAIRSC_E_CUDA, "column blocking lost entries (%lld vs %d)", base, nnz));
       CUB(dalloc(&c->rpb, hr.size()));
       CUB(cudaMemcpyAsync(c->rpb, hr.data(), sizeof(int32_t) * hr.size(), cudaMemcpyHostToDevice, c->st));
+      // unit weights: after the build only the single-vector SpMV reads W here, and it streams column
+      // indices only (pairs need an unblocked CSR, block Lanczos and the dense projector keep the values)
+      const bool drop_vals = c->unit && c->bsz == 1 && !g_build_keep_values;
       int* ci2 = nullptr;
       double* vv2 = nullptr;
       CUB(dalloc(&ci2, nnz));
-      CUB(dalloc(&vv2, nnz));
-      launch_colblk_scatter(c->rp, c->ci, c->vv, n, nb, c->rpb, ci2, vv2, c->st);
+      if (!drop_vals) CUB(dalloc(&vv2, nnz));
+      launch_colblk_scatter(c->rp, c->ci, drop_vals ? nullptr : c->vv, n, nb, c->rpb, ci2, vv2, c->st);
       CUB(cudaGetLastError());
       CUB(cudaStreamSynchronize(c->st));
       cudaFree(c->ci);
       cudaFree(c->vv);
       c->ci = ci2;
       c->vv = vv2;
+      // the value array's HBM (8 nnz bytes) goes back to the Krylov basis, up to the preferred size
+      if (drop_vals && opts.max_basis <= 0 && c->m < m_pref && !(opts.comm || opts.virtual_parts > 1)) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > 0) {
+          const double vbytes = 8.0 * (double)c->ldv;
+          const double fixed = ((double)k + 15.0) * vbytes + 256.0 * (1 << 20);
+          const int mfit = (int)std::floor((0.97 * (double)fr - fixed) / (2.0 * vbytes)) - 1;
+          int mnew = std::min(m_pref, mfit);
+          if (c->lagged) mnew = std::min(mnew, std::min(192, n - hh));
+          if (mnew > c->m) {
+            c->m = m = mnew;
+            c->keep = opts.keep > 0 ? opts.keep : k + (m - k) / 4;
+            c->keep = std::max(std::min(c->keep, m - 1), std::min(k, m - 1));
+          }
+        }
+      }
       c->nblk = nb;
       const double mdb = (double)nnz / n / nb;
       int vsb = 2;
@@ -693,7 +735,9 @@ extern "C" sfairsc_status sfairsc_build_operator_dense(const sfairsc_csr* W, con
     gz = gzd;
   }
   sfairsc_ctx* c = nullptr;
+  g_build_keep_values = true;
   sfairsc_status st0 = sfairsc_build_operator_ex(W, gz, 1, k, normalized, &opts, &c);
+  g_build_keep_values = false;
   if (gzd) cudaFree(gzd);
   if (st0 != SFAIRSC_OK) return st0;
   if (r == 0) {
@@ -846,7 +890,7 @@ static sfairsc_status project_dev(sfairsc_ctx* c, const double* x, double* y) {
 }
 
 static sfairsc_status lap_dev(sfairsc_ctx* c, const double* x, double* y) {
-  ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
+  ProfScope ps(c, K_SPMV, c->csr_bytes_spmv() + 3 * c->vb() + 1.0 * c->n);
   ctx_spmv(c, x, y);
   CHECK_LAUNCH();
   return SFAIRSC_OK;
@@ -1081,7 +1125,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
     // ---- expand column j: r = L^sigma v_j, CGS2 against V[:, 0:j+1], v_{j+1} = r/|r| ----
     // (no host synchronisation inside the expansion; breakdowns are detected at the next sync)
     {
-      ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
+      ProfScope ps(c, K_SPMV, c->csr_bytes_spmv() + 3 * c->vb() + 1.0 * c->n);
       ctx_spmv(c, c->vp, c->vt);
     }
     if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);

@@ -72,8 +72,10 @@ __device__ __forceinline__ void ld_row(const double* __restrict__ p, int c, doub
 // cmode (column-blocked SpMV for a gathered vector too large for L2, config 5):
 //   0 whole matrix (write t, epilogue); 1 first column block (write t); 2 middle (t -= W_b p);
 //   3 last (t -= W_b p, epilogue).  g.rp is then the block's row offsets into the block-major CSR.
+// UNIT (unit-weight graphs): no value stream; p is then the gathered vector (normalized: q = s o p)
+// and p_self the vector itself, the row sum scaled by s_i (normalized).
 template <int VS, int NB, bool NORM, bool CG = false, int cmode = 0, bool DQ = false, bool PIPE = false,
-          bool LONGR = false>
+          bool LONGR = false, bool UNIT = false>
 __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __restrict__ row_split,
                                                    const double* __restrict__ p, const double* __restrict__ p_self,
                                                    double* __restrict__ t, double* partials, unsigned* counter,
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
       const int e = pa + lane + q * VS;
       const bool ok = e < pb;
       pc[q] = ok ? ld_stream(ci + e) : row;
-      pw[q] = ok ? ld_stream(vv + e) : 0.0;
+      pw[q] = ok ? (UNIT ? 1.0 : ld_stream(vv + e)) : 0.0;
     }
   }
   for (int base = r0; base < r1; base += NG) {
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
         const int e = pa + lane + q * VS;
         const bool ok = e < pb;
         pc[q] = ok ? ld_stream(ci + e) : nrow;
-        pw[q] = ok ? ld_stream(vv + e) : 0.0;
+        pw[q] = ok ? (UNIT ? 1.0 : ld_stream(vv + e)) : 0.0;
       }
       if (valid) {
 #pragma unroll
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
             if (e < b) {
               double x[NB];
               ld_row<NB, CG>(p, ld_stream(ci + e), x);
-              const double wv = ld_stream(vv + e);
+              const double wv = UNIT ? 1.0 : ld_stream(vv + e);
 #pragma unroll
               for (int c = 0; c < NB; ++c) acc[c] = fma(wv, x[c], acc[c]);
             }
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
           const int e = e0 + q * VS;
           const bool ok = e < b;
           cix[q] = ok ? ld_stream(ci + e) : row;
-          w[q] = ok ? ld_stream(vv + e) : 0.0;
+          w[q] = ok ? (UNIT ? 1.0 : ld_stream(vv + e)) : 0.0;
         }
 #pragma unroll
         for (int q = 0; q < U; ++q) {
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
             const int e = e0 + q * 32;
             const bool ok = e < lb;
             cix[q] = ok ? ld_stream(ci + e) : 0;
-            w[q] = ok ? ld_stream(vv + e) : 0.0;
+            w[q] = ok ? (UNIT ? 1.0 : ld_stream(vv + e)) : 0.0;
           }
 #pragma unroll
           for (int q = 0; q < U; ++q) {
@@ -220,6 +222,13 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
         m &= m - 1;
       }
       if (my_long) acc[0] = along;
+    }
+    if constexpr (UNIT && NORM) {
+      if (valid && lane == 0) {
+        const double si = g.s[row];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) acc[c] *= si;
+      }
     }
     if (valid && lane == 0) {
       double pi[NB];
@@ -755,20 +764,26 @@ static int rgrid(int n) { return std::max(1, std::min((n + 4 * kThreads - 1) / (
 template <int VS, int NB>
 static void spmm_vs(const GraphDev& g, const int* split, int grid, const double* p, const double* ps, double* t,
                     double* partials, unsigned* counter, double* bsum_t, cudaStream_t st, int cmode = 0) {
-  if (NB == 1 && g_spmv_gather == 1 && !g.Q) {
+  if (NB == 1 && g_spmv_gather == 1 && !g.Q && !g.unit) {
     if (g.normalized)
       k_spmm<VS, NB, true, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
     else
       k_spmm<VS, NB, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
     return;
   }
-  if (NB == 1 && cmode == 0 && !g.Q && g_spmv_pipe) {
+  if (NB == 1 && cmode == 0 && !g.Q && !g.unit && g_spmv_pipe) {
     if (g.normalized) k_spmm<VS, NB, true, false, 0, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
     else k_spmm<VS, NB, false, false, 0, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
     return;
   }
 #define SPMM_CM(CM)                                                                                              \
-  if (NB == 1 && g.skewed && !g.Q) {                                                                         \
+  if (NB == 1 && g.unit && !g.Q && g.skewed) {                                                               \
+    if (g.normalized) k_spmm<VS, NB, true, false, CM, false, false, true, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
+    else k_spmm<VS, NB, false, false, CM, false, false, true, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
+  } else if (NB == 1 && g.unit && !g.Q) {                                                                    \
+    if (g.normalized) k_spmm<VS, NB, true, false, CM, false, false, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
+    else k_spmm<VS, NB, false, false, CM, false, false, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
+  } else if (NB == 1 && g.skewed && !g.Q) {                                                                  \
     if (g.normalized) k_spmm<VS, NB, true, false, CM, false, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
     else k_spmm<VS, NB, false, false, CM, false, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
   } else if (NB == 1 && g.Q) {                                                                               \
@@ -828,7 +843,7 @@ __global__ void k_colblk_scatter(const int* __restrict__ rp, const int* __restri
       const int d0 = rpb[(size_t)q * (n + 1) + i], d1 = rpb[(size_t)q * (n + 1) + i + 1];
       for (int e = d0; e < d1; ++e, ++src) {
         ci2[e] = ci[src];
-        vv2[e] = vv[src];
+        if (vv) vv2[e] = vv[src];  // vv == nullptr: pattern only (unit weights)
       }
     }
   }

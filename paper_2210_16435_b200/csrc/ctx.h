@@ -109,6 +109,9 @@ struct sfairsc_ctx {
   // rpb[b*(n+1) + i] = start of row i in column block b; nblk = 1: plain CSR
   int nblk = 1, vs_blk = 2;
   bool skewed = false;  // max degree > 16 x mean degree (config 5's Pareto degrees)
+  bool unit = false;    // unit-weight pattern: ctx_spmv streams column indices only (GraphDev::unit)
+  double* vq = nullptr; // normalized unit-weight SpMV: gathered q = s o p
+  double* vq_lz = nullptr; // the same for the lagged solver's p~, written by its normalisation kernel
   int* rpb = nullptr;
   double *pairP = nullptr, *pairT = nullptr, *pairY = nullptr;  // pair apply (lazily allocated)
   // dense constraint basis (§8(f) N4, sfairsc_build_operator_dense): Q n x qr row-major (ldq); nullptr: groups
@@ -146,6 +149,13 @@ struct sfairsc_ctx {
     G.skewed = skewed;
     return G;
   }
+  // the graph as ctx_spmv sees it (single-vector SpMV: the unit-weight kernels when the pattern allows)
+  GraphDev gs() const {
+    GraphDev G = g();
+    G.unit = unit_spmv();
+    return G;
+  }
+  bool unit_spmv() const { return unit && !Qr; }  // the dense-projector SpMV keeps its value-streaming kernel
   ProjDesc pd() const {
     ProjDesc P{Qr ? qr : h, isb, uh};
     P.Q = Qr;
@@ -156,6 +166,8 @@ struct sfairsc_ctx {
   double vb() const { return 8.0 * n; }                      // one fp64 n-vector
   double sgb() const { return (normalized ? 8.0 * n : 0.0) + 1.0 * n; }  // s (normalized) + group ids
   double csr_bytes() const { return 12.0 * nnz + 4.0 * (n + 1); }
+  // bytes of W the single-vector SpMV reads (unit weights: column indices and row offsets only)
+  double csr_bytes_spmv() const { return (unit_spmv() ? 4.0 : 12.0) * nnz + 4.0 * (n + 1); }
   int gpasses() const { return (h + kHB - 1) / kHB; }
 };
 
@@ -165,7 +177,8 @@ sfairsc_status fail(sfairsc_status st, const char* fmt, ...);
 sfairsc_status apply_dev(sfairsc_ctx* c, const double* x, double* y);  // y = L^sigma x (device vectors)
 sfairsc_status true_residuals(sfairsc_ctx* c, const double* theta, int k, double* max_out);  // over X
 // t = L p (+ B^T t, p^T t into bs_t) through the plain or the column-blocked CSR
-void ctx_spmv(sfairsc_ctx* c, const double* p, double* t);
+// t = L p (+ epilogue B^T t, p^T t); q_pre: s o p already formed (normalized unit-weight graphs), else nullptr
+void ctx_spmv(sfairsc_ctx* c, const double* p, double* t, const double* q_pre = nullptr);
 sfairsc_status apply_pair_dev(sfairsc_ctx* c, const double* x0, const double* x1, double* y0, double* y1);
 double now_s();
 }

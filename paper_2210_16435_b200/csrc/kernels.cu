@@ -31,7 +31,7 @@ static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b)
 // ----------------------------------------------------------------------------
 // build-time kernels (A0-A3)
 // ----------------------------------------------------------------------------
-enum { F_CSR = 1, F_NEG = 2, F_ASYM = 4, F_ISO = 8, F_GRP = 16 };
+enum { F_CSR = 1, F_NEG = 2, F_ASYM = 4, F_ISO = 8, F_GRP = 16, F_NONUNIT = 32 };
 
 __global__ void k_validate(GraphDev g, int check_sym, int* flags) {
   const int n = g.n;
@@ -53,6 +53,7 @@ __global__ void k_validate(GraphDev g, int check_sym, int* flags) {
       prev = j;
       if (!(w >= 0.0)) f |= F_NEG;  // also NaN
       if (j == i && w != 0.0) f |= F_CSR;
+      if (w != 1.0 || j == i) f |= F_NONUNIT;  // not a unit-weight pattern (informational)
       if (check_sym && j >= 0 && j < n && j != i) {
         int lo = g.rp[j], hi = g.rp[j + 1] - 1, found = -1;
         while (lo <= hi) {
@@ -84,6 +85,10 @@ __global__ void k_degrees(GraphDev g, double* d, int* flags) {
 
 __global__ void k_inv_sqrt(const double* d, double* s, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) s[i] = 1.0 / sqrt(d[i]);
+}
+
+__global__ void k_scale_vec(const double* __restrict__ s, const double* __restrict__ p, double* __restrict__ q, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) q[i] = s[i] * p[i];
 }
 
 __global__ void k_scale_values(const int* rp, const int* ci, double* vv, const double* s, int n) {
@@ -524,6 +529,10 @@ void launch_degrees(const GraphDev& g, double* d, int* flags, cudaStream_t st) {
 void launch_inv_sqrt(const double* d, double* s, int n, cudaStream_t st) {
   bump();
   k_inv_sqrt<<<stream_grid(n), kThreads, 0, st>>>(d, s, n);
+}
+void launch_scale_vec(const double* s, const double* p, double* q, int n, cudaStream_t st) {
+  bump();
+  k_scale_vec<<<stream_grid(n), kThreads, 0, st>>>(s, p, q, n);
 }
 void launch_scale_values(const int* rp, const int* ci, double* vv, const double* s, int n, cudaStream_t st) {
   bump();

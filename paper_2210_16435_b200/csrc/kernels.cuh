@@ -41,6 +41,9 @@ struct GraphDev {
   const double* Q = nullptr;
   int ldq = 0, qr = 0;
   bool skewed = false;  // heavy-tailed degrees: the SpMV gives rows longer than 32 VS slots a whole warp
+  // unit weights (every stored w_ij = 1, no diagonal entries): the single-vector SpMV streams only the
+  // column indices; normalized graphs then gather q = s o p and scale the row sum by s_i
+  bool unit = false;
 };
 
 // ---- build-time kernels -----------------------------------------------------
@@ -48,6 +51,8 @@ void launch_validate_csr(const GraphDev& g, int check_sym, int* flags, cudaStrea
 void launch_degrees(const GraphDev& g, double* d, int* flags, cudaStream_t st);
 void launch_scale_values(const int* rp, const int* ci, double* vv, const double* s, int n, cudaStream_t st);
 void launch_inv_sqrt(const double* d, double* s, int n, cudaStream_t st);
+// q = s o p (normalized unit-weight SpMV input)
+void launch_scale_vec(const double* s, const double* p, double* q, int n, cudaStream_t st);
 // row sums of |L| columns -> max into *out (sigma = ||L||_1)
 void launch_sigma(const GraphDev& g, double* partials, unsigned* counter, double* out, cudaStream_t st);
 void launch_group_check(const int32_t* groups, int n, int h, uint8_t* grp, int* flags, cudaStream_t st);

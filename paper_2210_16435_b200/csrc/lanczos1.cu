@@ -493,7 +493,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lz_update_r(GraphDev g, ProjDes
 template <bool NORM, bool DQ = false>
 __global__ void __launch_bounds__(kThreads) k_lz_norm(GraphDev g, ProjDesc pd, const double* __restrict__ w,
                                                       const double* nb, const double* dots, int nd, LzDev d, int jrow,
-                                                      double* __restrict__ vt, double* __restrict__ p, double* bs_v) {
+                                                      double* __restrict__ vt, double* __restrict__ p, double* bs_v,
+                                                      double* __restrict__ q) {
   __shared__ double gam[kHB];
   __shared__ double s_inv;
   if (threadIdx.x == 0) {
@@ -532,6 +533,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_norm(GraphDev g, ProjDesc pd, c
     const double pi = vi - proj_row<DQ, NORM>(g, i, gam);
     vt[i] = pi;
     p[i] = pi;
+    if (NORM && q) q[i] = g.s[i] * pi;  // unit-weight SpMV input s o p~ (ctx_spmv's gathered vector)
   }
 }
 
@@ -617,17 +619,18 @@ void launch_lz_update(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& 
   else lz_update_m<false>(g, pd, a, grid, st);
 }
 void launch_lz_norm(const GraphDev& g, const ProjDesc& pd, const double* w, const double* nb, const double* dots,
-                    int nd, const LzDev& d, int jrow, double* vt, double* p, double* bs_v, cudaStream_t st) {
+                    int nd, const LzDev& d, int jrow, double* vt, double* p, double* bs_v, cudaStream_t st,
+                    double* q) {
   bump_launch();
   if (g.Q) {
-    if (g.normalized) k_lz_norm<true, true><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v);
-    else k_lz_norm<false, true><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v);
+    if (g.normalized) k_lz_norm<true, true><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v, q);
+    else k_lz_norm<false, true><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v, q);
     return;
   }
   if (g.normalized)
-    k_lz_norm<true><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v);
+    k_lz_norm<true><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v, q);
   else
-    k_lz_norm<false><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v);
+    k_lz_norm<false><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v, q);
 }
 
 // ---------------------------------------------------------------------------
@@ -659,14 +662,14 @@ struct Lagged {
 
   void norm(const double* w, const double* dots, int nd, int jrow, int flag_idx) {
     ProfScope ps(c, K_NORMALIZE, 3 * c->vb() + c->sgb());
-    launch_lz_norm(c->g(), c->pd(), w, c->nb, dots, nd, dev(flag_idx), jrow, c->vr, c->vp, c->bs_v, c->st);
+    launch_lz_norm(c->g(), c->pd(), w, c->nb, dots, nd, dev(flag_idx), jrow, c->vr, c->vp, c->bs_v, c->st, c->unit_spmv() ? c->vq_lz : nullptr);
   }
 
   // one Lanczos step at column j (A5-A9)
   sfairsc_status step(int j) {
     {
-      ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
-      ctx_spmv(c, c->vp, c->vt);  // epilogue: B^T t and p~^T t (bs_t[kHB])
+      ProfScope ps(c, K_SPMV, c->csr_bytes_spmv() + 3 * c->vb() + 1.0 * c->n);
+      ctx_spmv(c, c->vp, c->vt, c->vq_lz);  // epilogue: B^T t and p~^T t (bs_t[kHB]); vq_lz = s o p~ (unit)
     }
     {
       ProfScope ps(c, K_OTHER, 0.0);

@@ -48,6 +48,7 @@ void launch_lz_coef(const LzDev& d, int j, cudaStream_t st);
 void launch_lz_update(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st);
 // v~ = p~ = P(w/|w|) -> vt, p; s = dots/|w| (nd entries); H row jrow (jrow >= 0); B^T v~ -> bs_v
 void launch_lz_norm(const GraphDev& g, const ProjDesc& pd, const double* w, const double* nb, const double* dots,
-                    int nd, const LzDev& d, int jrow, double* vt, double* p, double* bs_v, cudaStream_t st);
+                    int nd, const LzDev& d, int jrow, double* vt, double* p, double* bs_v, cudaStream_t st,
+                    double* q = nullptr);
 
 }  // namespace sfz

@@ -56,6 +56,8 @@ out["stats"] = st
 prof = lib.profile_read(ctx)
 out["eigs_kernels"] = {kk: {"ms": v["ms"], "launches": v["launches"],
                             "us": 1e3 * v["ms"] / max(1, v["launches"])} for kk, v in prof.items() if v["launches"]}
+print(json.dumps(out), flush=True)  # the solve's record first (the checks below are separate)
+ctx.close()  # the checks need the memory the basis held
 if ev is not None:
     out["evals"] = [float(x) for x in ev]
     G = Xd @ Xd.T
@@ -72,4 +74,3 @@ if ev is not None:
     out["FtX_normwise"] = out["FtX_rel"] / Fnorm
     out["lambda1_rel"] = abs(out["evals"][0]) / st["sigma"]
 print(json.dumps(out, indent=1), flush=True)
-ctx.close()

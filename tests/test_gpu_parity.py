@@ -63,6 +63,53 @@ def test_operator_pieces_match_oracle(gpu_lib, idx):
     ctx.close()
 
 
+@pytest.mark.parametrize("n,h,p,normalized,colblk", [(37, 2, 0.3, False, None), (1031, 5, 0.01, True, None),
+                                                     (2000, 20, 0.01, False, None), (3001, 3, 0.004, True, "0.01")])
+def test_unit_weight_spmv_matches_oracle(gpu_lib, monkeypatch, n, h, p, normalized, colblk):
+    """Unit-weight graphs take the pattern-only SpMV (no value stream; normalized:
+    gathers of s o x, row sums scaled by s_i).  L x and L^sigma x against the oracle
+    (P:292); the last case also runs column-blocked (3 blocks)."""
+    if colblk:
+        monkeypatch.setenv("SFAIRSC_COLBLK_MB", colblk)
+    g = random_graph(n, h, p=p, seed=n, weights="unit")
+    lib = gpu_lib
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, normalized)
+    ctx = _ctx(lib, g, 1, normalized)
+    assert ctx.info()["unit_weights"] == 1
+    x = np.random.default_rng(n).standard_normal(g.n)
+    tol = 1e-13 * op.sigma * np.abs(x).max()
+    assert np.abs(lib.sfairsc_laplacian(ctx, x) - op.Ln @ x).max() <= tol
+    assert np.abs(lib.sfairsc_apply(ctx, x) - op.apply(x)).max() <= tol
+    ctx.close()
+    gw = random_graph(n, h, p=p, seed=n, weights="uniform")
+    ctx = _ctx(lib, gw, 1, normalized)
+    assert ctx.info()["unit_weights"] == 0
+    ctx.close()
+
+
+@pytest.mark.parametrize("normalized", [False, True])
+def test_unit_pattern_eigs_match_scaled_weights(gpu_lib, normalized):
+    """The same graph as unit weights (pattern-only SpMV) and with every weight 2
+    (value-streaming SpMV): L_n is invariant under W -> 2W, L = D - W doubles
+    (P:123), so the eigenvalues agree (normalized) or double (unnormalized)
+    and the eigenvector subspaces coincide."""
+    g = random_graph(3000, 4, p=0.004, seed=11, weights="unit")
+    lib = gpu_lib
+    k = 6
+    ctx = _ctx(lib, g, k, normalized)
+    assert ctx.info()["unit_weights"] == 1
+    ev1, X1, st1 = lib.sfairsc_eigs(ctx, k, 1e-10)
+    ctx.close()
+    ctx = lib.sfairsc_build_operator(g.row_ptr, g.col, 2.0 * g.val, g.groups.astype(np.int32), k, normalized, h=g.h)
+    assert ctx.info()["unit_weights"] == 0
+    ev2, X2, st2 = lib.sfairsc_eigs(ctx, k, 1e-10)
+    ctx.close()
+    scale = 1.0 if normalized else 2.0
+    assert np.allclose(ev2[1:], scale * ev1[1:], rtol=1e-8, atol=0)
+    assert abs(ev1[0]) <= 1e-10 * st1["sigma"] and abs(ev2[0]) <= 1e-10 * st2["sigma"]
+    assert subspace_sin(X1.T, X2.T) <= 1e-6
+
+
 def test_operator_device_tensors(gpu_lib):
     import torch
     g, _ = baseline_config(1)
@@ -330,12 +377,14 @@ def test_config4_full_size_properties(gpu_lib):
 
 # --- column-blocked SpMV (the config-5 path: gathered vector larger than L2) ------------------
 
+@pytest.mark.parametrize("weights", ["uniform", "unit"])
 @pytest.mark.parametrize("normalized", [False, True])
-def test_column_blocked_spmv_matches_oracle(gpu_lib, normalized, monkeypatch):
+def test_column_blocked_spmv_matches_oracle(gpu_lib, normalized, weights, monkeypatch):
     """Force the block-major CSR (normally chosen for n > ~8M) on a small graph:
-    SpMV, L^sigma and the eigensolve must equal the oracle as for the plain CSR."""
+    SpMV, L^sigma and the eigensolve must equal the oracle as for the plain CSR
+    (unit weights: pattern-only SpMV, the value array dropped after the build)."""
     monkeypatch.setenv("SFAIRSC_COLBLK_MB", "0.003")  # 3 KB column blocks -> several blocks at n ~ 1000
-    g = random_graph(1031, 5, p=0.02, seed=21, weights="uniform")
+    g = random_graph(1031, 5, p=0.02, seed=21, weights=weights)
     op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, normalized)
     ctx = _ctx(gpu_lib, g, 6, normalized)
     monkeypatch.delenv("SFAIRSC_COLBLK_MB")
