@@ -183,6 +183,7 @@ def main():
     ap.add_argument("--ref-applies", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kmeans", action="store_true")
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--apply-only", action="store_true", help="exploration: skip the solves")
     args = ap.parse_args()
@@ -364,6 +365,22 @@ def main():
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(el_t.item()) / args.steps,
                "note": "host-timed (perf_counter) with device synchronised; CSR+groups H2D inside build, X D2H inside eigs"}
 
+    # ---- Alg. 3 step 4 (not part of the metric): k-means on the rows of H, labels left on the device ----
+    kmeans = None
+    if ws == 1 and not args.no_kmeans and not args.apply_only:
+        ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, normalized, h=g.h, cuda_stream=stream.cuda_stream)
+        lib.sfairsc_eigs(ctx, k, tol, evecs=X)
+        lab = torch.empty(n_loc, dtype=torch.int32, device=dev)
+        l0 = lib.launch_count()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, wcss = lib.sfairsc_embed_kmeans(ctx, 1, lab)
+        torch.cuda.synchronize()
+        kmeans = {"s": time.perf_counter() - t0, "wcss": wcss, "gpu_launches": lib.launch_count() - l0,
+                  "note": "sfairsc_embed_kmeans(seed 1) on a fresh solve's eigenvectors: k-means++ + Lloyd "
+                          "(<= 300 iterations) x 10 restarts (reading R16); outside every timed region"}
+        ctx.close()
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g, cfg)
@@ -396,6 +413,7 @@ def main():
             "roofline": roofline,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "kmeans": kmeans,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "spmv_vector": info["spmv_vector"],

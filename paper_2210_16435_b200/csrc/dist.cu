@@ -135,7 +135,7 @@ constexpr int kDT = 256;
 // col -> owner * n_max + (col - cut_owner); flags: out of range / diagonal / unsorted / negative
 __global__ void k_remap_validate(const int* rp, int* ci, const double* vv, int n_loc, long long r0, long long n,
                                  const long long* cuts, int nparts, int n_max, int* flags) {
-  int f = 0;
+  int f = 0, nonunit = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_loc; i += gridDim.x * blockDim.x) {
     const int a = rp[i], b = rp[i + 1];
     if (b < a) {
@@ -148,6 +148,7 @@ __global__ void k_remap_validate(const int* rp, int* ci, const double* vv, int n
       if (j < 0 || j >= n || j <= prev) f |= 1;
       if (j == r0 + i && vv[e] != 0.0) f |= 1;
       if (!(vv[e] >= 0.0)) f |= 2;
+      if (vv[e] != 1.0 || j == r0 + i) nonunit = 1;
       prev = j;
       int lo = 0, hi = nparts - 1;  // owner: cuts[o] <= j < cuts[o+1]
       while (lo < hi) {
@@ -158,6 +159,7 @@ __global__ void k_remap_validate(const int* rp, int* ci, const double* vv, int n
     }
   }
   if (f) atomicOr(flags, f);
+  if (nonunit) atomicOr(flags + 1, 1);  // local, informational: this part's rows are not a unit-weight pattern
 }
 
 __global__ void k_degrees_d(const int* rp, const double* vv, int n_loc, double* d, int* flags) {
@@ -261,6 +263,7 @@ struct DistPart {
   int nblk = 1, vs_blk = 2;
   int* rpb = nullptr;
   bool skewed = false;  // heavy-tailed local degrees: long rows get a whole warp in the SpMV
+  bool unit = false;    // unnormalized unit-weight rows: the pattern-only SpMV (GraphDev::unit)
   double *vr = nullptr, *vy = nullptr, *vt = nullptr;  // v~ (lagged), w, t
   double *V = nullptr, *Vb = nullptr, *X = nullptr;
   double *partials = nullptr, *partials2 = nullptr;
@@ -279,6 +282,7 @@ struct DistPart {
     G.grp = grp;
     G.normalized = normalized;
     G.skewed = skewed;
+    G.unit = unit && !normalized;
     return G;
   }
   double* bs_t() const { return small; }
@@ -568,10 +572,13 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
     const size_t pc = std::max<size_t>((size_t)p.spmv_grid * 4 * kBT, (size_t)c->num_sms * 8 * (kMaxJ + 2));
     CU(dal(&p.partials, pc));
     CU(dal(&p.partials2, (size_t)c->num_sms * 8 * (kHB + 2)));
-    int f = 0;
-    CU(cudaMemcpyAsync(&f, p.flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    int f2[2] = {0, 0};
+    CU(cudaMemcpyAsync(f2, p.flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    hflags |= f;
+    hflags |= f2[0];
+    // unit weights (unnormalized): each part decides for its own rows; the gathered p~ is used as is
+    p.unit = !c->normalized && p.nnz_loc > 0 && f2[1] == 0 &&
+             !(getenv("SFAIRSC_UNIT") && atoi(getenv("SFAIRSC_UNIT")) == 0);
   }
   // flags: OR over all parts (max over ranks)
   {
