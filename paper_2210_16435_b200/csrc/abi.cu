@@ -510,12 +510,6 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   // unit-weight pattern (every stored w_ij = 1): the single-vector SpMV needs no value stream
   // (env SFAIRSC_UNIT=0 keeps the value-streaming kernel, for A/B measurements)
   c->unit = nnz > 0 && !(hflags & 32) && !(getenv("SFAIRSC_UNIT") && atoi(getenv("SFAIRSC_UNIT")) == 0);
-  if (c->unit && c->normalized) {
-    CUB(dalloc(&c->vq, c->ldv));
-    CUB(dalloc(&c->vq_lz, c->ldv));
-    CUB(cudaMemsetAsync(c->vq, 0, sizeof(double) * c->ldv, c->st));
-    CUB(cudaMemsetAsync(c->vq_lz, 0, sizeof(double) * c->ldv, c->st));
-  }
   // A1: degrees d = W 1
   launch_degrees(c->g(), c->dg, c->flags, c->st);
   CUB(cudaMemcpyAsync(&hflags, c->flags, sizeof(int), cudaMemcpyDeviceToHost, c->st));
@@ -596,6 +590,14 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
       while (vsb < 32 && vsb * 4 < mdb) vsb *= 2;
       c->vs_blk = vsb;
     }
+  }
+  // normalized pattern-only SpMV: its gathered vector s o p (vq_lz: the lagged solver's, written by its
+  // normalisation kernel)
+  if (c->unit_spmv() && c->normalized) {
+    CUB(dalloc(&c->vq, c->ldv));
+    CUB(dalloc(&c->vq_lz, c->ldv));
+    CUB(cudaMemsetAsync(c->vq, 0, sizeof(double) * c->ldv, c->st));
+    CUB(cudaMemsetAsync(c->vq_lz, 0, sizeof(double) * c->ldv, c->st));
   }
   // A3: factored basis of range(C): beta_s = sum_{V_s} s_i^2, u_s = |V_s| beta_s^{-1/2}
   c->sgrid = sweep_grid(n, c->num_sms);

@@ -155,7 +155,10 @@ struct sfairsc_ctx {
     G.unit = unit_spmv();
     return G;
   }
-  bool unit_spmv() const { return unit && !Qr; }  // the dense-projector SpMV keeps its value-streaming kernel
+  // the dense-projector SpMV keeps its value-streaming kernel; normalized graphs take the pattern-only kernel only
+  // when column-blocked: unblocked, the gathers alone bound the SpMV and the extra s o p pass costs what the
+  // smaller stream saves (config 4: 720 vs 722 us SpMV, +5 us normalisation)
+  bool unit_spmv() const { return unit && !Qr && (!normalized || nblk > 1); }
   ProjDesc pd() const {
     ProjDesc P{Qr ? qr : h, isb, uh};
     P.Q = Qr;

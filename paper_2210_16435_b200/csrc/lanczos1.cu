@@ -488,6 +488,135 @@ __global__ void __launch_bounds__(kThreads, 1) k_lz_update_r(GraphDev g, ProjDes
 }
 
 // ---------------------------------------------------------------------------
+// The single sweep with 64-row chunks and row PAIRS held in registers: thread
+// (p, cg) = (lane, warp) owns rows 2p, 2p+1 of the chunk and columns cg + 8q.
+// Its basis values are read from shared memory once (16-byte loads) and serve
+// both the row combinations (phase 1, with {cs_l, cg_l} as one 16-byte broadcast)
+// and the dots (phase 3); the dots stay per thread until one warp sum at the end.
+// Same stage layout and TMA ring as k_lz_update.
+// ---------------------------------------------------------------------------
+template <int MAXQ, bool NORM>
+__global__ void __launch_bounds__(kThreads, 1) k_lz_update_p(GraphDev g, ProjDesc pd, LzSweepArgs a, int kStages,
+                                                              const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) double dsm[];
+  __shared__ __align__(8) unsigned long long bars[kMaxStages];
+  __shared__ __align__(16) double2 csg[kLMaxJ + 1];
+  __shared__ __align__(16) double red[2][8][kR];
+  __shared__ __align__(16) double rw[kR], rv[kR];
+  __shared__ double gam[kHB];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int pr = lane, cgp = w;  // row pair (2 pr, 2 pr + 1), column group (columns cgp + 8 q)
+  const int n = g.n, J = a.J;
+  const int nchunks = (n + kR - 1) / kR;
+  const size_t stage_elems = lz_stage_doubles(J);
+  for (int l = tid; l < J; l += kThreads) csg[l] = make_double2(a.cs[l], a.cg[l]);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    double gw[kHB];
+    gamma_serial(a.bs_t, 1.0, pd, gam);
+    gamma_serial(a.bs_v, 1.0, pd, gw);
+    for (int s = 0; s < pd.h; ++s) gam[s] -= a.sigma * gw[s];
+  }
+  __syncthreads();
+  const double ay = a.lz[LZ_AY], av = a.lz[LZ_AV], invmu = a.lz[LZ_INVMU];
+  const int my_chunks = (nchunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  if (w == 0)
+    for (int it = 0; it < kStages && it < my_chunks; ++it)
+      lz_issue<false>(a, g, &tmap, blockIdx.x + it * gridDim.x, dsm + it * stage_elems, &bars[it], lane);
+
+  double colacc[MAXQ];
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) colacc[q] = 0.0;
+  double accJ = 0.0;  // dots with the new column v_j (column J, group J % 8)
+  double v2[1 + kHB];
+#pragma unroll
+  for (int q = 0; q < 1 + kHB; ++q) v2[q] = 0.0;
+
+  for (int it = 0; it < my_chunks; ++it) {
+    const int c = blockIdx.x + it * gridDim.x;
+    const int st = it % kStages;
+    const double* buf = dsm + st * stage_elems;
+    mbar_wait(&bars[st], (unsigned)((it / kStages) & 1));
+    const double* vts = buf + (size_t)J * kR;
+    const double* ts = vts + kR;
+    const double* ssc = ts + kR;
+    const uint8_t* gs = reinterpret_cast<const uint8_t*>(ssc + kR);
+    const long long row0 = (long long)c * kR;
+    double2 vreg[MAXQ];
+    double ps[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, pg[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [q parity][row]
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+      const int l = cgp + 8 * q;
+      if (l < J) {
+        vreg[q] = *reinterpret_cast<const double2*>(buf + (size_t)l * kR + 2 * pr);
+        const double2 cc = csg[l];
+        ps[q & 1][0] = fma(vreg[q].x, cc.x, ps[q & 1][0]);
+        ps[q & 1][1] = fma(vreg[q].y, cc.x, ps[q & 1][1]);
+        pg[q & 1][0] = fma(vreg[q].x, cc.y, pg[q & 1][0]);
+        pg[q & 1][1] = fma(vreg[q].y, cc.y, pg[q & 1][1]);
+      } else {
+        vreg[q] = make_double2(0.0, 0.0);
+      }
+    }
+    *reinterpret_cast<double2*>(&red[0][cgp][2 * pr]) = make_double2(ps[0][0] + ps[1][0], ps[0][1] + ps[1][1]);
+    *reinterpret_cast<double2*>(&red[1][cgp][2 * pr]) = make_double2(pg[0][0] + pg[1][0], pg[0][1] + pg[1][1]);
+    __syncthreads();
+    if (tid < kR) {
+      const long long gi = row0 + tid;
+      double wv = 0.0, vj = 0.0;
+      if (gi < n) {
+        double sumS = 0.0, sumG = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          sumS += red[0][q][tid];
+          sumG += red[1][q][tid];
+        }
+        const double vti = vts[tid];
+        vj = fma(vti, invmu, -sumS);
+        const int gg = gs[tid];
+        const double y = NORM ? fma(-ssc[tid], gam[gg], ts[tid]) : ts[tid] - gam[gg];
+        wv = fma(ay, y, fma(av, vti, -sumG));
+        a.vj_out[gi] = vj;
+        a.w_out[gi] = wv;
+        v2[0] = fma(wv, wv, v2[0]);
+        const double sv = NORM ? ssc[tid] * wv : wv;
+#pragma unroll
+        for (int q = 0; q < kHB; ++q)
+          if (q == gg) v2[1 + q] += sv;
+      }
+      rw[tid] = wv;
+      rv[tid] = vj;
+    }
+    __syncthreads();
+    const double2 wp = *reinterpret_cast<const double2*>(&rw[2 * pr]);
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) colacc[q] = fma(vreg[q].y, wp.y, fma(vreg[q].x, wp.x, colacc[q]));
+    if (cgp == (J & 7)) {
+      const double2 vp = *reinterpret_cast<const double2*>(&rv[2 * pr]);
+      accJ = fma(vp.y, wp.y, fma(vp.x, wp.x, accJ));
+    }
+    __syncthreads();  // stage `st` and rw/rv consumed
+    if (w == 0 && it + kStages < my_chunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      lz_issue<false>(a, g, &tmap, blockIdx.x + (it + kStages) * gridDim.x, dsm + st * stage_elems, &bars[st], lane);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) {
+    const int l = cgp + 8 * q;
+    const double sdot = warp_sum(colacc[q]);
+    if (lane == 0 && l < J) a.partials[(size_t)blockIdx.x * (J + 1) + l] = sdot;
+  }
+  {
+    const double sdot = warp_sum(accJ);
+    if (lane == 0 && cgp == (J & 7)) a.partials[(size_t)blockIdx.x * (J + 1) + J] = sdot;
+  }
+  block_reduce_store<1 + kHB>(v2, a.partials2 + (size_t)blockIdx.x * (1 + kHB));
+  ticket_finalize<1 + kHB>(a.partials2, a.counter, a.nb, 1 + min(pd.h, kHB));
+}
+
+// ---------------------------------------------------------------------------
 // normalise: v~ = w/|w|, p~ = P v~, B^T v~, s = dots/|w|, |p~|^2, H row j+1
 // ---------------------------------------------------------------------------
 template <bool NORM, bool DQ = false>
@@ -582,7 +711,25 @@ static void lz_update_r_launch(const GraphDev& g, const ProjDesc& pd, const LzSw
   if (a.J > 0) encode_colmajor_map(a.V, a.ld, a.J, kR2, &tmap);
   k_lz_update_r<MAXQ, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap);
 }
-int g_lz_sweep = 0;  // 0: 64-row smem kernel, 256 threads (default, measured fastest); 2: same with 512 threads; 1: register-held rows, 32-row chunks (env SFAIRSC_LZ_SWEEP)
+template <int MAXQ, bool NORM>
+static void lz_update_p_launch(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid,
+                               cudaStream_t st) {
+  const size_t stage = lz_stage_doubles(a.J) * sizeof(double);
+  const int stages = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, kRingBytes / stage));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_lz_update_p<MAXQ, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(kRingBytes, 2 * lz_stage_doubles(kLMaxJ) * sizeof(double)));
+    attr = true;
+  }
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  if (a.J > 0) encode_colmajor_map(a.V, a.ld, a.J, kR, &tmap);
+  k_lz_update_p<MAXQ, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap);
+}
+// 3: 64-row chunks, register-held row pairs (default: config 4 sweep 768 -> 612 us); 0: 64-row smem kernel,
+// 256 threads; 2: the same with 512 threads; 1: register-held rows, 32-row chunks (env SFAIRSC_LZ_SWEEP)
+int g_lz_sweep = 3;
 template <bool NORM>
 static void lz_update_m(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st) {
   if (g_lz_sweep == 1) {
@@ -590,6 +737,12 @@ static void lz_update_m(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs
     if (a.J <= 64) lz_update_r_launch<8, NORM>(g, pd, a, G, st);
     else if (a.J <= 128) lz_update_r_launch<16, NORM>(g, pd, a, G, st);
     else lz_update_r_launch<24, NORM>(g, pd, a, G, st);
+    return;
+  }
+  if (g_lz_sweep == 3 && !g.Q) {
+    if (a.J <= 64) lz_update_p_launch<8, NORM>(g, pd, a, grid, st);
+    else if (a.J <= 128) lz_update_p_launch<16, NORM>(g, pd, a, grid, st);
+    else lz_update_p_launch<24, NORM>(g, pd, a, grid, st);
     return;
   }
   if (g_lz_sweep == 2) {  // 512 threads: 16 warps, 8 column groups

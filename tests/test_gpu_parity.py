@@ -64,11 +64,12 @@ def test_operator_pieces_match_oracle(gpu_lib, idx):
 
 
 @pytest.mark.parametrize("n,h,p,normalized,colblk", [(37, 2, 0.3, False, None), (1031, 5, 0.01, True, None),
-                                                     (2000, 20, 0.01, False, None), (3001, 3, 0.004, True, "0.01")])
+                                                     (2000, 20, 0.01, False, None), (3001, 3, 0.004, True, "0.01"),
+                                                     (2500, 4, 0.006, False, "0.01")])
 def test_unit_weight_spmv_matches_oracle(gpu_lib, monkeypatch, n, h, p, normalized, colblk):
-    """Unit-weight graphs take the pattern-only SpMV (no value stream; normalized:
-    gathers of s o x, row sums scaled by s_i).  L x and L^sigma x against the oracle
-    (P:292); the last case also runs column-blocked (3 blocks)."""
+    """Unit-weight graphs take the pattern-only SpMV (no value stream; normalized, when
+    column-blocked: gathers of s o x, row sums scaled by s_i).  L x and L^sigma x
+    against the oracle; the last two cases run column-blocked."""
     if colblk:
         monkeypatch.setenv("SFAIRSC_COLBLK_MB", colblk)
     g = random_graph(n, h, p=p, seed=n, weights="unit")
