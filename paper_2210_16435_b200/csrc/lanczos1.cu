@@ -53,19 +53,22 @@ constexpr int kLMaxJ = 191;  // basis columns swept (+1 new column in the dots: 
 // ---------------------------------------------------------------------------
 // coefficient step (one CTA)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_lz_coef(LzDev d, int j) {
-  __shared__ double ss[kLMaxJ + 1], bt[kLMaxJ + 1], u[kLMaxJ + 1], v[kLMaxJ + 1], red[kThreads / 32][3];
+// one CTA of kCoefT threads (the O(m^2) work is latency-bound: more threads, shorter chains)
+constexpr int kCoefT = 1024;
+__global__ void __launch_bounds__(kCoefT) k_lz_coef(LzDev d, int j) {
+  __shared__ double ss[kLMaxJ + 1], bt[kLMaxJ + 1], u[kLMaxJ + 1], v[kLMaxJ + 1], red[kCoefT / 32][3];
+  __shared__ double upart[4][kLMaxJ + 1];
   __shared__ double sh_mu, sh_alpha, sh_kappa;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int ld = d.ldH;
-  for (int l = tid; l < j; l += kThreads) {
+  for (int l = tid; l < j; l += kCoefT) {
     ss[l] = d.s[l];
     bt[l] = d.H[(size_t)l * ld + j];  // row j: b~
   }
   __syncthreads();
   // |s|^2, b~ . s
   double a0 = 0.0, a1 = 0.0;
-  for (int l = tid; l < j; l += kThreads) {
+  for (int l = tid; l < j; l += kCoefT) {
     a0 = fma(ss[l], ss[l], a0);
     a1 = fma(bt[l], ss[l], a1);
   }
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_coef(LzDev d, int j) {
   __syncthreads();
   if (tid == 0) {
     double s2 = 0.0, bs = 0.0;
-    for (int q = 0; q < kThreads / 32; ++q) {
+    for (int q = 0; q < kCoefT / 32; ++q) {
       s2 += red[q][0];
       bs += red[q][1];
     }
@@ -98,26 +101,32 @@ __global__ void __launch_bounds__(kThreads) k_lz_coef(LzDev d, int j) {
   // H[:j,:j] += s b~^T ; H[j,:j] = mu b~   (column c of H gets s * b~_c)
   for (int c = 0; c < j; ++c)  // only the columns with b~_c != 0 (normally just c = j-1)
     if (bt[c] != 0.0)
-      for (int r = tid; r < j; r += kThreads) d.H[(size_t)c * ld + r] = fma(ss[r], bt[c], d.H[(size_t)c * ld + r]);
+      for (int r = tid; r < j; r += kCoefT) d.H[(size_t)c * ld + r] = fma(ss[r], bt[c], d.H[(size_t)c * ld + r]);
   __syncthreads();
-  for (int l = tid; l < j; l += kThreads) d.H[(size_t)l * ld + j] = mu * bt[l];
+  for (int l = tid; l < j; l += kCoefT) d.H[(size_t)l * ld + j] = mu * bt[l];
   // u = H_j s (thread per row, coalesced over columns), v = H_j^T s (warp per column, coalesced down it)
-  for (int l = tid; l < j; l += kThreads) {
-    double au = 0.0;
-    for (int i = 0; i < j; ++i) au = fma(d.H[(size_t)i * ld + l], ss[i], au);
-    u[l] = au;
+  {  // u: 4 partial sums per row over quarters of the columns, combined in order below
+    const int l = tid & 255, qt = tid >> 8;
+    if (l < j) {
+      const int i0 = j * qt / 4, i1 = j * (qt + 1) / 4;
+      double au = 0.0;
+      for (int i = i0; i < i1; ++i) au = fma(d.H[(size_t)i * ld + l], ss[i], au);
+      upart[qt][l] = au;
+    }
   }
-  for (int l = w; l < j; l += kThreads / 32) {
+  for (int l = w; l < j; l += kCoefT / 32) {
     double av = 0.0;
     for (int i = lane; i < j; i += 32) av = fma(d.H[(size_t)l * ld + i], ss[i], av);
     av = warp_sum(av);
     if (lane == 0) v[l] = av;
   }
   __syncthreads();
+  for (int l = tid; l < j; l += kCoefT) u[l] = ((upart[0][l] + upart[1][l]) + upart[2][l]) + upart[3][l];
+  __syncthreads();
   // z = v + mu^2 b~ ; zeta = p~^T t + sigma (omega - |p~|^2)
   a0 = 0.0;
   a1 = 0.0;
-  for (int l = tid; l < j; l += kThreads) {
+  for (int l = tid; l < j; l += kCoefT) {
     const double z = fma(mu * mu, bt[l], v[l]);
     a0 = fma(ss[l], z, a0);      // s.z
     a1 = fma(ss[l], u[l], a1);   // s.H s
@@ -132,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_coef(LzDev d, int j) {
   __syncthreads();
   if (tid == 0) {
     double sz = 0.0, shs = 0.0;
-    for (int q = 0; q < kThreads / 32; ++q) {
+    for (int q = 0; q < kCoefT / 32; ++q) {
       sz += red[q][0];
       shs += red[q][1];
     }
@@ -150,7 +159,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_coef(LzDev d, int j) {
   }
   __syncthreads();
   const double kappa = sh_kappa;
-  for (int l = tid; l < j; l += kThreads) {
+  for (int l = tid; l < j; l += kCoefT) {
     const double z = fma(mu * mu, bt[l], v[l]);
     const double c = (z - u[l]) / mu;
     d.H[(size_t)j * ld + l] = c;                  // column j: c
@@ -764,7 +773,7 @@ static void lz_update_m(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs
 
 void launch_lz_coef(const LzDev& d, int j, cudaStream_t st) {
   bump_launch();
-  k_lz_coef<<<1, kThreads, 0, st>>>(d, j);
+  k_lz_coef<<<1, kCoefT, 0, st>>>(d, j);
 }
 void launch_lz_update(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st) {
   bump_launch();
@@ -827,7 +836,7 @@ struct Lagged {
     {
       ProfScope ps(c, K_OTHER, 0.0);
       bump_launch();
-      k_lz_coef<<<1, kThreads, 0, c->st>>>(dev(j), j);
+      k_lz_coef<<<1, kCoefT, 0, c->st>>>(dev(j), j);
     }
     {
       ProfScope ps(c, K_UPDDOT, (j + 4) * c->vb() + c->sgb());
