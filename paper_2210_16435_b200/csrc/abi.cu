@@ -604,7 +604,9 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   // SpMV partition: CTA b owns rows with cumulative (nnz + 4 rows) weight in [b, b+1)/G
   {
     const long long total = (long long)nnz + 4LL * n;
-    int G = std::max(1, std::min(c->num_sms * 8, (n + 31) / 32));
+    // CTAs per SM of the SpMV grid (env SFAIRSC_SPMV_CPS for A/B: 8 default)
+    const int cps = getenv("SFAIRSC_SPMV_CPS") ? std::max(1, atoi(getenv("SFAIRSC_SPMV_CPS"))) : 8;
+    int G = std::max(1, std::min(c->num_sms * cps, (n + 31) / 32));
     std::vector<int32_t> split(G + 1);
     split[0] = 0;
     split[G] = n;
