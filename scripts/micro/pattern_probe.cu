@@ -148,6 +148,51 @@ __global__ void __launch_bounds__(256) spmv_v(int n, const int* __restrict__ rp,
     if (lane == 0) Y[row] = acc;
   }
 }
+
+// variant V2: values streamed, each VS-lane group handles two rows per iteration (2U gathers in flight)
+template <int VS, int U>
+__global__ void __launch_bounds__(256) spmv_v2(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                               const double* __restrict__ vv, const double* __restrict__ X,
+                                               double* __restrict__ Y) {
+  const int lane = threadIdx.x % VS;
+  const int g0 = (blockIdx.x * 256 + threadIdx.x) / VS;
+  const int ng = gridDim.x * 256 / VS;
+  for (int row = g0; row < n; row += 2 * ng) {
+    const int rowb = row + ng;
+    double acc = 0.0, accb = 0.0;
+    const int a = __ldg(rp + row), e1 = __ldg(rp + row + 1);
+    const int ab = rowb < n ? __ldg(rp + rowb) : 0, e1b = rowb < n ? __ldg(rp + rowb + 1) : 0;
+    int e0 = a + lane, f0 = ab + lane;
+    while (e0 < e1 || f0 < e1b) {
+      int c[U], cb[U];
+      double w[U], wb[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const bool ok = e0 + q * VS < e1, okb = f0 + q * VS < e1b;
+        c[q] = ok ? ld_s(ci + e0 + q * VS) : 0;
+        w[q] = ok ? ld_s(vv + e0 + q * VS) : 0.0;
+        cb[q] = okb ? ld_s(ci + f0 + q * VS) : 0;
+        wb[q] = okb ? ld_s(vv + f0 + q * VS) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        acc = fma(w[q], __ldg(X + c[q]), acc);
+        accb = fma(wb[q], __ldg(X + cb[q]), accb);
+      }
+      e0 += U * VS;
+      f0 += U * VS;
+    }
+#pragma unroll
+    for (int o = VS / 2; o > 0; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      accb += __shfl_xor_sync(0xffffffffu, accb, o);
+    }
+    if (lane == 0) {
+      Y[row] = acc;
+      if (rowb < n) Y[rowb] = accb;
+    }
+  }
+}
 int main() {
   const int n = 4000000, deg = 32;
   const long long nnz = (long long)n * deg;
@@ -199,6 +244,9 @@ int main() {
     const int grid = sms * gm;
     printf("grid = %d x SMs\n", gm);
     run("values  VS=8 U=4", true, [&] { spmv_v<8, 4><<<grid, 256>>>(n, rp, ci, vv, X, Y); });
+    run("values2 VS=8 U=4 (2 rows/group)", true, [&] { spmv_v2<8, 4><<<grid, 256>>>(n, rp, ci, vv, X, Y); });
+    run("values2 VS=4 U=4 (2 rows/group)", true, [&] { spmv_v2<4, 4><<<grid, 256>>>(n, rp, ci, vv, X, Y); });
+    run("values  VS=8 U=8", true, [&] { spmv_v<8, 8><<<grid, 256>>>(n, rp, ci, vv, X, Y); });
     run("pattern VS=8 U=4", false, [&] { spmv_p<8, 4><<<grid, 256>>>(n, rp, ci, X, Y); });
     run("pattern VS=8 U=2", false, [&] { spmv_p<8, 2><<<grid, 256>>>(n, rp, ci, X, Y); });
     run("pattern VS=4 U=4", false, [&] { spmv_p<4, 4><<<grid, 256>>>(n, rp, ci, X, Y); });
