@@ -428,8 +428,9 @@ __global__ void __launch_bounds__(kThreads) k_ritz_dmma(const double* __restrict
 
 // ---------------------------------------------------------------------------
 // Ritz GEMM v2 (default): Vout = V Y on the fp64 tensor cores (DMMA
-// m8n8k4), CTA tile 128 rows x 128 columns so V is streamed once for p <= 128,
-// 8 warps as 4 (rows) x 2 (cols), each 32 x 64 = 4 x 8 DMMA tiles.  The V
+// m8n8k4), CTA tile 128 rows x GN columns (GN = 64 / 96 / 128: the smallest
+// that covers p, so V is streamed once for p <= 128 with little padding), 8 warps
+// as 4 (rows) x 2 (cols), each 32 x GN/2 = 4 x GN/16 DMMA tiles.  The V
 // tile (16 columns x 128 rows) arrives by cp.async into a double-buffered
 // shared-memory ring; the Y tile (column-major m x p, 16 k x 128 cols) is
 // register-staged and stored transposed.  Shared-memory row stride 136
@@ -442,14 +443,16 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_b
                : "memory");
 }
 
+template <int GN>  // CTA tile columns: 64, 96 or 128 (the smallest that covers p, else 128)
 __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __restrict__ V, long long ld, int n, int m,
                                                             const double* __restrict__ Y, int p,
                                                             double* __restrict__ Vout) {
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                      // [2][kGK][kGS]
   double* Bs = gsm + 2 * kGK * kGS;      // [2][kGK][kGS]
-  const int ncol = (p + kGN - 1) / kGN;
-  const int col0 = (int)(blockIdx.x % ncol) * kGN;
+  constexpr int NBT = GN / 16;  // 8-column DMMA tiles per warp (2 warp columns)
+  const int ncol = (p + GN - 1) / GN;
+  const int col0 = (int)(blockIdx.x % ncol) * GN;
   const long long row0 = (long long)(blockIdx.x / ncol) * kGM;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wr = w & 3, wc = w >> 2;
@@ -475,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __rest
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int l = k0 + bk0 + q;
-      breg[q] = (c < p && l < m) ? __ldg(Y + (size_t)c * m + l) : 0.0;
+      breg[q] = (bcol < GN && c < p && l < m) ? __ldg(Y + (size_t)c * m + l) : 0.0;
     }
   };
   auto store_b = [&](int buf) {
@@ -483,11 +486,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __rest
 #pragma unroll
     for (int q = 0; q < 8; ++q) dst[(bk0 + q) * kGS + bcol] = breg[q];
   };
-  double acc[4][8][2];
+  double acc[4][NBT][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < NBT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   load_a(0, 0);
   load_b(0);
@@ -506,15 +509,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __rest
     const double* B = Bs + buf * kGK * kGS;
 #pragma unroll
     for (int ks = 0; ks < kGK; ks += 4) {
-      double af[4], bf[8];
+      double af[4], bf[NBT];
 #pragma unroll
       for (int a = 0; a < 4; ++a) af[a] = A[(ks + tq) * kGS + wr * 32 + a * 8 + gq];
 #pragma unroll
-      for (int b = 0; b < 8; ++b) bf[b] = B[(ks + tq) * kGS + wc * 64 + b * 8 + gq];
+      for (int b = 0; b < NBT; ++b) bf[b] = B[(ks + tq) * kGS + wc * (GN / 2) + b * 8 + gq];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 8; ++b)
+        for (int b = 0; b < NBT; ++b)
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                        : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
                        : "d"(af[a]), "d"(bf[b]));
@@ -527,10 +530,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __rest
     const long long i = row0 + wr * 32 + a * 8 + gq;
     if (i >= n) continue;
 #pragma unroll
-    for (int b = 0; b < 8; ++b)
+    for (int b = 0; b < NBT; ++b)
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const int col = col0 + wc * 64 + b * 8 + 2 * tq + q;
+        const int col = col0 + wc * (GN / 2) + b * 8 + 2 * tq + q;
         if (col < p) Vout[(long long)col * ld + i] = acc[a][b][q];
       }
   }
@@ -658,14 +661,18 @@ void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y
   if (p <= 0 || n <= 0) return;
   bump_launch();
   if (g_ritz_kind == 2 && ld % 2 == 0 && ld >= (long long)((n + kGM - 1) / kGM) * kGM) {
-    static bool attr = false;
     const int smem = 4 * kGK * kGS * (int)sizeof(double);
+    static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_ritz_dmma2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_ritz_dmma2<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_ritz_dmma2<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_ritz_dmma2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
-    const long long grid = (long long)((p + kGN - 1) / kGN) * ((n + kGM - 1) / kGM);
-    k_ritz_dmma2<<<grid, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
+    const long long rows = (n + kGM - 1) / kGM;
+    if (p <= 64) k_ritz_dmma2<64><<<rows, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
+    else if (p <= 96) k_ritz_dmma2<96><<<rows, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
+    else k_ritz_dmma2<128><<<rows * ((p + kGN - 1) / kGN), kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
     return;
   }
   if (g_ritz_kind == 1) {
