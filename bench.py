@@ -39,6 +39,14 @@ sys.path.insert(0, ROOT)
 
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
 
+METRIC = "projected-operator applies/s (L^sigma inside the full s-FairSC eigensolve); time-to-k-eigvecs = ms_per_step"
+
+
+def workload(args, g, normalized, k, tol):
+    """The workload string both arms print (same config, same metric)."""
+    return (f"BASELINE config {args.config}" + (" (reduced n)" if args.n else "")
+            + f": normalized={normalized} m-SBM n={g.n}, nnz={g.nnz}, h={g.h}, k={k}, tol={tol}")
+
 
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -157,12 +165,11 @@ def run_reference(args):
     cpu = time.process_time() - c0
     value = args.steps * per_step / wall
     cores = max(1, round(cpu / wall))
-    line = {"metric": "projected-operator applies/s (L^sigma, s-FairSC)", "value": value, "unit": "applies/s",
+    line = {"metric": METRIC, "value": value, "unit": "applies/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"BASELINE config {args.config}: m-SBM n={g.n}, h={g.h}, k={cfg['k_eig']}, "
-                                   f"normalized={cfg['normalized']}, nnz={g.nnz}",
+            "config": {"workload": workload(args, g, cfg["normalized"], cfg["k_eig"], cfg["tol"]),
                        "step": f"{per_step} oracle applies (the full ARPACK solve does not finish in minutes at this size)"},
             "cpu_baseline": {"value": value, "unit": "applies/s", "cores": cores, "kind": "oracle",
                              "sample": f"{args.steps}x{per_step} Tier-S applies, scipy, n={g.n}"},
@@ -391,13 +398,12 @@ def main():
     elif rank == 0:
         last = stats[-1]
         line = {
-            "metric": "projected-operator applies/s (L^sigma inside the full s-FairSC eigensolve); time-to-k-eigvecs = ms_per_step",
+            "metric": METRIC,
             "value": value, "unit": "applies/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / max(1, args.steps), "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE config {args.config}" + (" (reduced n)" if args.n else "")
-                                   + f": normalized={normalized} m-SBM n={g.n}, nnz={g.nnz}, h={g.h}, k={k}, tol={tol}",
+            "config": {"workload": workload(args, g, normalized, k, tol),
                        "step": "build operator from device CSR (A0-A3) + thick-restart Lanczos to k eigenpairs (A4-A11)",
                        "l2": f"inputs larger than L2 (CSR {(12 * g.nnz + 4 * g.n) / 1e9:.2f} GB, Krylov basis "
                              f"{8 * g.n * (last['basis_size'] + 1) / 1e9:.2f} GB >> 126 MB)",
