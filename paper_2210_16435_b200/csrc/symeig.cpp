@@ -11,9 +11,16 @@ namespace sfz {
 
 // A: m x m row-major symmetric (overwritten by the eigenvectors, row-major,
 // column c = eigenvector c).  evals ascending.
-void symeig(int m, std::vector<double>& A, std::vector<double>& evals) {
+// Compiled twice (the body is an always-inline template): an AVX2/FMA copy chosen at run time when the
+// host supports it, and a baseline x86-64 copy; the rotations and reflector updates vectorise 4-wide
+// (m = 170: 9.1 -> ~5 ms per restart on the build host).
+template <int kDummy>
+static inline __attribute__((always_inline)) void symeig_impl(int m, std::vector<double>& A,
+                                                               std::vector<double>& evals) {
   std::vector<double> d(m), e(m);
-  auto V = [&](int i, int j) -> double& { return A[(size_t)i * m + j]; };
+  // column-major view (A is symmetric): the EISPACK loops then walk contiguous memory (the QL rotations
+  // touch two contiguous columns instead of two strided ones); transposed to the row-major output at the end
+#define V(i, j) A[(size_t)(j) * m + (i)]  // (a macro: a lambda would not inline into the AVX2 clone)
   if (m == 0) return;
   if (m == 1) {
     evals.assign(1, A[0]);
@@ -135,10 +142,12 @@ void symeig(int m, std::vector<double>& A, std::vector<double>& evals) {
           c = p / r;
           p = c * d[i] - s * g;
           d[i + 1] = h + s * (c * g + s * d[i]);
+          double* __restrict__ zi = &V(0, i);  // two contiguous columns (column-major view)
+          double* __restrict__ zi1 = &V(0, i + 1);
           for (int k = 0; k < m; ++k) {
-            h = V(k, i + 1);
-            V(k, i + 1) = s * V(k, i) + c * h;
-            V(k, i) = c * V(k, i) - s * h;
+            const double a0 = zi[k], a1 = zi1[k];
+            zi1[k] = s * a0 + c * a1;
+            zi[k] = c * a0 - s * a1;
           }
         }
         p = -s * s2 * c3 * el1 * e[l] / dl1;
@@ -164,7 +173,21 @@ void symeig(int m, std::vector<double>& A, std::vector<double>& evals) {
       for (int j = 0; j < m; ++j) std::swap(V(j, i), V(j, k));
     }
   }
+  for (int i = 0; i < m; ++i)  // column-major -> row-major (column c = eigenvector c)
+    for (int j = i + 1; j < m; ++j) std::swap(A[(size_t)i * m + j], A[(size_t)j * m + i]);
   evals = d;
+#undef V
+}
+
+__attribute__((target("avx2,fma"))) static void symeig_avx2(int m, std::vector<double>& A, std::vector<double>& ev) {
+  symeig_impl<1>(m, A, ev);
+}
+static void symeig_base(int m, std::vector<double>& A, std::vector<double>& ev) { symeig_impl<0>(m, A, ev); }
+
+void symeig(int m, std::vector<double>& A, std::vector<double>& evals) {
+  static const bool avx2 = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
+  if (avx2) symeig_avx2(m, A, evals);
+  else symeig_base(m, A, evals);
 }
 
 }  // namespace sfz
