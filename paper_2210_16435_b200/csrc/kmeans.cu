@@ -11,6 +11,7 @@
 #include "device_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <vector>
@@ -33,6 +34,7 @@ void bump_launch();
 namespace {
 
 constexpr int kBlk = 1024;     // D2 prefix blocks
+int g_km_mma = 1;              // 1: tensor-core assignment with the exact guard; 0: direct (env SFAIRSC_KM_MMA)
 constexpr int kMaxDim = 64;    // k <= 64 handled in registers
 constexpr int kKmStream = 8;   // Philox stream of the k-means draws
 
@@ -234,6 +236,162 @@ __global__ void __launch_bounds__(kAsgWarps * 32) k_assign(const double* X, long
   if (changes) {
     ch = __reduce_add_sync(0xffffffffu, ch);
     if (lane == 0 && ch) atomicAdd(changes, ch);  // integer: order-independent
+  }
+}
+
+// Assignment on the fp64 tensor cores with an exact guard.  D~(i,c) = |h_i|^2 - 2 h_i.mu_c + |mu_c|^2
+// from a DMMA (mma.sync m8n8k4 f64) product of a 128-row tile of H with M^T; |D~ - D| <= E_i with
+// E_i = 4 (2 dim + 7) 2^-53 (|h_i| + max_c |mu_c|)^2 bounding the rounding of both D~ and the direct
+// D (R16 arithmetic: index-order sum of (h_d - mu_d)^2, no FMA).  Every c with D~(i,c) <= min_c D~ + 2 E_i
+// is a candidate; any other c has D(i,c) > D(i,c~) and cannot be (or tie) the minimum.  The candidates'
+// D are then evaluated with the R16 arithmetic in increasing c (ties to the lowest index): the labels and
+// dist are bit-identical to k_assign's.
+constexpr int kMmaRows = 128, kMmaAS = 136, kMmaBS = 72;  // tile rows, smem strides (= 8 mod 16 doubles)
+inline size_t asg_mma_smem(int dim) {
+  const int dp4 = (dim + 3) & ~3;
+  return sizeof(double) * ((size_t)dp4 * kMmaAS + (size_t)dp4 * kMmaBS + 64 + kMmaRows) +
+         sizeof(unsigned long long) * kMmaRows;
+}
+__global__ void __launch_bounds__(256, 2) k_assign_mma(const double* X, long long ld, const double* s, int n,
+                                                        int dim, int K, const double* mu, const int* old_labels,
+                                                        int* labels, double* dist, int* changes) {
+  extern __shared__ __align__(16) double sm[];
+  const int dp4 = (dim + 3) & ~3;
+  double* As = sm;                                  // [dp4][kMmaAS]  h (scaled rows), column d contiguous
+  double* Bs = As + (size_t)dp4 * kMmaAS;           // [dp4][kMmaBS]  M^T, zero-padded to 64 columns
+  double* musq = Bs + (size_t)dp4 * kMmaBS;         // [64]
+  double* hn = musq + 64;                           // [128]
+  unsigned long long* cmask = reinterpret_cast<unsigned long long*>(hn + kMmaRows);  // [128] candidate sets
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int KT = (K + 7) >> 3;  // 8-column DMMA tiles that hold centroids
+  for (int e = tid; e < dp4 * kMmaBS; e += 256) {
+    const int d = e / kMmaBS, c = e - d * kMmaBS;
+    Bs[e] = (d < dim && c < K) ? mu[c * dim + d] : 0.0;
+  }
+  __syncthreads();
+  if (tid < 64) {
+    double a = 0.0;
+    for (int d = 0; d < dim; ++d) a += Bs[d * kMmaBS + tid] * Bs[d * kMmaBS + tid];
+    musq[tid] = a;
+  }
+  __syncthreads();
+  double mumax = 0.0;
+  for (int c = 0; c < K; ++c) mumax = fmax(mumax, musq[c]);
+  mumax = sqrt(mumax);
+  const double eunit = 4.0 * (2.0 * dim + 7.0) * 0x1p-53;
+  int ch = 0;
+  const int ntiles = (n + kMmaRows - 1) / kMmaRows;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long row0 = (long long)tile * kMmaRows;
+    // stage the tile: As[d][r] = h_{row0+r, d} (R16 scaling s_i x, rounded like k_assign's load_row)
+    for (int e = tid; e < dp4 * kMmaRows; e += 256) {
+      const int d = e >> 7, r = e & (kMmaRows - 1);
+      const long long i = row0 + r;
+      double v = 0.0;
+      if (d < dim && i < n) {
+        const double x = X[(long long)d * ld + i];
+        v = s ? __dmul_rn(s[i], x) : x;
+      }
+      As[d * kMmaAS + r] = v;
+    }
+    if (tid < kMmaRows) cmask[tid] = 0ull;
+    __syncthreads();
+    if (tid < kMmaRows) {
+      double a = 0.0;
+      for (int d = 0; d < dim; ++d) a += As[d * kMmaAS + tid] * As[d * kMmaAS + tid];
+      hn[tid] = a;
+    }
+    // C = H_tile M^T: warp w owns rows 16 w .. 16 w + 15 (2 row tiles) and all KT column tiles
+    double acc[2][8][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int ks = 0; ks < dp4; ks += 4) {
+      double af[2], bf[8];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) af[a] = As[(ks + tq) * kMmaAS + w * 16 + a * 8 + gq];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) bf[b] = Bs[(ks + tq) * kMmaBS + b * 8 + gq];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (b < KT)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                         : "d"(af[a]), "d"(bf[b]));
+    }
+    __syncthreads();  // hn ready
+    // approximate distances, row minima (lane: rows 16w + 8a + gq, columns 8b + 2tq + q)
+    double dmin[2] = {INFINITY, INFINITY};
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int r = w * 16 + a * 8 + gq;
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int c = b * 8 + 2 * tq + q;
+          if (b < KT && c < K) {
+            acc[a][b][q] = hn[r] - 2.0 * acc[a][b][q] + musq[c];
+            dmin[a] = fmin(dmin[a], acc[a][b][q]);
+          }
+        }
+      dmin[a] = fmin(dmin[a], __shfl_xor_sync(0xffffffffu, dmin[a], 1));
+      dmin[a] = fmin(dmin[a], __shfl_xor_sync(0xffffffffu, dmin[a], 2));
+    }
+    // candidates: D~ <= min D~ + 2 E_i
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int r = w * 16 + a * 8 + gq;
+      const double nh = sqrt(hn[r]) + mumax;
+      const double thr = dmin[a] + 2.0 * eunit * nh * nh;
+      unsigned long long m = 0ull;
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int c = b * 8 + 2 * tq + q;
+          if (b < KT && c < K && !(acc[a][b][q] > thr)) m |= 1ull << c;  // NaN-safe: NaN -> candidate
+        }
+      m |= __shfl_xor_sync(0xffffffffu, m, 1);
+      m |= __shfl_xor_sync(0xffffffffu, m, 2);
+      if (tq == 0) cmask[r] = m;
+    }
+    __syncthreads();
+    // exact R16 distances of the candidates, increasing c
+    if (tid < kMmaRows) {
+      const long long i = row0 + tid;
+      if (i < n) {
+        unsigned long long m = cmask[tid];
+        if (m == 0ull) m = (K >= 64) ? ~0ull : ((1ull << K) - 1ull);
+        double best = 0.0;
+        int bl = -1;
+        while (m) {
+          const int c = __ffsll((long long)m) - 1;
+          m &= m - 1;
+          double a = 0.0;
+          for (int d = 0; d < dim; ++d) {
+            const double t = __dsub_rn(As[d * kMmaAS + tid], Bs[d * kMmaBS + c]);
+            a = __dadd_rn(a, __dmul_rn(t, t));
+          }
+          if (bl < 0 || a < best) {
+            best = a;
+            bl = c;
+          }
+        }
+        if (old_labels && old_labels[i] != bl) ++ch;
+        labels[i] = bl;
+        dist[i] = best;
+      }
+    }
+    __syncthreads();  // As / cmask reused by the next tile
+  }
+  if (changes) {
+    ch = __reduce_add_sync(0xffffffffu, ch);
+    if (lane == 0 && ch) atomicAdd(changes, ch);
   }
 }
 
@@ -449,6 +607,11 @@ struct KM {
 
   int grid_rows() const { return std::max(1, std::min((n + 255) / 256, sms * 8)); }
   void assign(const int* old_lab, int* new_lab, int* changes) {
+    if (g_km_mma) {  // tensor-core distances with the exact guard (same labels)
+      k_assign_mma<<<std::max(1, std::min((n + kMmaRows - 1) / kMmaRows, 2 * sms)), 256, asg_mma_smem(dim), st>>>(
+          X, ld, s, n, dim, K, b->mu, old_lab, new_lab, b->dist, changes);
+      return;
+    }
     constexpr int NW = asg_warps<DP>();
     k_assign<DP, 4><<<grid_asg(), NW * 32, asg_smem(K, dim, NW), st>>>(X, ld, s, n, dim, K, b->mu, old_lab, new_lab,
                                                                      b->dist, changes);
@@ -582,6 +745,7 @@ struct KM {
 }  // namespace
 
 sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, int32_t memspace, double* objective) {
+  if (getenv("SFAIRSC_KM_MMA")) g_km_mma = atoi(getenv("SFAIRSC_KM_MMA"));
   const int n = ctx_n(ctx), K = ctx_k(ctx);
   long long ld = 0;
   const double* X = ctx_X(ctx, &ld);
@@ -618,6 +782,7 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
     KCU(cudaMalloc(&b->used, sizeof(int) * (K + 1)));
     static bool attr = false;
     if (!attr) {
+      cudaFuncSetAttribute(k_assign_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asg_mma_smem(64));
       auto big = [](const void* f) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); };
       big((const void*)k_centroid_partials<8>);
       big((const void*)k_centroid_partials<16>);

@@ -336,6 +336,26 @@ def test_kmeans_device_labels_and_determinism(gpu_lib):
     assert np.array_equal(a, b.cpu().numpy()) and w1 == w2
 
 
+@pytest.mark.parametrize("n,h,k,normalized", [(3001, 3, 13, True), (2500, 4, 8, False), (4000, 2, 64, True)])
+def test_kmeans_tensor_core_assignment_is_exact(gpu_lib, monkeypatch, n, h, k, normalized):
+    """The tensor-core assignment (DMMA distances + exact guard) must reproduce the
+    direct R16 assignment bit for bit: same labels, same WCSS (k = 13: ragged DMMA
+    tiles; k = 64: the widest embedding)."""
+    g = random_graph(n, h, p=8.0 / n, seed=k, weights="uniform")
+    ctx = _ctx(gpu_lib, g, k, normalized)
+    gpu_lib.sfairsc_eigs(ctx, k, 1e-10)
+    try:
+        monkeypatch.setenv("SFAIRSC_KM_MMA", "0")
+        lab0, w0 = gpu_lib.sfairsc_embed_kmeans(ctx, 7)
+        monkeypatch.setenv("SFAIRSC_KM_MMA", "1")
+        lab1, w1 = gpu_lib.sfairsc_embed_kmeans(ctx, 7)
+    finally:
+        monkeypatch.setenv("SFAIRSC_KM_MMA", "1")
+        ctx.close()
+    assert np.array_equal(lab0, lab1)
+    assert w0 == w1
+
+
 # --- BASELINE configs 3 and 4 ------------------------------------------------------
 
 def test_eigs_config3_reduced_vs_tier_s(gpu_lib):
