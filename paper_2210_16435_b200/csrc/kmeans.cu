@@ -285,15 +285,24 @@ __global__ void __launch_bounds__(256, 2) k_assign_mma(const double* X, long lon
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long long row0 = (long long)tile * kMmaRows;
     // stage the tile: As[d][r] = h_{row0+r, d} (R16 scaling s_i x, rounded like k_assign's load_row)
-    for (int e = tid; e < dp4 * kMmaRows; e += 256) {
-      const int d = e >> 7, r = e & (kMmaRows - 1);
+    {  // thread (r = tid & 127, d0 = tid >> 7) stages dims d0, d0 + 2, ...: 16 loads in flight per batch
+      const int r = tid & (kMmaRows - 1), d0 = tid >> 7;
       const long long i = row0 + r;
-      double v = 0.0;
-      if (d < dim && i < n) {
-        const double x = X[(long long)d * ld + i];
-        v = s ? __dmul_rn(s[i], x) : x;
+      const bool rv = i < n;
+      const double si = (s && rv) ? s[i] : 1.0;
+      for (int dbase = 0; dbase < dp4; dbase += 32) {
+        double v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int d = dbase + d0 + 2 * q;
+          v[q] = (rv && d < dim) ? __ldg(X + (long long)d * ld + i) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int d = dbase + d0 + 2 * q;
+          if (d < dp4) As[d * kMmaAS + r] = s ? __dmul_rn(si, v[q]) : v[q];
+        }
       }
-      As[d * kMmaAS + r] = v;
     }
     if (tid < kMmaRows) cmask[tid] = 0ull;
     __syncthreads();
@@ -413,25 +422,27 @@ __global__ void __launch_bounds__(256) k_dist_own(const double* X, long long ld,
 // quarter q = t / 64 and adds that quarter's rows of each tile, in row order, into
 // the quarter's private accumulator; the four accumulators are combined in fixed
 // order.  Every sum is therefore in a fixed order, independent of timing.
-constexpr int kCpThreads = 256, kCpQ = 4;
-inline size_t cp_smem_r(int K, int dim, int R) {
-  return sizeof(double) * ((size_t)kCpQ * (K * dim + K) + 2 * (size_t)(dim + 1) * (R + 1)) + sizeof(int) * 2 * R;
+// Q row groups, 64 Q threads: thread (column c, group q).  Q = 4 with up to 128-row tiles (Q = 8 with
+// 64-row tiles measured slower at config 4: 0.83 vs 0.71 ms).
+inline size_t cp_smem_qr(int K, int dim, int Q, int R) {
+  return sizeof(double) * ((size_t)Q * (K * dim + K) + 2 * (size_t)(dim + 1) * (R + 1)) + sizeof(int) * 2 * R;
 }
-inline int cp_rows(int K, int dim) {
-  int R = 128;
-  while (R > 32 && cp_smem_r(K, dim, R) > 220 * 1024) R /= 2;
-  return R;
+inline void cp_config(int K, int dim, int* Q, int* R) {
+  *Q = 4;
+  *R = 128;
+  while (*R > 32 && cp_smem_qr(K, dim, 4, *R) > 220 * 1024) *R /= 2;
 }
 template <int DP>
-__global__ void __launch_bounds__(kCpThreads) k_centroid_partials(const double* X, long long ld, const double* s,
-                                                                  int n, int dim, int K, int R, const int* labels,
-                                                                  double* partials) {
-  extern __shared__ double acc[];  // [kCpQ][W], tiles [2][dim + 1][R + 1] (row dim = s), labels [2][R]
+__global__ void __launch_bounds__(512) k_centroid_partials(const double* X, long long ld, const double* s, int n,
+                                                           int dim, int K, int Q, int R, const int* labels,
+                                                           double* partials) {
+  extern __shared__ double acc[];  // [Q][W], tiles [2][dim + 1][R + 1] (row dim = s), labels [2][R]
   const int RP = R + 1;             // padded column stride: lanes on consecutive columns hit different banks
   const int W = K * dim + K;
-  double* tiles = acc + (size_t)kCpQ * W;
+  const int NT = blockDim.x;        // 64 Q
+  double* tiles = acc + (size_t)Q * W;
   int* tl = reinterpret_cast<int*>(tiles + 2 * (size_t)(dim + 1) * RP);
-  for (int e = threadIdx.x; e < kCpQ * W; e += blockDim.x) acc[e] = 0.0;
+  for (int e = threadIdx.x; e < Q * W; e += NT) acc[e] = 0.0;
   const long long i0 = (long long)n * blockIdx.x / gridDim.x, i1 = (long long)n * (blockIdx.x + 1) / gridDim.x;
   const int ntiles = (int)((i1 - i0 + R - 1) / R);
   auto prefetch = [&](int t) {
@@ -440,17 +451,17 @@ __global__ void __launch_bounds__(kCpThreads) k_centroid_partials(const double* 
       int* lb = tl + (t & 1) * R;
       const long long r0 = i0 + (long long)t * R;
       const int ncol = dim + (s ? 1 : 0);
-      const int r = threadIdx.x & (R - 1), dstep = kCpThreads / R;  // R: power of two <= kCpThreads
+      const int r = threadIdx.x & (R - 1), dstep = NT / R;  // R: power of two <= NT
       if (r0 + r < i1)
         for (int d = threadIdx.x / R; d < ncol; d += dstep)
           cp_async8(tb + (size_t)d * RP + r, d < dim ? X + (long long)d * ld + r0 + r : s + r0 + r);
-      for (int r = threadIdx.x; r < R; r += blockDim.x)
+      for (int r = threadIdx.x; r < R; r += NT)
         if (r0 + r < i1) cp_async4(lb + r, labels + r0 + r);
     }
     cp_commit();
   };
   prefetch(0);
-  const int c = threadIdx.x & 63, q = threadIdx.x >> 6, RQ = R / kCpQ;
+  const int c = threadIdx.x & 63, q = threadIdx.x >> 6, RQ = R / Q;
   double* a = acc + (size_t)q * W;
   for (int t = 0; t < ntiles; ++t) {
     prefetch(t + 1);
@@ -483,8 +494,11 @@ __global__ void __launch_bounds__(kCpThreads) k_centroid_partials(const double* 
   }
   cp_wait<0>();
   __syncthreads();
-  for (int e = threadIdx.x; e < W; e += blockDim.x)
-    partials[(size_t)blockIdx.x * W + e] = ((acc[e] + acc[W + e]) + acc[2 * W + e]) + acc[3 * W + e];
+  for (int e = threadIdx.x; e < W; e += NT) {
+    double v = acc[e];
+    for (int g = 1; g < Q; ++g) v += acc[(size_t)g * W + e];  // fixed order
+    partials[(size_t)blockIdx.x * W + e] = v;
+  }
 }
 
 __global__ void k_means_div(const double* sums, int K, int dim, double* mu) {
@@ -661,8 +675,10 @@ struct KM {
   sfairsc_status means(const int* lab) {
     const int W = K * dim + K;
     bump_launch();
-    const int R = cp_rows(K, dim);
-    k_centroid_partials<DP><<<b->G, kCpThreads, cp_smem_r(K, dim, R), st>>>(X, ld, s, n, dim, K, R, lab, b->partials);
+    int Q = 4, R = 128;
+    cp_config(K, dim, &Q, &R);
+    k_centroid_partials<DP><<<b->G, 64 * Q, cp_smem_qr(K, dim, Q, R), st>>>(X, ld, s, n, dim, K, Q, R, lab,
+                                                                           b->partials);
     launch_reduce_cols(b->partials, b->G, W, b->sums, st);
     bump_launch();
     k_means_div<<<std::max(1, (K * dim + 255) / 256), 256, 0, st>>>(b->sums, K, dim, b->mu);
