@@ -11,6 +11,7 @@
 #include "device_common.cuh"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <limits>
@@ -35,6 +36,9 @@ namespace {
 
 constexpr int kBlk = 1024;     // D2 prefix blocks
 int g_km_mma = 1;              // 1: tensor-core assignment with the exact guard; 0: direct (env SFAIRSC_KM_MMA)
+int g_km_debug = 0;            // env SFAIRSC_DEBUG: per-iteration label changes on stderr
+int g_km_incr = 1;             // 1: incremental cluster sums between full recomputations (env SFAIRSC_KM_INCR)
+constexpr int kKmRefresh = 16; // full recomputation at least every 16 Lloyd iterations (bounds the drift)
 constexpr int kMaxDim = 64;    // k <= 64 handled in registers
 constexpr int kKmStream = 8;   // Philox stream of the k-means draws
 
@@ -501,6 +505,104 @@ __global__ void __launch_bounds__(512) k_centroid_partials(const double* X, long
   }
 }
 
+// ---- incremental centroid sums (Lloyd iterations where few labels change) ----
+// Changed rows per 128-row tile, in row order: cnt[t], idx[128 t + j].
+constexpr int kDT = 128;
+__global__ void __launch_bounds__(kDT) k_changed_slots(const int* lab_old, const int* lab_new, int n, int* cnt,
+                                                       int* idx) {
+  __shared__ int wc[kDT / 32];
+  const int t = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long i = (long long)t * kDT + threadIdx.x;
+  const bool chg = i < n && lab_old[i] != lab_new[i];
+  const unsigned m = __ballot_sync(0xffffffffu, chg);
+  if (lane == 0) wc[w] = __popc(m);
+  __syncthreads();
+  int base = 0;
+  for (int q = 0; q < w; ++q) base += wc[q];
+  if (chg) idx[(size_t)t * kDT + base + __popc(m & ((1u << lane) - 1u))] = (int)i;
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int q = 0; q < kDT / 32; ++q) tot += wc[q];
+    cnt[t] = tot;
+  }
+}
+// Per-CTA delta of the cluster sums and counts over the changed rows of a contiguous tile range, in row
+// order: sums[new] += [h_i, 1], sums[old] -= [h_i, 1] (column owners, fixed order).  partials[b][K dim + K].
+constexpr int kDeltaThreads = 256, kDeltaTilesPerRound = 256, kDeltaSub = 64;
+inline size_t delta_smem(int K, int dim) {
+  return sizeof(double) * ((size_t)K * dim + K + (size_t)kDeltaSub * (dim + 1)) +
+         sizeof(int) * ((size_t)kDeltaTilesPerRound * kDT + kDeltaTilesPerRound + 2 * kDeltaSub + 64);
+}
+__global__ void __launch_bounds__(kDeltaThreads) k_centroid_delta(const double* X, long long ld, const double* s, int n,
+                                                                   int dim, int K, const int* lab_old,
+                                                                   const int* lab_new, const int* cnt, const int* idx,
+                                                                   double* partials) {
+  extern __shared__ __align__(16) double dacc[];  // [K dim + K] | h [kDeltaSub][dim + 1] | ints
+  const int W = K * dim + K;
+  double* hb = dacc + W;
+  int* list = reinterpret_cast<int*>(hb + (size_t)kDeltaSub * (dim + 1));
+  int* tofs = list + kDeltaTilesPerRound * kDT;
+  int* lo = tofs + kDeltaTilesPerRound;
+  int* ln = lo + kDeltaSub;
+  int* misc = ln + kDeltaSub;
+  for (int e = threadIdx.x; e < W; e += blockDim.x) dacc[e] = 0.0;
+  const int T = (n + kDT - 1) / kDT;
+  const int t0 = (int)((long long)T * blockIdx.x / gridDim.x), t1 = (int)((long long)T * (blockIdx.x + 1) / gridDim.x);
+  for (int r0 = t0; r0 < t1; r0 += kDeltaTilesPerRound) {
+    const int nt = min(kDeltaTilesPerRound, t1 - r0);
+    __syncthreads();
+    if (threadIdx.x == 0) {  // exclusive offsets of the round's tiles (serial: <= 256 small adds)
+      int acc = 0;
+      for (int q = 0; q < nt; ++q) {
+        tofs[q] = acc;
+        acc += cnt[r0 + q];
+      }
+      misc[0] = acc;
+    }
+    __syncthreads();
+    const int total = misc[0];
+    for (int q = threadIdx.x; q < nt; q += blockDim.x) {
+      const int c = cnt[r0 + q], o = tofs[q];
+      for (int j = 0; j < c; ++j) list[o + j] = idx[(size_t)(r0 + q) * kDT + j];
+    }
+    __syncthreads();
+    for (int b0 = 0; b0 < total; b0 += kDeltaSub) {
+      const int nb = min(kDeltaSub, total - b0);
+      for (int e = threadIdx.x; e < nb * dim; e += blockDim.x) {
+        const int j = e / dim, d = e - j * dim;
+        const int i = list[b0 + j];
+        const double x = X[(long long)d * ld + i];
+        hb[j * (dim + 1) + d] = s ? __dmul_rn(s[i], x) : x;
+      }
+      for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+        const int i = list[b0 + j];
+        lo[j] = lab_old[i];
+        ln[j] = lab_new[i];
+      }
+      __syncthreads();
+      const int c = threadIdx.x;
+      if (c < dim) {
+        for (int j = 0; j < nb; ++j) {
+          const double v = hb[j * (dim + 1) + c];
+          dacc[ln[j] * dim + c] += v;
+          dacc[lo[j] * dim + c] -= v;
+        }
+      } else if (c == dim) {
+        for (int j = 0; j < nb; ++j) {
+          dacc[K * dim + ln[j]] += 1.0;
+          dacc[K * dim + lo[j]] -= 1.0;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < W; e += blockDim.x) partials[(size_t)blockIdx.x * W + e] = dacc[e];
+}
+__global__ void k_add_sums(double* sums, const double* delta, int W) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < W; e += gridDim.x * blockDim.x) sums[e] += delta[e];
+}
+
 __global__ void k_means_div(const double* sums, int K, int dim, double* mu) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * dim; e += gridDim.x * blockDim.x) {
     const double cnt = sums[K * dim + e / dim];
@@ -585,6 +687,8 @@ inline double uniform_host(uint64_t seed, unsigned c0, unsigned c1, unsigned c2)
 struct KmBuf {
   int n = 0, K = 0, G = 0, nblk = 0;
   double *D2 = nullptr, *bsum = nullptr, *mu = nullptr, *dist = nullptr, *partials = nullptr, *sums = nullptr;
+  double* dsum = nullptr;               // delta of the sums (incremental iterations)
+  int *tcnt = nullptr, *tidx = nullptr;  // changed rows per 128-row tile
   double* bval = nullptr;
   int *lab = nullptr, *lab2 = nullptr, *best = nullptr, *idx = nullptr, *changes = nullptr, *bidx = nullptr,
       *used = nullptr;
@@ -592,7 +696,7 @@ struct KmBuf {
 void km_free(void* p) {
   KmBuf* b = static_cast<KmBuf*>(p);
   void* ptrs[] = {b->D2, b->bsum, b->mu, b->dist, b->partials, b->sums, b->bval, b->lab, b->lab2, b->best, b->idx,
-                  b->changes, b->bidx, b->used};
+                  b->changes, b->bidx, b->used, b->dsum, b->tcnt, b->tidx};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete b;
@@ -686,6 +790,24 @@ struct KM {
     return SFAIRSC_OK;
   }
 
+  // sums(lab) = sums(prev) + delta(prev -> lab), then mu (few changed labels: the changed rows only)
+  sfairsc_status means_delta(const int* prev, const int* lab) {
+    const int W = K * dim + K;
+    const int T = (n + kDT - 1) / kDT;
+    bump_launch();
+    k_changed_slots<<<T, kDT, 0, st>>>(prev, lab, n, b->tcnt, b->tidx);
+    bump_launch();
+    k_centroid_delta<<<b->G, kDeltaThreads, delta_smem(K, dim), st>>>(X, ld, s, n, dim, K, prev, lab, b->tcnt,
+                                                                      b->tidx, b->partials);
+    launch_reduce_cols(b->partials, b->G, W, b->dsum, st);
+    bump_launch();
+    k_add_sums<<<std::max(1, (W + 255) / 256), 256, 0, st>>>(b->sums, b->dsum, W);
+    bump_launch();
+    k_means_div<<<std::max(1, (K * dim + 255) / 256), 256, 0, st>>>(b->sums, K, dim, b->mu);
+    KCU(cudaGetLastError());
+    return SFAIRSC_OK;
+  }
+
   sfairsc_status run(uint64_t seed, int restarts, int max_iters, double* best_wcss) {
     std::vector<double> hb(std::max(b->nblk, K) + 8);
     std::vector<double> counts(K);
@@ -698,8 +820,17 @@ struct KM {
       assign(nullptr, b->lab, nullptr);
       int* lab = b->lab;
       int* lab_new = b->lab2;
+      int last_ch = n, since_full = 0;
       for (int it = 0; it < max_iters; ++it) {
-        TRY_(means(lab));
+        // cluster sums: full recomputation on the first iteration, every kKmRefresh-th, and after many changes;
+        // otherwise the previous sums plus the changed rows' contributions (lab_new holds the previous labels)
+        if (!g_km_incr || it == 0 || since_full + 1 >= kKmRefresh || (long long)last_ch * 16 > n) {
+          TRY_(means(lab));
+          since_full = 0;
+        } else {
+          TRY_(means_delta(lab_new, lab));
+          ++since_full;
+        }
         KCU(cudaMemcpyAsync(counts.data(), b->sums + (size_t)K * dim, sizeof(double) * K, cudaMemcpyDeviceToHost, st));
         KCU(cudaStreamSynchronize(st));
         bool any_empty = false;
@@ -735,7 +866,10 @@ struct KM {
         int ch = 0;
         KCU(cudaMemcpyAsync(&ch, b->changes, sizeof(int), cudaMemcpyDeviceToHost, st));
         KCU(cudaStreamSynchronize(st));
+        if (g_km_debug && (it < 10 || it % 25 == 0))
+          fprintf(stderr, "[sfairsc] kmeans restart %d iteration %d: %d labels changed\n", r, it, ch);
         if (ch == 0) break;
+        last_ch = ch;
         std::swap(lab, lab_new);
       }
       // final centroids of the final labels, WCSS
@@ -762,6 +896,8 @@ struct KM {
 
 sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, int32_t memspace, double* objective) {
   if (getenv("SFAIRSC_KM_MMA")) g_km_mma = atoi(getenv("SFAIRSC_KM_MMA"));
+  g_km_debug = getenv("SFAIRSC_DEBUG") ? atoi(getenv("SFAIRSC_DEBUG")) : 0;
+  if (getenv("SFAIRSC_KM_INCR")) g_km_incr = atoi(getenv("SFAIRSC_KM_INCR"));
   const int n = ctx_n(ctx), K = ctx_k(ctx);
   long long ld = 0;
   const double* X = ctx_X(ctx, &ld);
@@ -788,6 +924,9 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
     KCU(cudaMalloc(&b->dist, sizeof(double) * n));
     KCU(cudaMalloc(&b->partials, sizeof(double) * (size_t)b->G * W));
     KCU(cudaMalloc(&b->sums, sizeof(double) * W));
+    KCU(cudaMalloc(&b->dsum, sizeof(double) * W));
+    KCU(cudaMalloc(&b->tcnt, sizeof(int) * ((n + kDT - 1) / kDT)));
+    KCU(cudaMalloc(&b->tidx, sizeof(int) * (size_t)((n + kDT - 1) / kDT) * kDT));
     KCU(cudaMalloc(&b->bval, sizeof(double) * b->nblk));
     KCU(cudaMalloc(&b->lab, sizeof(int) * n));
     KCU(cudaMalloc(&b->lab2, sizeof(int) * n));
@@ -799,6 +938,7 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_assign_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asg_mma_smem(64));
+      cudaFuncSetAttribute(k_centroid_delta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)delta_smem(64, 64));
       auto big = [](const void* f) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); };
       big((const void*)k_centroid_partials<8>);
       big((const void*)k_centroid_partials<16>);

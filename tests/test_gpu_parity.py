@@ -356,6 +356,26 @@ def test_kmeans_tensor_core_assignment_is_exact(gpu_lib, monkeypatch, n, h, k, n
     assert w0 == w1
 
 
+def test_kmeans_incremental_sums_match_full(gpu_lib, monkeypatch):
+    """Lloyd iterations with few changed labels update the cluster sums from the
+    changed rows only (full recomputation every 16 iterations): same clustering as
+    recomputing every iteration, WCSS equal to rounding."""
+    from oracle.metrics import ari
+    g = random_graph(30000, 3, p=8.0 / 30000, seed=5, weights="uniform")
+    ctx = _ctx(gpu_lib, g, 12, True)
+    gpu_lib.sfairsc_eigs(ctx, 12, 1e-10)
+    try:
+        monkeypatch.setenv("SFAIRSC_KM_INCR", "0")
+        lab0, w0 = gpu_lib.sfairsc_embed_kmeans(ctx, 3)
+        monkeypatch.setenv("SFAIRSC_KM_INCR", "1")
+        lab1, w1 = gpu_lib.sfairsc_embed_kmeans(ctx, 3)
+    finally:
+        monkeypatch.setenv("SFAIRSC_KM_INCR", "1")
+        ctx.close()
+    assert ari(lab0, lab1) >= 0.999
+    assert abs(w0 - w1) <= 1e-9 * abs(w0)
+
+
 # --- BASELINE configs 3 and 4 ------------------------------------------------------
 
 def test_eigs_config3_reduced_vs_tier_s(gpu_lib):
