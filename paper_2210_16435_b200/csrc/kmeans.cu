@@ -38,6 +38,7 @@ constexpr int kBlk = 1024;     // D2 prefix blocks
 int g_km_mma = 1;              // 1: tensor-core assignment with the exact guard; 0: direct (env SFAIRSC_KM_MMA)
 int g_km_debug = 0;            // env SFAIRSC_DEBUG: per-iteration label changes on stderr
 int g_km_incr = 1;             // 1: incremental cluster sums between full recomputations (env SFAIRSC_KM_INCR)
+int g_km_prune = 0;            // 1: bound-pruned assignment (env SFAIRSC_KM_PRUNE)
 constexpr int kKmRefresh = 16; // full recomputation at least every 16 Lloyd iterations (bounds the drift)
 constexpr int kMaxDim = 64;    // k <= 64 handled in registers
 constexpr int kKmStream = 8;   // Philox stream of the k-means draws
@@ -603,6 +604,170 @@ __global__ void k_add_sums(double* sums, const double* delta, int W) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < W; e += gridDim.x * blockDim.x) sums[e] += delta[e];
 }
 
+// ---- bound-pruned assignment (Hamerly's bounds, made exact) ----
+// Per row: ub >= the true distance to the assigned centroid, lb <= the true distance to every other one
+// (true = exact arithmetic on the stored centroids).  A centroid that moved by delta_c loosens them:
+// ub += delta_a, lb -= max_{c != a} delta_c.  If ub (1 + eta) < lb (1 - eta), the assigned centroid is
+// strictly nearest by a relative margin far above the rounding of the R16 distance sum, so the direct
+// evaluation would return the same label: the row is skipped.  Other rows are evaluated directly over all
+// centroids (R16 arithmetic, ties to the lowest index) and get fresh bounds.
+constexpr double kEta = 1e-12;
+__global__ void k_shift(const double* mu, const double* mu_old, int K, int dim, double* shift) {
+  __shared__ double sh[64];
+  const int c = threadIdx.x;
+  if (c < K) {
+    double a = 0.0;
+    for (int d = 0; d < dim; ++d) {
+      const double t = mu[c * dim + d] - mu_old[c * dim + d];
+      a += t * t;
+    }
+    sh[c] = sqrt(a) * (1.0 + kEta) + 1e-300;  // >= the true shift
+    shift[c] = sh[c];
+  }
+  __syncthreads();
+  if (c == 0) {
+    double m1 = 0.0, m2 = 0.0;
+    int am = -1;
+    for (int q = 0; q < K; ++q) {
+      if (sh[q] > m1) {
+        m2 = m1;
+        m1 = sh[q];
+        am = q;
+      } else if (sh[q] > m2) {
+        m2 = sh[q];
+      }
+    }
+    shift[K] = m1;
+    shift[K + 1] = m2;
+    shift[K + 2] = (double)am;
+  }
+}
+// prune test per row; rows that need an evaluation are listed per 128-row tile in row order (force: all)
+__global__ void __launch_bounds__(kDT) k_prune_test(const int* lab_old, int* lab_new, double* ub, double* lb, int n,
+                                                    int K, const double* shift, int force, int* cnt, int* idx) {
+  __shared__ int wc[kDT / 32];
+  const int t = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long i = (long long)t * kDT + threadIdx.x;
+  bool need = false;
+  if (i < n) {
+    need = true;
+    if (!force) {
+      const int a = lab_old[i];
+      const int am = (int)shift[K + 2];
+      const double u = ub[i] + shift[a];
+      const double l = lb[i] - (a == am ? shift[K + 1] : shift[K]);
+      if (l > 0.0 && u * (1.0 + kEta) < l * (1.0 - kEta)) {
+        need = false;
+        lab_new[i] = a;
+        ub[i] = u;
+        lb[i] = l;
+      }
+    }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, need);
+  if (lane == 0) wc[w] = __popc(m);
+  __syncthreads();
+  int base = 0;
+  for (int q = 0; q < w; ++q) base += wc[q];
+  if (need) idx[(size_t)t * kDT + base + __popc(m & ((1u << lane) - 1u))] = (int)i;
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int q = 0; q < kDT / 32; ++q) tot += wc[q];
+    cnt[t] = tot;
+  }
+}
+// direct R16 evaluation of the listed rows (all centroids): label, dist, fresh bounds
+constexpr int kEvalTilesPerRound = 64;
+inline size_t eval_smem(int K, int dim) {
+  return sizeof(double) * (size_t)K * ((dim + 1) & ~1) + sizeof(int) * ((size_t)kEvalTilesPerRound * kDT + 64 + 8);
+}
+template <int DP>
+__global__ void __launch_bounds__(256) k_eval_listed(const double* X, long long ld, const double* s, int n, int dim,
+                                                     int K, const double* mu, const int* old_labels, int* labels,
+                                                     double* dist, double* ub, double* lb, const int* cnt,
+                                                     const int* idx, int* changes) {
+  extern __shared__ __align__(16) double smu[];  // [K][dimp] | list | tile offsets
+  const int dimp = (dim + 1) & ~1;
+  int* list = reinterpret_cast<int*>(smu + (size_t)K * dimp);
+  int* tofs = list + kEvalTilesPerRound * kDT;
+  for (int e = threadIdx.x; e < K * dimp; e += blockDim.x) {
+    const int c = e / dimp, d = e - c * dimp;
+    smu[e] = d < dim ? mu[c * dim + d] : 0.0;
+  }
+  const int T = (n + kDT - 1) / kDT;
+  const int t0 = (int)((long long)T * blockIdx.x / gridDim.x), t1 = (int)((long long)T * (blockIdx.x + 1) / gridDim.x);
+  int ch = 0;
+  for (int r0 = t0; r0 < t1; r0 += kEvalTilesPerRound) {
+    const int nt = min(kEvalTilesPerRound, t1 - r0);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int q = 0; q < nt; ++q) {
+        tofs[q] = acc;
+        acc += cnt[r0 + q];
+      }
+      tofs[64] = acc;
+    }
+    __syncthreads();
+    const int total = tofs[64];
+    for (int q = threadIdx.x; q < nt; q += blockDim.x) {
+      const int c = cnt[r0 + q], o = tofs[q];
+      for (int j = 0; j < c; ++j) list[o + j] = idx[(size_t)(r0 + q) * kDT + j];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < total; j += blockDim.x) {
+      const int i = list[j];
+      double h[DP];
+      load_row<DP>(X, ld, s, i, dim, h);
+      double best = 0.0, second = INFINITY;
+      int bl = 0;
+      for (int c0 = 0; c0 < K; c0 += 4) {
+        double a[4];
+        const double* m[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a[u] = 0.0;
+          m[u] = smu + min(c0 + u, K - 1) * dimp;
+        }
+#pragma unroll
+        for (int d = 0; d < DP; d += 2)
+          if (d < dim) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double2 q = *reinterpret_cast<const double2*>(m[u] + d);
+              const double e0 = __dsub_rn(h[d], q.x);
+              a[u] = __dadd_rn(a[u], __dmul_rn(e0, e0));
+              if (d + 1 < dim) {
+                const double e1 = __dsub_rn(h[d + 1], q.y);
+                a[u] = __dadd_rn(a[u], __dmul_rn(e1, e1));
+              }
+            }
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + u < K) {
+            if (c0 + u == 0 || a[u] < best) {
+              if (c0 + u > 0) second = fmin(second, best);
+              best = a[u];
+              bl = c0 + u;
+            } else {
+              second = fmin(second, a[u]);
+            }
+          }
+      }
+      if (old_labels && old_labels[i] != bl) ++ch;
+      labels[i] = bl;
+      dist[i] = best;
+      ub[i] = sqrt(best) * (1.0 + kEta);
+      lb[i] = K > 1 ? sqrt(second) * (1.0 - kEta) : INFINITY;
+    }
+  }
+  if (changes) {
+    ch = __reduce_add_sync(0xffffffffu, ch);
+    if ((threadIdx.x & 31) == 0 && ch) atomicAdd(changes, ch);
+  }
+}
+
 __global__ void k_means_div(const double* sums, int K, int dim, double* mu) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * dim; e += gridDim.x * blockDim.x) {
     const double cnt = sums[K * dim + e / dim];
@@ -688,6 +853,7 @@ struct KmBuf {
   int n = 0, K = 0, G = 0, nblk = 0;
   double *D2 = nullptr, *bsum = nullptr, *mu = nullptr, *dist = nullptr, *partials = nullptr, *sums = nullptr;
   double* dsum = nullptr;               // delta of the sums (incremental iterations)
+  double *ub = nullptr, *lb = nullptr, *mu_old = nullptr, *shift = nullptr;  // pruned assignment
   int *tcnt = nullptr, *tidx = nullptr;  // changed rows per 128-row tile
   double* bval = nullptr;
   int *lab = nullptr, *lab2 = nullptr, *best = nullptr, *idx = nullptr, *changes = nullptr, *bidx = nullptr,
@@ -696,7 +862,7 @@ struct KmBuf {
 void km_free(void* p) {
   KmBuf* b = static_cast<KmBuf*>(p);
   void* ptrs[] = {b->D2, b->bsum, b->mu, b->dist, b->partials, b->sums, b->bval, b->lab, b->lab2, b->best, b->idx,
-                  b->changes, b->bidx, b->used, b->dsum, b->tcnt, b->tidx};
+                  b->changes, b->bidx, b->used, b->dsum, b->tcnt, b->tidx, b->ub, b->lb, b->mu_old, b->shift};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete b;
@@ -733,6 +899,20 @@ struct KM {
     constexpr int NW = asg_warps<DP>();
     k_assign<DP, 4><<<grid_asg(), NW * 32, asg_smem(K, dim, NW), st>>>(X, ld, s, n, dim, K, b->mu, old_lab, new_lab,
                                                                      b->dist, changes);
+  }
+  // bound-pruned assignment: force = evaluate every row (bounds initialisation)
+  void assign_pruned(const int* old_lab, int* new_lab, int* changes, bool force) {
+    const int T = (n + kDT - 1) / kDT;
+    if (!force) {
+      bump_launch();
+      k_shift<<<1, 64, 0, st>>>(b->mu, b->mu_old, K, dim, b->shift);
+    }
+    bump_launch();
+    k_prune_test<<<T, kDT, 0, st>>>(old_lab ? old_lab : new_lab, new_lab, b->ub, b->lb, n, K, b->shift,
+                                    force ? 1 : 0, b->tcnt, b->tidx);
+    bump_launch();
+    k_eval_listed<DP><<<std::max(1, std::min(T, sms)), 256, eval_smem(K, dim), st>>>(
+        X, ld, s, n, dim, K, b->mu, old_lab, new_lab, b->dist, b->ub, b->lb, b->tcnt, b->tidx, changes);
   }
   int grid_asg() const { return std::max(1, std::min((n + 255) / 256, sms)); }
 
@@ -817,13 +997,15 @@ struct KM {
     for (int r = 0; r < restarts; ++r) {
       TRY_(seed_centers(seed, r, hb));
       bump_launch();
-      assign(nullptr, b->lab, nullptr);
+      if (g_km_prune) assign_pruned(nullptr, b->lab, nullptr, true);
+      else assign(nullptr, b->lab, nullptr);
       int* lab = b->lab;
       int* lab_new = b->lab2;
       int last_ch = n, since_full = 0;
       for (int it = 0; it < max_iters; ++it) {
         // cluster sums: full recomputation on the first iteration, every kKmRefresh-th, and after many changes;
         // otherwise the previous sums plus the changed rows' contributions (lab_new holds the previous labels)
+        if (g_km_prune) KCU(cudaMemcpyAsync(b->mu_old, b->mu, sizeof(double) * K * dim, cudaMemcpyDeviceToDevice, st));
         if (!g_km_incr || it == 0 || since_full + 1 >= kKmRefresh || (long long)last_ch * 16 > n) {
           TRY_(means(lab));
           since_full = 0;
@@ -862,7 +1044,8 @@ struct KM {
         }
         KCU(cudaMemsetAsync(b->changes, 0, sizeof(int), st));
         bump_launch();
-        assign(lab, lab_new, b->changes);
+        if (g_km_prune) assign_pruned(lab, lab_new, b->changes, false);
+        else assign(lab, lab_new, b->changes);
         int ch = 0;
         KCU(cudaMemcpyAsync(&ch, b->changes, sizeof(int), cudaMemcpyDeviceToHost, st));
         KCU(cudaStreamSynchronize(st));
@@ -898,6 +1081,7 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
   if (getenv("SFAIRSC_KM_MMA")) g_km_mma = atoi(getenv("SFAIRSC_KM_MMA"));
   g_km_debug = getenv("SFAIRSC_DEBUG") ? atoi(getenv("SFAIRSC_DEBUG")) : 0;
   if (getenv("SFAIRSC_KM_INCR")) g_km_incr = atoi(getenv("SFAIRSC_KM_INCR"));
+  if (getenv("SFAIRSC_KM_PRUNE")) g_km_prune = atoi(getenv("SFAIRSC_KM_PRUNE"));
   const int n = ctx_n(ctx), K = ctx_k(ctx);
   long long ld = 0;
   const double* X = ctx_X(ctx, &ld);
@@ -925,6 +1109,10 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
     KCU(cudaMalloc(&b->partials, sizeof(double) * (size_t)b->G * W));
     KCU(cudaMalloc(&b->sums, sizeof(double) * W));
     KCU(cudaMalloc(&b->dsum, sizeof(double) * W));
+    KCU(cudaMalloc(&b->ub, sizeof(double) * n));
+    KCU(cudaMalloc(&b->lb, sizeof(double) * n));
+    KCU(cudaMalloc(&b->mu_old, sizeof(double) * K * dim));
+    KCU(cudaMalloc(&b->shift, sizeof(double) * (K + 4)));
     KCU(cudaMalloc(&b->tcnt, sizeof(int) * ((n + kDT - 1) / kDT)));
     KCU(cudaMalloc(&b->tidx, sizeof(int) * (size_t)((n + kDT - 1) / kDT) * kDT));
     KCU(cudaMalloc(&b->bval, sizeof(double) * b->nblk));
@@ -940,6 +1128,12 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
       cudaFuncSetAttribute(k_assign_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asg_mma_smem(64));
       cudaFuncSetAttribute(k_centroid_delta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)delta_smem(64, 64));
       auto big = [](const void* f) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); };
+      big((const void*)k_eval_listed<8>);
+      big((const void*)k_eval_listed<16>);
+      big((const void*)k_eval_listed<32>);
+      big((const void*)k_eval_listed<48>);
+      big((const void*)k_eval_listed<56>);
+      big((const void*)k_eval_listed<64>);
       big((const void*)k_centroid_partials<8>);
       big((const void*)k_centroid_partials<16>);
       big((const void*)k_centroid_partials<32>);

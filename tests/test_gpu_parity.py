@@ -356,6 +356,26 @@ def test_kmeans_tensor_core_assignment_is_exact(gpu_lib, monkeypatch, n, h, k, n
     assert w0 == w1
 
 
+@pytest.mark.parametrize("n,h,k,normalized", [(30000, 3, 12, True), (20000, 2, 5, False), (6000, 3, 64, True)])
+def test_kmeans_bound_pruned_assignment_is_exact(gpu_lib, monkeypatch, n, h, k, normalized):
+    """Rows whose Hamerly bounds (with a 1e-12 relative margin) prove the assigned
+    centroid strictly nearest are skipped: the labels and WCSS must equal the
+    unpruned assignment's bit for bit."""
+    g = random_graph(n, h, p=8.0 / n, seed=k + 1, weights="uniform")
+    ctx = _ctx(gpu_lib, g, k, normalized)
+    gpu_lib.sfairsc_eigs(ctx, k, 1e-10)
+    try:
+        monkeypatch.setenv("SFAIRSC_KM_PRUNE", "0")
+        lab0, w0 = gpu_lib.sfairsc_embed_kmeans(ctx, 11)
+        monkeypatch.setenv("SFAIRSC_KM_PRUNE", "1")
+        lab1, w1 = gpu_lib.sfairsc_embed_kmeans(ctx, 11)
+    finally:
+        monkeypatch.delenv("SFAIRSC_KM_PRUNE")
+        ctx.close()
+    assert np.array_equal(lab0, lab1)
+    assert w0 == w1
+
+
 def test_kmeans_incremental_sums_match_full(gpu_lib, monkeypatch):
     """Lloyd iterations with few changed labels update the cluster sums from the
     changed rows only (full recomputation every 16 iterations): same clustering as
