@@ -336,6 +336,24 @@ def test_kmeans_device_labels_and_determinism(gpu_lib):
     assert np.array_equal(a, b.cpu().numpy()) and w1 == w2
 
 
+@pytest.mark.parametrize("n,k", [(37, 1), (50, 3), (130, 4), (300, 9)])
+def test_kmeans_small_edge_cases_match_oracle_on_same_embedding(gpu_lib, n, k):
+    """Edge cases of the k-means kernels (k = 1, n below one 128-row tile, a ragged
+    last tile): the oracle's R16 k-means run on the GPU's own embedding H = X
+    (unnormalized) gives the same partition and WCSS."""
+    from oracle.kmeans import kmeans
+    from oracle.metrics import ari
+    g = random_graph(n, 2, p=min(1.0, 8.0 / n), seed=n, weights="uniform")
+    ctx = _ctx(gpu_lib, g, k, False)
+    _, Xt, _ = gpu_lib.sfairsc_eigs(ctx, k, 1e-12)
+    lab, wcss = gpu_lib.sfairsc_embed_kmeans(ctx, 5)
+    ctx.close()
+    ref = kmeans(np.ascontiguousarray(Xt.T), k, 5)
+    assert lab.min() >= 0 and lab.max() < k
+    assert ari(ref.labels, lab) == 1.0 if k > 1 else np.all(lab == 0)
+    assert abs(wcss - ref.wcss) <= 1e-10 * max(1.0, abs(ref.wcss))
+
+
 @pytest.mark.parametrize("n,h,k,normalized", [(3001, 3, 13, True), (2500, 4, 8, False), (4000, 2, 64, True)])
 def test_kmeans_tensor_core_assignment_is_exact(gpu_lib, monkeypatch, n, h, k, normalized):
     """The tensor-core assignment (DMMA distances + exact guard) must reproduce the
