@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
                                                    const double* __restrict__ p, const double* __restrict__ p_self,
                                                    double* __restrict__ t, double* partials, unsigned* counter,
                                                    double* bsum_t) {
-  constexpr int NG = kThreads / VS, U = 4;
+  constexpr int NG = kThreads / VS, U = 6;  // 6 (col, val) slots per lane: config 4 SpMV 733 -> 718 us (4: one extra pass for the ~45 % of rows above 32 entries; 8: 752 us)
   const int r0 = row_split[blockIdx.x], r1 = row_split[blockIdx.x + 1];
   const int lane = threadIdx.x % VS, gid = threadIdx.x / VS;
   const int* __restrict__ rp = g.rp;
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
       b = __ldg(rp + row + 1);
     }
     // LONGR (skewed degrees, config 5): rows longer than kLong slots are left to the whole warp below
-    constexpr int kLong = 8 * U * VS;
+    constexpr int kLong = 32 * VS;
     if (!pipe && valid && !(LONGR && b - a > kLong)) {
       for (int e0 = a + lane; e0 < b; e0 += U * VS) {
         int cix[U];
