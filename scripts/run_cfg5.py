@@ -20,6 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--restarts", type=int, default=400)
 ap.add_argument("--m", type=int, default=0)
+ap.add_argument("--kmeans", action="store_true", help="Alg. 3 step 4 after the solve (no X copy, no property checks)")
 args = ap.parse_args()
 dev = torch.device("cuda:0")
 torch.cuda.set_device(0)
@@ -41,9 +42,9 @@ del g
 torch.cuda.empty_cache()
 lib.profile_enable(ctx, True)
 t = time.time()
-Xd = torch.empty((k, out["n"]), dtype=torch.float64, device=dev)
+Xd = None if args.kmeans else torch.empty((k, out["n"]), dtype=torch.float64, device=dev)
 try:
-    ev, _, st = lib.sfairsc_eigs(ctx, k, cfg["tol"], evecs=Xd)
+    ev, _, st = lib.sfairsc_eigs(ctx, k, cfg["tol"], evecs=Xd, want_evecs=Xd is not None)
     out["status"] = "OK"
 except lib.SfairscError as e:
     st = ctx.last_stats
@@ -56,6 +57,19 @@ out["stats"] = st
 prof = lib.profile_read(ctx)
 out["eigs_kernels"] = {kk: {"ms": v["ms"], "launches": v["launches"],
                             "us": 1e3 * v["ms"] / max(1, v["launches"])} for kk, v in prof.items() if v["launches"]}
+if args.kmeans and ev is not None:
+    lab = torch.empty(out["n"], dtype=torch.int32, device=dev)
+    l0 = lib.launch_count()
+    torch.cuda.synchronize()
+    t = time.time()
+    _, wcss = lib.sfairsc_embed_kmeans(ctx, 1, lab)
+    torch.cuda.synchronize()
+    out["kmeans"] = {"s": time.time() - t, "wcss": wcss, "launches": lib.launch_count() - l0,
+                     "cluster_sizes_min_max": [int(torch.bincount(lab.long(), minlength=k).min()),
+                                               int(torch.bincount(lab.long(), minlength=k).max())]}
+    print(json.dumps(out), flush=True)
+    ctx.close()
+    sys.exit(0)
 print(json.dumps(out), flush=True)  # the solve's record first (the checks below are separate)
 ctx.close()  # the checks need the memory the basis held
 if ev is not None:
