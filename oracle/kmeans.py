@@ -76,29 +76,40 @@ def kmeanspp_seed(Y, K, seed, r):
     return np.array(idx)
 
 
+def lloyd(Y, mu, max_iters=300):
+    """Lloyd iterations from the centroids mu (R16): assign (ties to the lowest index),
+    recompute the means, re-seed every empty cluster (increasing index) at the point
+    farthest from its assigned centroid (first index of the maximum, each point used
+    once), stop when no label changes.  Returns (labels, centroids, wcss)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    mu = np.array(mu, dtype=np.float64)
+    K = mu.shape[0]
+    lab, _ = _assign(Y, mu)
+    for _it in range(max_iters):
+        mu, counts = _means(Y, lab, K, mu)
+        if np.any(counts == 0):
+            dist = _sqdist_labels(Y, mu, lab)
+            used = np.zeros(len(Y), bool)
+            for c in np.flatnonzero(counts == 0):
+                dd = np.where(used, -1.0, dist)
+                i = int(np.argmax(dd))  # first index of the maximum
+                used[i] = True
+                mu[c] = Y[i]
+        new, _ = _assign(Y, mu)
+        if np.array_equal(new, lab):
+            break
+        lab = new
+    mu, _ = _means(Y, lab, K, mu)
+    wcss = float(np.sum(_sqdist_labels(Y, mu, lab)))
+    return lab, mu, wcss
+
+
 def kmeans(Y, K, seed, n_restarts=10, max_iters=300) -> KMeansResult:
     Y = np.asarray(Y, dtype=np.float64)
     best = None
     for r in range(n_restarts):
         idx = kmeanspp_seed(Y, K, seed, r)
-        mu = Y[idx].copy()
-        lab, _ = _assign(Y, mu)
-        for _it in range(max_iters):
-            mu, counts = _means(Y, lab, K, mu)
-            if np.any(counts == 0):
-                dist = _sqdist_labels(Y, mu, lab)
-                used = np.zeros(len(Y), bool)
-                for c in np.flatnonzero(counts == 0):
-                    dd = np.where(used, -1.0, dist)
-                    i = int(np.argmax(dd))  # first index of the maximum
-                    used[i] = True
-                    mu[c] = Y[i]
-            new, _ = _assign(Y, mu)
-            if np.array_equal(new, lab):
-                break
-            lab = new
-        mu, _ = _means(Y, lab, K, mu)
-        wcss = float(np.sum(_sqdist_labels(Y, mu, lab)))
+        lab, mu, wcss = lloyd(Y, Y[idx], max_iters)
         if best is None or wcss < best.wcss:
             best = KMeansResult(lab.copy(), mu.copy(), wcss, r)
     return best

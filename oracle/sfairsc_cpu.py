@@ -14,6 +14,8 @@ Tier D (tests/test_oracle_sparse.py) at n <= 2000.
 from __future__ import annotations
 
 import dataclasses
+import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import scipy.linalg as sla
@@ -30,6 +32,20 @@ class SparseOperator:
     sigma: float
     d: np.ndarray
     normalized: bool
+    threads: int = 1  # > 1: L_n x by row blocks on a thread pool (scipy releases the GIL; same rows, same sums)
+    _blocks: list = dataclasses.field(default=None, repr=False)
+    _pool: object = dataclasses.field(default=None, repr=False)
+
+    def spmv(self, x: np.ndarray) -> np.ndarray:
+        """L_n x (or L x).  With threads > 1 the rows are cut into contiguous blocks,
+        each block's products computed by scipy exactly as in the single call."""
+        if self.threads <= 1 or x.ndim != 1:
+            return self.Ln @ x
+        if self._blocks is None:
+            cuts = np.linspace(0, self.n, self.threads + 1).astype(np.int64)
+            self._blocks = [self.Ln[cuts[i]:cuts[i + 1]] for i in range(self.threads)]
+            self._pool = ThreadPoolExecutor(self.threads)
+        return np.concatenate(list(self._pool.map(lambda B: B @ x, self._blocks)))
 
     def P(self, w: np.ndarray) -> np.ndarray:
         """P w = w - C z with z = (C^T C)^{-1} C^T w."""
@@ -41,7 +57,7 @@ class SparseOperator:
     def apply(self, w: np.ndarray) -> np.ndarray:
         """L^sigma w = P(L_n(P w)) - sigma P w + sigma w."""
         Pw = self.P(w)
-        return self.P(self.Ln @ Pw) - self.sigma * Pw + self.sigma * w
+        return self.P(self.spmv(Pw)) - self.sigma * Pw + self.sigma * w
 
     def linear_operator(self) -> spla.LinearOperator:
         return spla.LinearOperator((self.n, self.n), matvec=self.apply, matmat=self.apply,
@@ -49,7 +65,8 @@ class SparseOperator:
 
 
 def build_operator(W: sp.csr_matrix, groups: np.ndarray, h: int, normalized: bool,
-                   sigma: float | None = None, F: np.ndarray | None = None) -> SparseOperator:
+                   sigma: float | None = None, F: np.ndarray | None = None,
+                   threads: int = 1) -> SparseOperator:
     """Alg. 3 steps 1-2: L = D - W; L_n = D^{-1/2} L D^{-1/2}; C = D^{-1/2} F."""
     W = sp.csr_matrix(W)
     n = W.shape[0]
@@ -75,7 +92,9 @@ def build_operator(W: sp.csr_matrix, groups: np.ndarray, h: int, normalized: boo
     cho = sla.cho_factor(C.T @ C) if C.shape[1] > 0 else None
     if sigma is None:
         sigma = float(abs(Ln).sum(axis=0).max())  # ||L_n||_1, max column sum
-    return SparseOperator(n, Ln, C, cho, float(sigma), d, normalized)
+    if threads == 0:
+        threads = len(os.sched_getaffinity(0))
+    return SparseOperator(n, Ln, C, cho, float(sigma), d, normalized, threads)
 
 
 @dataclasses.dataclass
