@@ -13,14 +13,23 @@ k = 50 smallest eigenpairs at the residual target, incl. the final true
 residual check.  `value` = operator applies L^sigma w executed per second
 over the timed steps (whole job); `ms_per_step` = time-to-k-eigenvectors.
 
-Also reported: an apply-only measurement (back-to-back L^sigma applies),
-`roofline` of the dominant kernel from CUDA events recorded around every
-launch inside the timed region, `e2e` through the C ABI from host buffers,
-and `cpu_baseline` = the oracle (Tier S, the paper's matrix-free operator in
-scipy) timed on a bounded sample.
+The timed solves run with the library's per-launch profiling OFF.  Also
+reported: the §8(d) metric-1 apply rate (>= 200 back-to-back single-vector
+L^sigma applies, CUDA events on the launching stream, median of 5) and the
+paired-apply rate; `roofline` of the dominant kernel from one extra profiled
+solve run right after the timed region (CUDA events around every launch on
+the library's stream); `e2e` through the C ABI from pinned host buffers; and
+`cpu_baseline` = the oracle (Tier S, the paper's matrix-free operator, scipy
+SpMV threaded over the host's cores) on a bounded sample, with a host record.
+
+Multi-GPU (torchrun, N > 1): one problem row-partitioned over the ranks
+(NCCL INIT logging on, so the rank count is visible in the log).
+`--config 5 --max-restarts R` runs the 50M-vertex DC-SBM graph (generated on
+each GPU) with a fixed thick-restart budget: applies/s of the same Lanczos
+work at every N (the E(P) measurement of §8(d) metric 2).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C] [--n N] [--tol T]
+                    [--config C] [--n N] [--tol T] [--max-restarts R]
 """
 from __future__ import annotations
 
@@ -108,22 +117,45 @@ def _dist_env():
     return ws, rank, local
 
 
-def make_graph(cfg_id, n_override, rank):
-    """The BASELINE config's graph; every rank of a row-partitioned run
-    generates the same seeded graph and keeps its row block."""
+def make_graph(cfg_id, n_override, device="cpu"):
+    """The BASELINE config's graph (configs 1-4: numpy m-SBM on the host; config 5: the DC-SBM
+    generated on `device`).  Every rank of a row-partitioned run generates the same seeded graph
+    and keeps its row block."""
+    if cfg_id == 5:
+        from synth.dcsbm import config5
+        return config5(n=n_override, device=device)
     from synth import baseline_config
     return baseline_config(cfg_id, n=n_override)
 
 
-def cpu_baseline(g, cfg, budget_s=15.0):
-    """The oracle as it stands (Tier S matrix-free L^sigma apply, scipy) on a
-    bounded sample: as many applies as fit in ~budget_s.  cores = CPU-time /
-    wall-time actually used."""
-    from oracle import sfairsc_cpu
-    t0 = time.perf_counter()
-    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, cfg["normalized"])
-    t_build = time.perf_counter() - t0
-    w = np.random.default_rng(0).standard_normal(g.n)
+def host_record():
+    """The CPU the oracle baseline runs on: lscpu summary, affinity, BLAS, RAM."""
+    rec = {"logical_cpus": os.cpu_count(), "affinity_cpus": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU max MHz",
+                             "NUMA node(s)"):
+                rec[k.strip()] = v.strip()
+    except Exception as e:  # noqa: BLE001
+        rec["lscpu"] = f"unavailable: {e}"
+    try:
+        from threadpoolctl import threadpool_info
+        rec["blas"] = [{k: d.get(k) for k in ("internal_api", "version", "num_threads", "architecture")}
+                       for d in threadpool_info() if d.get("user_api") == "blas"]
+    except Exception as e:  # noqa: BLE001
+        rec["blas"] = f"unavailable: {e}"
+    try:
+        with open("/proc/meminfo") as f:
+            rec["mem_total_gb"] = round(int(f.readline().split()[1]) / 1048576, 1)
+    except Exception:  # noqa: BLE001
+        pass
+    return rec
+
+
+def _oracle_applies(op, n, budget_s, max_applies=None):
+    w = np.random.default_rng(0).standard_normal(n)
     c0 = time.process_time()
     t0 = time.perf_counter()
     cnt = 0
@@ -131,48 +163,58 @@ def cpu_baseline(g, cfg, budget_s=15.0):
         w = op.apply(w)
         w /= np.linalg.norm(w)
         cnt += 1
-        if time.perf_counter() - t0 > budget_s:
+        if time.perf_counter() - t0 > budget_s or (max_applies and cnt >= max_applies):
             break
     wall = time.perf_counter() - t0
-    cpu = time.process_time() - c0
+    return cnt, wall, time.process_time() - c0
+
+
+def cpu_baseline(g, cfg, budget_s=15.0):
+    """The oracle as it stands (Tier S matrix-free L^sigma apply: scipy CSR SpMV cut into
+    row blocks on a thread pool over every core of the affinity set, normal-equations projector on
+    the threaded BLAS) on a bounded sample: as many applies as fit in ~budget_s.  cores = CPU time /
+    wall time actually used."""
+    from oracle import sfairsc_cpu
+    t0 = time.perf_counter()
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, cfg["normalized"], threads=0)
+    t_build = time.perf_counter() - t0
+    cnt, wall, cpu = _oracle_applies(op, g.n, budget_s)
     return {"value": cnt / wall, "unit": "applies/s", "cores": max(1, round(cpu / wall)), "kind": "oracle",
-            "sample": f"{cnt} Tier-S L^sigma applies (scipy CSR SpMV + normal-equations projector, P:799-818) on "
-                      f"the same n={g.n} graph in {wall:.1f} s (operator build {t_build:.1f} s excluded); "
-                      f"host has {os.cpu_count()} logical cores",
-            "s_per_apply": wall / cnt}
+            "threads": op.threads,
+            "sample": f"{cnt} Tier-S L^sigma applies (scipy CSR SpMV on {op.threads} threads + normal-equations "
+                      f"projector, P:799-818) on the same n={g.n} graph in {wall:.1f} s (operator build "
+                      f"{t_build:.1f} s excluded); the full ARPACK solve at this size does not finish in minutes",
+            "s_per_apply": wall / cnt, "host": host_record()}
 
 
 def run_reference(args):
     ws, rank, _ = _dist_env()
     if rank != 0:
         return
-    g, cfg = make_graph(args.config, args.n, 0)
+    g, cfg = make_graph(args.config, args.n)
+    if args.config == 5:
+        g = g.host()
     from oracle import sfairsc_cpu
-    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, cfg["normalized"])
-    w = np.random.default_rng(0).standard_normal(g.n)
+    op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, cfg["normalized"], threads=0)
     per_step = args.ref_applies
     for _ in range(args.warmup):
-        for _ in range(per_step):
-            w = op.apply(w)
-            w /= np.linalg.norm(w)
-    c0 = time.process_time()
-    t0 = time.perf_counter()
+        _oracle_applies(op, g.n, 1e9, per_step)
+    cnt, wall, cpu = 0, 0.0, 0.0
     for _ in range(args.steps):
-        for _ in range(per_step):
-            w = op.apply(w)
-            w /= np.linalg.norm(w)
-    wall = time.perf_counter() - t0
-    cpu = time.process_time() - c0
-    value = args.steps * per_step / wall
+        c, w_, p_ = _oracle_applies(op, g.n, 1e9, per_step)
+        cnt, wall, cpu = cnt + c, wall + w_, cpu + p_
+    value = cnt / wall
     cores = max(1, round(cpu / wall))
     line = {"metric": METRIC, "value": value, "unit": "applies/s",
-            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(1, args.steps),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": workload(args, g, cfg["normalized"], cfg["k_eig"], cfg["tol"]),
                        "step": f"{per_step} oracle applies (the full ARPACK solve does not finish in minutes at this size)"},
             "cpu_baseline": {"value": value, "unit": "applies/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{args.steps}x{per_step} Tier-S applies, scipy, n={g.n}"},
+                             "threads": op.threads,
+                             "sample": f"{args.steps}x{per_step} Tier-S applies, scipy SpMV on {op.threads} threads, "
+                                       f"n={g.n}", "host": host_record()},
             "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -186,6 +228,8 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n", type=int, default=None, help="override n (reduced-size runs; not a bench value)")
     ap.add_argument("--tol", type=float, default=None)
+    ap.add_argument("--max-restarts", type=int, default=0,
+                    help="> 0: fixed thick-restart budget (scaling runs; the solve reports applies/s of that work)")
     ap.add_argument("--apply-reps", type=int, default=200)
     ap.add_argument("--ref-applies", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -197,9 +241,12 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    ws, rank, local = _dist_env()
+    if ws > 1:  # the rank count of every communicator shows up in the log (driver evidence)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     import torch
     import torch.distributed as dist
-    ws, rank, local = _dist_env()
     if ws > 1:
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
     torch.cuda.set_device(local)
@@ -207,35 +254,68 @@ def main():
     from paper_2210_16435_b200 import lib
 
     t_gen = time.perf_counter()
-    g, cfg = make_graph(args.config, args.n, rank)
+    g, cfg = make_graph(args.config, args.n, device=dev)
+    on_device = args.config == 5
+    torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     k = cfg["k_eig"]
     tol = args.tol if args.tol is not None else cfg["tol"]
     normalized = cfg["normalized"]
-    # N > 1: one config-4 problem row-partitioned across the ranks: each rank holds an
-    # nnz-balanced row block of W and of every n-vector; NCCL all-gather / all-reduce inside the solver
+    n_glob, nnz_glob = g.n, g.nnz
+    # N > 1: one problem row-partitioned across the ranks: each rank holds an nnz-balanced
+    # row block of W and of every n-vector; NCCL all-gather / all-reduce inside the solver
     comm, row_kw = None, {}
-    h_rp, h_ci, h_vv, h_gr = g.row_ptr, g.col, g.val, g.groups.astype(np.int32)
-    if ws > 1:
-        comm = lib.comm_from_torch(local)
-        cuts = lib.partition_rows(g.row_ptr, ws)
-        h_rp, h_ci, h_vv, h_gr = lib.row_block(g.row_ptr, g.col, g.val, g.groups, int(cuts[rank]),
-                                               int(cuts[rank + 1]))
-        row_kw = {"comm": comm, "n_global": g.n, "row_offset": int(cuts[rank])}
-    n_loc = len(h_rp) - 1
-    rp = torch.from_numpy(h_rp).to(dev)
-    ci = torch.from_numpy(h_ci).to(dev)
-    vv = torch.from_numpy(h_vv).to(dev)
-    gr = torch.from_numpy(h_gr).to(dev)
+    if on_device:
+        rp_all = g.row_ptr.cpu().numpy() if ws > 1 else None
+        r0, r1 = 0, g.n
+        if ws > 1:
+            comm = lib.comm_from_torch(local)
+            cuts = lib.partition_rows(rp_all, ws)
+            r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+            row_kw = {"comm": comm, "n_global": g.n, "row_offset": r0}
+        a, b = int(g.row_ptr[r0].item()), int(g.row_ptr[r1].item())
+        rp = (g.row_ptr[r0:r1 + 1] - a).to(torch.int32).contiguous()
+        ci = g.col[a:b].contiguous()
+        vv = g.val[a:b].contiguous()
+        gr = g.groups[r0:r1].to(torch.int32).contiguous()
+        del g
+        g = None
+        torch.cuda.empty_cache()
+        h = cfg["h"] if "h" in cfg else 8
+        h_rp = h_ci = h_vv = h_gr = None
+    else:
+        h_rp, h_ci, h_vv, h_gr = g.row_ptr, g.col, g.val, g.groups.astype(np.int32)
+        if ws > 1:
+            comm = lib.comm_from_torch(local)
+            cuts = lib.partition_rows(g.row_ptr, ws)
+            h_rp, h_ci, h_vv, h_gr = lib.row_block(g.row_ptr, g.col, g.val, g.groups, int(cuts[rank]),
+                                                   int(cuts[rank + 1]))
+            row_kw = {"comm": comm, "n_global": g.n, "row_offset": int(cuts[rank])}
+        rp = torch.from_numpy(h_rp).to(dev)
+        ci = torch.from_numpy(h_ci).to(dev)
+        vv = torch.from_numpy(h_vv).to(dev)
+        gr = torch.from_numpy(h_gr).to(dev)
+        h = g.h
+    n_loc = rp.numel() - 1
     X = torch.empty((k, n_loc), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
+    budget = {"max_restarts": args.max_restarts} if args.max_restarts > 0 else {}
+
+    def solve(ctx, evecs):
+        try:
+            ev, _, st = lib.sfairsc_eigs(ctx, k, tol, evecs=evecs, want_evecs=evecs is not None)
+        except lib.SfairscError as e:  # a restart budget ends without convergence: the work done is the step
+            if not (budget and e.name == "E_NO_CONVERGENCE"):
+                raise
+            ev, st = np.full(k, np.nan), ctx.last_stats
+        return ev, st
 
     def step(profile=False):
-        ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, normalized, h=g.h, cuda_stream=stream.cuda_stream,
-                                         **row_kw)
+        ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, normalized, h=h, cuda_stream=stream.cuda_stream,
+                                         **row_kw, **budget)
         if profile:
             lib.profile_enable(ctx, True)
-        ev, _, st = lib.sfairsc_eigs(ctx, k, tol, evecs=X)
+        ev, st = solve(ctx, X)
         prof = lib.profile_read(ctx) if profile else None
         info = ctx.info()
         ctx.close()
@@ -253,23 +333,22 @@ def main():
         step()
     barrier()
     torch.cuda.synchronize()
-    # ---- timed region (device clock, CUDA events on the launching stream) ----
+    # ---- timed region (device clock, CUDA events on the launching stream; library profiling off) ----
     launches0 = lib.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    stats, profs = [], []
+    stats = []
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(args.steps):
-            ev, st, prof, info = step(profile=True)
+            ev, st, _, info = step()
             stats.append(st)
-            profs.append(prof)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-    ms = e0.elapsed_time(e1)
+    ms = e0.elapsed_time(e1) if args.steps else 0.0
     launches = lib.launch_count() - launches0
     ms_t = torch.tensor([ms], device=dev)
     if ws > 1:
@@ -278,74 +357,93 @@ def main():
     applies = sum(s["applies"] for s in stats)  # one partitioned problem: every rank counts the same applies
     value = applies / (ms / 1e3) if ms > 0 else 0.0
 
-    # ---- per-kernel roofline (events around every launch inside the timed region) ----
+    # ---- per-kernel roofline: one extra solve with CUDA events around every launch (not timed above) ----
     peak, peak_kind = _peaks()
-    kinds = {}
-    for p in profs:
-        for name, d in p.items():
-            a = kinds.setdefault(name, {"ms": 0.0, "launches": 0, "alg_bytes": 0.0})
-            for f in a:
-                a[f] += d[f]
-    if not kinds:
-        kinds = {"spmv": {"ms": 0.0, "launches": 0, "alg_bytes": 0.0}}
-    tot_kernel_ms = sum(v["ms"] for v in kinds.values())
-    dom = max(kinds, key=lambda x: kinds[x]["ms"])
-    d = kinds[dom]
-    achieved = d["alg_bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get(dom)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs copy bandwidth)",
-                "traffic": traffic, "share_of_step": d["ms"] / ms if ms > 0 else None,
-                "alg_bytes_per_launch": d["alg_bytes"] / max(1, d["launches"]),
-                "us_per_launch": 1e3 * d["ms"] / max(1, d["launches"]),
-                "per_kernel": {kk: {"ms": v["ms"], "launches": v["launches"],
-                                    "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
-                                    "share": v["ms"] / tot_kernel_ms if tot_kernel_ms else None}
-                               for kk, v in sorted(kinds.items(), key=lambda x: -x[1]["ms"]) if v["launches"]}}
+    roofline = None
+    if args.steps:
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        _, pst, prof, _ = step(profile=True)
+        p1.record(stream)
+        torch.cuda.synchronize()
+        prof_ms = p0.elapsed_time(p1)
+        kinds = {kk: v for kk, v in prof.items() if v["launches"]}
+        tot_kernel_ms = sum(v["ms"] for v in kinds.values())
+        dom = max(kinds, key=lambda x: kinds[x]["ms"])
+        d = kinds[dom]
+        achieved = d["alg_bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(dom)
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "frac_of_8TBps_nominal": achieved / 8000.0,
+                    "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs copy bandwidth)",
+                    "traffic": traffic, "share_of_step": d["ms"] / prof_ms if prof_ms > 0 else None,
+                    "alg_bytes_per_launch": d["alg_bytes"] / max(1, d["launches"]),
+                    "us_per_launch": 1e3 * d["ms"] / max(1, d["launches"]),
+                    "measured": "one profiled solve right after the timed region: CUDA events around every launch "
+                                "on the library's (= the bench's) stream; algorithmic bytes per DESIGN.md §6",
+                    "profiled_solve_ms": prof_ms, "profiled_solve_applies": pst["applies"],
+                    "per_kernel": {kk: {"ms": v["ms"], "launches": v["launches"],
+                                        "us_per_launch": 1e3 * v["ms"] / v["launches"],
+                                        "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
+                                        "share": v["ms"] / tot_kernel_ms if tot_kernel_ms else None}
+                                   for kk, v in sorted(kinds.items(), key=lambda x: -x[1]["ms"])}}
 
-    # ---- apply-only: back-to-back L^sigma applies (north-star apply metric) ----
-    ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, normalized, h=g.h, cuda_stream=stream.cuda_stream,
-                                     **row_kw)
+    # ---- applies: §8(d) metric 1 (single-vector, >= 200 back-to-back, median of 5) and paired ----
+    ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, normalized, h=h, cuda_stream=stream.cuda_stream, **row_kw)
     info = ctx.info()
-    nv = 8
-    xs = torch.randn((nv, n_loc), dtype=torch.float64, device=dev)
+    reps = max(200, args.apply_reps)
+    x1 = torch.randn(n_loc, dtype=torch.float64, device=dev, generator=torch.Generator(dev).manual_seed(7))
+    nb = 8 if ws == 1 else 1
+    xs = x1.repeat(nb, 1)
     ys = torch.empty_like(xs)
+    single = lib.sfairsc_apply_single if ws == 1 else lib.sfairsc_apply
     for _ in range(2):
-        lib.sfairsc_apply(ctx, xs, ys)
-    lib.profile_enable(ctx, True)
-    reps = max(1, args.apply_reps // nv)
+        single(ctx, xs, ys)
     a0 = torch.cuda.Event(enable_timing=True)
     a1 = torch.cuda.Event(enable_timing=True)
-    a0.record(stream)
-    for _ in range(reps):
-        lib.sfairsc_apply(ctx, xs, ys)
-    a1.record(stream)
-    torch.cuda.synchronize()
-    apply_ms = a0.elapsed_time(a1) / (reps * nv)
-    ap_prof = lib.profile_read(ctx)
+    runs = []
+    for _ in range(5):
+        barrier()
+        a0.record(stream)
+        for _ in range(reps // nb):
+            single(ctx, xs, ys)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        runs.append(a0.elapsed_time(a1) / ((reps // nb) * nb))
+    apply_ms = float(np.median(runs))
+    n, nnz = n_glob, nnz_glob
+    alg_single = 12.0 * nnz + 4.0 * (n + 1) + 9.0 * n + 16.0 * n  # CSR + (d or s) + g + w + y
+    apply_only = {"metric1_single_applies_per_s": 1e3 / apply_ms, "us_per_apply": 1e3 * apply_ms,
+                  "alg_bytes_per_apply": alg_single, "alg_GBps": alg_single / (apply_ms / 1e3) / 1e9,
+                  "frac_of_peak": alg_single / (apply_ms / 1e3) / 1e9 / peak,
+                  "frac_of_8TBps_nominal": alg_single / (apply_ms / 1e3) / 1e9 / 8000.0,
+                  "runs_us": [1e3 * r for r in runs], "applies_per_run": (reps // nb) * nb,
+                  "how": "sfairsc_apply_ex(SFAIRSC_APPLY_SINGLE) on copies of one seeded vector, one SpMV per apply; "
+                         "CUDA events on the launching stream around each run, median of 5 runs"}
+    if ws == 1 and h <= 16:  # interleaved pairs: one SpMM per two applies
+        for _ in range(2):
+            lib.sfairsc_apply(ctx, xs, ys)
+        a0.record(stream)
+        for _ in range(reps // nb):
+            lib.sfairsc_apply(ctx, xs, ys)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        pair_ms = a0.elapsed_time(a1) / ((reps // nb) * nb)
+        alg_pair = (12.0 * nnz + 4.0 * (n + 1) + 9.0 * n) / 2.0 + 16.0 * n
+        apply_only["paired"] = {"applies_per_s": 1e3 / pair_ms, "us_per_apply": 1e3 * pair_ms,
+                                "alg_bytes_per_apply": alg_pair, "alg_GBps": alg_pair / (pair_ms / 1e3) / 1e9}
     ctx.close()
-    n, nnz = g.n, g.nnz
-    # algorithmic bytes per apply: CSR + w + y + d|s + g; the library applies vectors in pairs through one
-    # SpMM of the interleaved pair (h <= 16), so the CSR, d|s and g are read once per two applies
-    paired = g.h <= 16 and nv >= 2 and ws == 1
-    alg_apply = ((12.0 * nnz + 4.0 * (n + 1) + 9.0 * n) / (2.0 if paired else 1.0)) + 8.0 * n * 2
-    spmv_alg = ap_prof["spmv"]["alg_bytes"] / max(1, ap_prof["spmv"]["launches"])
-    spmv_us = 1e3 * ap_prof["spmv"]["ms"] / max(1, ap_prof["spmv"]["launches"])
-    apply_only = {"applies_per_s": 1e3 / apply_ms, "us_per_apply": 1e3 * apply_ms,
-                  "alg_bytes_per_apply": alg_apply, "alg_GBps": alg_apply / (apply_ms / 1e3) / 1e9,
-                  "frac_of_peak": alg_apply / (apply_ms / 1e3) / 1e9 / peak,
-                  "frac_of_8TBps_nominal": alg_apply / (apply_ms / 1e3) / 1e9 / 8000.0,
-                  "spmv_us": spmv_us, "spmv_alg_GBps": spmv_alg / (spmv_us / 1e6) / 1e9,
-                  "paired": paired,
-                  "note": "events around each of the 4 kernels add ~1-2 us per kernel; the us_per_apply bracket is one event pair per batch"}
 
     # ---- e2e through the C ABI from pinned host buffers ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.steps:
+        if on_device:
+            h_rp, h_ci, h_vv, h_gr = rp.cpu().numpy(), ci.cpu().numpy(), vv.cpu().numpy(), gr.cpu().numpy()
         hrp = torch.from_numpy(h_rp).pin_memory()
         hci = torch.from_numpy(h_ci).pin_memory()
         hvv = torch.from_numpy(h_vv).pin_memory()
@@ -356,9 +454,9 @@ def main():
         t0 = time.perf_counter()
         e2e_app = 0
         for _ in range(args.steps):
-            ctx = lib.sfairsc_build_operator(hrp, hci, hvv, hgr, k, normalized, h=g.h, cuda_stream=stream.cuda_stream,
-                                             **row_kw)
-            ev, _, st = lib.sfairsc_eigs(ctx, k, tol, evecs=hX)
+            ctx = lib.sfairsc_build_operator(hrp, hci, hvv, hgr, k, normalized, h=h, cuda_stream=stream.cuda_stream,
+                                             **row_kw, **budget)
+            _, st = solve(ctx, hX)
             e2e_app += st["applies"]
             ctx.close()
         torch.cuda.synchronize()
@@ -374,9 +472,9 @@ def main():
 
     # ---- Alg. 3 step 4 (not part of the metric): k-means on the rows of H, labels left on the device ----
     kmeans = None
-    if ws == 1 and not args.no_kmeans and not args.apply_only:
-        ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, normalized, h=g.h, cuda_stream=stream.cuda_stream)
-        lib.sfairsc_eigs(ctx, k, tol, evecs=X)
+    if ws == 1 and not args.no_kmeans and not args.apply_only and not budget:
+        ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, normalized, h=h, cuda_stream=stream.cuda_stream)
+        solve(ctx, X)
         lab = torch.empty(n_loc, dtype=torch.int32, device=dev)
         l0 = lib.launch_count()
         torch.cuda.synchronize()
@@ -389,12 +487,12 @@ def main():
         ctx.close()
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not on_device:
         cpu = cpu_baseline(g, cfg)
 
     if rank == 0 and args.apply_only:
-        print(json.dumps({"apply_only": apply_only, "n": g.n, "nnz": g.nnz, "spmv_vector": info["spmv_vector"],
-                          "generator_s": t_gen, "apply_profile": ap_prof}), flush=True)
+        print(json.dumps({"apply_only": apply_only, "n": n_glob, "nnz": nnz_glob, "spmv_vector": info["spmv_vector"],
+                          "generator_s": t_gen}), flush=True)
     elif rank == 0:
         last = stats[-1]
         line = {
@@ -403,18 +501,22 @@ def main():
             "ms_per_step": ms / max(1, args.steps), "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(args, g, normalized, k, tol),
-                       "step": "build operator from device CSR (A0-A3) + thick-restart Lanczos to k eigenpairs (A4-A11)",
-                       "l2": f"inputs larger than L2 (CSR {(12 * g.nnz + 4 * g.n) / 1e9:.2f} GB, Krylov basis "
-                             f"{8 * g.n * (last['basis_size'] + 1) / 1e9:.2f} GB >> 126 MB)",
+            "config": {"workload": f"BASELINE config {args.config}" + (" (reduced n)" if args.n else "")
+                                   + f": normalized={normalized} {'DC-SBM' if args.config == 5 else 'm-SBM'} "
+                                     f"n={n_glob}, nnz={nnz_glob}, h={h}, k={k}, tol={tol}"
+                                   + (f", thick-restart budget {args.max_restarts}" if budget else ""),
+                       "step": "build operator from device CSR (A0-A3) + thick-restart Lanczos to k eigenpairs (A4-A11)"
+                               + (f"; stopped after {args.max_restarts} restarts (fixed work per N)" if budget else ""),
+                       "l2": f"inputs larger than L2 (CSR {(12 * nnz_glob + 4 * n_glob) / 1e9:.2f} GB, Krylov basis "
+                             f"{8 * n_glob * (last['basis_size'] + 1) / 1e9:.2f} GB >> 126 MB)",
                        "parallelism": "1 GPU" if ws == 1 else f"row-partitioned over {ws} GPUs (NCCL all-gather of "
                                                                f"the projected vector + fused all-reduces per step)",
                        "generator_s": t_gen},
-            "solve": {"applies_per_step": applies / args.steps, "steps": last["steps"], "restarts": last["restarts"],
-                      "breakdowns": last["breakdowns"], "max_resid_rel": last["max_resid_rel"],
-                      "gap_est": last["gap_est"], "sigma": last["sigma"], "converged": last["converged"],
-                      "basis": last["basis_size"], "kept": last["kept"], "lambda_k": float(ev[-1]),
-                      "lambda_2": float(ev[1]) if len(ev) > 1 else None},
+            "solve": {"applies_per_step": applies / max(1, args.steps), "steps": last["steps"],
+                      "restarts": last["restarts"], "breakdowns": last["breakdowns"],
+                      "max_resid_rel": last["max_resid_rel"], "gap_est": last["gap_est"], "sigma": last["sigma"],
+                      "converged": last["converged"], "basis": last["basis_size"], "kept": last["kept"],
+                      "lambda_k": float(ev[-1]), "lambda_2": float(ev[1]) if len(ev) > 1 else None},
             "apply_only": apply_only,
             "roofline": roofline,
             "e2e": e2e,

@@ -180,6 +180,12 @@ sfairsc_status sfairsc_embed_kmeans(sfairsc_ctx *ctx, uint64_t seed, int32_t *la
  * y = t - s o (gamma_t - sigma gamma_x)_g.  x, y: n x nvec, same memspace. */
 sfairsc_status sfairsc_apply(sfairsc_ctx *ctx, const double *x, double *y, int32_t nvec,
                              int32_t memspace);
+/* sfairsc_apply with flags: SFAIRSC_APPLY_SINGLE = every vector through its own
+ * single-vector SpMV (no interleaved pairs) — the §8(d) metric-1 apply, one L^sigma
+ * application at a time.  Same arguments, ownership and errors as sfairsc_apply. */
+#define SFAIRSC_APPLY_SINGLE 1
+sfairsc_status sfairsc_apply_ex(sfairsc_ctx *ctx, const double *x, double *y, int32_t nvec,
+                                int32_t memspace, int32_t flags);
 
 /* y = P x (P:807-818 in factored form) for nvec column vectors. */
 sfairsc_status sfairsc_project(sfairsc_ctx *ctx, const double *x, double *y, int32_t nvec,

@@ -22,7 +22,7 @@ INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(PKG, "build")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsfairsc.so")
-SOURCES = ["kernels.cu", "krylov.cu", "block.cu", "abi.cu", "lanczos_block.cu", "lanczos1.cu", "dist.cu", "kmeans.cu", "symeig.cpp"]
+SOURCES = ["kernels.cu", "krylov.cu", "block.cu", "abi.cu", "lanczos_block.cu", "lanczos1.cu", "dist.cu", "kmeans.cu", "spmv_tma.cu", "symeig.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]

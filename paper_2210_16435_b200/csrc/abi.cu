@@ -95,7 +95,7 @@ static void free_ctx(sfairsc_ctx* c) {
   if (!c) return;
   if (c->dist) dist_free(c->dist);
   if (c->km && c->km_free) c->km_free(c->km);
-  void* ptrs[] = {c->rp, c->ci, c->row_split, c->vv, c->dg, c->s, c->grp, c->isb, c->uh, c->partials, c->counters,
+  void* ptrs[] = {c->tiles, c->cta_tiles, c->prp, c->pci, c->pvv, c->rp, c->ci, c->row_split, c->vv, c->dg, c->s, c->grp, c->isb, c->uh, c->partials, c->counters,
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
                   c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta,
                   c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags, c->Hdev, c->sdev, c->lz, c->partials2, c->dd, c->rpb,
@@ -221,6 +221,16 @@ void sfz::ctx_spmv(sfairsc_ctx* c, const double* p, double* t, const double* q_p
   } else if (c->unit_spmv() && c->normalized) {
     launch_scale_vec(c->s, p, c->vq, c->n, c->st);
     pg = c->vq;
+  }
+  if (c->nblk <= 1 && c->tiles && !c->Qr) {
+    GraphDev g = c->gs();
+    g.rp = c->prp;
+    g.ci = c->pci;
+    g.vv = c->pvv;
+    g.nnz = c->nnz_pad;
+    launch_spmv_tma(g, c->vs, c->tiles, c->cta_tiles, c->tma_grid, pg, p, t, c->partials, c->counters + 1, c->bs_t,
+                    c->st);
+    return;
   }
   if (c->nblk <= 1) {
     launch_spmm(c->gs(), 1, c->vs, c->row_split, c->spmv_grid, pg, t, c->partials, c->counters + 1, c->bs_t, c->st, p);
@@ -447,9 +457,10 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   }
 
   // device allocations
-  CUB(dalloc(&c->rp, n + 1));
-  CUB(dalloc(&c->ci, nnz));
-  CUB(dalloc(&c->vv, nnz));
+  // CSR padded by 8 entries: the TMA SpMV's bulk copies round their ranges out to 16-byte boundaries
+  CUB(dalloc(&c->rp, n + 1 + 8));
+  CUB(dalloc(&c->ci, nnz + 8));
+  CUB(dalloc(&c->vv, nnz + 8));
   // per-vertex arrays padded to ldv rows (the TMA sweeps stage whole 64-row chunks)
   CUB(dalloc(&c->dg, c->ldv));
   CUB(cudaMemset(c->dg, 0, sizeof(double) * c->ldv));
@@ -622,6 +633,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     c->spmv_grid = G;
     CUB(dalloc(&c->row_split, G + 1));
     CUB(cudaMemcpyAsync(c->row_split, split.data(), sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, c->st));
+
     const double mean_deg = n > 0 ? (double)nnz / n : 0.0;
     {
       int maxdeg = 0;
@@ -630,9 +642,35 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     }
     int vs = 2;
     while (vs < 32 && vs * 4 < mean_deg) vs *= 2;
+    const bool tma = c->nblk <= 1 && nnz > 0 && !c->Qr && !(getenv("SFAIRSC_SPMV_TMA") && atoi(getenv("SFAIRSC_SPMV_TMA")) == 0);
+    if (tma) {  // the TMA SpMV's lane reads 4-entry blocks: VS = largest power of two <= mean degree / 4
+      vs = 2;
+      while (vs < 32 && vs * 8 <= mean_deg) vs *= 2;
+    }
     c->vs = opts.spmv_vector > 0 ? opts.spmv_vector : vs;
     if (c->vs != 2 && c->vs != 4 && c->vs != 8 && c->vs != 16 && c->vs != 32)
       return bail(fail(SFAIRSC_E_INVALID_ARG, "spmv_vector must be 2,4,8,16 or 32"));
+    // TMA-fed SpMV (spmv_tma.cu): row-aligned tiles
+    // padded CSR copy (rows start at multiples of 4 entries) + tiles; the plain CSR stays for the other kernels
+    if (tma) {
+      std::vector<int2> tiles;
+      std::vector<int> cta, prp;
+      spmv_tma_layout(hrp.data(), n, spmv_tma_ctas_per_sm(c->vs, c->normalized, c->unit_spmv()) * c->num_sms, prp,
+                      tiles, cta);
+      c->tma_grid = (int)cta.size() - 1;
+      CUB(dalloc(&c->tiles, tiles.size()));
+      CUB(dalloc(&c->cta_tiles, cta.size()));
+      CUB(dalloc(&c->prp, prp.size() + 8));
+      c->nnz_pad = prp[n];
+      CUB(dalloc(&c->pci, (size_t)prp[n]));
+      if (!c->unit_spmv()) CUB(dalloc(&c->pvv, (size_t)prp[n]));
+      CUB(cudaMemcpyAsync(c->tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, c->st));
+      CUB(cudaMemcpyAsync(c->cta_tiles, cta.data(), sizeof(int) * cta.size(), cudaMemcpyHostToDevice, c->st));
+      CUB(cudaMemcpyAsync(c->prp, prp.data(), sizeof(int) * prp.size(), cudaMemcpyHostToDevice, c->st));
+      launch_pad_csr(c->rp, c->ci, c->pvv ? c->vv : nullptr, n, c->prp, c->pci, c->pvv, c->st);
+      CUB(cudaGetLastError());
+      CUB(cudaStreamSynchronize(c->st));  // the host vectors die here
+    }
   }
   // partial buffers: max over users
   {
@@ -840,7 +878,7 @@ extern "C" void sfairsc_destroy(sfairsc_ctx* c) {
 // apply / project / laplacian entry points
 // --------------------------------------------------------------------------
 static sfairsc_status vec_io(sfairsc_ctx* c, const double* x, double* y, int32_t nvec, int32_t memspace,
-                             sfairsc_status (*op)(sfairsc_ctx*, const double*, double*)) {
+                             sfairsc_status (*op)(sfairsc_ctx*, const double*, double*), bool allow_pairs = true) {
   if (!c || !x || !y || nvec < 0) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
   if (memspace != SFAIRSC_MEM_HOST && memspace != SFAIRSC_MEM_DEVICE) return fail(SFAIRSC_E_INVALID_ARG, "memspace");
   if (c->dist) {  // row-partitioned: vectors hold this process's rows; only the operator apply is offered
@@ -864,7 +902,7 @@ static sfairsc_status vec_io(sfairsc_ctx* c, const double* x, double* y, int32_t
   }
   const size_t nb = sizeof(double) * c->n;
   int v0 = 0;
-  if (op == apply_dev && pair_ok(c) && nvec >= 2 && memspace == SFAIRSC_MEM_DEVICE) {
+  if (op == apply_dev && allow_pairs && pair_ok(c) && nvec >= 2 && memspace == SFAIRSC_MEM_DEVICE) {
     for (; v0 + 1 < nvec; v0 += 2)
       TRY(apply_pair_dev(c, x + (size_t)v0 * c->n, x + (size_t)(v0 + 1) * c->n, y + (size_t)v0 * c->n,
                          y + (size_t)(v0 + 1) * c->n));
@@ -902,6 +940,11 @@ static sfairsc_status lap_dev(sfairsc_ctx* c, const double* x, double* y) {
 
 extern "C" sfairsc_status sfairsc_apply(sfairsc_ctx* c, const double* x, double* y, int32_t nvec, int32_t memspace) {
   return vec_io(c, x, y, nvec, memspace, apply_dev);
+}
+extern "C" sfairsc_status sfairsc_apply_ex(sfairsc_ctx* c, const double* x, double* y, int32_t nvec,
+                                           int32_t memspace, int32_t flags) {
+  if (flags & ~SFAIRSC_APPLY_SINGLE) return fail(SFAIRSC_E_INVALID_ARG, "unknown apply flags");
+  return vec_io(c, x, y, nvec, memspace, apply_dev, (flags & SFAIRSC_APPLY_SINGLE) == 0);
 }
 extern "C" sfairsc_status sfairsc_project(sfairsc_ctx* c, const double* x, double* y, int32_t nvec,
                                           int32_t memspace) {

@@ -83,6 +83,12 @@ struct sfairsc_ctx {
   int tma_mode2 = 0;   // update+norm sweep: register kernel (measured faster); env SFAIRSC_TMA_MODE2=1: TMA
   // device buffers
   int *rp = nullptr, *ci = nullptr, *row_split = nullptr;
+  int2* tiles = nullptr;       // TMA SpMV tiles (spmv_tma.cu): (first row, first entry), ntiles + 1
+  int* cta_tiles = nullptr;    // tile range per CTA, tma_grid + 1
+  int tma_grid = 0;
+  int *prp = nullptr, *pci = nullptr;  // padded CSR of the TMA SpMV (rows at multiples of 4 entries, pads col = -1)
+  double* pvv = nullptr;               // its values, split block layout (nullptr: unit-weight pattern SpMV)
+  int nnz_pad = 0;                     // padded entries (a multiple of 4)
   double *vv = nullptr, *dg = nullptr, *s = nullptr;
   uint8_t* grp = nullptr;
   double *isb = nullptr, *uh = nullptr;

@@ -133,9 +133,25 @@ namespace {
 constexpr int kDT = 256;
 
 // col -> owner * n_max + (col - cut_owner); flags: out of range / diagonal / unsorted / negative
+// symmetry fingerprint of an entry (i, j, w): W = W^T  <=>  the multiset {(i, j, w)} equals {(j, i, w)},
+// so sum_e [h(i, j, w) - h(j, i, w)] = 0 (mod 2^64) over all entries of all parts; an asymmetric W leaves
+// a nonzero sum except with probability ~2^-64 (h asymmetric in (i, j), splitmix64 finaliser)
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ unsigned long long sym_hash(long long i, long long j, double w) {
+  return mix64(mix64((unsigned long long)i) ^ ((unsigned long long)j * 0xD6E8FEB86659FD93ull)) ^
+         mix64((unsigned long long)__double_as_longlong(w));
+}
+
 __global__ void k_remap_validate(const int* rp, int* ci, const double* vv, int n_loc, long long r0, long long n,
-                                 const long long* cuts, int nparts, int n_max, int* flags) {
+                                 const long long* cuts, int nparts, int n_max, int* flags,
+                                 unsigned long long* symsum) {
   int f = 0, nonunit = 0;
+  unsigned long long hs = 0ull;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_loc; i += gridDim.x * blockDim.x) {
     const int a = rp[i], b = rp[i + 1];
     if (b < a) {
@@ -149,6 +165,7 @@ __global__ void k_remap_validate(const int* rp, int* ci, const double* vv, int n
       if (j == r0 + i && vv[e] != 0.0) f |= 1;
       if (!(vv[e] >= 0.0)) f |= 2;
       if (vv[e] != 1.0 || j == r0 + i) nonunit = 1;
+      if (j >= 0 && j < n) hs += sym_hash(r0 + i, j, vv[e]) - sym_hash(j, r0 + i, vv[e]);
       prev = j;
       int lo = 0, hi = nparts - 1;  // owner: cuts[o] <= j < cuts[o+1]
       while (lo < hi) {
@@ -160,6 +177,7 @@ __global__ void k_remap_validate(const int* rp, int* ci, const double* vv, int n
   }
   if (f) atomicOr(flags, f);
   if (nonunit) atomicOr(flags + 1, 1);  // local, informational: this part's rows are not a unit-weight pattern
+  if (hs) atomicAdd(symsum, hs);        // integer: order-independent
 }
 
 __global__ void k_degrees_d(const int* rp, const double* vv, int n_loc, double* d, int* flags) {
@@ -481,7 +499,10 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
   D->parts.resize(D->P);
   const int m = c->m;
   int hflags = 0;
-  for (int q = 0; q < D->P; ++q) {
+  // per-part setup; a failure (e.g. OOM) on one rank must not leave the others blocked in the collectives
+  // below, so the first local failure is recorded and agreed on (max over ranks) with the CSR flags
+  unsigned long long symsum = 0ull;
+  auto build_part = [&](int q) -> sfairsc_status {
     DistPart& p = D->parts[q];
     p.q = D->part0 + q;
     const long long a = D->comm ? 0 : D->cuts[q], b = D->comm ? W->n_rows : D->cuts[q + 1];  // rows in W
@@ -519,6 +540,7 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
     CU(cudaMemsetAsync(p.counters, 0, 16 * sizeof(unsigned), st));
     CU(dal(&p.flags, 8));
     CU(cudaMemsetAsync(p.flags, 0, 8 * sizeof(int), st));
+    unsigned long long* psym = reinterpret_cast<unsigned long long*>(p.flags + 2);
     CU(dal(&p.small, 1024));
     CU(cudaMemsetAsync(p.small, 0, 1024 * sizeof(double), st));
     for (double** v : {&p.vr, &p.vy, &p.vt}) {
@@ -534,7 +556,7 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
     // A0: remap columns to the gathered layout + local validation
     bump_launch();
     k_remap_validate<<<grid_for(p.n_loc), kDT, 0, st>>>(p.rp, p.ci, p.vv, p.n_loc, p.r0, D->n, D->cuts_dev,
-                                                        D->P_total, D->n_max, p.flags);
+                                                        D->P_total, D->n_max, p.flags, psym);
     // A1: degrees
     bump_launch();
     k_degrees_d<<<grid_for(p.n_loc), kDT, 0, st>>>(p.rp, p.vv, p.n_loc, p.dg, p.flags);
@@ -572,24 +594,52 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
     const size_t pc = std::max<size_t>((size_t)p.spmv_grid * 4 * kBT, (size_t)c->num_sms * 8 * (kMaxJ + 2));
     CU(dal(&p.partials, pc));
     CU(dal(&p.partials2, (size_t)c->num_sms * 8 * (kHB + 2)));
-    int f2[2] = {0, 0};
-    CU(cudaMemcpyAsync(f2, p.flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    int f2[4] = {0, 0, 0, 0};
+    CU(cudaMemcpyAsync(f2, p.flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     hflags |= f2[0];
+    unsigned long long ps_ = 0ull;
+    std::memcpy(&ps_, f2 + 2, sizeof(ps_));
+    symsum += ps_;
     // unit weights (unnormalized): each part decides for its own rows; the gathered p~ is used as is
     p.unit = !c->normalized && p.nnz_loc > 0 && f2[1] == 0 &&
              !(getenv("SFAIRSC_UNIT") && atoi(getenv("SFAIRSC_UNIT")) == 0);
+      return SFAIRSC_OK;
+  };
+  sfairsc_status local_st = SFAIRSC_OK;
+  std::string local_msg;
+  for (int q = 0; q < D->P && local_st == SFAIRSC_OK; ++q) {
+    local_st = build_part(q);
+    if (local_st != SFAIRSC_OK) local_msg = sfairsc_last_error();
   }
-  // flags: OR over all parts (max over ranks)
-  {
-    double fl = (double)hflags;
+  // symmetry: the fingerprint sums of all parts / ranks must cancel (mod 2^64).  Across NCCL ranks they
+  // are summed as four 16-bit limbs in doubles (exact), recombined mod 2^64; every rank takes part even
+  // after a local failure (its limbs are then 0 and its status is agreed on below).
+  if (D->comm) {
+    double limbs[4];
+    for (int q = 0; q < 4; ++q) limbs[q] = local_st == SFAIRSC_OK ? (double)((symsum >> (16 * q)) & 0xFFFFull) : 0.0;
     double* t = D->parts[0].scal();
-    CU(cudaMemcpyAsync(t, &fl, sizeof(double), cudaMemcpyHostToDevice, st));
-    TRY(allreduce(D, st, 1, [](const DistPart& p) { return p.scal(); }, true));
-    CU(cudaMemcpyAsync(&fl, t, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(t, limbs, 4 * sizeof(double), cudaMemcpyHostToDevice, st));
+    TRY(allreduce(D, st, 4, [](const DistPart& p) { return p.scal(); }));
+    CU(cudaMemcpyAsync(limbs, t, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    hflags = (int)fl;
+    symsum = 0ull;
+    for (int q = 0; q < 4; ++q) symsum += (unsigned long long)limbs[q] << (16 * q);  // carries wrap mod 2^64
   }
+  if (symsum != 0ull && c->check_symmetry) hflags |= 4;
+  // flags and the local status: max over parts / ranks
+  {
+    double fl[2] = {(double)hflags, (double)local_st};
+    double* t = D->parts[0].scal();
+    CU(cudaMemcpyAsync(t, fl, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+    TRY(allreduce(D, st, 2, [](const DistPart& p) { return p.scal(); }, true));
+    CU(cudaMemcpyAsync(fl, t, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    hflags = (int)fl[0];
+    if (local_st != SFAIRSC_OK) return fail(local_st, "%s", local_msg.c_str());
+    if ((int)fl[1] != SFAIRSC_OK) return fail((sfairsc_status)(int)fl[1], "another rank failed its build (status %d)", (int)fl[1]);
+  }
+  if (hflags & 4) return fail(SFAIRSC_E_ASYMMETRIC, "W is not symmetric (distributed fingerprint of (i, j, w) vs (j, i, w))");
   if (hflags & 1) return fail(SFAIRSC_E_CSR_INVALID, "CSR invalid (row_ptr/col range, unsorted or duplicate columns, or nonzero diagonal)");
   if (hflags & 2) return fail(SFAIRSC_E_NEGATIVE_WEIGHT, "negative or NaN weight (P:121)");
   if (hflags & 8) return fail(SFAIRSC_E_ISOLATED_VERTEX, "isolated vertex: d_i = 0 (P:127-128)");

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace sfz {
 
 constexpr int kThreads = 256;  // CTA size of every streaming kernel
@@ -194,6 +196,16 @@ void launch_pair_project(const GraphDev& g, const ProjDesc& pd, const double* x0
                          const double* bsum, double* p, cudaStream_t st);
 void launch_pair_finish(const GraphDev& g, const ProjDesc& pd, const double* t, const double* bsum_t,
                         const double* bsum_x, double sigma, double* y0, double* y1, cudaStream_t st);
+
+// TMA-fed single-vector SpMV (spmv_tma.cu): t = L p + epilogue B^T t, p^T t (same outputs as launch_spmv)
+int spmv_tma_ctas_per_sm(int vs, bool normalized, bool unit);
+void spmv_tma_layout(const int* hrp, int n, int G, std::vector<int>& prp, std::vector<int2>& tiles,
+                     std::vector<int>& cta_tiles);
+void launch_pad_csr(const int* rp, const int* ci, const double* vv, int n, const int* prp, int* pci, double* pvv,
+                    cudaStream_t st);
+void launch_spmv_tma(const GraphDev& g, int vs, const int2* tiles, const int* cta_tiles, int grid, const double* p,
+                     const double* p_self, double* t, double* partials, unsigned* counter, double* bsum_t,
+                     cudaStream_t st);
 
 // ---- dense constraint basis (§8(f) N4) -----------------------------------------------
 // out[a*r + b] (a <= b) = sum_i M(i,a) M(i,b), M(i,a) = M[i*rs + a*cs] (fixed-order block reduction)

@@ -83,6 +83,7 @@ def _load():
         "sfairsc_eigs": (C.c_int, [P, C.c_int32, C.c_double, P, P, C.c_int32, C.POINTER(Stats)]),
         "sfairsc_embed_kmeans": (C.c_int, [P, C.c_uint64, P, C.c_int32, P]),
         "sfairsc_apply": (C.c_int, [P, P, P, C.c_int32, C.c_int32]),
+        "sfairsc_apply_ex": (C.c_int, [P, P, P, C.c_int32, C.c_int32, C.c_int32]),
         "sfairsc_project": (C.c_int, [P, P, P, C.c_int32, C.c_int32]),
         "sfairsc_laplacian": (C.c_int, [P, P, P, C.c_int32]),
         "sfairsc_get_info": (C.c_int, [P, C.POINTER(Info)]),
@@ -287,6 +288,14 @@ def _vec_call(fn, ctx, x, y):
 def sfairsc_apply(ctx: Context, x, y=None):
     """y = L^sigma x; x is (n,) or (nvec, n) (rows = vectors)."""
     return _vec_call(_lib.sfairsc_apply, ctx, x, y)
+
+
+APPLY_SINGLE = 1
+
+
+def sfairsc_apply_single(ctx: Context, x, y=None):
+    """y = L^sigma x one vector per SpMV (sfairsc_apply_ex with SFAIRSC_APPLY_SINGLE)."""
+    return _vec_call(lambda h, xp, yp, nv, ms: _lib.sfairsc_apply_ex(h, xp, yp, nv, ms, APPLY_SINGLE), ctx, x, y)
 
 
 def sfairsc_project(ctx: Context, x, y=None):

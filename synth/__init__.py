@@ -10,7 +10,7 @@ concrete parameterisations, plus the small structured
 graphs the oracle pins use (disjoint cliques, P-closed-1 in SURVEY §8(c)).
 """
 from .msbm import (MSBMGraph, msbm, baseline_config, exp1_msbm, planted_cliques,
-                   random_graph, random_laplacian, CONFIGS)
+                   random_graph, random_laplacian, hub_graph, CONFIGS)
 
 __all__ = ["MSBMGraph", "msbm", "baseline_config", "exp1_msbm", "planted_cliques",
-           "random_graph", "random_laplacian", "CONFIGS"]
+           "random_graph", "random_laplacian", "hub_graph", "CONFIGS"]

@@ -376,3 +376,22 @@ def random_graph(n, h, *, p=0.3, seed=0, weights="uniform", group_counts=None) -
     w = np.ones(len(keys)) if weights == "unit" else _rng(seed, 5).uniform(0.5, 1.5, len(keys))
     row_ptr, col, val = _to_csr(n, keys, w)
     return MSBMGraph(n, row_ptr, col, val, groups, clusters, h, 0, dict(name="random", p=p, seed=seed))
+
+
+def hub_graph(n, h, *, hub_degrees=(1500, 5000), p=0.004, seed=0, weights="uniform") -> MSBMGraph:
+    """G(n, p) plus hub vertices 0, 1, ... joined to hub_degrees[i] distinct random vertices:
+    rows longer than any SpMV tile (edge cases of the row-aligned tiling).  For oracle pins."""
+    groups = _draw_groups(n, h, seed, None, None)
+    clusters = np.full(n, -1, np.int32)
+    rng = _rng(seed, 4)
+    iu, ju = np.triu_indices(n, 1)
+    hit = rng.random(len(iu)) < p
+    keys = [iu[hit].astype(np.int64) * n + ju[hit]]
+    for hub, deg in enumerate(hub_degrees):
+        nb = rng.choice(np.arange(hub + 1, n), size=min(deg, n - hub - 1), replace=False)
+        keys.append(hub * n + nb.astype(np.int64))
+    keys = _sorted_unique(np.concatenate(keys))
+    keys, _ = _repair_isolated(n, keys, clusters, seed)
+    w = np.ones(len(keys)) if weights == "unit" else _rng(seed, 5).uniform(0.5, 1.5, len(keys))
+    row_ptr, col, val = _to_csr(n, keys, w)
+    return MSBMGraph(n, row_ptr, col, val, groups, clusters, h, 0, dict(name="hub", seed=seed))
