@@ -379,6 +379,9 @@ def main():
             with open(tp) as f:
                 traffic = json.load(f).get(dom)
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "spmv_variant": ("pattern-only: unit weights detected at build, the implied values are not "
+                                     "streamed; bytes still count 12 B per entry (SURVEY §8(d))")
+                    if info.get("unit_weights") else "value-streaming CSR",
                     "frac": achieved / peak, "frac_of_8TBps_nominal": achieved / 8000.0,
                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs copy bandwidth)",
                     "traffic": traffic, "share_of_step": d["ms"] / prof_ms if prof_ms > 0 else None,

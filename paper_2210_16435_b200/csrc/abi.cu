@@ -171,7 +171,7 @@ sfairsc_status sfz::apply_dev(sfairsc_ctx* c, const double* x, double* y) {
     launch_project(c->g(), c->pd(), x, c->bs_w, 1.0, c->vp, c->st);
   }
   {
-    ProfScope ps(c, K_SPMV, c->csr_bytes_spmv() + 3 * c->vb() + 1.0 * c->n);
+    ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
     ctx_spmv(c, c->vp, c->vt);
   }
   if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
@@ -228,7 +228,7 @@ void sfz::ctx_spmv(sfairsc_ctx* c, const double* p, double* t, const double* q_p
     g.ci = c->pci;
     g.vv = c->pvv;
     g.nnz = c->nnz_pad;
-    launch_spmv_tma(g, c->vs, c->tiles, c->cta_tiles, c->tma_grid, pg, p, t, c->partials, c->counters + 1, c->bs_t,
+    launch_spmv_tma(g, c->vs, c->spmv_shape, c->tiles, c->cta_tiles, c->tma_grid, pg, p, t, c->partials, c->counters + 1, c->bs_t,
                     c->st);
     return;
   }
@@ -352,17 +352,6 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   c->max_restarts = opts.max_restarts > 0 ? opts.max_restarts : 100000;
   c->check_symmetry = opts.check_symmetry;
   c->debug = getenv("SFAIRSC_DEBUG") ? atoi(getenv("SFAIRSC_DEBUG")) : 0;
-  if (getenv("SFAIRSC_SWEEP")) c->sweep_kind = atoi(getenv("SFAIRSC_SWEEP"));
-  if (getenv("SFAIRSC_TMA_MODE2")) c->tma_mode2 = atoi(getenv("SFAIRSC_TMA_MODE2"));
-  if (getenv("SFAIRSC_RITZ")) sfz::g_ritz_kind = atoi(getenv("SFAIRSC_RITZ"));
-  if (getenv("SFAIRSC_SPMV")) sfz::g_spmv_kind = atoi(getenv("SFAIRSC_SPMV"));
-  if (getenv("SFAIRSC_LZ_SWEEP")) sfz::g_lz_sweep = atoi(getenv("SFAIRSC_LZ_SWEEP"));
-  if (getenv("SFAIRSC_GATHER")) sfz::g_spmv_gather = atoi(getenv("SFAIRSC_GATHER"));
-  if (getenv("SFAIRSC_SPMV_PIPE")) sfz::g_spmv_pipe = atoi(getenv("SFAIRSC_SPMV_PIPE"));
-  if (c->sweep_kind == 3) {  // TMA with one 1-D copy per column (A/B only)
-    sfz::g_tma_use2d = 0;
-    c->sweep_kind = 2;
-  }
   auto bail = [&](sfairsc_status st) {
     free_ctx(c);
     return st;
@@ -602,6 +591,8 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
       c->vs_blk = vsb;
     }
   }
+  // the single-vector SpMV is the TMA-fed tile kernel unless column-blocked or dense-projected
+  c->spmv_tma = c->nblk <= 1 && nnz > 0 && !c->Qr && !(getenv("SFAIRSC_SPMV_TMA") && atoi(getenv("SFAIRSC_SPMV_TMA")) == 0);
   // normalized pattern-only SpMV: its gathered vector s o p (vq_lz: the lagged solver's, written by its
   // normalisation kernel)
   if (c->unit_spmv() && c->normalized) {
@@ -615,9 +606,8 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   // SpMV partition: CTA b owns rows with cumulative (nnz + 4 rows) weight in [b, b+1)/G
   {
     const long long total = (long long)nnz + 4LL * n;
-    // CTAs per SM of the SpMV grid (env SFAIRSC_SPMV_CPS for A/B: 8 default)
-    const int cps = getenv("SFAIRSC_SPMV_CPS") ? std::max(1, atoi(getenv("SFAIRSC_SPMV_CPS"))) : 8;
-    int G = std::max(1, std::min(c->num_sms * cps, (n + 31) / 32));
+    // 8 CTAs per SM (5 and 10 measured slower)
+    int G = std::max(1, std::min(c->num_sms * 8, (n + 31) / 32));
     std::vector<int32_t> split(G + 1);
     split[0] = 0;
     split[G] = n;
@@ -642,10 +632,10 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     }
     int vs = 2;
     while (vs < 32 && vs * 4 < mean_deg) vs *= 2;
-    const bool tma = c->nblk <= 1 && nnz > 0 && !c->Qr && !(getenv("SFAIRSC_SPMV_TMA") && atoi(getenv("SFAIRSC_SPMV_TMA")) == 0);
-    if (tma) {  // the TMA SpMV's lane reads 4-entry blocks: VS = largest power of two <= mean degree / 4
-      vs = 2;
-      while (vs < 32 && vs * 8 <= mean_deg) vs *= 2;
+    const bool tma = c->spmv_tma;
+    if (tma) {  // the TMA SpMV's lane reads 4-entry blocks, two per pass: VS = largest power of two <= mean degree / 16
+      vs = 2;    // (config 4, mean degree 32: VS 2 525 us, VS 4 543 us; config 3, 64: VS 4 170 us, VS 2 272 us)
+      while (vs < 32 && vs * 32 <= mean_deg) vs *= 2;
     }
     c->vs = opts.spmv_vector > 0 ? opts.spmv_vector : vs;
     if (c->vs != 2 && c->vs != 4 && c->vs != 8 && c->vs != 16 && c->vs != 32)
@@ -655,8 +645,12 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     if (tma) {
       std::vector<int2> tiles;
       std::vector<int> cta, prp;
-      spmv_tma_layout(hrp.data(), n, spmv_tma_ctas_per_sm(c->vs, c->normalized, c->unit_spmv()) * c->num_sms, prp,
-                      tiles, cta);
+      // tiles of <= 2048 padded entries / 128 rows, 2-deep ring: config 4 SpMV 579 -> 525 us against 1024 / 64
+      // (profiles/r2_exp/spmv_tile_sweep.jsonl; 1536-4096 entries, 64-128 rows, 3 stages and 12 gathers per lane
+      // in flight measured equal or slower)
+      c->spmv_shape = spmv_tile_shape(2048, 128, 2, c->unit_spmv());
+      spmv_tma_layout(hrp.data(), n, spmv_tma_ctas_per_sm(c->vs, c->normalized, c->unit_spmv(), c->spmv_shape) * c->num_sms,
+                      c->spmv_shape, prp, tiles, cta);
       c->tma_grid = (int)cta.size() - 1;
       CUB(dalloc(&c->tiles, tiles.size()));
       CUB(dalloc(&c->cta_tiles, cta.size()));
@@ -932,7 +926,7 @@ static sfairsc_status project_dev(sfairsc_ctx* c, const double* x, double* y) {
 }
 
 static sfairsc_status lap_dev(sfairsc_ctx* c, const double* x, double* y) {
-  ProfScope ps(c, K_SPMV, c->csr_bytes_spmv() + 3 * c->vb() + 1.0 * c->n);
+  ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
   ctx_spmv(c, x, y);
   CHECK_LAUNCH();
   return SFAIRSC_OK;
@@ -1020,12 +1014,8 @@ struct Lanczos {
 
   // one sweep; returns the grid used (= number of partial rows)
   int sweep(int mode, const SweepArgs& a) {
-    if (c->sweep_kind == 1 && mode != 2 && sweep_tma_ok(a.J)) {  // smem-staged dots sweeps
-      const int G = sweep_smem_grid(c->n, a.J, c->num_sms);
-      launch_sweep_smem(mode, c->g(), c->pd(), a, G, c->st);
-      return G;
-    }
-    if (c->sweep_kind == 2 && sweep_tma_ok(a.J) && (mode != 2 || c->tma_mode2)) {
+    // dots-type modes: TMA-fed persistent sweep; update + norm (mode 2): the register kernel (measured faster)
+    if (sweep_tma_ok(a.J) && mode != 2) {
       const int G = sweep_tma_grid(c->n, c->num_sms);
       launch_sweep_tma(mode, c->g(), c->pd(), a, G, c->st);
       return G;
@@ -1172,7 +1162,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
     // ---- expand column j: r = L^sigma v_j, CGS2 against V[:, 0:j+1], v_{j+1} = r/|r| ----
     // (no host synchronisation inside the expansion; breakdowns are detected at the next sync)
     {
-      ProfScope ps(c, K_SPMV, c->csr_bytes_spmv() + 3 * c->vb() + 1.0 * c->n);
+      ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
       ctx_spmv(c, c->vp, c->vt);
     }
     if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);

@@ -40,19 +40,11 @@ __host__ __device__ constexpr size_t bstage_doubles(int J) {
   return (size_t)(J + NB + 1) * kR + 16;
 }
 
-__device__ __forceinline__ double ld_cg(const double* p) {  // L2 only (no L1 allocation)
-  double v;
-  asm("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-int g_spmv_gather = 0;  // 0: __ldg gathers (default); 1: ld.global.cg (env SFAIRSC_GATHER)
-int g_spmv_pipe = 0;    // 1: software-pipelined CSR slots (env SFAIRSC_SPMV_PIPE=1; measured equal, off by default)
-
 // NB doubles of row c of an interleaved block
-template <int NB, bool CG = false>
+template <int NB>
 __device__ __forceinline__ void ld_row(const double* __restrict__ p, int c, double (&x)[NB]) {
   if constexpr (NB == 1) {
-    x[0] = CG ? ld_cg(p + c) : __ldg(p + c);
+    x[0] = __ldg(p + c);
   } else {
     const double2* q = reinterpret_cast<const double2*>(p) + (size_t)c * (NB / 2);
 #pragma unroll
@@ -74,8 +66,7 @@ __device__ __forceinline__ void ld_row(const double* __restrict__ p, int c, doub
 //   3 last (t -= W_b p, epilogue).  g.rp is then the block's row offsets into the block-major CSR.
 // UNIT (unit-weight graphs): no value stream; p is then the gathered vector (normalized: q = s o p)
 // and p_self the vector itself, the row sum scaled by s_i (normalized).
-template <int VS, int NB, bool NORM, bool CG = false, int cmode = 0, bool DQ = false, bool PIPE = false,
-          bool LONGR = false, bool UNIT = false>
+template <int VS, int NB, bool NORM, int cmode = 0, bool DQ = false, bool LONGR = false, bool UNIT = false>
 __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __restrict__ row_split,
                                                    const double* __restrict__ p, const double* __restrict__ p_self,
                                                    double* __restrict__ t, double* partials, unsigned* counter,
@@ -89,85 +80,20 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
   double ptacc[NB];  // p^T t (lane-0 rows)
 #pragma unroll
   for (int c = 0; c < NB; ++c) ptacc[c] = 0.0;
-  // software pipeline (PIPE): the (col, val) slots of the next row group are loaded before the
-  // gathers of the current one, so the CSR stream latency overlaps the L2 gathers
-  const bool pipe = PIPE;
-  int pa = 0, pb = 0, pc[U];
-  double pw[U];
-  if (pipe) {
-    const int row = r0 + gid;
-    if (row < r1) {
-      pa = __ldg(rp + row);
-      pb = __ldg(rp + row + 1);
-    }
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const int e = pa + lane + q * VS;
-      const bool ok = e < pb;
-      pc[q] = ok ? ld_stream(ci + e) : row;
-      pw[q] = ok ? (UNIT ? 1.0 : ld_stream(vv + e)) : 0.0;
-    }
-  }
   for (int base = r0; base < r1; base += NG) {
     const int row = base + gid;
     const bool valid = row < r1;
     double acc[NB];
 #pragma unroll
     for (int c = 0; c < NB; ++c) acc[c] = 0.0;
-    if (pipe) {
-      const int a = pa, b = pb;
-      int cc[U];
-      double ww[U];
-#pragma unroll
-      for (int q = 0; q < U; ++q) {
-        cc[q] = pc[q];
-        ww[q] = pw[q];
-      }
-      const int nrow = row + NG;  // prefetch the next row group's first slots
-      pa = 0;
-      pb = 0;
-      if (nrow < r1) {
-        pa = __ldg(rp + nrow);
-        pb = __ldg(rp + nrow + 1);
-      }
-#pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const int e = pa + lane + q * VS;
-        const bool ok = e < pb;
-        pc[q] = ok ? ld_stream(ci + e) : nrow;
-        pw[q] = ok ? (UNIT ? 1.0 : ld_stream(vv + e)) : 0.0;
-      }
-      if (valid) {
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-          double x[NB];
-          ld_row<NB, CG>(p, cc[q], x);
-#pragma unroll
-          for (int c = 0; c < NB; ++c) acc[c] = fma(ww[q], x[c], acc[c]);
-        }
-        for (int e0 = a + lane + U * VS; e0 < b; e0 += U * VS) {  // rows longer than U*VS
-#pragma unroll
-          for (int q = 0; q < U; ++q) {
-            const int e = e0 + q * VS;
-            if (e < b) {
-              double x[NB];
-              ld_row<NB, CG>(p, ld_stream(ci + e), x);
-              const double wv = UNIT ? 1.0 : ld_stream(vv + e);
-#pragma unroll
-              for (int c = 0; c < NB; ++c) acc[c] = fma(wv, x[c], acc[c]);
-            }
-          }
-        }
-      }
-    }
     int a = 0, b = 0;
-    if (!pipe && valid) {
+    if (valid) {
       a = __ldg(rp + row);
       b = __ldg(rp + row + 1);
     }
     // LONGR (skewed degrees, config 5): rows longer than kLong slots are left to the whole warp below
     constexpr int kLong = 32 * VS;
-    if (!pipe && valid && !(LONGR && b - a > kLong)) {
+    if (valid && !(LONGR && b - a > kLong)) {
       for (int e0 = a + lane; e0 < b; e0 += U * VS) {
         int cix[U];
         double w[U];
@@ -181,7 +107,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
 #pragma unroll
         for (int q = 0; q < U; ++q) {
           double x[NB];
-          ld_row<NB, CG>(p, cix[q], x);
+          ld_row<NB>(p, cix[q], x);
 #pragma unroll
           for (int c = 0; c < NB; ++c) acc[c] = fma(w[q], x[c], acc[c]);
         }
@@ -213,7 +139,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(GraphDev g, const int* __rest
 #pragma unroll
           for (int q = 0; q < U; ++q) {
             double x[1];
-            ld_row<1, CG>(p, cix[q], x);
+            ld_row<1>(p, cix[q], x);
             sacc = fma(w[q], x[0], sacc);
           }
         }
@@ -761,43 +687,36 @@ static int n_sms() {
 static int sgrid(int n) { return std::max(1, std::min((n + kThreads - 1) / kThreads, n_sms() * 8)); }
 static int rgrid(int n) { return std::max(1, std::min((n + 4 * kThreads - 1) / (4 * kThreads), n_sms() * 2)); }
 
+// instantiation map: the pattern-only, long-row (skewed degrees) and dense-projector variants exist for single
+// vectors (NB = 1) only; column-blocked modes (cmode 1-3) likewise
+template <int VS, int NB, int CM>
+static void spmm_cm(const GraphDev& g, const int* split, int grid, const double* p, const double* ps, double* t,
+                    double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
+  using K = void (*)(GraphDev, const int*, const double*, const double*, double*, double*, unsigned*, double*);
+  auto go = [&](K kern) { kern<<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); };
+  if constexpr (NB == 1) {
+    const bool nm = g.normalized;
+    if (g.Q) return go(nm ? k_spmm<VS, 1, true, CM, true> : k_spmm<VS, 1, false, CM, true>);
+    if (g.unit && g.skewed)
+      return go(nm ? k_spmm<VS, 1, true, CM, false, true, true> : k_spmm<VS, 1, false, CM, false, true, true>);
+    if (g.unit) return go(nm ? k_spmm<VS, 1, true, CM, false, false, true> : k_spmm<VS, 1, false, CM, false, false, true>);
+    if (g.skewed) return go(nm ? k_spmm<VS, 1, true, CM, false, true> : k_spmm<VS, 1, false, CM, false, true>);
+  }
+  go(g.normalized ? k_spmm<VS, NB, true, CM> : k_spmm<VS, NB, false, CM>);
+}
 template <int VS, int NB>
 static void spmm_vs(const GraphDev& g, const int* split, int grid, const double* p, const double* ps, double* t,
                     double* partials, unsigned* counter, double* bsum_t, cudaStream_t st, int cmode = 0) {
-  if (NB == 1 && g_spmv_gather == 1 && !g.Q && !g.unit) {
-    if (g.normalized)
-      k_spmm<VS, NB, true, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
-    else
-      k_spmm<VS, NB, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
-    return;
+  if constexpr (NB == 1) {
+    switch (cmode) {
+      case 0: return spmm_cm<VS, 1, 0>(g, split, grid, p, ps, t, partials, counter, bsum_t, st);
+      case 1: return spmm_cm<VS, 1, 1>(g, split, grid, p, ps, t, partials, counter, bsum_t, st);
+      case 2: return spmm_cm<VS, 1, 2>(g, split, grid, p, ps, t, partials, counter, bsum_t, st);
+      default: return spmm_cm<VS, 1, 3>(g, split, grid, p, ps, t, partials, counter, bsum_t, st);
+    }
+  } else {
+    spmm_cm<VS, NB, 0>(g, split, grid, p, ps, t, partials, counter, bsum_t, st);
   }
-  if (NB == 1 && cmode == 0 && !g.Q && !g.unit && g_spmv_pipe) {
-    if (g.normalized) k_spmm<VS, NB, true, false, 0, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
-    else k_spmm<VS, NB, false, false, 0, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
-    return;
-  }
-#define SPMM_CM(CM)                                                                                              \
-  if (NB == 1 && g.unit && !g.Q && g.skewed) {                                                               \
-    if (g.normalized) k_spmm<VS, NB, true, false, CM, false, false, true, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
-    else k_spmm<VS, NB, false, false, CM, false, false, true, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
-  } else if (NB == 1 && g.unit && !g.Q) {                                                                    \
-    if (g.normalized) k_spmm<VS, NB, true, false, CM, false, false, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
-    else k_spmm<VS, NB, false, false, CM, false, false, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
-  } else if (NB == 1 && g.skewed && !g.Q) {                                                                  \
-    if (g.normalized) k_spmm<VS, NB, true, false, CM, false, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
-    else k_spmm<VS, NB, false, false, CM, false, false, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
-  } else if (NB == 1 && g.Q) {                                                                               \
-    if (g.normalized) k_spmm<VS, NB, true, false, CM, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
-    else k_spmm<VS, NB, false, false, CM, true><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
-  } else if (g.normalized) k_spmm<VS, NB, true, false, CM><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t); \
-  else k_spmm<VS, NB, false, false, CM><<<grid, kThreads, 0, st>>>(g, split, p, ps, t, partials, counter, bsum_t);
-  switch (cmode) {
-    case 0: SPMM_CM(0) break;
-    case 1: SPMM_CM(1) break;
-    case 2: SPMM_CM(2) break;
-    default: SPMM_CM(3) break;
-  }
-#undef SPMM_CM
 }
 void launch_spmv_colblock(const GraphDev& g, int vs, const int* split, int grid, const double* p, double* t,
                           double* partials, unsigned* counter, double* bsum_t, int cmode, cudaStream_t st,
@@ -896,7 +815,11 @@ static void bsweep_launch(const GraphDev& g, const ProjDesc& pd, const BlockSwee
 }
 template <int MODE, int NB, bool NORM>
 static void bsweep_m(const GraphDev& g, const ProjDesc& pd, const BlockSweepArgs& a, int grid, cudaStream_t st) {
-  if (MODE == 2 || a.J <= 32) bsweep_launch<MODE, 4, NB, NORM>(g, pd, a, grid, st);
+  if constexpr (MODE == 2) {  // update + norm: no per-column dots
+    bsweep_launch<MODE, 4, NB, NORM>(g, pd, a, grid, st);
+    return;
+  }
+  if (a.J <= 32) bsweep_launch<MODE, 4, NB, NORM>(g, pd, a, grid, st);
   else if (a.J <= 64) bsweep_launch<MODE, 8, NB, NORM>(g, pd, a, grid, st);
   else if (a.J <= 128) bsweep_launch<MODE, 16, NB, NORM>(g, pd, a, grid, st);
   else bsweep_launch<MODE, 24, NB, NORM>(g, pd, a, grid, st);
@@ -920,11 +843,8 @@ int bsweep_grid(int n) { return std::max(1, std::min((n + kR - 1) / kR, n_sms())
 void launch_bsweep(int mode, int nb, const GraphDev& g, const ProjDesc& pd, const BlockSweepArgs& a, int grid,
                    cudaStream_t st) {
   bump_launch();
-  switch (nb) {
-    case 1: bsweep_nb<1>(mode, g, pd, a, grid, st); break;
-    case 2: bsweep_nb<2>(mode, g, pd, a, grid, st); break;
-    default: bsweep_nb<4>(mode, g, pd, a, grid, st); break;
-  }
+  if (nb == 2) bsweep_nb<2>(mode, g, pd, a, grid, st);  // block Lanczos: block size 2 or 4
+  else bsweep_nb<4>(mode, g, pd, a, grid, st);
 }
 
 void launch_bqr1(int nb, int n, double* R, const double* nbo, double* partials, unsigned* counter, double* g2,

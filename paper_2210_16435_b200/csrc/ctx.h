@@ -79,8 +79,6 @@ struct sfairsc_ctx {
   int m = 20, keep = 0, max_restarts = 100000;
   int check_symmetry = 1;
   int debug = 0;
-  int sweep_kind = 2;  // 0 register sweeps, 1 smem-staged, 2 TMA 2-D tensor (default), 3 TMA 1-D (env SFAIRSC_SWEEP)
-  int tma_mode2 = 0;   // update+norm sweep: register kernel (measured faster); env SFAIRSC_TMA_MODE2=1: TMA
   // device buffers
   int *rp = nullptr, *ci = nullptr, *row_split = nullptr;
   int2* tiles = nullptr;       // TMA SpMV tiles (spmv_tma.cu): (first row, first entry), ntiles + 1
@@ -89,6 +87,8 @@ struct sfairsc_ctx {
   int *prp = nullptr, *pci = nullptr;  // padded CSR of the TMA SpMV (rows at multiples of 4 entries, pads col = -1)
   double* pvv = nullptr;               // its values, split block layout (nullptr: unit-weight pattern SpMV)
   int nnz_pad = 0;                     // padded entries (a multiple of 4)
+  bool spmv_tma = false;               // the single-vector SpMV is the TMA-fed tile kernel
+  sfz::SpmvTileShape spmv_shape;       // its tile shape and ring depth
   double *vv = nullptr, *dg = nullptr, *s = nullptr;
   uint8_t* grp = nullptr;
   double *isb = nullptr, *uh = nullptr;
@@ -161,10 +161,9 @@ struct sfairsc_ctx {
     G.unit = unit_spmv();
     return G;
   }
-  // the dense-projector SpMV keeps its value-streaming kernel; normalized graphs take the pattern-only kernel only
-  // when column-blocked: unblocked, the gathers alone bound the SpMV and the extra s o p pass costs what the
-  // smaller stream saves (config 4: 720 vs 722 us SpMV, +5 us normalisation)
-  bool unit_spmv() const { return unit && !Qr && (!normalized || nblk > 1); }
+  // the dense-projector SpMV keeps its value-streaming kernel; normalized graphs take the pattern-only kernel
+  // when column-blocked or TMA-fed (the LSU-fed round-1 kernel was gather-bound either way: config 4 720 vs 722 us)
+  bool unit_spmv() const { return unit && !Qr && (!normalized || nblk > 1 || spmv_tma); }
   ProjDesc pd() const {
     ProjDesc P{Qr ? qr : h, isb, uh};
     P.Q = Qr;
@@ -174,9 +173,9 @@ struct sfairsc_ctx {
   // algorithmic bytes: one read/write of each operand
   double vb() const { return 8.0 * n; }                      // one fp64 n-vector
   double sgb() const { return (normalized ? 8.0 * n : 0.0) + 1.0 * n; }  // s (normalized) + group ids
+  // the CSR stream counts 12 B per entry even when the pattern-only SpMV leaves implied unit
+  // values unread (the pattern-only kernel is a labelled variant, not a smaller workload)
   double csr_bytes() const { return 12.0 * nnz + 4.0 * (n + 1); }
-  // bytes of W the single-vector SpMV reads (unit weights: column indices and row offsets only)
-  double csr_bytes_spmv() const { return (unit_spmv() ? 4.0 : 12.0) * nnz + 4.0 * (n + 1); }
   int gpasses() const { return (h + kHB - 1) / kHB; }
 };
 

@@ -55,7 +55,9 @@ __global__ void k_validate(GraphDev g, int check_sym, int* flags) {
       if (j == i && w != 0.0) f |= F_CSR;
       if (w != 1.0 || j == i) f |= F_NONUNIT;  // not a unit-weight pattern (informational)
       if (check_sym && j >= 0 && j < n && j != i) {
-        int lo = g.rp[j], hi = g.rp[j + 1] - 1, found = -1;
+        // partner row j is not validated by this thread: clamp its range into [0, nnz) (a malformed row_ptr
+        // is flagged by j's own thread; the search must not read outside ci)
+        int lo = max(0, g.rp[j]), hi = min(g.nnz, g.rp[j + 1]) - 1, found = -1;
         while (lo <= hi) {
           const int mid = lo + ((hi - lo) >> 1);  // rp values reach 1.6e9: no lo + hi overflow
           const int cm = g.ci[mid];
@@ -203,63 +205,6 @@ __global__ void __launch_bounds__(kThreads) k_finish(GraphDev g, ProjDesc pd, co
       y[i] = NORM ? fma(-g.s[i], gi, t[i]) : t[i] - gi;
     }
   }
-}
-
-// ----------------------------------------------------------------------------
-// SpMV t = L p with fused B^T t epilogue (A5).
-// CTA b owns rows [row_split[b], row_split[b+1]) (balanced by nnz + rows);
-// VS lanes per row, consecutive row groups -> contiguous col/val streams.
-// normalized: t_i = p_i - sum_j (s_i w_ij s_j) p_j ; unnormalized: d_i p_i - sum_j w_ij p_j
-// ----------------------------------------------------------------------------
-template <int VS, bool NORM>
-__global__ void __launch_bounds__(kThreads, 6) k_spmv(GraphDev g, const int* __restrict__ row_split,
-                                                      const double* __restrict__ p, double* __restrict__ t,
-                                                      double* partials, unsigned* counter, double* bsum_t, int nout) {
-  constexpr int NG = kThreads / VS;
-  const int r0 = row_split[blockIdx.x], r1 = row_split[blockIdx.x + 1];
-  const int lane = threadIdx.x % VS, gid = threadIdx.x / VS;
-  const int* __restrict__ rp = g.rp;
-  const int* __restrict__ ci = g.ci;
-  const double* __restrict__ vv = g.vv;
-  // main loop: t only (group-sum accumulators are not live here -> fewer registers, more warps)
-  for (int base = r0; base < r1; base += NG) {
-    const int row = base + gid;
-    const bool valid = row < r1;
-    double sum = 0.0;
-    if (valid) {
-      const int a = __ldg(rp + row), b = __ldg(rp + row + 1);
-      int e = a + lane;
-      for (; e + 3 * VS < b; e += 4 * VS) {
-        const int c0 = ld_stream(ci + e), c1 = ld_stream(ci + e + VS);
-        const int c2 = ld_stream(ci + e + 2 * VS), c3 = ld_stream(ci + e + 3 * VS);
-        const double w0 = ld_stream(vv + e), w1 = ld_stream(vv + e + VS);
-        const double w2 = ld_stream(vv + e + 2 * VS), w3 = ld_stream(vv + e + 3 * VS);
-        const double x0 = __ldg(p + c0), x1 = __ldg(p + c1), x2 = __ldg(p + c2), x3 = __ldg(p + c3);
-        sum = fma(w0, x0, sum);
-        sum = fma(w1, x1, sum);
-        sum = fma(w2, x2, sum);
-        sum = fma(w3, x3, sum);
-      }
-      for (; e < b; e += VS) sum = fma(ld_stream(vv + e), __ldg(p + ld_stream(ci + e)), sum);
-    }
-#pragma unroll
-    for (int o = VS / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (valid && lane == 0) {
-      const double pi = __ldg(p + row);
-      t[row] = (NORM ? pi : __ldg(g.dg + row) * pi) - sum;
-    }
-  }
-  // epilogue: B^T t over this CTA's rows (re-read from L2, fixed order)
-  __syncthreads();
-  double acc[kHB];
-#pragma unroll
-  for (int q = 0; q < kHB; ++q) acc[q] = 0.0;
-  for (int row = r0 + threadIdx.x; row < r1; row += kThreads) {
-    const double ti = __ldcg(t + row);
-    add_group(acc, g.grp[row], NORM ? g.s[row] * ti : ti);
-  }
-  block_reduce_store<kHB>(acc, partials + (size_t)blockIdx.x * kHB);
-  ticket_finalize<kHB>(partials, counter, bsum_t, nout);
 }
 
 // ----------------------------------------------------------------------------
@@ -419,37 +364,6 @@ __global__ void k_random(double* x, int n, uint64_t seed, unsigned c1, unsigned 
     x[i] = philox_uniform(seed, (unsigned)i, c1, stream, 0u) - 0.5;
 }
 
-// Ritz vectors Vout[:, c] = sum_{l<m} V[:, l] Y[l, c]  (A10).  64 rows x 4 column
-// groups per CTA; Y (m x p) staged in shared memory, row-major.
-template <int PC>
-__global__ void __launch_bounds__(kThreads) k_ritz(const double* __restrict__ V, long long ld, int n, int m,
-                                                   const double* __restrict__ Y, int p, double* __restrict__ Vout) {
-  extern __shared__ double Ys[];  // [m][p]
-  for (int e = threadIdx.x; e < m * p; e += kThreads) {
-    const int l = e / p, c = e % p;
-    Ys[e] = Y[(size_t)c * m + l];
-  }
-  __syncthreads();
-  const int r = threadIdx.x & 63, cg = threadIdx.x >> 6;
-  for (int chunk = blockIdx.x; chunk * 64 < n; chunk += gridDim.x) {
-    const int i = chunk * 64 + r;
-    if (i >= n) continue;
-    double acc[PC];
-#pragma unroll
-    for (int cc = 0; cc < PC; ++cc) acc[cc] = 0.0;
-    for (int l = 0; l < m; ++l) {
-      const double v = V[(long long)l * ld + i];
-      const double* yr = Ys + l * p + cg;
-#pragma unroll
-      for (int cc = 0; cc < PC; ++cc)
-        if (cg + 4 * cc < p) acc[cc] = fma(v, yr[4 * cc], acc[cc]);
-    }
-#pragma unroll
-    for (int cc = 0; cc < PC; ++cc)
-      if (cg + 4 * cc < p) Vout[(long long)(cg + 4 * cc) * ld + i] = acc[cc];
-  }
-}
-
 __global__ void __launch_bounds__(kThreads) k_resid(const double* __restrict__ y, const double* __restrict__ x,
                                                     double theta, int n, double* partials, unsigned* counter,
                                                     double* out) {
@@ -591,29 +505,11 @@ void launch_finish(const GraphDev& g, const ProjDesc& pd, const double* t, const
     k_finish<false><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_w, sigma, y);
 }
 
-template <int VS>
-static void spmv_vs(const GraphDev& g, const int* row_split, int grid, const double* p, double* t, double* partials,
-                    unsigned* counter, double* bsum_t, cudaStream_t st) {
-  if (g.normalized)
-    k_spmv<VS, true><<<grid, kThreads, 0, st>>>(g, row_split, p, t, partials, counter, bsum_t, kHB);
-  else
-    k_spmv<VS, false><<<grid, kThreads, 0, st>>>(g, row_split, p, t, partials, counter, bsum_t, kHB);
-}
-int g_spmv_kind = 1;  // 1: predicated 4-deep gather kernel (block.cu k_spmm<VS,1>), 0: k_spmv (A/B, env SFAIRSC_SPMV)
+// t = L p + epilogue B^T t, p^T t: the predicated multi-gather kernel (block.cu k_spmm<VS, 1>); the single-vector
+// solvers call the TMA-fed tile kernel (spmv_tma.cu) instead where the graph allows
 void launch_spmv(const GraphDev& g, int vs, const int* row_split, int grid, const double* p, double* t,
                  double* partials, unsigned* counter, double* bsum_t, cudaStream_t st) {
-  if (g_spmv_kind == 1) {
-    launch_spmm(g, 1, vs, row_split, grid, p, t, partials, counter, bsum_t, st);
-    return;
-  }
-  bump();
-  switch (vs) {
-    case 2: spmv_vs<2>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
-    case 4: spmv_vs<4>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
-    case 8: spmv_vs<8>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
-    case 16: spmv_vs<16>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
-    default: spmv_vs<32>(g, row_split, grid, p, t, partials, counter, bsum_t, st); break;
-  }
+  launch_spmm(g, 1, vs, row_split, grid, p, t, partials, counter, bsum_t, st);
 }
 
 int sweep_grid(int n, int num_sms) { return std::max(1, std::min(cdiv(n, kThreads), num_sms * 4)); }
@@ -668,18 +564,6 @@ void launch_random(double* x, int n, uint64_t seed, unsigned c1, unsigned stream
   k_random<<<stream_grid(n), kThreads, 0, st>>>(x, n, seed, c1, stream);
 }
 
-template <int PC>
-static void ritz_pc(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout, cudaStream_t st) {
-  const size_t smem = (size_t)m * p * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_ritz<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
-  const int grid = std::max(1, std::min(cdiv(n, 64), num_sms_cached() * 2));
-  bump();
-  k_ritz<PC><<<grid, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
-}
 void launch_ritz(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout, cudaStream_t st) {
   launch_ritz_rb(V, ld, n, m, Y, p, Vout, st);
 }

@@ -96,16 +96,7 @@ int sweep_grid(int n, int num_sms);
 long long launch_count();  // kernels launched by this process so far
 void launch_sweep(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st);
 // TMA-fed persistent sweeps (krylov.cu); J <= 192, grid <= #SMs
-extern int g_tma_use2d;
-extern int g_spmv_kind;
-extern int g_lz_sweep;
-extern int g_spmv_gather;
-extern int g_spmv_pipe;
-extern int g_ritz_kind;  // 1: DMMA (fp64 tensor cores, default), 0: register-blocked FMA  // 1: 2-D tensor-map TMA per chunk (default); 0: one 1-D bulk copy per column
-bool sweep_tma_ok(int J);  // also the J limit of the smem-staged sweeps
-int sweep_smem_grid(int n, int J, int num_sms);
-void launch_sweep_smem(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid,
-                       cudaStream_t st);
+bool sweep_tma_ok(int J);
 int sweep_tma_grid(int n, int num_sms);
 void launch_sweep_tma(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st);
 void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout,
@@ -198,14 +189,19 @@ void launch_pair_finish(const GraphDev& g, const ProjDesc& pd, const double* t, 
                         const double* bsum_x, double sigma, double* y0, double* y1, cudaStream_t st);
 
 // TMA-fed single-vector SpMV (spmv_tma.cu): t = L p + epilogue B^T t, p^T t (same outputs as launch_spmv)
-int spmv_tma_ctas_per_sm(int vs, bool normalized, bool unit);
-void spmv_tma_layout(const int* hrp, int n, int G, std::vector<int>& prp, std::vector<int2>& tiles,
-                     std::vector<int>& cta_tiles);
+struct SpmvTileShape {  // row-aligned tiles of <= tn padded entries and <= tr rows; `stages`-deep smem ring
+  int tn = 2048, tr = 128, stages = 2;
+  int val_off = 0, col_off = 0, rp_off = 0, ps_off = 0, ds_off = 0, gr_off = 0, stage_bytes = 0;
+};
+SpmvTileShape spmv_tile_shape(int tn, int tr, int stages, bool unit);
+int spmv_tma_ctas_per_sm(int vs, bool normalized, bool unit, const SpmvTileShape& S);
+void spmv_tma_layout(const int* hrp, int n, int G, const SpmvTileShape& S, std::vector<int>& prp,
+                     std::vector<int2>& tiles, std::vector<int>& cta_tiles);
 void launch_pad_csr(const int* rp, const int* ci, const double* vv, int n, const int* prp, int* pci, double* pvv,
                     cudaStream_t st);
-void launch_spmv_tma(const GraphDev& g, int vs, const int2* tiles, const int* cta_tiles, int grid, const double* p,
-                     const double* p_self, double* t, double* partials, unsigned* counter, double* bsum_t,
-                     cudaStream_t st);
+void launch_spmv_tma(const GraphDev& g, int vs, const SpmvTileShape& S, const int2* tiles, const int* cta_tiles,
+                     int grid, const double* p, const double* p_self, double* t, double* partials, unsigned* counter,
+                     double* bsum_t, cudaStream_t st);
 
 // ---- dense constraint basis (§8(f) N4) -----------------------------------------------
 // out[a*r + b] (a <= b) = sum_i M(i,a) M(i,b), M(i,a) = M[i*rs + a*cs] (fixed-order block reduction)

@@ -871,7 +871,8 @@ void km_free(void* p) {
 #define KCU(expr)                                                         \
   do {                                                                    \
     cudaError_t e_ = (expr);                                              \
-    if (e_ != cudaSuccess) return ctx_fail(SFAIRSC_E_CUDA, cudaGetErrorString(e_)); \
+    if (e_ != cudaSuccess)                                                \
+      return ctx_fail(e_ == cudaErrorMemoryAllocation ? SFAIRSC_E_OOM : SFAIRSC_E_CUDA, cudaGetErrorString(e_)); \
   } while (0)
 
 #define TRY_(e)                      \
@@ -1097,8 +1098,8 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
     b = new KmBuf();
     *slot = b;
     ctx_set_km_free(ctx, km_free);
-    b->n = n;
-    b->K = K;
+    b->n = -1;  // set to (n, K) only once every buffer below is allocated: a failed call is never reused
+    b->K = -1;
     b->nblk = (n + kBlk - 1) / kBlk;
     b->G = std::max(1, std::min(ctx_num_sms(ctx), (n + 1023) / 1024));  // one CTA per SM (shared memory)
     const int W = K * dim + K;
@@ -1123,6 +1124,8 @@ sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, 
     KCU(cudaMalloc(&b->changes, sizeof(int) * 4));
     KCU(cudaMalloc(&b->bidx, sizeof(int) * b->nblk));
     KCU(cudaMalloc(&b->used, sizeof(int) * (K + 1)));
+    b->n = n;
+    b->K = K;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_assign_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asg_mma_smem(64));

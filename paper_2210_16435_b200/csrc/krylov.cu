@@ -1,16 +1,15 @@
-// libsfairsc — TMA-fed reorthogonalisation sweeps and the Ritz GEMM (sm_100a).
+// libsfairsc — TMA-fed reorthogonalisation sweeps (CGS2 solver option) and the Ritz GEMM (sm_100a).
 //
-// Sweeps (the dominant per-step cost at large k):
-// a persistent CTA per SM walks 64-row chunks of the Krylov basis V
-// (column-major, ld = ldv).  For each chunk, warp 0 issues one 1-D bulk copy
-// (cp.async.bulk, the TMA engine) per basis column plus one for the vector
-// chunk into a 2-stage shared-memory ring guarded by mbarriers
-// (complete_tx), so the basis is streamed from HBM exactly once per sweep and
-// both the update r' = r - V c and the dots V^T r' of the fused CGS2 sweep
-// read it from shared memory.
+// Sweeps: a persistent CTA per SM walks 64-row chunks of the
+// Krylov basis V (column-major, ld = ldv).  For each chunk, warp 0 issues one 2-D
+// tensor copy (cp.async.bulk.tensor, the TMA engine) of the (64 rows x J columns)
+// box plus 1-D bulk copies of the vector chunk into a shared-memory ring guarded by
+// mbarriers (complete_tx), so the basis is streamed from HBM exactly once per sweep
+// and both the update r' = r - V c and the dots V^T r' read it from shared memory.
+// (One 1-D copy per column only when the driver lacks the tensor-map encoder.)
 //
-// Ritz GEMM (A10): Vout = V Y, register-blocked fp64 FMA (8 rows x 4 cols per
-// thread, 128 x 64 CTA tiles, k-chunks of 16 staged in shared memory).
+// Ritz GEMM (A10): Vout = V Y on the fp64 tensor cores (DMMA m8n8k4, k_ritz_dmma2);
+// register-blocked fp64 FMA (k_ritz_rb) for a basis without 128-row padding.
 #include "device_common.cuh"
 #include "tma.cuh"
 
@@ -195,109 +194,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep_tma(GraphDev g, ProjDesc 
 }
 
 // ---------------------------------------------------------------------------
-// Shared-memory-staged sweeps for the dots-type modes (0: finish + dots,
-// 1: update + dots, 3: dots).  Each CTA walks 64-row chunks; phase A loads the
-// chunk of the J basis columns with plain coalesced loads (4 column groups x
-// 64 rows; ~J/4 independent loads in flight per thread) into shared memory
-// (mode 1 also forms the update partials on the fly); phase B forms the dots
-// from shared memory, so every basis element is read from HBM exactly once.
-// Several CTAs per SM overlap one CTA's loads with another's dots.
-// ---------------------------------------------------------------------------
-template <int MODE, int MAXCW, bool NORM>
-__global__ void __launch_bounds__(kThreads) k_sweep_smem(GraphDev g, ProjDesc pd, SweepArgs a) {
-  extern __shared__ __align__(16) double Vs[];  // [J][kR]
-  __shared__ double coef[kTmaMaxJ];
-  __shared__ double red[4][kR];
-  __shared__ double rs[kR];
-  __shared__ double gam[256];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int n = g.n, J = a.J;
-  const long long ld = a.ld;
-  if (MODE == 1)
-    for (int l = tid; l < J; l += kThreads) coef[l] = a.coef[l];
-  if (MODE == 0 && tid == 0) {
-    __shared__ double gw[256];
-    gamma_serial(a.bsum_t, 1.0, pd, gam);
-    gamma_serial(a.bsum_w, 1.0, pd, gw);
-    for (int s = 0; s < pd.h; ++s) gam[s] = gam[s] - a.sigma * gw[s];
-  }
-  __syncthreads();
-  const int nchunks = (n + kR - 1) / kR;
-  const int c0 = (int)((long long)nchunks * blockIdx.x / gridDim.x);
-  const int c1 = (int)((long long)nchunks * (blockIdx.x + 1) / gridDim.x);
-  double colacc[MAXCW];
-#pragma unroll
-  for (int cc = 0; cc < MAXCW; ++cc) colacc[cc] = 0.0;
-  const int i = tid % kR, cg = tid / kR;
-  for (int c = c0; c < c1; ++c) {
-    const long long row0 = (long long)c * kR;
-    // ---- phase A: stage V[chunk, 0:J] (and the mode-1 update partials) ----
-    {
-      const double* __restrict__ vp = a.V + row0 + i;
-      double part = 0.0;
-      int l = cg;
-      for (; l + 12 < J; l += 16) {
-        const double v0 = vp[(long long)l * ld], v1 = vp[(long long)(l + 4) * ld];
-        const double v2 = vp[(long long)(l + 8) * ld], v3 = vp[(long long)(l + 12) * ld];
-        Vs[l * kR + i] = v0;
-        Vs[(l + 4) * kR + i] = v1;
-        Vs[(l + 8) * kR + i] = v2;
-        Vs[(l + 12) * kR + i] = v3;
-        if (MODE == 1) {
-          part = fma(v0, coef[l], part);
-          part = fma(v1, coef[l + 4], part);
-          part = fma(v2, coef[l + 8], part);
-          part = fma(v3, coef[l + 12], part);
-        }
-      }
-      for (; l < J; l += 4) {
-        const double v0 = vp[(long long)l * ld];
-        Vs[l * kR + i] = v0;
-        if (MODE == 1) part = fma(v0, coef[l], part);
-      }
-      if (MODE == 1) red[cg][i] = part;
-    }
-    if (MODE == 1) __syncthreads();
-    if (tid < kR) {
-      const long long gi = row0 + tid;
-      double x = 0.0;
-      if (gi < n) {
-        if (MODE == 0) {
-          x = NORM ? fma(-g.s[gi], gam[g.grp[gi]], a.xin[gi]) : a.xin[gi] - gam[g.grp[gi]];
-          a.xout[gi] = x;
-        } else if (MODE == 1) {
-          x = a.xin[gi] - (((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid]);
-          a.xout[gi] = x;
-        } else {
-          x = a.xin[gi];
-        }
-      }
-      rs[tid] = x;
-    }
-    __syncthreads();
-    // ---- phase B: dots from shared memory ----
-    const double r0 = rs[lane], r1 = rs[lane + 32];
-#pragma unroll
-    for (int cc = 0; cc < MAXCW; ++cc) {
-      const int l = w + cc * (kThreads / 32);
-      if (l < J) {
-        colacc[cc] = fma(Vs[l * kR + lane], r0, colacc[cc]);
-        colacc[cc] = fma(Vs[l * kR + lane + 32], r1, colacc[cc]);
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int cc = 0; cc < MAXCW; ++cc) {
-    const int l = w + cc * (kThreads / 32);
-    if (l < J) {
-      const double s = warp_sum(colacc[cc]);
-      if (lane == 0) a.partials[(size_t)blockIdx.x * J + l] = s;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Ritz GEMM  Vout[:, c] = sum_l V[:, l] Y[l, c]
 // ---------------------------------------------------------------------------
 template <int TN>
@@ -352,77 +248,6 @@ __global__ void __launch_bounds__(kThreads) k_ritz_rb(const double* __restrict__
       const long long i = row0 + rg + 16 * q;
       if (i < n) Vout[(long long)col * ld + i] = acc[q][c];
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Ritz GEMM on the fp64 tensor cores: DMMA mma.sync.m8n8k4.f64.
-// CTA tile 128 rows x 64 columns, 8 warps as 4 (rows) x 2 (cols), each warp a
-// 32 x 32 block = 4 x 4 DMMA tiles (32 fp64 accumulators per lane).  K staged
-// through shared memory in chunks of 16 with bank-conflict-free strides
-// (stride = 4 mod 16 doubles).  Fragment layouts (PTX m8n8k4 .f64):
-//   A(8x4, row):  a = A[lane>>2][lane&3];   B(4x8, col): b = B[lane&3][lane>>2];
-//   C(8x8):       c_i = C[lane>>2][2*(lane&3) + i].
-// ---------------------------------------------------------------------------
-constexpr int kDM = 128, kDN = 64, kDK = 16, kAS = kDM + 4, kBS = kDN + 4;
-
-__global__ void __launch_bounds__(kThreads) k_ritz_dmma(const double* __restrict__ V, long long ld, int n, int m,
-                                                        const double* __restrict__ Y, int p,
-                                                        double* __restrict__ Vout) {
-  __shared__ double As[kDK][kAS];
-  __shared__ double Bs[kDK][kBS];
-  const int ncol = (p + kDN - 1) / kDN;
-  const int col0 = (int)(blockIdx.x % ncol) * kDN;
-  const long long row0 = (long long)(blockIdx.x / ncol) * kDM;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int wr = w & 3, wc = w >> 2;  // warp tile origin: rows wr*32, cols wc*32
-  const int gq = lane >> 2, tq = lane & 3;
-  double acc[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  for (int k0 = 0; k0 < m; k0 += kDK) {
-    for (int e = tid; e < kDK * kDM; e += kThreads) {
-      const int kk = e / kDM, r = e % kDM;
-      const int l = k0 + kk;
-      const long long i = row0 + r;
-      As[kk][r] = (l < m && i < n) ? V[(long long)l * ld + i] : 0.0;
-    }
-    for (int e = tid; e < kDK * kDN; e += kThreads) {
-      const int kk = e / kDN, cc = e % kDN;
-      const int l = k0 + kk, c = col0 + cc;
-      Bs[kk][cc] = (l < m && c < p) ? Y[(size_t)c * m + l] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int ks = 0; ks < kDK; ks += 4) {
-      double af[4], bf[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) af[a] = As[ks + tq][wr * 32 + a * 8 + gq];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = Bs[ks + tq][wc * 32 + b * 8 + gq];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
-                       : "d"(af[a]), "d"(bf[b]));
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const long long i = row0 + wr * 32 + a * 8 + gq;
-    if (i >= n) continue;
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int col = col0 + wc * 32 + b * 8 + 2 * tq + q;
-        if (col < p) Vout[(long long)col * ld + i] = acc[a][b][q];
-      }
   }
 }
 
@@ -574,8 +399,6 @@ bool encode_colmajor_map(const double* base, long long ld, int cols, int box_row
 // tensor map over V viewed as 2-D [J columns][ld rows] (fp64), box {64 rows, J columns}
 static bool encode_basis_map(const SweepArgs& a, CUtensorMap* m) { return encode_colmajor_map(a.V, a.ld, a.J, kR, m); }
 
-int g_tma_use2d = 1;
-
 template <int MODE, int MAXCW, bool NORM>
 static void tma_launch(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
   const size_t stage = stage_doubles(a.J) * sizeof(double);
@@ -588,7 +411,7 @@ static void tma_launch(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a
   }
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  int use2d = g_tma_use2d && encode_basis_map(a, &tmap);
+  const int use2d = encode_basis_map(a, &tmap);  // 1-D copies per column only if the driver lacks the encoder
   k_sweep_tma<MODE, MAXCW, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap, use2d);
 }
 
@@ -604,43 +427,6 @@ static void tma_n(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int
   else tma_m<MODE, false>(g, pd, a, grid, st);
 }
 
-template <int MODE, int MAXCW, bool NORM>
-static void smem_launch(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sweep_smem<MODE, MAXCW, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((size_t)kTmaMaxJ * kR * sizeof(double)));
-    attr = true;
-  }
-  k_sweep_smem<MODE, MAXCW, NORM><<<grid, kThreads, (size_t)a.J * kR * sizeof(double), st>>>(g, pd, a);
-}
-template <int MODE, bool NORM>
-static void smem_m(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
-  if (a.J <= 64) smem_launch<MODE, 8, NORM>(g, pd, a, grid, st);
-  else if (a.J <= 128) smem_launch<MODE, 16, NORM>(g, pd, a, grid, st);
-  else smem_launch<MODE, 24, NORM>(g, pd, a, grid, st);
-}
-template <int MODE>
-static void smem_n(const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid, cudaStream_t st) {
-  if (g.normalized) smem_m<MODE, true>(g, pd, a, grid, st);
-  else smem_m<MODE, false>(g, pd, a, grid, st);
-}
-// grid: as many CTAs per SM as shared memory allows (<= 8), at most one chunk each
-int sweep_smem_grid(int n, int J, int num_sms) {
-  const size_t smem = (size_t)std::max(J, 1) * kR * sizeof(double) + 8 * 1024;
-  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / smem));
-  return std::max(1, std::min((n + kR - 1) / kR, num_sms * per_sm));
-}
-void launch_sweep_smem(int mode, const GraphDev& g, const ProjDesc& pd, const SweepArgs& a, int grid,
-                       cudaStream_t st) {
-  bump_launch();
-  switch (mode) {
-    case 0: smem_n<0>(g, pd, a, grid, st); break;
-    case 1: smem_n<1>(g, pd, a, grid, st); break;
-    default: smem_n<3>(g, pd, a, grid, st); break;
-  }
-}
-
 bool sweep_tma_ok(int J) { return J >= 1 && J <= kTmaMaxJ; }
 int sweep_tma_grid(int n, int num_sms) { return std::max(1, std::min((n + kR - 1) / kR, num_sms)); }
 
@@ -654,13 +440,11 @@ void launch_sweep_tma(int mode, const GraphDev& g, const ProjDesc& pd, const Swe
   }
 }
 
-int g_ritz_kind = 2;  // 2: DMMA 128x128 tiles, cp.async ring (default); 1: DMMA 128x64; 0: register-blocked FMA
-
 void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y, int p, double* Vout,
                     cudaStream_t st) {
   if (p <= 0 || n <= 0) return;
   bump_launch();
-  if (g_ritz_kind == 2 && ld % 2 == 0 && ld >= (long long)((n + kGM - 1) / kGM) * kGM) {
+  if (ld % 2 == 0 && ld >= (long long)((n + kGM - 1) / kGM) * kGM) {  // DMMA tiles (every library-owned basis)
     const int smem = 4 * kGK * kGS * (int)sizeof(double);
     static bool attr = false;
     if (!attr) {
@@ -675,11 +459,7 @@ void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y
     else k_ritz_dmma2<128><<<rows * ((p + kGN - 1) / kGN), kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
     return;
   }
-  if (g_ritz_kind == 1) {
-    const long long grid = (long long)((p + kDN - 1) / kDN) * ((n + kDM - 1) / kDM);
-    k_ritz_dmma<<<grid, kThreads, 0, st>>>(V, ld, n, m, Y, p, Vout);
-    return;
-  }
+  // fallback (a basis without 128-row padding): register-blocked FMA
   if (p <= 32) {
     const long long grid = (long long)((p + 31) / 32) * ((n + 127) / 128);
     k_ritz_rb<32><<<grid, kThreads, 0, st>>>(V, ld, n, m, Y, p, Vout);

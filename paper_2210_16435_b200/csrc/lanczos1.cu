@@ -352,151 +352,6 @@ __global__ void __launch_bounds__(NT, 1) k_lz_update(GraphDev g, ProjDesc pd, Lz
 }
 
 // ---------------------------------------------------------------------------
-// The same sweep with the basis rows held in registers (default): 32-row
-// chunks (deeper TMA ring), thread (i, cg) keeps V[i, cg + 8q] in registers
-// across both phases, so shared memory is read once per element and the
-// dots accumulate per thread (one warp = one column group x 32 rows, reduced
-// by a warp sum at the end).
-// stage (doubles): [J][kR2] basis | v~[kR2] | t[kR2] | s[kR2] | grp bytes (pad 128 B)
-// ---------------------------------------------------------------------------
-constexpr int kR2 = 32;
-__host__ __device__ constexpr size_t lz2_stage_doubles(int J) { return (size_t)(J + 3) * kR2 + 16; }
-
-__device__ __forceinline__ void lz2_issue(const LzSweepArgs& a, const GraphDev& g, const CUtensorMap* tmap, int c,
-                                          double* buf, unsigned long long* bar, int lane) {
-  const int J = a.J;
-  const long long row0 = (long long)c * kR2;
-  unsigned bytes = (unsigned)((J + 2) * kR2 * sizeof(double)) + kR2;
-  if (g.normalized) bytes += kR2 * sizeof(double);
-  if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
-  __syncwarp();
-  if (lane == 0) {
-    if (J > 0) tensor2d_g2s(buf, tmap, (int)row0, 0, bar);
-    bulk_g2s(buf + (size_t)J * kR2, a.vt + row0, kR2 * sizeof(double), bar);
-    bulk_g2s(buf + (size_t)(J + 1) * kR2, a.t + row0, kR2 * sizeof(double), bar);
-  } else if (lane == 1) {
-    bulk_g2s(buf + (size_t)(J + 3) * kR2, g.grp + row0, kR2, bar);
-    if (g.normalized) bulk_g2s(buf + (size_t)(J + 2) * kR2, g.s + row0, kR2 * sizeof(double), bar);
-  }
-}
-
-template <int MAXQ, bool NORM>
-__global__ void __launch_bounds__(kThreads, 1) k_lz_update_r(GraphDev g, ProjDesc pd, LzSweepArgs a, int kStages,
-                                                              const __grid_constant__ CUtensorMap tmap) {
-  extern __shared__ __align__(128) double dsm[];
-  __shared__ __align__(8) unsigned long long bars[kMaxStages];
-  __shared__ double cs[kLMaxJ + 1], cg[kLMaxJ + 1];
-  __shared__ double red[2][8][kR2];
-  __shared__ double rw[kR2], rv[kR2];
-  __shared__ double gam[kHB];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int i = lane, cgp = w;  // row in chunk, column group (columns cgp + 8q)
-  const int n = g.n, J = a.J;
-  const int nchunks = (n + kR2 - 1) / kR2;
-  const size_t stage_elems = lz2_stage_doubles(J);
-  for (int l = tid; l < J; l += kThreads) {
-    cs[l] = a.cs[l];
-    cg[l] = a.cg[l];
-  }
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    double gw[kHB];
-    gamma_serial(a.bs_t, 1.0, pd, gam);
-    gamma_serial(a.bs_v, 1.0, pd, gw);
-    for (int s = 0; s < pd.h; ++s) gam[s] -= a.sigma * gw[s];
-  }
-  __syncthreads();
-  const double ay = a.lz[LZ_AY], av = a.lz[LZ_AV], invmu = a.lz[LZ_INVMU];
-  const int my_chunks = (nchunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  if (w == 0)
-    for (int it = 0; it < kStages && it < my_chunks; ++it)
-      lz2_issue(a, g, &tmap, blockIdx.x + it * gridDim.x, dsm + it * stage_elems, &bars[it], lane);
-
-  double colacc[MAXQ];
-#pragma unroll
-  for (int q = 0; q < MAXQ; ++q) colacc[q] = 0.0;
-  double accJ = 0.0;  // dots with the new column v_j (column J, group J % 8)
-  double v2[1 + kHB];
-#pragma unroll
-  for (int q = 0; q < 1 + kHB; ++q) v2[q] = 0.0;
-
-  for (int it = 0; it < my_chunks; ++it) {
-    const int c = blockIdx.x + it * gridDim.x;
-    const int st = it % kStages;
-    const double* buf = dsm + st * stage_elems;
-    mbar_wait(&bars[st], (unsigned)((it / kStages) & 1));
-    const double* vts = buf + (size_t)J * kR2;
-    const double* ts = vts + kR2;
-    const double* ssc = ts + kR2;
-    const uint8_t* gs = reinterpret_cast<const uint8_t*>(ssc + kR2);
-    const long long row0 = (long long)c * kR2;
-    double vreg[MAXQ];
-    double ps = 0.0, pg = 0.0;
-#pragma unroll
-    for (int q = 0; q < MAXQ; ++q) {
-      const int l = cgp + 8 * q;
-      vreg[q] = (l < J) ? buf[(size_t)l * kR2 + i] : 0.0;
-      if (l < J) {
-        ps = fma(vreg[q], cs[l], ps);
-        pg = fma(vreg[q], cg[l], pg);
-      }
-    }
-    red[0][cgp][i] = ps;
-    red[1][cgp][i] = pg;
-    __syncthreads();
-    if (w == 0) {
-      const long long gi = row0 + i;
-      double wv = 0.0, vj = 0.0;
-      if (gi < n) {
-        double sumS = 0.0, sumG = 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          sumS += red[0][q][i];
-          sumG += red[1][q][i];
-        }
-        const double vti = vts[i];
-        vj = fma(vti, invmu, -sumS);
-        const int gg = gs[i];
-        const double y = NORM ? fma(-ssc[i], gam[gg], ts[i]) : ts[i] - gam[gg];
-        wv = fma(ay, y, fma(av, vti, -sumG));
-        a.vj_out[gi] = vj;
-        a.w_out[gi] = wv;
-        v2[0] = fma(wv, wv, v2[0]);
-        const double sv = NORM ? ssc[i] * wv : wv;
-#pragma unroll
-        for (int q = 0; q < kHB; ++q)
-          if (q == gg) v2[1 + q] += sv;
-      }
-      rw[i] = wv;
-      rv[i] = vj;
-    }
-    __syncthreads();
-    const double wi = rw[i];
-#pragma unroll
-    for (int q = 0; q < MAXQ; ++q) colacc[q] = fma(vreg[q], wi, colacc[q]);
-    if (cgp == (J & 7)) accJ = fma(rv[i], wi, accJ);
-    __syncthreads();  // stage `st` and rw/rv consumed
-    if (w == 0 && it + kStages < my_chunks) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      lz2_issue(a, g, &tmap, blockIdx.x + (it + kStages) * gridDim.x, dsm + st * stage_elems, &bars[st], lane);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < MAXQ; ++q) {
-    const int l = cgp + 8 * q;
-    const double sdot = warp_sum(colacc[q]);
-    if (lane == 0 && l < J) a.partials[(size_t)blockIdx.x * (J + 1) + l] = sdot;
-  }
-  {
-    const double sdot = warp_sum(accJ);
-    if (lane == 0 && cgp == (J & 7)) a.partials[(size_t)blockIdx.x * (J + 1) + J] = sdot;
-  }
-  block_reduce_store<1 + kHB>(v2, a.partials2 + (size_t)blockIdx.x * (1 + kHB));
-  ticket_finalize<1 + kHB>(a.partials2, a.counter, a.nb, 1 + min(pd.h, kHB));
-}
-
-// ---------------------------------------------------------------------------
 // The single sweep with 64-row chunks and row PAIRS held in registers: thread
 // (p, cg) = (lane, warp) owns rows 2p, 2p+1 of the chunk and columns cg + 8q.
 // Its basis values are read from shared memory once (16-byte loads) and serve
@@ -705,22 +560,6 @@ static void lz_update_launch(const GraphDev& g, const ProjDesc& pd, const LzSwee
   k_lz_update<MAXCW, NORM, NT, DQ><<<grid, NT, stages * stage, st>>>(g, pd, a, stages, tmap);
 }
 template <int MAXQ, bool NORM>
-static void lz_update_r_launch(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid,
-                               cudaStream_t st) {
-  constexpr size_t kRing2 = 212 * 1024;
-  const size_t stage = lz2_stage_doubles(a.J) * sizeof(double);
-  const int stages = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, kRing2 / stage));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_lz_update_r<MAXQ, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRing2);
-    attr = true;
-  }
-  CUtensorMap tmap;
-  std::memset(&tmap, 0, sizeof(tmap));
-  if (a.J > 0) encode_colmajor_map(a.V, a.ld, a.J, kR2, &tmap);
-  k_lz_update_r<MAXQ, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap);
-}
-template <int MAXQ, bool NORM>
 static void lz_update_p_launch(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid,
                                cudaStream_t st) {
   const size_t stage = lz_stage_doubles(a.J) * sizeof(double);
@@ -736,39 +575,19 @@ static void lz_update_p_launch(const GraphDev& g, const ProjDesc& pd, const LzSw
   if (a.J > 0) encode_colmajor_map(a.V, a.ld, a.J, kR, &tmap);
   k_lz_update_p<MAXQ, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap);
 }
-// 3: 64-row chunks, register-held row pairs (default: config 4 sweep 768 -> 612 us); 0: 64-row smem kernel,
-// 256 threads; 2: the same with 512 threads; 1: register-held rows, 32-row chunks (env SFAIRSC_LZ_SWEEP)
-int g_lz_sweep = 3;
+// group projector: 64-row chunks, register-held row pairs (config 4 sweep 768 -> 612 us against the
+// shared-memory kernel); dense projector (§8(f) N4): the shared-memory kernel, whose stage carries the Q rows
 template <bool NORM>
 static void lz_update_m(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& a, int grid, cudaStream_t st) {
-  if (g_lz_sweep == 1) {
-    const int G = std::max(1, std::min((g.n + kR2 - 1) / kR2, grid));
-    if (a.J <= 64) lz_update_r_launch<8, NORM>(g, pd, a, G, st);
-    else if (a.J <= 128) lz_update_r_launch<16, NORM>(g, pd, a, G, st);
-    else lz_update_r_launch<24, NORM>(g, pd, a, G, st);
-    return;
-  }
-  if (g_lz_sweep == 3 && !g.Q) {
+  if (!g.Q) {
     if (a.J <= 64) lz_update_p_launch<8, NORM>(g, pd, a, grid, st);
     else if (a.J <= 128) lz_update_p_launch<16, NORM>(g, pd, a, grid, st);
     else lz_update_p_launch<24, NORM>(g, pd, a, grid, st);
     return;
   }
-  if (g_lz_sweep == 2) {  // 512 threads: 16 warps, 8 column groups
-    if (a.J + 1 <= 64) lz_update_launch<4, NORM, 512>(g, pd, a, grid, st);
-    else if (a.J + 1 <= 128) lz_update_launch<8, NORM, 512>(g, pd, a, grid, st);
-    else lz_update_launch<12, NORM, 512>(g, pd, a, grid, st);
-    return;
-  }
-  if (g.Q) {  // dense projector (§8(f) N4)
-    if (a.J + 1 <= 64) lz_update_launch<8, NORM, 256, true>(g, pd, a, grid, st);
-    else if (a.J + 1 <= 128) lz_update_launch<16, NORM, 256, true>(g, pd, a, grid, st);
-    else lz_update_launch<24, NORM, 256, true>(g, pd, a, grid, st);
-    return;
-  }
-  if (a.J + 1 <= 64) lz_update_launch<8, NORM, 256>(g, pd, a, grid, st);
-  else if (a.J + 1 <= 128) lz_update_launch<16, NORM, 256>(g, pd, a, grid, st);
-  else lz_update_launch<24, NORM, 256>(g, pd, a, grid, st);
+  if (a.J + 1 <= 64) lz_update_launch<8, NORM, 256, true>(g, pd, a, grid, st);
+  else if (a.J + 1 <= 128) lz_update_launch<16, NORM, 256, true>(g, pd, a, grid, st);
+  else lz_update_launch<24, NORM, 256, true>(g, pd, a, grid, st);
 }
 
 void launch_lz_coef(const LzDev& d, int j, cudaStream_t st) {
@@ -830,7 +649,7 @@ struct Lagged {
   // one Lanczos step at column j (A5-A9)
   sfairsc_status step(int j) {
     {
-      ProfScope ps(c, K_SPMV, c->csr_bytes_spmv() + 3 * c->vb() + 1.0 * c->n);
+      ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
       ctx_spmv(c, c->vp, c->vt, c->vq_lz);  // epilogue: B^T t and p~^T t (bs_t[kHB]); vq_lz = s o p~ (unit)
     }
     {

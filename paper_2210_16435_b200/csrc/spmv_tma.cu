@@ -15,7 +15,7 @@
 //     entries of a block with one 16-byte shared load of col and one of each value half —
 //     consecutive lanes read consecutive 16 bytes: conflict-free, ~0.1 wavefront per entry;
 //   * the CSR never passes through the LSU: a producer warp copies each row-aligned TILE
-//     (<= kTileNnz padded entries, <= kTileRows rows) — row_ptr, col, val and the per-row
+//     (<= S.tn padded entries, <= S.tr rows) — row_ptr, col, val and the per-row
 //     epilogue operands (p_self, d or s, group ids) — into a shared-memory ring with
 //     cp.async.bulk (TMA engine, mbarrier completion, L2 evict-first for the stream);
 //   * consumer warps take VS lanes per row; lane l handles the row's 4-entry blocks
@@ -38,23 +38,28 @@ namespace sfz {
 void bump_launch();
 
 namespace {
-constexpr int kTileNnz = 1024;   // padded entries per tile (row-aligned; a longer row is its own tile)
-constexpr int kTileRows = 64;    // rows per tile
-constexpr int kSpmvStages = 2;   // shared-memory ring depth
 constexpr int kPad = 4;          // rows start at multiples of kPad entries (16-byte col, 32-byte val)
-// stage layout (bytes): val lo [kTileNnz / 2] f64 | val hi [kTileNnz / 2] f64 | col [kTileNnz] i32 |
-//                       row_ptr [kTileRows + 8] i32 |
-//                       p_self [kTileRows + 2] f64 | d or s [kTileRows + 2] f64 | group ids [kTileRows + 32] u8
-constexpr int kValOff = 0;
-constexpr int kColOff = kValOff + kTileNnz * 8;
-constexpr int kRpOff = kColOff + kTileNnz * 4;
-constexpr int kPsOff = kRpOff + (kTileRows + 8) * 4;
-constexpr int kDsOff = kPsOff + (kTileRows + 2) * 8;
-constexpr int kGrOff = kDsOff + (kTileRows + 2) * 8;
-constexpr int kStageBytes = ((kGrOff + kTileRows + 32) + 127) / 128 * 128;
 constexpr int kConsumers = kThreads;           // 8 consumer warps
 constexpr int kSpmvThreads = kConsumers + 32;  // + 1 producer warp
+constexpr int kMaxStages = 4;
 }  // namespace
+
+// stage layout (bytes): [val lo | val hi] (tn f64, absent for unit weights) | col [tn] i32 |
+//                       row_ptr [tr + 8] i32 | p_self [tr + 2] f64 | d or s [tr + 2] f64 | group ids [tr + 32] u8
+SpmvTileShape spmv_tile_shape(int tn, int tr, int stages, bool unit) {
+  SpmvTileShape S;
+  S.tn = tn;
+  S.tr = tr;
+  S.stages = std::max(1, std::min(stages, kMaxStages));
+  S.val_off = 0;
+  S.col_off = unit ? 0 : tn * 8;
+  S.rp_off = S.col_off + tn * 4;
+  S.ps_off = (S.rp_off + (tr + 8) * 4 + 15) / 16 * 16;
+  S.ds_off = S.ps_off + (tr + 2) * 8;
+  S.gr_off = S.ds_off + (tr + 2) * 8;
+  S.stage_bytes = ((S.gr_off + tr + 32) + 127) / 128 * 128;
+  return S;
+}
 
 __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
                                               uint64_t pol) {
@@ -74,7 +79,7 @@ __device__ __forceinline__ void consumers_sync() {  // named barrier 1 over the 
 // tiles[t] = (first row, first padded entry) of tile t; tiles[ntiles] = (n, padded nnz).  CTA b
 // owns tiles [cta_tiles[b], cta_tiles[b + 1]).  g.rp / g.ci / g.vv are the padded CSR.
 template <bool NORM, bool UNIT>
-__device__ __forceinline__ void spmv_issue(const GraphDev& g, const double* __restrict__ p_self,
+__device__ __forceinline__ void spmv_issue(const GraphDev& g, const SpmvTileShape& S, const double* __restrict__ p_self,
                                            const int2* __restrict__ tiles, int tt, unsigned char* buf,
                                            unsigned long long* bar, uint64_t pol_stream, uint64_t pol_keep) {
   const int2 a = tiles[tt], b = tiles[tt + 1];
@@ -82,33 +87,34 @@ __device__ __forceinline__ void spmv_issue(const GraphDev& g, const double* __re
   const int r_al = ra & ~3, r_end = (rb + 1 + 3) & ~3;  // row_ptr[ra .. rb] inclusive
   const int d_al = ra & ~1, d_end = (rb + 1) & ~1;      // f64 per-row operands
   const int g_al = ra & ~15, g_end = (rb + 15) & ~15;   // u8 group ids
-  const bool inl = eb - ea <= kTileNnz && eb > ea;      // a long row (one tile) is read from global memory
+  const bool inl = eb - ea <= S.tn && eb > ea;          // a long row (one tile) is read from global memory
   unsigned bytes = (unsigned)(r_end - r_al) * 4u + 2u * (unsigned)(d_end - d_al) * 8u + (unsigned)(g_end - g_al);
   if (inl) bytes += (unsigned)(eb - ea) * (UNIT ? 4u : 12u);
   mbar_arrive_expect_tx(bar, bytes);
-  bulk_g2s_hint(buf + kRpOff, g.rp + r_al, (unsigned)(r_end - r_al) * 4u, bar, pol_stream);
-  bulk_g2s_hint(buf + kPsOff, p_self + d_al, (unsigned)(d_end - d_al) * 8u, bar, pol_keep);
-  bulk_g2s_hint(buf + kDsOff, (NORM ? g.s : g.dg) + d_al, (unsigned)(d_end - d_al) * 8u, bar, pol_stream);
-  bulk_g2s_hint(buf + kGrOff, g.grp + g_al, (unsigned)(g_end - g_al), bar, pol_stream);
+  bulk_g2s_hint(buf + S.rp_off, g.rp + r_al, (unsigned)(r_end - r_al) * 4u, bar, pol_stream);
+  bulk_g2s_hint(buf + S.ps_off, p_self + d_al, (unsigned)(d_end - d_al) * 8u, bar, pol_keep);
+  bulk_g2s_hint(buf + S.ds_off, (NORM ? g.s : g.dg) + d_al, (unsigned)(d_end - d_al) * 8u, bar, pol_stream);
+  bulk_g2s_hint(buf + S.gr_off, g.grp + g_al, (unsigned)(g_end - g_al), bar, pol_stream);
   if (inl) {
-    bulk_g2s_hint(buf + kColOff, g.ci + ea, (unsigned)(eb - ea) * 4u, bar, pol_stream);
+    bulk_g2s_hint(buf + S.col_off, g.ci + ea, (unsigned)(eb - ea) * 4u, bar, pol_stream);
     if (!UNIT) {  // g.vv = [lo | hi], each half nnz_pad / 2 doubles (g.nnz = padded entries)
-      bulk_g2s_hint(buf + kValOff, g.vv + ea / 2, (unsigned)(eb - ea) * 4u, bar, pol_stream);
-      bulk_g2s_hint(buf + kValOff + kTileNnz * 4, g.vv + (size_t)g.nnz / 2 + ea / 2, (unsigned)(eb - ea) * 4u, bar,
+      bulk_g2s_hint(buf + S.val_off, g.vv + ea / 2, (unsigned)(eb - ea) * 4u, bar, pol_stream);
+      bulk_g2s_hint(buf + S.val_off + S.tn * 4, g.vv + (size_t)g.nnz / 2 + ea / 2, (unsigned)(eb - ea) * 4u, bar,
                     pol_stream);
     }
   }
 }
 
-template <int VS, bool NORM, bool UNIT>
-__global__ void __launch_bounds__(kSpmvThreads, 5) k_spmv_tma(GraphDev g, const int2* __restrict__ tiles,
+template <int VS, bool NORM, bool UNIT, int UB>
+__global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv_tma(GraphDev g, const SpmvTileShape S, const int2* __restrict__ tiles,
                                                                const int* __restrict__ cta_tiles,
                                                                const double* __restrict__ p,
                                                                const double* __restrict__ p_self,
                                                                double* __restrict__ t, double* partials,
                                                                unsigned* counter, double* bsum_t) {
   extern __shared__ __align__(128) unsigned char sm[];
-  __shared__ __align__(8) unsigned long long full[kSpmvStages], empty[kSpmvStages];
+  __shared__ __align__(8) unsigned long long full[kMaxStages], empty[kMaxStages];
+  const int NS = S.stages;
   constexpr int NG = kConsumers / VS;
   __shared__ double gsm[NG][kBT];  // per row group: B^T t (kHB) and p^T t
   __shared__ double lred[kConsumers / 32];
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 5) k_spmv_tma(GraphDev g, const 
   const int t0 = cta_tiles[blockIdx.x], nt = cta_tiles[blockIdx.x + 1] - t0;
   for (int e = tid; e < NG * kBT; e += kSpmvThreads) (&gsm[0][0])[e] = 0.0;
   if (tid == 0) {
-    for (int s = 0; s < kSpmvStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers / 32);
     }
@@ -130,40 +136,40 @@ __global__ void __launch_bounds__(kSpmvThreads, 5) k_spmv_tma(GraphDev g, const 
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
       for (int it = 0; it < nt; ++it) {
-        const int st = it % kSpmvStages;
-        if (it >= kSpmvStages) {
-          mbar_wait(&empty[st], (unsigned)(((it / kSpmvStages) - 1) & 1));
+        const int st = it % NS;
+        if (it >= NS) {
+          mbar_wait(&empty[st], (unsigned)(((it / NS) - 1) & 1));
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
         }
-        spmv_issue<NORM, UNIT>(g, p_self, tiles, t0 + it, sm + st * kStageBytes, &full[st], pol_stream, pol_keep);
+        spmv_issue<NORM, UNIT>(g, S, p_self, tiles, t0 + it, sm + st * S.stage_bytes, &full[st], pol_stream, pol_keep);
       }
     }
   } else {  // ---- consumers ----
     for (int it = 0; it < nt; ++it) {
-      const int st = it % kSpmvStages;
-      const unsigned char* buf = sm + st * kStageBytes;
+      const int st = it % NS;
+      const unsigned char* buf = sm + st * S.stage_bytes;
       const int2 a = tiles[t0 + it], b = tiles[t0 + it + 1];
       const int ra = a.x, rb = b.x, ea = a.y, eb = b.y;
-      mbar_wait(&full[st], (unsigned)((it / kSpmvStages) & 1));
-      const int* srp = reinterpret_cast<const int*>(buf + kRpOff) + (ra & 3);  // srp[r - ra] = row_ptr[r]
-      const double* sps = reinterpret_cast<const double*>(buf + kPsOff) + (ra & 1);
-      const double* sds = reinterpret_cast<const double*>(buf + kDsOff) + (ra & 1);
-      const uint8_t* sgr = reinterpret_cast<const uint8_t*>(buf + kGrOff) + (ra & 15);
-      if (eb - ea <= kTileNnz) {
-        const int4* scol = reinterpret_cast<const int4*>(buf + kColOff);       // block j: entries ea + 4j ..
-        const double2* svlo = reinterpret_cast<const double2*>(buf + kValOff);  // block j: entries 0, 1
-        const double2* svhi = reinterpret_cast<const double2*>(buf + kValOff + kTileNnz * 4);  // entries 2, 3
+      mbar_wait(&full[st], (unsigned)((it / NS) & 1));
+      const int* srp = reinterpret_cast<const int*>(buf + S.rp_off) + (ra & 3);  // srp[r - ra] = row_ptr[r]
+      const double* sps = reinterpret_cast<const double*>(buf + S.ps_off) + (ra & 1);
+      const double* sds = reinterpret_cast<const double*>(buf + S.ds_off) + (ra & 1);
+      const uint8_t* sgr = reinterpret_cast<const uint8_t*>(buf + S.gr_off) + (ra & 15);
+      if (eb - ea <= S.tn) {
+        const int4* scol = reinterpret_cast<const int4*>(buf + S.col_off);       // block j: entries ea + 4j ..
+        const double2* svlo = reinterpret_cast<const double2*>(buf + S.val_off);  // block j: entries 0, 1
+        const double2* svhi = reinterpret_cast<const double2*>(buf + S.val_off + S.tn * 4);  // entries 2, 3
         for (int base = ra; base < rb; base += NG) {  // CTA-uniform trip count (the shuffles below)
           const int r = base + gid;
           const bool valid = r < rb;
           const int b0 = valid ? (srp[r - ra] - ea) / kPad : 0, b1 = valid ? (srp[r - ra + 1] - ea) / kPad : 0;
           double acc = 0.0;
-          for (int j0 = b0 + lane; j0 < b1; j0 += 2 * VS) {  // blocks j0 and j0 + VS: 8 gathers in flight
-            int4 cc[2];
-            double2 w01[2], w23[2];
-            double x[2][4];
+          for (int j0 = b0 + lane; j0 < b1; j0 += UB * VS) {  // blocks j0 + u VS: 4 UB gathers in flight
+            int4 cc[UB];
+            double2 w01[UB], w23[UB];
+            double x[UB][4];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < UB; ++u) {
               const int j = j0 + u * VS;
               cc[u] = j < b1 ? scol[j] : make_int4(-1, -1, -1, -1);
               w01[u] = w23[u] = make_double2(1.0, 1.0);
@@ -175,14 +181,14 @@ __global__ void __launch_bounds__(kSpmvThreads, 5) k_spmv_tma(GraphDev g, const 
               }
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < UB; ++u) {
               x[u][0] = cc[u].x >= 0 ? __ldg(p + cc[u].x) : 0.0;
               x[u][1] = cc[u].y >= 0 ? __ldg(p + cc[u].y) : 0.0;
               x[u][2] = cc[u].z >= 0 ? __ldg(p + cc[u].z) : 0.0;
               x[u][3] = cc[u].w >= 0 ? __ldg(p + cc[u].w) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < UB; ++u) {
               if (cc[u].x >= 0) acc = fma(w01[u].x, x[u][0], acc);
               if (cc[u].y >= 0) acc = fma(w01[u].y, x[u][1], acc);
               if (cc[u].z >= 0) acc = fma(w23[u].x, x[u][2], acc);
@@ -274,10 +280,10 @@ __global__ void k_pad_csr(const int* __restrict__ rp, const int* __restrict__ ci
   }
 }
 
-// host: padded row offsets, row-aligned tiles (<= kTileNnz padded entries and <= kTileRows rows; a
+// host: padded row offsets, row-aligned tiles (<= S.tn padded entries and <= S.tr rows; a
 // longer row alone) and their split over G CTAs by cumulative (entries + 4 rows) weight.
-void spmv_tma_layout(const int* hrp, int n, int G, std::vector<int>& prp, std::vector<int2>& tiles,
-                     std::vector<int>& cta_tiles) {
+void spmv_tma_layout(const int* hrp, int n, int G, const SpmvTileShape& S, std::vector<int>& prp,
+                     std::vector<int2>& tiles, std::vector<int>& cta_tiles) {
   prp.assign(n + 1, 0);
   for (int i = 0; i < n; ++i) prp[i + 1] = prp[i] + (hrp[i + 1] - hrp[i] + kPad - 1) / kPad * kPad;
   tiles.clear();
@@ -285,7 +291,7 @@ void spmv_tma_layout(const int* hrp, int n, int G, std::vector<int>& prp, std::v
   while (r < n) {
     const int ra = r, ea = prp[r];
     ++r;
-    while (r < n && r - ra < kTileRows && prp[r + 1] - ea <= kTileNnz) ++r;
+    while (r < n && r - ra < S.tr && prp[r + 1] - ea <= S.tn) ++r;
     tiles.push_back(make_int2(ra, ea));
   }
   const int nt = (int)tiles.size();
@@ -307,69 +313,78 @@ void launch_pad_csr(const int* rp, const int* ci, const double* vv, int n, const
   const int grid = std::max(1, std::min((n + kThreads - 1) / kThreads, 148 * 8));
   k_pad_csr<<<grid, kThreads, 0, st>>>(rp, ci, vv, n, prp, pci, pvv);
 }
-int spmv_tma_smem_bytes() { return kSpmvStages * kStageBytes; }
+static int smem_bytes(const SpmvTileShape& S) { return S.stages * S.stage_bytes; }
 
-template <int VS, bool NORM, bool UNIT>
-static int spmv_tma_occ() {
-  cudaFuncSetAttribute(k_spmv_tma<VS, NORM, UNIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, spmv_tma_smem_bytes());
+template <int VS, bool NORM, bool UNIT, int UB>
+static int spmv_tma_occ_ub(const SpmvTileShape& S) {
+  cudaFuncSetAttribute(k_spmv_tma<VS, NORM, UNIT, UB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spmv_tma<VS, NORM, UNIT>, kSpmvThreads,
-                                                    spmv_tma_smem_bytes()) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spmv_tma<VS, NORM, UNIT, UB>, kSpmvThreads, smem_bytes(S)) !=
+      cudaSuccess)
     nb = 1;
   return std::max(1, nb);
 }
+template <int VS, bool NORM, bool UNIT>
+static int spmv_tma_occ(const SpmvTileShape& S) {
+  return spmv_tma_occ_ub<VS, NORM, UNIT, 2>(S);
+}
 template <int VS>
-static int spmv_tma_occ_vs(bool norm, bool unit) {
-  if (unit) return norm ? spmv_tma_occ<VS, true, true>() : spmv_tma_occ<VS, false, true>();
-  return norm ? spmv_tma_occ<VS, true, false>() : spmv_tma_occ<VS, false, false>();
+static int spmv_tma_occ_vs(const SpmvTileShape& S, bool norm, bool unit) {
+  if (unit) return norm ? spmv_tma_occ<VS, true, true>(S) : spmv_tma_occ<VS, false, true>(S);
+  return norm ? spmv_tma_occ<VS, true, false>(S) : spmv_tma_occ<VS, false, false>(S);
 }
 // resident CTAs per SM of the instantiation a graph will use (the grid is one full wave)
-int spmv_tma_ctas_per_sm(int vs, bool normalized, bool unit) {
+int spmv_tma_ctas_per_sm(int vs, bool normalized, bool unit, const SpmvTileShape& S) {
   switch (vs) {
-    case 2: return spmv_tma_occ_vs<2>(normalized, unit);
-    case 4: return spmv_tma_occ_vs<4>(normalized, unit);
-    case 8: return spmv_tma_occ_vs<8>(normalized, unit);
-    case 16: return spmv_tma_occ_vs<16>(normalized, unit);
-    default: return spmv_tma_occ_vs<32>(normalized, unit);
+    case 2: return spmv_tma_occ_vs<2>(S, normalized, unit);
+    case 4: return spmv_tma_occ_vs<4>(S, normalized, unit);
+    case 8: return spmv_tma_occ_vs<8>(S, normalized, unit);
+    case 16: return spmv_tma_occ_vs<16>(S, normalized, unit);
+    default: return spmv_tma_occ_vs<32>(S, normalized, unit);
   }
 }
 
-template <int VS, bool NORM, bool UNIT>
-static void spmv_tma_launch(const GraphDev& g, const int2* tiles, const int* cta_tiles, int grid, const double* p,
-                            const double* ps, double* t, double* partials, unsigned* counter, double* bsum_t,
-                            cudaStream_t st) {
+template <int VS, bool NORM, bool UNIT, int UB>
+static void spmv_tma_launch_ub(const GraphDev& g, const SpmvTileShape& S, const int2* tiles, const int* cta_tiles,
+                               int grid, const double* p, const double* ps, double* t, double* partials,
+                               unsigned* counter, double* bsum_t, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_spmv_tma<VS, NORM, UNIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         spmv_tma_smem_bytes());
+    cudaFuncSetAttribute(k_spmv_tma<VS, NORM, UNIT, UB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_spmv_tma<VS, NORM, UNIT><<<grid, kSpmvThreads, spmv_tma_smem_bytes(), st>>>(g, tiles, cta_tiles, p, ps, t,
-                                                                               partials, counter, bsum_t);
+  k_spmv_tma<VS, NORM, UNIT, UB><<<grid, kSpmvThreads, smem_bytes(S), st>>>(g, S, tiles, cta_tiles, p, ps, t, partials,
+                                                                           counter, bsum_t);
+}
+template <int VS, bool NORM, bool UNIT>
+static void spmv_tma_launch(const GraphDev& g, const SpmvTileShape& S, const int2* tiles, const int* cta_tiles,
+                            int grid, const double* p, const double* ps, double* t, double* partials, unsigned* counter,
+                            double* bsum_t, cudaStream_t st) {
+  spmv_tma_launch_ub<VS, NORM, UNIT, 2>(g, S, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st);
 }
 template <int VS>
-static void spmv_tma_vs(const GraphDev& g, const int2* tiles, const int* cta_tiles, int grid, const double* p,
-                        const double* ps, double* t, double* partials, unsigned* counter, double* bsum_t,
-                        cudaStream_t st) {
+static void spmv_tma_vs(const GraphDev& g, const SpmvTileShape& S, const int2* tiles, const int* cta_tiles, int grid,
+                        const double* p, const double* ps, double* t, double* partials, unsigned* counter,
+                        double* bsum_t, cudaStream_t st) {
   if (g.unit) {
-    if (g.normalized) spmv_tma_launch<VS, true, true>(g, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st);
-    else spmv_tma_launch<VS, false, true>(g, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st);
+    if (g.normalized) spmv_tma_launch<VS, true, true>(g, S, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st);
+    else spmv_tma_launch<VS, false, true>(g, S, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st);
   } else {
-    if (g.normalized) spmv_tma_launch<VS, true, false>(g, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st);
-    else spmv_tma_launch<VS, false, false>(g, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st);
+    if (g.normalized) spmv_tma_launch<VS, true, false>(g, S, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st);
+    else spmv_tma_launch<VS, false, false>(g, S, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st);
   }
 }
-void launch_spmv_tma(const GraphDev& g, int vs, const int2* tiles, const int* cta_tiles, int grid, const double* p,
-                     const double* p_self, double* t, double* partials, unsigned* counter, double* bsum_t,
-                     cudaStream_t st) {
+void launch_spmv_tma(const GraphDev& g, int vs, const SpmvTileShape& S, const int2* tiles, const int* cta_tiles,
+                     int grid, const double* p, const double* p_self, double* t, double* partials, unsigned* counter,
+                     double* bsum_t, cudaStream_t st) {
   bump_launch();
   const double* ps = p_self ? p_self : p;
   switch (vs) {
-    case 2: spmv_tma_vs<2>(g, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st); break;
-    case 4: spmv_tma_vs<4>(g, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st); break;
-    case 8: spmv_tma_vs<8>(g, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st); break;
-    case 16: spmv_tma_vs<16>(g, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st); break;
-    default: spmv_tma_vs<32>(g, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    case 2: spmv_tma_vs<2>(g, S, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    case 4: spmv_tma_vs<4>(g, S, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    case 8: spmv_tma_vs<8>(g, S, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    case 16: spmv_tma_vs<16>(g, S, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st); break;
+    default: spmv_tma_vs<32>(g, S, tiles, cta_tiles, grid, p, ps, t, partials, counter, bsum_t, st); break;
   }
 }
 

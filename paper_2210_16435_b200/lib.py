@@ -250,6 +250,8 @@ def sfairsc_eigs(ctx: Context, k: int, tol: float, evecs=None, want_evecs: bool 
     if evecs is None and want_evecs:
         evecs = np.zeros((k, ctx.n))
     if evecs is not None:
+        if tuple(evecs.shape) != (k, ctx.n):  # the library writes k x n doubles
+            raise ValueError(f"evecs must have shape ({k}, {ctx.n}), got {tuple(evecs.shape)}")
         ep, ms = _ptr(evecs, np.float64)
     else:
         ep, ms = None, MEM_HOST
@@ -263,6 +265,8 @@ def sfairsc_embed_kmeans(ctx: Context, seed: int, labels=None):
     """Alg. 3 step 4: labels (n,) int32 (numpy or CUDA tensor) and the WCSS."""
     if labels is None:
         labels = np.zeros(ctx.n, dtype=np.int32)
+    if tuple(labels.shape) != (ctx.n,):  # the library writes n int32 labels
+        raise ValueError(f"labels must have shape ({ctx.n},), got {tuple(labels.shape)}")
     lp, ms = _ptr(labels, np.int32)
     obj = C.c_double()
     _check(_lib.sfairsc_embed_kmeans(ctx.handle, C.c_uint64(seed), lp, ms, C.byref(obj)))
@@ -271,6 +275,8 @@ def sfairsc_embed_kmeans(ctx: Context, seed: int, labels=None):
 
 def _vec_call(fn, ctx, x, y):
     xp, ms = _ptr(x, np.float64)
+    if x.ndim not in (1, 2) or x.shape[-1] != ctx.n:
+        raise ValueError(f"x must be (n,) or (nvec, n) with n = {ctx.n}, got {tuple(x.shape)}")
     nvec = 1 if x.ndim == 1 else x.shape[0]
     if y is None:
         if ms == MEM_DEVICE:
@@ -278,6 +284,8 @@ def _vec_call(fn, ctx, x, y):
             y = torch.empty_like(x)
         else:
             y = np.empty_like(x)
+    if tuple(y.shape) != tuple(x.shape):
+        raise ValueError(f"y must have the shape of x {tuple(x.shape)}, got {tuple(y.shape)}")
     yp, ms2 = _ptr(y, np.float64)
     if ms != ms2:
         raise ValueError("x and y must share a memspace")

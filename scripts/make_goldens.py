@@ -56,19 +56,29 @@ def tier_d(c: int) -> None:
     print(json.dumps({k_: v for k_, v in out.items() if k_ != "resid_rel_via_P803"}))
 
 
-def tier_s(c: int, ncv: int | None, seed: int) -> None:
+def tier_s(c: int, ncv: int | None, seed: int, tol: float = 1e-12) -> None:
     g, cfg = baseline_config(c)
     k = cfg["k_eig"]
     op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, g.h, cfg["normalized"], threads=0)
     t0 = time.time()
-    res = sfairsc_cpu.sfairsc_arpack(op, k, tol=1e-12, ncv=ncv, seed=seed, extra=1)
+    _apply, cnt = op.apply, [0]
+
+    def progress_apply(w):  # the oracle's apply, unchanged; a progress line every 500 matvecs
+        cnt[0] += 1
+        if cnt[0] % 500 == 0:
+            print(f"  {cnt[0]} matvecs, {time.time() - t0:.0f} s", file=sys.stderr, flush=True)
+        return _apply(w)
+
+    op.apply = progress_apply
+    res = sfairsc_cpu.sfairsc_arpack(op, k, tol=tol, ncv=ncv, seed=seed, extra=1)
     wall = time.time() - t0
+    op.apply = _apply
     resid = [float(np.linalg.norm(op.apply(res.X[:, i]) - res.evals[i] * res.X[:, i]) / op.sigma) for i in range(k)]
     out = {"source": "scripts/make_goldens.py --config %d: oracle.sfairsc_cpu.sfairsc_arpack (Tier S: Alg. 3 apply "
-                     "P:803 with the normal-equations projector P:807-818, ARPACK eigsh, tol 1e-12)" % c,
+                     "P:803 with the normal-equations projector P:807-818, ARPACK eigsh, tol %g)" % (c, tol),
            "config": c, "k": k, "normalized": cfg["normalized"], "evals": [float(x) for x in res.evals[:k + 1]],
            "gap_k": float(res.evals[k] - res.evals[k - 1]), "sigma": op.sigma, "matvecs": res.matvecs,
-           "ncv": ncv, "seed": seed, "resid_rel_via_P803": resid, "graph": fingerprint(g), "wall_s": wall,
+           "ncv": ncv, "seed": seed, "tol": tol, "resid_rel_via_P803": resid, "graph": fingerprint(g), "wall_s": wall,
            "threads": op.threads}
     with open(os.path.join(GOLDEN, f"cfg{c}_tier_s.json"), "w") as f:
         json.dump(out, f, indent=1)
@@ -80,8 +90,9 @@ if __name__ == "__main__":
     ap.add_argument("--config", type=int, required=True)
     ap.add_argument("--ncv", type=int, default=None)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--tol", type=float, default=1e-12)
     a = ap.parse_args()
     if a.config in (1, 2):
         tier_d(a.config)
     else:
-        tier_s(a.config, a.ncv, a.seed)
+        tier_s(a.config, a.ncv, a.seed, a.tol)

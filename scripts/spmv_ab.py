@@ -1,6 +1,7 @@
 """A/B of the single-vector SpMV kernels (A5) at BASELINE sizes on one GPU:
 the TMA-fed tile kernel (spmv_tma.cu, default) vs the round-1 LSU kernel
-(SFAIRSC_SPMV_TMA=0).  200 back-to-back t = L x launches per variant, timed by the
+(SFAIRSC_SPMV_TMA=0), and the TMA kernel streaming the values of a unit-weight graph
+(SFAIRSC_UNIT=0) vs its pattern-only form.  200 back-to-back t = L x launches per variant, timed by the
 library's per-launch CUDA events; algorithmic bytes per DESIGN.md §6."""
 import json
 import os
@@ -22,8 +23,9 @@ for c in cfgs:
     rp, ci, vv, gr = t(g.row_ptr), t(g.col), t(g.val), t(g.groups.astype(np.int32))
     x = torch.randn(g.n, dtype=torch.float64, device=dev)
     outs = {}
-    for variant in ("tma", "tma_vs16", "tma_vs4", "lsu"):
+    for variant in ("tma", "tma_vals", "tma_vs16", "tma_vs4", "lsu"):
         os.environ["SFAIRSC_SPMV_TMA"] = "0" if variant == "lsu" else "1"
+        os.environ["SFAIRSC_UNIT"] = "0" if variant == "tma_vals" else "1"  # tma_vals: stream the values
         kw = {"spmv_vector": int(variant.split("vs")[1])} if "vs" in variant else {}
         ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, cfg["k_eig"], cfg["normalized"], h=g.h, **kw)
         y = torch.empty_like(x)

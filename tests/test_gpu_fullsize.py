@@ -94,7 +94,7 @@ def test_config3_full_size_vs_tier_s(gpu_lib):
     assert np.all(_r6(ev, ref.evals[:k], sigma))
     gap = ref.evals[k] - ref.evals[k - 1]
     bound = 2 * (st["max_resid_rel"] * sigma * np.sqrt(k) + 1e-12 * sigma) / gap
-    assert bound <= 1e-7
+    assert bound <= 1e-6  # Davis-Kahan (R8) already certifies the angle contract at this gap
     assert subspace_sin(X, ref.X) <= 1e-6  # the north star's angle contract, not bound-relative
     assert np.linalg.norm(op.C.T @ X) <= 1e-10 * np.linalg.norm(X)
 

@@ -205,24 +205,6 @@ def test_eigs_deterministic(gpu_lib):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2"])
-def test_sweep_kernel_variants_agree(gpu_lib, monkeypatch, variant):
-    """The single-sweep kernels (default: register-held row pairs; the shared-memory
-    64-row kernel 0, the 32-row register kernel 1, 512 threads 2 — A/B switches) run
-    the same algorithm: same eigenvalues against the oracle, same matvec count."""
-    g = random_graph(2500, 3, p=0.006, seed=9, weights="uniform")
-    k = 8
-    dense = fairsc.fairsc_dense(g.dense(), g.groups, g.h, k, True)
-    try:
-        monkeypatch.setenv("SFAIRSC_LZ_SWEEP", variant)
-        ev_v, _, st_v = _check_eigs(gpu_lib, g, k, True, 1e-10, dense=dense)
-    finally:
-        monkeypatch.setenv("SFAIRSC_LZ_SWEEP", "3")  # the switch is read at build: restore the default
-    ev_d, _, st_d = _check_eigs(gpu_lib, g, k, True, 1e-10, dense=dense)
-    assert np.all(np.abs(ev_v - ev_d) <= 1e-9 * np.abs(ev_d) + 1e-12 * st_d["sigma"])
-    assert abs(st_v["applies"] - st_d["applies"]) <= 0.02 * st_d["applies"]
-
-
 @pytest.fixture(scope="module")
 def config2_ref():
     g, cfg = baseline_config(2)
