@@ -128,7 +128,7 @@ typedef struct {
   int32_t device, num_sms;
   int32_t unit_weights;   /* 1: every stored w_ij = 1 (no diagonal entries): the single-vector SpMV
                              streams only column indices (normalized: gathers s o x, row sums scaled by s_i) */
-  int32_t reserved;
+  int32_t constraint_rank; /* rank of C: h - 1 for group fairness; the numerical rank of C for a dense F */
 } sfairsc_info;
 
 void sfairsc_default_opts(sfairsc_opts *opts);
@@ -149,12 +149,16 @@ sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr *W, const int32_t *gr
                                          sfairsc_ctx **out);
 
 /* §8(f) N4 — general linear constraints C^T H = 0 with a dense constraint matrix F (n x r,
- * column-major, 0 <= r <= 16; e.g. the random-F Laplacian of Experiment 4, or
- * overlapping groups; P:465-490 take F as input): C = D^{-1/2} F (normalized) or F,
- * Q = orth(C) by CholQR2 on the device (SFAIRSC_E_RANK_DEFICIENT if rank C < r), and every
- * projector step applies P = I - Q Q^T with the dense rows of Q (Q^T x fused into the SpMV
- * epilogue and the basis sweep, x - Q (Q^T x) into the normalisation).  F in W's memspace.
- * Single GPU, single-sweep solver.  sfairsc_eigs / sfairsc_apply / embed_kmeans as usual. */
+ * column-major, 0 <= r <= 64; e.g. the random-F Laplacian of Experiment 4, or
+ * overlapping groups; P:465-490 take F as input): C = D^{-1/2} F (normalized) or F.
+ * P = I - C C^+ (C^+ the pseudo-inverse, i.e. the minimum-norm least-squares solve
+ * of P:815-820, so a rank-deficient C is allowed): Q = an orthonormal basis of range(C) from
+ * the eigendecomposition of C^T C with numerical rank rq = #{eigenvalues > 1e-14 x the largest}
+ * (reading R21), then one Cholesky-QR step; rq must be <= 16 (SFAIRSC_E_INVALID_ARG otherwise),
+ * k <= n - rq (SFAIRSC_E_K_TOO_LARGE).  Every projector step applies P = I - Q Q^T with the
+ * dense rows of Q (Q^T x fused into the SpMV epilogue and the basis sweep, x - Q (Q^T x) into
+ * the normalisation).  sfairsc_info.constraint_rank reports rq.  F in W's memspace.  Single GPU,
+ * single-sweep solver.  sfairsc_eigs / sfairsc_apply / embed_kmeans as usual. */
 sfairsc_status sfairsc_build_operator_dense(const sfairsc_csr *W, const double *F, int32_t r, int32_t k,
                                             int32_t normalized, const sfairsc_opts *opts, sfairsc_ctx **out);
 

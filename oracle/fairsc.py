@@ -61,12 +61,19 @@ def laplacian(W: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     return np.diag(d) - W, d
 
 
-def nullspace_basis(F: np.ndarray) -> np.ndarray:
-    """Z = U(:, h:n) from the full SVD F = U Sigma V^T (Alg. 2 step 2)."""
+def nullspace_basis(F: np.ndarray, rank_tol: float | None = None) -> np.ndarray:
+    """Z = U(:, h:n) from the full SVD F = U Sigma V^T (Alg. 2 step 2).
+
+    rank_tol (reading R21, a rank-deficient F of §8(f) N4): Z = null(F^T) = U(:, r:n) with
+    r = #{i : Sigma_i > rank_tol Sigma_1}, the numerical rank (the textbook null space
+    from the SVD).  None: F must have full column rank (Lemma 2.1(i) for group F)."""
     n, q = F.shape
     if q == 0:
         return np.eye(n)
     U, S, Vt = np.linalg.svd(F, full_matrices=True)
+    if rank_tol is not None:
+        r = int(np.sum(S > rank_tol * S[0])) if S[0] > 0 else 0
+        return U[:, r:]
     if S[-1] <= 1e-12 * S[0]:
         raise OracleInputError("F rank deficient (Lemma 2.1(i) violated)")
     return U[:, q:]
@@ -101,7 +108,8 @@ def validate_W(W: np.ndarray) -> None:
         raise OracleInputError("W is not a valid weighted adjacency matrix")
 
 
-def fairsc_dense_F(W: np.ndarray, F: np.ndarray, k: int, normalized: bool, extra: int = 1) -> FairSCResult:
+def fairsc_dense_F(W: np.ndarray, F: np.ndarray, k: int, normalized: bool, extra: int = 1,
+                   rank_tol: float | None = None) -> FairSCResult:
     """Algorithm 2 (FairSC), P:465-490, for a given constraint matrix F (n x r;
     the paper's algorithm takes F as its input).  Returns the k smallest
     eigenpairs of the fair-SC problem plus `extra` further eigenvalues.
@@ -115,7 +123,7 @@ def fairsc_dense_F(W: np.ndarray, F: np.ndarray, k: int, normalized: bool, extra
     validate_W(W)
     n = W.shape[0]
     L, d = laplacian(W)  # step 1
-    Z = nullspace_basis(np.asarray(F, dtype=np.float64).reshape(n, -1))  # step 2: Z = null(F^T)
+    Z = nullspace_basis(np.asarray(F, dtype=np.float64).reshape(n, -1), rank_tol)  # step 2: Z = null(F^T)
     A = Z.T @ L @ Z
     A = 0.5 * (A + A.T)
     kk = min(k + extra, Z.shape[1])

@@ -147,7 +147,7 @@ extern "C" sfairsc_status sfairsc_get_info(const sfairsc_ctx* c, sfairsc_info* i
   info->device = c->device;
   info->num_sms = c->num_sms;
   info->unit_weights = c->unit ? 1 : 0;
-  info->reserved = 0;
+  info->constraint_rank = c->Qr || c->rank_in > 0 ? c->qr : std::max(0, c->h - 1);
   return SFAIRSC_OK;
 }
 
@@ -746,7 +746,7 @@ extern "C" sfairsc_status sfairsc_build_operator_dense(const sfairsc_csr* W, con
                                                        int32_t normalized, const sfairsc_opts* opts_in,
                                                        sfairsc_ctx** out) {
   if (!W || !out || (r > 0 && !F)) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
-  if (r < 0 || r > kHB) return fail(SFAIRSC_E_INVALID_ARG, "r must be in [0, %d]", kHB);
+  if (r < 0 || r > kMaxFCols) return fail(SFAIRSC_E_INVALID_ARG, "r must be in [0, %d]", kMaxFCols);
   *out = nullptr;
   sfairsc_opts opts;
   sfairsc_default_opts(&opts);
@@ -755,12 +755,12 @@ extern "C" sfairsc_status sfairsc_build_operator_dense(const sfairsc_csr* W, con
   if (opts.block_size > 1 || opts.reorth == 1)
     return fail(SFAIRSC_E_INVALID_ARG, "dense constraints use the single-sweep solver (block_size 0/1, reorth 0/2)");
   const long long n = W->n_rows;
-  if (n < 2 || (long long)k > n - r) return fail(SFAIRSC_E_K_TOO_LARGE, "k=%d > n - r = %lld", k, n - r);
+  if (n < 2 || k < 1 || (long long)k > n - 1) return fail(SFAIRSC_E_K_TOO_LARGE, "k=%d > n - 1 = %lld", k, n - 1);
   opts.block_size = 1;
   opts.reorth = 2;
   if (opts.max_basis <= 0) {
     int m = std::min(192, std::max(std::max(2 * k + 10, 17 * k / 5), 20));
-    opts.max_basis = (int)std::min<long long>(m, n - r - 1);
+    opts.max_basis = (int)std::min<long long>(m, n - std::min<long long>(r, kHB) - 1);
   }
   std::vector<int32_t> zeros((size_t)n, 0);
   int32_t* gz = zeros.data();
@@ -785,14 +785,12 @@ extern "C" sfairsc_status sfairsc_build_operator_dense(const sfairsc_csr* W, con
     return s;
   };
   const int ni = (int)n;
-  c->qr = r;
-  c->ldq = (r + 1) / 2 * 2;  // 16-byte rows for the TMA bulk copies
-  double *Cd = nullptr, *Q1 = nullptr, *G = nullptr, *Ud = nullptr;
+  double *Cd = nullptr, *Q1 = nullptr, *G = nullptr, *Td = nullptr;
   auto cleanup = [&]() {
     if (Cd) cudaFree(Cd);
     if (Q1) cudaFree(Q1);
     if (G) cudaFree(G);
-    if (Ud) cudaFree(Ud);
+    if (Td) cudaFree(Td);
   };
 #define CUD(expr)                                                                                       \
   do {                                                                                                  \
@@ -807,52 +805,90 @@ extern "C" sfairsc_status sfairsc_build_operator_dense(const sfairsc_csr* W, con
   CUD(cudaMemcpyAsync(Cd, F, sizeof(double) * (size_t)n * r,
                       W->memspace == SFAIRSC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
   if (c->normalized) launch_scale_rows(Cd, n, ni, r, c->s, c->st);  // C = D^{-1/2} F
+  CUD(cudaMalloc(&G, sizeof(double) * r * r));
+  CUD(cudaMalloc(&Td, sizeof(double) * r * kHB));
+  // pass 0, rank revealing (reading R21; P:819-822 allow any C whose least-squares problem min ||C z - w|| the
+  // projector solves): G = C^T C = V diag(lam) V^T; the numerical rank rq = #{lam_i > 1e-14 lam_max} (singular
+  // values above 1e-7 of the largest: what a Gram matrix resolves in fp64); Q1 = C V_rq diag(lam_rq)^{-1/2} spans
+  // range(C) = the range of the P:809 projector's C (C^+ of a rank-deficient C: the minimum-norm LS solution)
+  std::vector<double> Gh((size_t)r * r), lam;
+  CUD(cudaMemsetAsync(G, 0, sizeof(double) * r * r, c->st));
+  launch_gram_pairs(Cd, 1, n, ni, r, G, c->st);
+  CUD(cudaMemcpyAsync(Gh.data(), G, sizeof(double) * r * r, cudaMemcpyDeviceToHost, c->st));
+  CUD(cudaStreamSynchronize(c->st));
+  for (int a = 0; a < r; ++a)
+    for (int b = 0; b < a; ++b) Gh[(size_t)a * r + b] = Gh[(size_t)b * r + a];
+  symeig(r, Gh, lam);  // ascending; Gh[a * r + c] = component a of eigenvector c
+  const double lmax = lam[r - 1];
+  int rq = 0;
+  for (int i = r - 1; i >= 0; --i)
+    if (lmax > 0.0 && lam[i] > 1e-14 * lmax) ++rq;
+  if (rq > kHB) {
+    cleanup();
+    return bail(fail(SFAIRSC_E_INVALID_ARG, "numerical rank %d of C exceeds %d (the projector's row width)", rq, kHB));
+  }
+  if ((long long)k > n - rq) {
+    cleanup();
+    return bail(fail(SFAIRSC_E_K_TOO_LARGE, "k=%d > n - rank(C) = %lld", k, n - rq));
+  }
+  c->qr = rq;
+  c->rank_in = r;  // dense-F context (constraint_rank = qr)
+  if (rq == 0) {  // C = 0: no constraint (P = I)
+    cleanup();
+    *out = c;
+    return SFAIRSC_OK;
+  }
+  c->ldq = (rq + 1) / 2 * 2;  // 16-byte rows for the TMA bulk copies
   CUD(cudaMalloc(&Q1, sizeof(double) * (size_t)c->ldv * c->ldq));
   CUD(cudaMemsetAsync(Q1, 0, sizeof(double) * (size_t)c->ldv * c->ldq, c->st));
   CUD(cudaMalloc(&c->Qr, sizeof(double) * (size_t)c->ldv * c->ldq));
   CUD(cudaMemsetAsync(c->Qr, 0, sizeof(double) * (size_t)c->ldv * c->ldq, c->st));
-  CUD(cudaMalloc(&G, sizeof(double) * r * r));
-  CUD(cudaMalloc(&Ud, sizeof(double) * r * r));
-  std::vector<double> Gh(r * r), U(r * r), Ui(r * r);
-  double maxdiag0 = 0.0;
-  for (int pass = 0; pass < 2; ++pass) {  // CholQR2: C -> Q1 -> Q
-    const double* Min = pass == 0 ? Cd : Q1;
-    const long long rs = pass == 0 ? 1 : c->ldq, cs = pass == 0 ? n : 1;
-    CUD(cudaMemsetAsync(G, 0, sizeof(double) * r * r, c->st));
-    launch_gram_pairs(Min, rs, cs, ni, r, G, c->st);
-    CUD(cudaMemcpyAsync(Gh.data(), G, sizeof(double) * r * r, cudaMemcpyDeviceToHost, c->st));
+  {
+    std::vector<double> T((size_t)r * rq);
+    for (int j = 0; j < rq; ++j) {  // largest eigenvalue first
+      const int col = r - 1 - j;
+      const double is = 1.0 / std::sqrt(lam[col]);
+      for (int a = 0; a < r; ++a) T[(size_t)a * rq + j] = Gh[(size_t)a * r + col] * is;
+    }
+    CUD(cudaMemcpyAsync(Td, T.data(), sizeof(double) * T.size(), cudaMemcpyHostToDevice, c->st));
+    launch_rows_times(Cd, 1, n, ni, r, rq, Td, Q1, c->ldq, c->st);
+    CUD(cudaGetLastError());
     CUD(cudaStreamSynchronize(c->st));
-    for (int a = 0; a < r; ++a)
-      for (int b = 0; b < a; ++b) Gh[a * r + b] = Gh[b * r + a];
-    if (pass == 0)
-      for (int a = 0; a < r; ++a) maxdiag0 = std::max(maxdiag0, Gh[a * r + a]);
-    // Cholesky G = U^T U (U upper); rank check on the first pass (Lemma 2.1(i) for group F)
-    std::fill(U.begin(), U.end(), 0.0);
-    for (int j = 0; j < r; ++j) {
-      double d = Gh[j * r + j];
-      for (int q = 0; q < j; ++q) d -= U[q * r + j] * U[q * r + j];
-      if (!(d > (pass == 0 ? 1e-24 * maxdiag0 : 0.25))) {
+  }
+  // pass 1: one Cholesky-QR step Q = Q1 U^{-1} (Q1^T Q1 = I up to cond(C)^2 eps: CholQR2 in total)
+  {
+    const int q = rq;
+    std::vector<double> Gq((size_t)q * q), U((size_t)q * q, 0.0), Ui((size_t)q * q, 0.0);
+    CUD(cudaMemsetAsync(G, 0, sizeof(double) * q * q, c->st));
+    launch_gram_pairs(Q1, c->ldq, 1, ni, q, G, c->st);
+    CUD(cudaMemcpyAsync(Gq.data(), G, sizeof(double) * q * q, cudaMemcpyDeviceToHost, c->st));
+    CUD(cudaStreamSynchronize(c->st));
+    for (int a = 0; a < q; ++a)
+      for (int b = 0; b < a; ++b) Gq[(size_t)a * q + b] = Gq[(size_t)b * q + a];
+    for (int j = 0; j < q; ++j) {  // G = U^T U (U upper)
+      double d = Gq[(size_t)j * q + j];
+      for (int p = 0; p < j; ++p) d -= U[(size_t)p * q + j] * U[(size_t)p * q + j];
+      if (!(d > 0.25)) {  // Q1 is orthonormal to far better than this unless the rank decision was wrong
         cleanup();
-        return bail(fail(SFAIRSC_E_RANK_DEFICIENT, "constraint matrix C has (numerical) rank < r = %d", r));
+        return bail(fail(SFAIRSC_E_RANK_DEFICIENT, "constraint basis lost orthogonality (rank decision %d of %d)", q, r));
       }
-      U[j * r + j] = std::sqrt(d);
-      for (int i = j + 1; i < r; ++i) {
-        double v = Gh[j * r + i];
-        for (int q = 0; q < j; ++q) v -= U[q * r + j] * U[q * r + i];
-        U[j * r + i] = v / U[j * r + j];
+      U[(size_t)j * q + j] = std::sqrt(d);
+      for (int i = j + 1; i < q; ++i) {
+        double v = Gq[(size_t)j * q + i];
+        for (int p = 0; p < j; ++p) v -= U[(size_t)p * q + j] * U[(size_t)p * q + i];
+        U[(size_t)j * q + i] = v / U[(size_t)j * q + j];
       }
     }
-    std::fill(Ui.begin(), Ui.end(), 0.0);
-    for (int j = 0; j < r; ++j) {
-      Ui[j * r + j] = 1.0 / U[j * r + j];
+    for (int j = 0; j < q; ++j) {
+      Ui[(size_t)j * q + j] = 1.0 / U[(size_t)j * q + j];
       for (int i = j - 1; i >= 0; --i) {
         double v = 0.0;
-        for (int q = i + 1; q <= j; ++q) v += U[i * r + q] * Ui[q * r + j];
-        Ui[i * r + j] = -v / U[i * r + i];
+        for (int p = i + 1; p <= j; ++p) v += U[(size_t)i * q + p] * Ui[(size_t)p * q + j];
+        Ui[(size_t)i * q + j] = -v / U[(size_t)i * q + i];
       }
     }
-    CUD(cudaMemcpyAsync(Ud, Ui.data(), sizeof(double) * r * r, cudaMemcpyHostToDevice, c->st));
-    launch_rows_times_upper(Min, rs, cs, ni, r, Ud, pass == 0 ? Q1 : c->Qr, c->ldq, c->st);
+    CUD(cudaMemcpyAsync(Td, Ui.data(), sizeof(double) * Ui.size(), cudaMemcpyHostToDevice, c->st));
+    launch_rows_times(Q1, c->ldq, 1, ni, q, q, Td, c->Qr, c->ldq, c->st);
     CUD(cudaGetLastError());
     CUD(cudaStreamSynchronize(c->st));
   }

@@ -123,6 +123,7 @@ struct sfairsc_ctx {
   // dense constraint basis (§8(f) N4, sfairsc_build_operator_dense): Q n x qr row-major (ldq); nullptr: groups
   double* Qr = nullptr;
   int qr = 0, ldq = 0;
+  int rank_in = 0;  // dense F: its column count (qr = the numerical rank of C)
   // row-partitioned contexts: all device state lives in dist
   sfz::DistCtx* dist = nullptr;
   // results

@@ -394,27 +394,29 @@ __global__ void k_scale_rows(double* M, long long ld, int n, int r, const double
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     for (int a = 0; a < r; ++a) M[(long long)a * ld + i] *= s[i];
 }
-// Qout[i, :] = Min[i, :] Ui (Ui upper triangular r x r row-major), Qout row-major (ldq)
-__global__ void k_rows_times_upper(const double* __restrict__ Min, long long rs, long long cs, int n, int r,
-                                   const double* __restrict__ Ui, double* __restrict__ Qout, int ldq) {
-  __shared__ double U[16 * 16];
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) U[e] = Ui[e];
+// Qout[i, :] = Min[i, :] T (T: r x rq row-major, r <= 64, rq <= 16), Qout row-major (ldq; columns rq..ldq zeroed)
+__global__ void k_rows_times(const double* __restrict__ Min, long long rs, long long cs, int n, int r, int rq,
+                             const double* __restrict__ T, double* __restrict__ Qout, int ldq) {
+  __shared__ double Ts[64 * 16];
+  for (int e = threadIdx.x; e < r * rq; e += blockDim.x) Ts[e] = T[e];
   __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    double row[16];
-    for (int a = 0; a < r; ++a) row[a] = Min[(long long)i * rs + (long long)a * cs];
-    for (int j = 0; j < ldq; ++j) {
-      double acc = 0.0;
-      if (j < r)
-        for (int l = 0; l <= j; ++l) acc = fma(row[l], U[l * r + j], acc);
-      Qout[(long long)i * ldq + j] = acc;
+    double acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+    for (int a = 0; a < r; ++a) {
+      const double m = Min[(long long)i * rs + (long long)a * cs];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < rq) acc[j] = fma(m, Ts[a * rq + j], acc[j]);
     }
+    for (int j = 0; j < ldq; ++j) Qout[(long long)i * ldq + j] = j < rq ? acc[j] : 0.0;
   }
 }
 void launch_gram_pairs(const double* M, long long rs, long long cs, int n, int r, double* out, cudaStream_t st);
 void launch_scale_rows(double* M, long long ld, int n, int r, const double* s, cudaStream_t st);
-void launch_rows_times_upper(const double* Min, long long rs, long long cs, int n, int r, const double* Ui,
-                             double* Qout, int ldq, cudaStream_t st);
+void launch_rows_times(const double* Min, long long rs, long long cs, int n, int r, int rq, const double* T,
+                       double* Qout, int ldq, cudaStream_t st);
 
 // ----------------------------------------------------------------------------
 // launch wrappers
@@ -584,9 +586,9 @@ void launch_scale_rows(double* M, long long ld, int n, int r, const double* s, c
   bump();
   k_scale_rows<<<stream_grid(n), kThreads, 0, st>>>(M, ld, n, r, s);
 }
-void launch_rows_times_upper(const double* Min, long long rs, long long cs, int n, int r, const double* Ui,
-                             double* Qout, int ldq, cudaStream_t st) {
+void launch_rows_times(const double* Min, long long rs, long long cs, int n, int r, int rq, const double* T,
+                       double* Qout, int ldq, cudaStream_t st) {
   bump();
-  k_rows_times_upper<<<stream_grid(n), kThreads, 0, st>>>(Min, rs, cs, n, r, Ui, Qout, ldq);
+  k_rows_times<<<stream_grid(n), kThreads, 0, st>>>(Min, rs, cs, n, r, rq, T, Qout, ldq);
 }
 }  // namespace sfz

@@ -207,9 +207,10 @@ void launch_spmv_tma(const GraphDev& g, int vs, const SpmvTileShape& S, const in
 // out[a*r + b] (a <= b) = sum_i M(i,a) M(i,b), M(i,a) = M[i*rs + a*cs] (fixed-order block reduction)
 void launch_gram_pairs(const double* M, long long rs, long long cs, int n, int r, double* out, cudaStream_t st);
 void launch_scale_rows(double* M, long long ld, int n, int r, const double* s, cudaStream_t st);
-// Qout (row-major, ldq) = M Ui, Ui upper triangular r x r (row-major, device)
-void launch_rows_times_upper(const double* Min, long long rs, long long cs, int n, int r, const double* Ui,
-                             double* Qout, int ldq, cudaStream_t st);
+constexpr int kMaxFCols = 64;  // dense constraint matrix F: at most 64 columns (numerical rank <= kHB)
+// Qout (row-major, ldq; columns rq..ldq zeroed) = M T, T: r x rq row-major (device), r <= 64, rq <= 16
+void launch_rows_times(const double* Min, long long rs, long long cs, int n, int r, int rq, const double* T,
+                       double* Qout, int ldq, cudaStream_t st);
 
 // ---- k-means ----------------------------------------------------------------------
 void launch_build_rows(const double* X, long long ldx, int n, int k, const double* s, double* H, cudaStream_t st);

@@ -66,7 +66,7 @@ class Info(C.Structure):
     _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("h", C.c_int32), ("k_build", C.c_int32),
                 ("normalized", C.c_int32), ("spmv_vector", C.c_int32), ("sigma", C.c_double),
                 ("device", C.c_int32), ("num_sms", C.c_int32), ("unit_weights", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("constraint_rank", C.c_int32)]
 
 
 def _load():

@@ -52,9 +52,43 @@ def test_dense_F_with_group_F_equals_group_path(gpu_lib):
     assert subspace_sin(Xa.T, Xb.T) <= 1e-6
 
 
-def test_dense_F_rank_deficient(gpu_lib):
-    g, F = random_laplacian(300, 0.05, 3, seed=1)
-    F[:, 2] = F[:, 0] - 2 * F[:, 1]
-    with pytest.raises(gpu_lib.SfairscError) as e:
+@pytest.mark.parametrize("normalized", [False, True])
+@pytest.mark.parametrize("n,r,extra,k", [(900, 3, 2, 5), (1300, 12, 12, 8)])
+def test_dense_F_rank_deficient_vs_oracle(gpu_lib, normalized, n, r, extra, k):
+    """Reading R21: F with r independent columns plus `extra` linear combinations of them
+    (24 columns of rank 12 in the second case: wider than the 16-wide projector rows) gives
+    the projector of range(F) (P = I - C C^+), the same eigenpairs as the oracle's
+    Alg. 2 with Z = null(F^T) at the numerical rank."""
+    g, F0 = random_laplacian(n, 8.0 / n, r, seed=n + r)
+    M = np.random.default_rng(r).standard_normal((r, extra))
+    F = np.hstack([F0, F0 @ M])  # rank r, r + extra columns
+    W = g.dense()
+    ref = fairsc.fairsc_dense_F(W, F, k, normalized, rank_tol=1e-7)
+    ref0 = fairsc.fairsc_dense_F(W, F0, k, normalized)  # range(F) = range(F0)
+    assert np.allclose(ref.evals, ref0.evals, rtol=1e-10, atol=1e-12)
+    ctx = gpu_lib.sfairsc_build_operator_dense(g.row_ptr, g.col, g.val, F, k, normalized)
+    assert ctx.info()["constraint_rank"] == r
+    ev, Xt, st = gpu_lib.sfairsc_eigs(ctx, k, 1e-10)
+    ctx.close()
+    sigma = st["sigma"]
+    X = Xt.T
+    assert st["converged"] == 1 and st["max_resid_rel"] <= 1e-9
+    assert np.all(np.abs(ev - ref.evals[:k]) <= 1e-8 * np.abs(ref.evals[:k]) + 1e-12 * sigma)
+    C = fairsc.constraint_matrix_F(W, F0, normalized)
+    assert np.linalg.norm(C.T @ X) <= 1e-10 * np.linalg.norm(C) * np.linalg.norm(X)
+    bound = 2 * (st["max_resid_rel"] * sigma * np.sqrt(k) + 1e-12 * sigma) / ref.gap
+    assert subspace_sin(X, ref.X) <= max(1e-6, bound)
+
+
+def test_dense_F_rank_limits(gpu_lib):
+    g, F = random_laplacian(400, 0.05, 17, seed=1)
+    with pytest.raises(gpu_lib.SfairscError) as e:  # numerical rank 17 > 16
         gpu_lib.sfairsc_build_operator_dense(g.row_ptr, g.col, g.val, F, 4, True)
-    assert e.value.name == "E_RANK_DEFICIENT"
+    assert e.value.name == "E_INVALID_ARG"
+    with pytest.raises(gpu_lib.SfairscError) as e:  # more than 64 columns
+        gpu_lib.sfairsc_build_operator_dense(g.row_ptr, g.col, g.val, np.hstack([F[:, :1]] * 65), 4, True)
+    assert e.value.name == "E_INVALID_ARG"
+    # all-zero F: no constraint (rank 0), the plain spectral problem
+    ctx = gpu_lib.sfairsc_build_operator_dense(g.row_ptr, g.col, g.val, np.zeros((g.n, 3)), 4, False)
+    assert ctx.info()["constraint_rank"] == 0
+    ctx.close()

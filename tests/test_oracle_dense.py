@@ -16,7 +16,7 @@ from scipy.sparse.csgraph import laplacian as csgraph_laplacian
 from conftest import GOLDEN
 from oracle import brute, fairsc
 from oracle.metrics import subspace_sin
-from synth import planted_cliques, random_graph
+from synth import planted_cliques, random_graph, random_laplacian
 
 
 def _golden_b2():
@@ -301,3 +301,21 @@ def test_dense_F_tier_s_matches_tier_d():
         op = sfairsc_cpu.build_operator(g.to_scipy(), g.groups, 1, normalized, F=F)
         s = sfairsc_cpu.sfairsc_arpack(op, 6, tol=1e-13, seed=1)
         assert np.allclose(s.evals[:6], d.evals[:6], atol=1e-10 * op.sigma)
+
+
+@pytest.mark.parametrize("normalized", [False, True])
+def test_rank_deficient_F_null_space_reading_R21(normalized):
+    """Reading R21 (rank-deficient F, §8(f) N4): Z = null(F^T) at the numerical rank.  Appending
+    linear combinations of the columns leaves range(F), hence null(F^T) and every fair eigenpair,
+    unchanged; without rank_tol the oracle refuses (Lemma 2.1(i) check)."""
+    g, F0 = random_laplacian(60, 0.2, 3, seed=2)
+    W = g.dense()
+    F = np.hstack([F0, F0 @ np.array([[1.0, -2.0], [0.5, 0.0], [0.0, 3.0]])])
+    a = fairsc.fairsc_dense_F(W, F, 6, normalized, rank_tol=1e-7)
+    b = fairsc.fairsc_dense_F(W, F0, 6, normalized)
+    assert np.allclose(a.evals, b.evals, rtol=1e-11, atol=1e-12)
+    assert subspace_sin(a.X, b.X) <= 1e-9
+    Z = fairsc.nullspace_basis(F, 1e-7)
+    assert Z.shape == (60, 57) and np.abs(F.T @ Z).max() <= 1e-12 * np.abs(F).max()
+    with pytest.raises(fairsc.OracleInputError):
+        fairsc.fairsc_dense_F(W, F, 6, normalized)

@@ -3,7 +3,7 @@ FairSC oracle on small cases (exploration; the parity tests are in tests/)."""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 from oracle import fairsc  # noqa: E402
