@@ -99,7 +99,7 @@ static void free_ctx(sfairsc_ctx* c) {
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
                   c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta,
                   c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags, c->Hdev, c->sdev, c->lz, c->partials2, c->dd, c->rpb,
-                  c->pairP, c->pairT, c->pairY, c->Qr, c->vq, c->vq_lz};
+                  c->pairP, c->pairT, c->pairY, c->Qr, c->vq, c->vq_lz, c->vrB, c->lzp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hp) cudaFreeHost(c->hp);
@@ -425,11 +425,18 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
       }
     }
   }
-  // single-vector reorthogonalisation: 0 auto (= lagged single sweep), 1 CGS2 (three sweeps), 2 lagged
-  if (opts.reorth < 0 || opts.reorth > 2) return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth must be 0, 1 or 2"));
+  // single-vector reorthogonalisation: 0 auto (= paired lagged sweeps where allowed, else lagged), 1 CGS2 (three
+  // sweeps per step), 2 lagged (one sweep per step), 3 paired (one sweep per two steps)
+  if (opts.reorth < 0 || opts.reorth > 3) return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth must be 0, 1, 2 or 3"));
   c->lagged = c->bsz == 1 && opts.reorth != 1 && hh <= kHB && m <= 192 && m <= n - hh && m > k;
-  if (opts.reorth == 2 && !c->lagged)
-    return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth=2 needs block_size 1, h <= 16 and k < m <= min(192, n-h)"));
+  if ((opts.reorth == 2 || opts.reorth == 3) && !c->lagged)
+    return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth=2/3 need block_size 1, h <= 16 and k < m <= min(192, n-h)"));
+  // paired steps: single GPU, group projector (the dense projector and row-partitioned builds keep one step
+  // per sweep); they need room for a pair after the first step of a cycle
+  c->paired = c->lagged && opts.reorth != 2 && !(opts.comm || opts.virtual_parts > 1) && !g_build_keep_values &&
+              m >= k + 4;
+  if (opts.reorth == 3 && !c->paired)
+    return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth=3 needs a single-GPU group-fairness build and m >= k + 4"));
   if (is_dist) {  // row-partitioned single-sweep Lanczos (dist.cu)
     if (!c->lagged) return bail(fail(SFAIRSC_E_INVALID_ARG, "row-partitioned builds need h <= 16, block_size 1, reorth 0/2"));
     {
@@ -714,7 +721,14 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     CUB(dalloc(&c->sdev, m + 2));
     CUB(dalloc(&c->lz, 16));
     CUB(cudaMemsetAsync(c->lz, 0, sizeof(double) * 16, c->st));
-    CUB(dalloc(&c->partials2, (size_t)c->num_sms * (kHB + 1) + 64));
+    CUB(dalloc(&c->partials2, (size_t)c->num_sms * (kHB + 2) + 64));
+    c->paired = c->paired && m <= kPairMaxM;  // the pair sweep's 2-stage ring fits up to J = m - 1 <= 185
+    if (c->paired) {
+      CUB(dalloc(&c->vrB, c->ldv));
+      CUB(cudaMemsetAsync(c->vrB, 0, sizeof(double) * c->ldv, c->st));
+      CUB(dalloc(&c->lzp, 8 * kMaxJ));
+      CUB(cudaMemsetAsync(c->lzp, 0, sizeof(double) * 8 * kMaxJ, c->st));
+    }
     CUB(dalloc(&c->dd, kMaxJ + 8));
     CUB(dalloc(&c->bflags, kMaxJ + 8));
     CUB(cudaMemsetAsync(c->bflags, 0, sizeof(int) * (kMaxJ + 8), c->st));

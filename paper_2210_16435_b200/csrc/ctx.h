@@ -110,6 +110,9 @@ struct sfairsc_ctx {
   int* bflags = nullptr;                                // per-step breakdown flags
   // single-sweep (lagged) Lanczos (lanczos1.cu); uses ldT = m + 2 for H
   bool lagged = false;
+  bool paired = false;     // lagged solver with two Lanczos steps per basis sweep (reorth 3, default where allowed)
+  double* vrB = nullptr;   // paired steps: the second lagged vector of a pair
+  double* lzp = nullptr;   // paired steps: epend | econv | cA | tr | pair dots (8 kMaxJ doubles)
   double *Hdev = nullptr, *sdev = nullptr, *lz = nullptr, *partials2 = nullptr, *dd = nullptr;
   // column-blocked CSR (the gathered vector exceeds L2, e.g. config 5): block-major copy of the CSR,
   // rpb[b*(n+1) + i] = start of row i in column block b; nblk = 1: plain CSR

@@ -10,7 +10,8 @@ namespace sfz {
 
 constexpr int kThreads = 256;  // CTA size of every streaming kernel
 constexpr int kHB = 16;        // group sums fused per kernel (h > 16: extra gsum passes)
-constexpr int kMaxJ = 512;     // max Krylov basis columns handled by the sweep kernels
+constexpr int kMaxJ = 512;
+constexpr int kPairMaxM = 186;  // paired Lanczos steps (lanczos1.cu): basis size limit of the pair sweep     // max Krylov basis columns handled by the sweep kernels
 constexpr int kBT = kHB + 1;   // per-vector stride of the SpMV epilogue output: B^T t (kHB) and p^T t
 
 // Factored projector coefficients (DESIGN.md §Factored projector).

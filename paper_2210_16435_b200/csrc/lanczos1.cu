@@ -61,6 +61,55 @@ __global__ void __launch_bounds__(kCoefT) k_lz_coef(LzDev d, int j) {
   __shared__ double sh_mu, sh_alpha, sh_kappa;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int ld = d.ldH;
+  // ---- paired steps: the stored odd column p = j - 1 of the last pair is V'' T (T = I but column p =
+  // [e; rho], e its measured defect): move the bookkeeping to the orthonormal basis V'' before anything
+  // reads it — H <- T H T^-1 on the j x j block, the lagged row b~ <- T^-T b~, s <- T^-T s
+  const int pcol = (d.epend && d.lz[LZ_PEND] == (double)(j - 1)) ? j - 1 : -1;
+  if (pcol >= 0) {
+    __shared__ double ee[kLMaxJ + 1], hle[kLMaxJ + 2];
+    __shared__ double sh_es;
+    const int p = pcol;  // == j - 1
+    const double rho = d.lz[LZ_PRHO];
+    for (int l = tid; l < p; l += kCoefT) ee[l] = d.epend[l];
+    __syncthreads();
+    for (int l = w; l <= p + 1; l += kCoefT / 32) {  // warp per row: rows 0..p and the lagged row j
+      const int row = (l == p + 1) ? j : l;
+      double acc = 0.0;
+      for (int c = lane; c < p; c += 32) acc = fma(d.H[(size_t)c * ld + row], ee[c], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) hle[l] = acc;
+    }
+    double es = 0.0;
+    for (int l = tid; l < p; l += kCoefT) es = fma(ee[l], d.s[l], es);
+    es = warp_sum(es);
+    if (lane == 0) red[w][0] = es;
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0;
+      for (int q = 0; q < kCoefT / 32; ++q) a += red[q][0];
+      sh_es = a;
+    }
+    const double hpp = d.H[(size_t)p * ld + p];
+    for (int l = tid; l < p; l += kCoefT)  // column p, rows < p
+      d.H[(size_t)p * ld + l] = (d.H[(size_t)p * ld + l] + ee[l] * hpp - hle[l] - ee[l] * hle[p]) / rho;
+    __syncthreads();
+    if (tid == 0) {
+      d.H[(size_t)p * ld + p] = hpp - hle[p];
+      d.H[(size_t)p * ld + j] = (d.H[(size_t)p * ld + j] - hle[p + 1]) / rho;  // lagged row, column p
+      d.s[p] = (d.s[p] - sh_es) / rho;
+      d.lz[LZ_CONV] = p;  // the next sweep rewrites column p; coefficient vectors go out in the stored basis
+      d.lz[LZ_CRHO] = rho;
+      d.lz[LZ_PEND] = -1.0;
+    }
+    for (int c = w; c < p; c += kCoefT / 32) {  // columns c < p: rows < p += e H[p, c]; row p *= rho
+      const double hpc = d.H[(size_t)c * ld + p];
+      for (int l = lane; l < p; l += 32) d.H[(size_t)c * ld + l] = fma(ee[l], hpc, d.H[(size_t)c * ld + l]);
+      __syncwarp();
+      if (lane == 0) d.H[(size_t)c * ld + p] = rho * hpc;
+    }
+    for (int l = tid; l < p; l += kCoefT) d.econv[l] = ee[l];
+    __syncthreads();
+  }
   for (int l = tid; l < j; l += kCoefT) {
     ss[l] = d.s[l];
     bt[l] = d.H[(size_t)l * ld + j];  // row j: b~
@@ -159,12 +208,31 @@ __global__ void __launch_bounds__(kCoefT) k_lz_coef(LzDev d, int j) {
   }
   __syncthreads();
   const double kappa = sh_kappa;
+  // the next sweep still holds the stored column q = LZ_CONV (not yet rewritten): coefficient vectors over
+  // V'' = V' T^-1 go out as T^-1 x over the stored columns (x_q / rho at q, x_l - e_l x_q / rho below it)
+  const int q = d.econv ? (int)d.lz[LZ_CONV] : -1;
   for (int l = tid; l < j; l += kCoefT) {
     const double z = fma(mu * mu, bt[l], v[l]);
     const double c = (z - u[l]) / mu;
     d.H[(size_t)j * ld + l] = c;                  // column j: c
-    d.cs[l] = ss[l] / mu;                         // v_j = v~/mu - V (s/mu)
-    d.cg[l] = u[l] / mu + c - kappa * ss[l];      // w = y/mu - kappa v~ - V g
+    const double csl = ss[l] / mu;                // v_j = v~/mu - V (s/mu)
+    const double cgl = u[l] / mu + c - kappa * ss[l];  // w = y/mu - kappa v~ - V g
+    if (q < 0) {
+      d.cs[l] = csl;
+      d.cg[l] = cgl;
+    } else {
+      ss[l] = csl;  // (ss and u are free now)
+      u[l] = cgl;
+    }
+  }
+  if (q >= 0) {
+    __syncthreads();
+    const double ir = 1.0 / d.lz[LZ_CRHO], csq = ss[q] * ir, cgq = u[q] * ir;
+    for (int l = tid; l < j; l += kCoefT) {
+      const double el = l < q ? d.econv[l] : 0.0;
+      d.cs[l] = l == q ? csq : fma(-el, csq, ss[l]);
+      d.cg[l] = l == q ? cgq : fma(-el, cgq, u[l]);
+    }
   }
 }
 
@@ -531,6 +599,347 @@ __global__ void __launch_bounds__(kThreads) k_lz_norm(GraphDev g, ProjDesc pd, c
 }
 
 // ---------------------------------------------------------------------------
+// Paired steps (two Lanczos steps per basis sweep, tests/tools/proto_pair.py).
+//
+// three-term vector of the pair's first step j (no basis pass): u = y/mu - kappa v~ - g_{j-1} v_{j-1}
+// (y = t - s o gam, the operator apply assembled as in the sweep; g_{j-1} v_{j-1} the only large term
+// of V_j g), |u|^2 and B^T u (last-CTA ticket) -> nb.  CTA 0 also records g_far = g with entries j-1
+// and j zeroed as the analytic projections of v~_{j+1} (the `dots` of the normalisation that follows),
+// subtracts g_far from column j of H (A v_j = V_j (c - g_far) + alpha v_j + |u| v~_{j+1}) and keeps
+// 1/mu_j for the pair's sweep.
+// ---------------------------------------------------------------------------
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) k_lz_three(GraphDev g, ProjDesc pd, const double* __restrict__ t,
+                                                       const double* __restrict__ vt, const double* __restrict__ vprev,
+                                                       LzDev d, int j, double* __restrict__ u_out, double* dots,
+                                                       double* cA, double* tr, double* partials, unsigned* counter,
+                                                       double* nb) {
+  __shared__ double gam[kHB];
+  if (threadIdx.x == 0) {
+    double gw[kHB];
+    gamma_serial(d.bs_t, 1.0, pd, gam);
+    gamma_serial(d.bs_v, 1.0, pd, gw);
+    for (int q = 0; q < pd.h; ++q) gam[q] -= d.sigma * gw[q];
+  }
+  __syncthreads();
+  const double ay = d.lz[LZ_AY], av = d.lz[LZ_AV], gj = d.cg[j - 1];
+  double acc[1 + kHB];
+#pragma unroll
+  for (int q = 0; q < 1 + kHB; ++q) acc[q] = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const int gg = g.grp[i];
+    const double y = NORM ? fma(-g.s[i], gam[gg], t[i]) : t[i] - gam[gg];
+    const double ui = fma(ay, y, fma(av, vt[i], -gj * vprev[i]));
+    u_out[i] = ui;
+    acc[0] = fma(ui, ui, acc[0]);
+    const double su = NORM ? g.s[i] * ui : ui;
+#pragma unroll
+    for (int q = 0; q < kHB; ++q)
+      if (q == gg) acc[1 + q] += su;
+  }
+  if (blockIdx.x == 0) {
+    for (int l = threadIdx.x; l <= j; l += blockDim.x) {
+      const double gf = (l >= j - 1) ? 0.0 : d.cg[l];
+      dots[l] = gf;
+      if (l < j) d.H[(size_t)j * d.ldH + l] -= gf;
+    }
+    // the pair's sweep needs step j's v_j coefficients after step j+1's coefficient step overwrote d.cs, and
+    // the rewrite coefficients of the stored column LZ_CONV (v'' = (v' - V[:, :q] e) / rho)
+    const int q = (int)d.lz[LZ_CONV];
+    const double ir = q >= 0 ? 1.0 / d.lz[LZ_CRHO] : 0.0;
+    for (int l = threadIdx.x; l < j; l += blockDim.x) {
+      cA[l] = d.cs[l];
+      tr[l] = l < q ? -d.econv[l] * ir : (l == q ? ir : 0.0);
+    }
+    if (threadIdx.x == 0) d.lz[LZ_INVMU_A] = d.lz[LZ_INVMU];
+  }
+  block_reduce_store<1 + kHB>(acc, partials + (size_t)blockIdx.x * (1 + kHB));
+  ticket_finalize<1 + kHB>(partials, counter, nb, 1 + min(pd.h, kHB));
+}
+
+// the pair's one sweep over the stored V[:, 0:J] (J = j), per row:
+//   v_j   = v~_j / mu_j - V cA                          (cA = s_j / mu_j, stored basis)
+//   v'    = v~_{j+1} / mu_{j+1} - V cB - cB_J v_j        (analytic projections: the odd column)
+//   w     = ay y + av v~_{j+1} - V gB - gB_J v_j         (y = t - s o gam of step j+1)
+//   v''   = V tr  (rewrite of the stored column LZ_CONV of the previous pair, if any)
+// writes V[:, j] = v_j, V[:, j+1] = v', w, V[:, conv] = v''; dots V^T w (J), V^T v' (J), v_j.w, v'.w,
+// v_j.v' -> partials [grid][2J + 3]; |w|^2, B^T w, |v'|^2 (ticket) -> nb [0], [1..16], [1 + kHB].
+// Stage (doubles): [J][kR] basis | v~_j | v~_{j+1} | t | s | grp bytes (the TMA ring of k_lz_update_p).
+struct LzPairArgs {
+  const double* V;
+  long long ld;
+  int J;
+  const double* vtA;  // v~_j
+  const double* vtB;  // v~_{j+1}
+  const double* t;    // L p~_{j+1}
+  double* vj_out;     // V[:, J]
+  double* vj1_out;    // V[:, J + 1]
+  double* w_out;
+  double* conv_out;   // V[:, conv] (nullptr: no rewrite)
+  const double* cA;   // step j: s/mu (stored basis, J)
+  const double* cB;   // step j+1: s/mu (J + 1)
+  const double* gB;   // step j+1: g (J + 1)
+  const double* tr;   // rewrite coefficients (J; zero beyond the rewritten column)
+  const double* lz;
+  const double* bs_t;
+  const double* bs_v;
+  double sigma;
+  double* partials;   // [grid][2J + 3]
+  double* partials2;  // [grid][2 + kHB]
+  unsigned* counter;
+  double* nb;
+};
+constexpr int kPairExtra = 3;  // vectors in a stage beside the basis and the s/grp rows: v~_j, v~_{j+1}, t
+__host__ __device__ constexpr size_t lzp_stage_doubles(int J) { return (size_t)(J + kPairExtra) * kR + kR + 16; }
+
+__device__ __forceinline__ void lzp_issue(const LzPairArgs& a, const GraphDev& g, const CUtensorMap* tmap, int c,
+                                          double* buf, unsigned long long* bar, int lane) {
+  const int J = a.J;
+  const long long row0 = (long long)c * kR;
+  unsigned bytes = (unsigned)((J + kPairExtra) * kR * sizeof(double)) + kR;
+  if (g.normalized) bytes += kR * sizeof(double);
+  if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+  __syncwarp();
+  if (lane == 0) {
+    if (J > 0) tensor2d_g2s(buf, tmap, (int)row0, 0, bar);
+    bulk_g2s(buf + (size_t)J * kR, a.vtA + row0, kR * sizeof(double), bar);
+    bulk_g2s(buf + (size_t)(J + 1) * kR, a.vtB + row0, kR * sizeof(double), bar);
+  } else if (lane == 1) {
+    bulk_g2s(buf + (size_t)(J + 2) * kR, a.t + row0, kR * sizeof(double), bar);
+    bulk_g2s(buf + (size_t)(J + 4) * kR, g.grp + row0, kR, bar);
+    if (g.normalized) bulk_g2s(buf + (size_t)(J + 3) * kR, g.s + row0, kR * sizeof(double), bar);
+  }
+}
+
+template <int MAXQ, bool NORM>
+__global__ void __launch_bounds__(kThreads, 1) k_lz_pair(GraphDev g, ProjDesc pd, LzPairArgs a, int kStages,
+                                                          const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) double dsm[];
+  __shared__ __align__(8) unsigned long long bars[kMaxStages];
+  __shared__ __align__(16) double2 cab[kLMaxJ + 1], cgt[kLMaxJ + 1];  // {cA, cB}, {gB, tr}
+  __shared__ __align__(16) double red[4][8][kR];
+  __shared__ __align__(16) double rw[kR], rv[kR], rv1[kR];
+  __shared__ double gsum[kHB][kR];  // B^T w per row slot (thread (row, 2) adds its rows in chunk order)
+  __shared__ double gam[kHB];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int pr = lane, cgp = w;
+  const int n = g.n, J = a.J;
+  const int nchunks = (n + kR - 1) / kR;
+  const size_t stage_elems = lzp_stage_doubles(J);
+  static_assert(kThreads == 4 * kR, "one thread per (row, combination) in the finishing phase");
+  const bool conv = a.conv_out != nullptr;
+  for (int e = tid; e < kHB * kR; e += kThreads) (&gsum[0][0])[e] = 0.0;
+  for (int l = tid; l < J; l += kThreads) {
+    cab[l] = make_double2(a.cA[l], a.cB[l]);
+    cgt[l] = make_double2(a.gB[l], conv ? a.tr[l] : 0.0);
+  }
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) mbar_init(&bars[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    double gw[kHB];
+    gamma_serial(a.bs_t, 1.0, pd, gam);
+    gamma_serial(a.bs_v, 1.0, pd, gw);
+    for (int q = 0; q < pd.h; ++q) gam[q] -= a.sigma * gw[q];
+  }
+  __syncthreads();
+  const double invA = a.lz[LZ_INVMU_A], invB = a.lz[LZ_INVMU], ay = a.lz[LZ_AY], av = a.lz[LZ_AV];
+  const double cBJ = a.cB[J], gBJ = a.gB[J];
+  const int my_chunks = (nchunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  if (w == 0)
+    for (int it = 0; it < kStages && it < my_chunks; ++it)
+      lzp_issue(a, g, &tmap, blockIdx.x + it * gridDim.x, dsm + it * stage_elems, &bars[it], lane);
+
+  double accW[MAXQ], accV[MAXQ];
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) accW[q] = accV[q] = 0.0;
+  double dJw = 0.0, dJ1w = 0.0, dJv1 = 0.0;  // v_j.w, v'.w, v_j.v'
+  double ww2 = 0.0, vv2 = 0.0;                // |w|^2, |v'|^2 (threads (row, 2) and (row, 1))
+
+  for (int it = 0; it < my_chunks; ++it) {
+    const int c = blockIdx.x + it * gridDim.x;
+    const int st = it % kStages;
+    const double* buf = dsm + st * stage_elems;
+    mbar_wait(&bars[st], (unsigned)((it / kStages) & 1));
+    const double* vAs = buf + (size_t)J * kR;
+    const double* vBs = vAs + kR;
+    const double* ts = vBs + kR;
+    const double* ssc = ts + kR;
+    const uint8_t* gs = reinterpret_cast<const uint8_t*>(ssc + kR);
+    const long long row0 = (long long)c * kR;
+    double2 vreg[MAXQ];
+    double pa[2] = {0.0, 0.0}, pb[2] = {0.0, 0.0}, pg[2] = {0.0, 0.0}, pt[2] = {0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+      const int l = cgp + 8 * q;
+      if (l < J) {
+        vreg[q] = *reinterpret_cast<const double2*>(buf + (size_t)l * kR + 2 * pr);
+        const double2 ab = cab[l], gt = cgt[l];
+        pa[0] = fma(vreg[q].x, ab.x, pa[0]);
+        pa[1] = fma(vreg[q].y, ab.x, pa[1]);
+        pb[0] = fma(vreg[q].x, ab.y, pb[0]);
+        pb[1] = fma(vreg[q].y, ab.y, pb[1]);
+        pg[0] = fma(vreg[q].x, gt.x, pg[0]);
+        pg[1] = fma(vreg[q].y, gt.x, pg[1]);
+        pt[0] = fma(vreg[q].x, gt.y, pt[0]);
+        pt[1] = fma(vreg[q].y, gt.y, pt[1]);
+      } else {
+        vreg[q] = make_double2(0.0, 0.0);
+      }
+    }
+    *reinterpret_cast<double2*>(&red[0][cgp][2 * pr]) = make_double2(pa[0], pa[1]);
+    *reinterpret_cast<double2*>(&red[1][cgp][2 * pr]) = make_double2(pb[0], pb[1]);
+    *reinterpret_cast<double2*>(&red[2][cgp][2 * pr]) = make_double2(pg[0], pg[1]);
+    *reinterpret_cast<double2*>(&red[3][cgp][2 * pr]) = make_double2(pt[0], pt[1]);
+    __syncthreads();
+    // thread (row rr, combination cc) sums the 8 column groups' partials of its combination and of v_j's
+    // (every output needs v_j) and finishes output cc of row rr: 0 v_j, 1 v', 2 w, 3 v''
+    const int rr = tid & (kR - 1), cc = tid >> 6;
+    {
+      // fixed-order pairwise sums of the 8 column groups (short dependency chains)
+      const double sum = ((red[cc][0][rr] + red[cc][1][rr]) + (red[cc][2][rr] + red[cc][3][rr])) +
+                         ((red[cc][4][rr] + red[cc][5][rr]) + (red[cc][6][rr] + red[cc][7][rr]));
+      const double s0 = ((red[0][0][rr] + red[0][1][rr]) + (red[0][2][rr] + red[0][3][rr])) +
+                        ((red[0][4][rr] + red[0][5][rr]) + (red[0][6][rr] + red[0][7][rr]));
+      const long long gi = row0 + rr;
+      const bool in = gi < n;
+      const double vj = fma(vAs[rr], invA, -s0);
+      double out = 0.0;
+      if (cc == 0) {
+        if (in) a.vj_out[gi] = vj;
+        rv[rr] = in ? vj : 0.0;
+      } else if (cc == 1) {
+        out = fma(-cBJ, vj, fma(vBs[rr], invB, -sum));
+        if (!in) out = 0.0;
+        if (in) a.vj1_out[gi] = out;
+        rv1[rr] = out;
+        vv2 = fma(out, out, vv2);
+      } else if (cc == 2) {
+        if (in) {
+          const int gg = gs[rr];
+          const double y = NORM ? fma(-ssc[rr], gam[gg], ts[rr]) : ts[rr] - gam[gg];
+          out = fma(-gBJ, vj, fma(ay, y, fma(av, vBs[rr], -sum)));
+          a.w_out[gi] = out;
+          ww2 = fma(out, out, ww2);
+          if (gg < kHB) gsum[gg][rr] += NORM ? ssc[rr] * out : out;
+        }
+        rw[rr] = out;
+      } else if (conv && in) {
+        a.conv_out[gi] = sum;
+      }
+    }
+    __syncthreads();  // rows finished; stage `st` (read only up to here) is free: refill it now
+    if (w == 0 && it + kStages < my_chunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      lzp_issue(a, g, &tmap, blockIdx.x + (it + kStages) * gridDim.x, dsm + st * stage_elems, &bars[st], lane);
+    }
+    const double2 wp = *reinterpret_cast<const double2*>(&rw[2 * pr]);
+    const double2 up = *reinterpret_cast<const double2*>(&rv1[2 * pr]);
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+      accW[q] = fma(vreg[q].y, wp.y, fma(vreg[q].x, wp.x, accW[q]));
+      accV[q] = fma(vreg[q].y, up.y, fma(vreg[q].x, up.x, accV[q]));
+    }
+    if (cgp == (J & 7)) {
+      const double2 vp = *reinterpret_cast<const double2*>(&rv[2 * pr]);
+      dJw = fma(vp.y, wp.y, fma(vp.x, wp.x, dJw));
+      dJv1 = fma(vp.y, up.y, fma(vp.x, up.x, dJv1));
+    }
+    if (cgp == ((J + 1) & 7)) dJ1w = fma(up.y, wp.y, fma(up.x, wp.x, dJ1w));
+    // (no barrier: red / rw / rv / rv1 are rewritten only after the next chunk's first barrier)
+  }
+  const size_t row = (size_t)blockIdx.x * (2 * J + 3);
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) {
+    const int l = cgp + 8 * q;
+    const double sw = warp_sum(accW[q]), sv = warp_sum(accV[q]);
+    if (lane == 0 && l < J) {
+      a.partials[row + l] = sw;
+      a.partials[row + J + 2 + l] = sv;
+    }
+  }
+  {
+    const double x = warp_sum(dJw), y = warp_sum(dJv1), z = warp_sum(dJ1w);
+    if (lane == 0 && cgp == (J & 7)) {
+      a.partials[row + J] = x;
+      a.partials[row + 2 * J + 2] = y;
+    }
+    if (lane == 0 && cgp == ((J + 1) & 7)) a.partials[row + J + 1] = z;
+  }
+  __syncthreads();  // gsum complete
+  double v2[2 + kHB];
+  v2[0] = ww2;
+  v2[1 + kHB] = vv2;
+#pragma unroll
+  for (int q = 0; q < kHB; ++q) v2[1 + q] = tid < kR ? gsum[q][tid] : 0.0;
+  block_reduce_store<2 + kHB>(v2, a.partials2 + (size_t)blockIdx.x * (2 + kHB));
+  ticket_finalize<2 + kHB>(a.partials2, a.counter, a.nb, 2 + kHB);
+}
+
+// after the pair's sweep (one CTA): dd = [V_J, v_j, v']^T w (J + 2) and e = [V_J, v_j]^T v' (J + 1) in
+// the stored basis; the column rewritten by this sweep (LZ_CONV) now holds v'' = V' T^-1 e_q: its dot
+// entries move to the new column, x_q <- (x_q - e_old . x[:q]) / rho_old.  The odd column J + 1 becomes
+// pending: epend = e, LZ_PRHO = sqrt(|v'|^2 - |e|^2), LZ_PEND = J + 1; the rewrite is done (LZ_CONV = -1).
+__global__ void __launch_bounds__(kCoefT) k_lz_pairpost(LzDev d, int J, const double* __restrict__ dd2,
+                                                        double* __restrict__ dd, const double* nb,
+                                                        const int* __restrict__ flags) {
+  __shared__ double r[2][kCoefT / 32];
+  __shared__ double sh[2];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int q = (int)d.lz[LZ_CONV];
+  double a0 = 0.0, a1 = 0.0;
+  if (q >= 0)
+    for (int l = tid; l < q; l += kCoefT) {
+      a0 = fma(d.econv[l], dd2[l], a0);
+      a1 = fma(d.econv[l], dd2[J + 2 + l], a1);
+    }
+  a0 = warp_sum(a0);
+  a1 = warp_sum(a1);
+  if (lane == 0) {
+    r[0][w] = a0;
+    r[1][w] = a1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int k = 0; k < kCoefT / 32; ++k) {
+      s0 += r[0][k];
+      s1 += r[1][k];
+    }
+    sh[0] = s0;
+    sh[1] = s1;
+  }
+  __syncthreads();
+  const double ir = q >= 0 ? 1.0 / d.lz[LZ_CRHO] : 1.0;
+  double e2 = 0.0;
+  for (int l = tid; l <= J + 1; l += kCoefT) {
+    double x = dd2[l];
+    if (l == q) x = (x - sh[0]) * ir;
+    dd[l] = x;
+    if (l <= J) {
+      double e = dd2[J + 2 + l];
+      if (l == q) e = (e - sh[1]) * ir;
+      d.epend[l] = e;
+      e2 = fma(e, e, e2);
+    }
+  }
+  e2 = warp_sum(e2);
+  __syncthreads();
+  if (lane == 0) r[0][w] = e2;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int k = 0; k < kCoefT / 32; ++k) s += r[0][k];
+    const double nv = nb[1 + kHB];  // |v'|^2
+    const double rho = sqrt(fmax(nv - s, 0.0));
+    // a breakdown in the pair (flags of steps J, J+1 so far) leaves v' to the restart sync's roll-back: no basis
+    // change from garbage (rho of a valid odd column is 1 to rounding)
+    const bool ok = flags[0] == 0 && flags[1] == 0 && rho > 0.5 && rho < 2.0;
+    d.lz[LZ_PRHO] = ok ? rho : 1.0;
+    d.lz[LZ_PEND] = ok ? J + 1 : -1.0;
+    d.lz[LZ_CONV] = -1.0;
+  }
+}
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 static int lz_sgrid(int n) {
@@ -590,6 +999,29 @@ static void lz_update_m(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs
   else lz_update_launch<24, NORM, 256, true>(g, pd, a, grid, st);
 }
 
+template <int MAXQ, bool NORM>
+static void lz_pair_launch(const GraphDev& g, const ProjDesc& pd, const LzPairArgs& a, int grid, cudaStream_t st) {
+  // ring budget: 227 KB per CTA minus the kernel's 34 KB of static shared memory (2 stages up to J = 185)
+  constexpr size_t kPairRing = 190 * 1024;
+  const size_t stage = lzp_stage_doubles(a.J) * sizeof(double);
+  const int stages = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, kPairRing / stage));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_lz_pair<MAXQ, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairRing);
+    attr = true;
+  }
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  if (a.J > 0) encode_colmajor_map(a.V, a.ld, a.J, kR, &tmap);
+  k_lz_pair<MAXQ, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap);
+}
+template <bool NORM>
+static void lz_pair_m(const GraphDev& g, const ProjDesc& pd, const LzPairArgs& a, int grid, cudaStream_t st) {
+  if (a.J <= 64) lz_pair_launch<8, NORM>(g, pd, a, grid, st);
+  else if (a.J <= 128) lz_pair_launch<16, NORM>(g, pd, a, grid, st);
+  else lz_pair_launch<24, NORM>(g, pd, a, grid, st);
+}
+
 void launch_lz_coef(const LzDev& d, int j, cudaStream_t st) {
   bump_launch();
   k_lz_coef<<<1, kCoefT, 0, st>>>(d, j);
@@ -624,6 +1056,8 @@ struct Lagged {
   int64_t applies = 0, steps = 0, restarts = 0, breakdowns = 0;
   unsigned inject = 0;
   double bd_tol = 0.0;
+  bool paired = false;  // two Lanczos steps per basis sweep (reorth 3)
+  bool pend = false;    // host mirror of LZ_PEND >= 0: the last pair's odd column awaits its rewrite
 
   LzDev dev(int j) const {
     LzDev d{};
@@ -638,8 +1072,108 @@ struct Lagged {
     d.flag = c->bflags + j;
     d.sigma = c->sigma;
     d.bd_tol = bd_tol;
+    d.epend = paired ? c->lzp : nullptr;
+    d.econv = paired ? c->lzp + kMaxJ : nullptr;
     return d;
   }
+  double* cA() const { return c->lzp + 2 * kMaxJ; }
+  double* trc() const { return c->lzp + 3 * kMaxJ; }
+  double* dd2() const { return c->lzp + 4 * kMaxJ; }  // 2 kMaxJ + 8
+  // no pending / rewritten column (start, restart, breakdown)
+  sfairsc_status clear_pair_state() {
+    pend = false;
+    if (!paired) return SFAIRSC_OK;
+    const double m1[5] = {-1.0, 1.0, -1.0, 1.0, 1.0};  // LZ_PEND, LZ_PRHO, LZ_CONV, LZ_CRHO, LZ_INVMU_A
+    std::memcpy(c->hp + 2048, m1, sizeof(m1));
+    CU(cudaMemcpyAsync(c->lz + LZ_PEND, c->hp + 2048, sizeof(m1), cudaMemcpyHostToDevice, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return SFAIRSC_OK;
+  }
+
+  // two Lanczos steps j, j+1 with ONE basis sweep (tests/tools/proto_pair.py)
+  sfairsc_status pair(int j) {
+    const GraphDev g = c->g();
+    const bool rewrite = pend;  // the previous pair's odd column j-1 is rewritten by this pair's sweep
+    {
+      ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
+      ctx_spmv(c, c->vp, c->vt, c->vq_lz);
+    }
+    {
+      ProfScope ps(c, K_OTHER, 0.0);
+      bump_launch();
+      k_lz_coef<<<1, kCoefT, 0, c->st>>>(dev(j), j);  // (+ the pending column's basis change)
+    }
+    {
+      ProfScope ps(c, K_NORMALIZE, 4 * c->vb() + c->sgb());
+      bump_launch();
+      // 8 CTAs per SM (partials: the SpMV's buffer, free again once its ticket is done)
+      const int G = std::max(1, std::min((c->n + kThreads - 1) / kThreads, c->num_sms * 8));
+      const double* vprev = c->V + (long long)(j - 1) * c->ldv;
+      if (c->normalized)
+        k_lz_three<true><<<G, kThreads, 0, c->st>>>(g, c->pd(), c->vt, c->vr, vprev, dev(j), j, c->vy, c->dd, cA(),
+                                                    trc(), c->partials, c->counters + 7, c->nb);
+      else
+        k_lz_three<false><<<G, kThreads, 0, c->st>>>(g, c->pd(), c->vt, c->vr, vprev, dev(j), j, c->vy, c->dd, cA(),
+                                                     trc(), c->partials, c->counters + 7, c->nb);
+    }
+    {
+      ProfScope ps(c, K_NORMALIZE, 3 * c->vb() + c->sgb());
+      launch_lz_norm(g, c->pd(), c->vy, c->nb, c->dd, j + 1, dev(j), j + 1, c->vrB, c->vp, c->bs_v, c->st,
+                     c->unit_spmv() ? c->vq_lz : nullptr);
+    }
+    {
+      ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
+      ctx_spmv(c, c->vp, c->vt, c->vq_lz);
+    }
+    {
+      ProfScope ps(c, K_OTHER, 0.0);
+      bump_launch();
+      k_lz_coef<<<1, kCoefT, 0, c->st>>>(dev(j + 1), j + 1);
+    }
+    {
+      ProfScope ps(c, K_UPDDOT, (j + 6 + (rewrite ? 1 : 0)) * c->vb() + c->sgb());
+      LzPairArgs a{};
+      a.V = c->V;
+      a.ld = c->ldv;
+      a.J = j;
+      a.vtA = c->vr;
+      a.vtB = c->vrB;
+      a.t = c->vt;
+      a.vj_out = c->V + (long long)j * c->ldv;
+      a.vj1_out = c->V + (long long)(j + 1) * c->ldv;
+      a.w_out = c->vy;
+      a.conv_out = rewrite ? c->V + (long long)(j - 1) * c->ldv : nullptr;
+      a.cA = cA();
+      a.cB = c->c1;
+      a.gB = c->c2;
+      a.tr = trc();
+      a.lz = c->lz;
+      a.bs_t = c->bs_t;
+      a.bs_v = c->bs_v;
+      a.sigma = c->sigma;
+      a.partials = c->partials;
+      a.partials2 = c->partials2;
+      a.counter = c->counters + 6;
+      a.nb = c->nb;
+      const int G = sweep_tma_grid(c->n, c->num_sms);
+      bump_launch();
+      if (c->normalized) lz_pair_m<true>(g, c->pd(), a, G, c->st);
+      else lz_pair_m<false>(g, c->pd(), a, G, c->st);
+      launch_reduce_cols(c->partials, G, 2 * j + 3, dd2(), c->st);
+    }
+    {
+      ProfScope ps(c, K_OTHER, 0.0);
+      bump_launch();
+      k_lz_pairpost<<<1, kCoefT, 0, c->st>>>(dev(j + 1), j, dd2(), c->dd, c->nb, c->bflags + j);
+    }
+    norm(c->vy, c->dd, j + 2, j + 2, j + 1);
+    CHECK_LAUNCH();
+    pend = true;
+    applies += 2;
+    steps += 2;
+    return SFAIRSC_OK;
+  }
+
 
   void norm(const double* w, const double* dots, int nd, int jrow, int flag_idx) {
     ProfScope ps(c, K_NORMALIZE, 3 * c->vb() + c->sgb());
@@ -692,6 +1226,7 @@ struct Lagged {
 
   // v~_j = random vector, projected, CGS2 (twice) against V[:, 0:j], normalised; s = 0, no coupling
   sfairsc_status random_start(int j) {
+    TRY(clear_pair_state());
     const GraphDev g = c->g();
     for (int attempt = 0; attempt < 5; ++attempt) {
       launch_random(c->vt, c->n, c->seed, 4096u + inject++, 7u, c->st);
@@ -752,6 +1287,7 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
   L.m = c->m;
   L.k = k;
   L.keep = c->keep;
+  L.paired = c->paired;
   const int m = L.m, keep = L.keep, n = c->n, ldH = c->ldT;
   const double tol_eff = std::min(tol, c->tol_cap);
   const double target = tol_eff * c->sigma;
@@ -765,17 +1301,28 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
   double gap = std::numeric_limits<double>::quiet_NaN();
   double max_resid = std::numeric_limits<double>::infinity();
   for (;;) {
-    while (j < m) TRY(L.step(j++));
+    {  // the first step of a cycle is a single step (its g couples every kept Ritz vector), and one more if
+       // the rest is odd; then pairs (paired builds) to m
+      const int j0 = j;
+      while (j < m) {
+        if (!L.paired || j == j0 || (m - j) % 2 == 1) TRY(L.step(j++));
+        else {
+          TRY(L.pair(j));
+          j += 2;
+        }
+      }
+    }
     // ---- sync ----
     CU(cudaMemcpyAsync(Hh.data(), c->Hdev, sizeof(double) * ldH * ldH, cudaMemcpyDeviceToHost, c->st));
     CU(cudaMemcpyAsync(sh.data(), c->sdev, sizeof(double) * m, cudaMemcpyDeviceToHost, c->st));
-    CU(cudaMemcpyAsync(c->hp, c->lz, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
-    CU(cudaMemcpyAsync(c->hp + 8, c->bflags, sizeof(int) * (m + 1), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(c->hp, c->lz, sizeof(double) * 16, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(c->hp + 16, c->bflags, sizeof(int) * (m + 1), cudaMemcpyDeviceToHost, c->st));
+    if (L.pend) CU(cudaMemcpyAsync(c->hp + 1024, c->lzp, sizeof(double) * m, cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
     if (c->prof.on) c->prof.resolve();
     int jb = -1;
     {
-      const int* fl = reinterpret_cast<const int*>(c->hp + 8);
+      const int* fl = reinterpret_cast<const int*>(c->hp + 16);
       for (int q = jsync; q < m; ++q)
         if (fl[q]) {
           jb = q;
@@ -785,7 +1332,7 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
     if (jb >= 0) {
       // flag 2 (coef): v~_jb numerically inside span(V_jb): columns 0..jb-1 valid, new v~_jb.
       // flag 1 (norm): |w| <= bd_tol, span(V_{jb+1}) invariant: columns 0..jb valid, new v~_{jb+1}.
-      const int* fl = reinterpret_cast<const int*>(c->hp + 8);
+      const int* fl = reinterpret_cast<const int*>(c->hp + 16);
       const int jn = (fl[jb] & 2) ? jb : jb + 1;
       if (c->debug) fprintf(stderr, "[sfairsc] lagged breakdown at step %d (flag %d)\n", jb, fl[jb]);
       L.breakdowns++;
@@ -795,6 +1342,42 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
       jsync = j;
       continue;
     }
+    // ---- paired steps: the last pair's odd column m-1 is still the stored v' = V'' T: move H, the lagged row
+    // and s to V'' (as the coefficient kernel does), and the Ritz coefficients back to the stored columns below
+    const bool tconv = L.pend;
+    const int pq = m - 1;
+    const double prho = c->hp[LZ_PRHO];
+    std::vector<double> pdef(tconv ? pq : 0);  // the pending column's defect e
+    if (tconv) {
+      for (int l = 0; l < pq; ++l) pdef[l] = c->hp[1024 + l];
+      auto H = [&](int r, int col) -> double& { return Hh[(size_t)col * ldH + r]; };
+      std::vector<double> hle(pq + 2, 0.0);
+      for (int l = 0; l <= pq + 1; ++l) {
+        const int row = (l == pq + 1) ? m : l;
+        double a = 0.0;
+        for (int cc = 0; cc < pq; ++cc) a += H(row, cc) * pdef[cc];
+        hle[l] = a;
+      }
+      double es = 0.0;
+      for (int l = 0; l < pq; ++l) es += pdef[l] * sh[l];
+      const double hpp = H(pq, pq);
+      for (int l = 0; l < pq; ++l) H(l, pq) = (H(l, pq) + pdef[l] * hpp - hle[l] - pdef[l] * hle[pq]) / prho;
+      H(pq, pq) = hpp - hle[pq];
+      H(m, pq) = (H(m, pq) - hle[pq + 1]) / prho;
+      for (int cc = 0; cc < pq; ++cc) {
+        const double hpc = H(pq, cc);
+        for (int l = 0; l < pq; ++l) H(l, cc) += pdef[l] * hpc;
+        H(pq, cc) = prho * hpc;
+      }
+      sh[pq] = (sh[pq] - es) / prho;
+    }
+    // coefficients x over V'' -> T^-1 x over the stored columns
+    auto to_stored = [&](double* x) {
+      if (!tconv) return;
+      const double xq = x[pq] / prho;
+      for (int l = 0; l < pq; ++l) x[l] -= pdef[l] * xq;
+      x[pq] = xq;
+    };
     // ---- Rayleigh-Ritz on sym(H_m + s b~^T) ----
     const double om = c->hp[LZ_OMEGA];
     double s2 = 0.0;
@@ -826,8 +1409,10 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
               (long long)L.restarts, (long long)L.steps, maxres, target, theta[k - 1], mu);
     if (converged || L.restarts >= c->max_restarts) {
       std::vector<double> Yc((size_t)m * k);
-      for (int cc = 0; cc < k; ++cc)
+      for (int cc = 0; cc < k; ++cc) {
         for (int l = 0; l < m; ++l) Yc[(size_t)cc * m + l] = Y[(size_t)l * m + cc];
+        to_stored(Yc.data() + (size_t)cc * m);
+      }
       CU(cudaMemcpyAsync(c->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, c->st));
       {
         ProfScope ps(c, K_RITZ, (double)(m + k) * c->vb());
@@ -845,6 +1430,7 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
       for (int l = 0; l < m; ++l) Yc[(size_t)cc * me + l] = Y[(size_t)l * m + cc];
     for (int l = 0; l < m; ++l) Yc[(size_t)keep * me + l] = -sh[l] / mu;
     Yc[(size_t)keep * me + m] = 1.0 / mu;
+    for (int cc = 0; cc <= keep; ++cc) to_stored(Yc.data() + (size_t)cc * me);
     CU(cudaMemcpyAsync(c->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, c->st));
     {
       ProfScope ps(c, K_RITZ, (double)(me + pe) * c->vb());
@@ -880,6 +1466,7 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
       L.norm(c->vy, nullptr, 0, -1, kMaxJ);
     }
     CHECK_LAUNCH();
+    TRY(L.clear_pair_state());
     j = keep;
     jsync = keep;
     L.restarts++;

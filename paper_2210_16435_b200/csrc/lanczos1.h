@@ -6,7 +6,12 @@
 namespace sfz {
 
 // scalar slots of the device state `lz`
-enum { LZ_OMEGA = 0, LZ_PNORM2 = 1, LZ_AY = 2, LZ_AV = 3, LZ_MU = 4, LZ_INVMU = 5, LZ_BETA = 6 };
+enum { LZ_OMEGA = 0, LZ_PNORM2 = 1, LZ_AY = 2, LZ_AV = 3, LZ_MU = 4, LZ_INVMU = 5, LZ_BETA = 6,
+       // paired steps (two Lanczos steps per basis sweep): the stored odd column
+       // LZ_PEND (-1: none) awaits its move to the orthonormal basis (defect e in epend, rho in
+       // LZ_PRHO); LZ_CONV (-1: none) = the column the next sweep rewrites (econv, LZ_CRHO), while the
+       // coefficient vectors are converted to the stored basis; LZ_INVMU_A = 1/mu of the pair's first step
+       LZ_PEND = 7, LZ_PRHO = 8, LZ_CONV = 9, LZ_CRHO = 10, LZ_INVMU_A = 11 };
 
 struct LzDev {
   double* H;       // (ldH x ldH) column-major; A V_j = V_j H[:j,:j] + v~_j H[j,:j] (lagged)
@@ -20,6 +25,8 @@ struct LzDev {
   int* flag;       // breakdown flag of this step
   double sigma;
   double bd_tol;
+  double* epend;   // paired steps: defect V^T v' of the pending odd column (LZ_PEND)
+  double* econv;   // the defect of the column being rewritten (LZ_CONV)
 };
 
 struct LzSweepArgs {

@@ -36,6 +36,8 @@ print(f"generated n={g.n} nnz={g.nnz} in {time.time() - t:.1f}s", file=sys.stder
 dev = torch.device("cuda:0")
 rp, ci, vv = (torch.from_numpy(a).to(dev) for a in (g.row_ptr, g.col, g.val))
 gr = torch.from_numpy(g.groups.astype(np.int32)).to(dev)
+torch.cuda.synchronize()
+torch.cuda.empty_cache()  # generator intermediates (config 5 is generated on the GPU) back before the build
 k = cfg["k_eig"]
 ctx = lib.sfairsc_build_operator(rp, ci, vv, gr, k, cfg["normalized"], h=g.h, max_restarts=args.restarts,
                                  spmv_vector=args.vs, block_size=args.bsz, max_basis=args.m, keep=args.keep,
