@@ -95,8 +95,10 @@ typedef struct {
                              thick-restart Lanczos (SpMM on b interleaved vectors, block CGS2, CholQR2;
                              requires h <= 16); 0 = auto (DESIGN.md §Block Lanczos) */
   int32_t reorth;         /* single-vector full reorthogonalisation: 1 = CGS2 (three basis sweeps per step),
-                             2 = lagged single sweep (one basis sweep per step, DESIGN.md §Single-sweep Lanczos;
-                             needs h <= 16, k < m <= min(192, n-h)); 0 = auto (2 where allowed, else 1) */
+                             2 = lagged single sweep (one basis sweep per step, DESIGN.md §6.2;
+                             needs h <= 16, k < m <= min(192, n-h)), 3 = paired steps (one basis sweep per
+                             TWO steps; single GPU, group constraints, k + 4 <= m <= 186);
+                             0 = auto (3 where allowed, else 2, else 1) */
   struct sfairsc_comm *comm; /* NULL: single GPU.  Else row-partitioned across the communicator's ranks
                              (SURVEY §8(e)): each rank passes its contiguous row block of W (row_offset,
                              n_rows, global n_cols; blocks tile [0, n) in rank order) and the groups of its

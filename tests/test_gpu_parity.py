@@ -127,9 +127,10 @@ def test_operator_device_tensors(gpu_lib):
     ctx.close()
 
 
-# eigensolver variants of the C ABI (sfairsc_opts): the default (single-sweep lagged
-# reorthogonalisation where allowed), three-sweep CGS2, and block Lanczos with b = 2
-SOLVERS = {"default": {}, "cgs2": {"reorth": 1}, "block2": {"block_size": 2}}
+# eigensolver variants of the C ABI (sfairsc_opts): the default (paired steps: two Lanczos steps per
+# basis sweep, reorth 3, where allowed), one lagged step per sweep (reorth 2), three-sweep CGS2, and block
+# Lanczos with b = 2
+SOLVERS = {"default": {}, "lagged1": {"reorth": 2}, "cgs2": {"reorth": 1}, "block2": {"block_size": 2}}
 
 
 def _check_eigs(lib, g, k, normalized, tol, dense=None, ref_evals=None, ref_X=None, gap=None, **kw):
@@ -628,3 +629,28 @@ def test_empty_and_invalid_inputs(gpu_lib):
     with pytest.raises(lib.SfairscError) as e:
         lib.sfairsc_build_operator(g.row_ptr, col, g.val, g.groups.astype(np.int32), 2, False)
     assert e.value.name == "E_CSR_INVALID"
+
+
+@pytest.mark.parametrize("normalized", [False, True])
+@pytest.mark.parametrize("n,k,m", [(1800, 6, 0), (2400, 9, 23), (3000, 12, 17)])
+def test_paired_steps_match_single_steps_and_oracle(gpu_lib, normalized, n, k, m):
+    """two Lanczos steps per basis sweep (reorth 3, the default) against one (reorth 2) and
+    the dense oracle: the same eigenvalues (R6), subspaces within the Davis-Kahan bound, an orthonormal
+    fair basis; small bases (m = 17 = k + 5: one pair per cycle after the single first steps) included."""
+    g = random_graph(n, 4, p=8.0 / n, seed=n + k, weights="uniform")
+    dense = fairsc.fairsc_dense(g.dense(), g.groups, g.h, k, normalized)
+    kw = {"max_basis": m} if m else {}
+    ev3, X3, st3 = _check_eigs(gpu_lib, g, k, normalized, 1e-10, dense=dense, reorth=3, **kw)
+    ev2, X2, st2 = _check_eigs(gpu_lib, g, k, normalized, 1e-10, dense=dense, reorth=2, **kw)
+    assert np.all(np.abs(ev3 - ev2) <= 1e-9 * np.abs(ev2) + 1e-12 * st2["sigma"])
+    assert abs(st3["applies"] - st2["applies"]) <= 0.1 * st2["applies"] + 10
+
+
+def test_paired_steps_option_errors(gpu_lib):
+    g = random_graph(600, 3, p=0.02, seed=5, weights="uniform")
+    with pytest.raises(gpu_lib.SfairscError) as e:  # reorth 3 needs the single-vector lagged solver
+        _ctx(gpu_lib, g, 4, True, reorth=3, block_size=2)
+    assert e.value.name == "E_INVALID_ARG"
+    with pytest.raises(gpu_lib.SfairscError) as e:
+        _ctx(gpu_lib, g, 4, True, reorth=4)
+    assert e.value.name == "E_INVALID_ARG"
