@@ -433,12 +433,12 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth=2/3 need block_size 1, h <= 16 and k < m <= min(192, n-h)"));
   // paired steps: single GPU, group projector (the dense projector and row-partitioned builds keep one step
   // per sweep); they need room for a pair after the first step of a cycle
-  c->paired = c->lagged && opts.reorth != 2 && !(opts.comm || opts.virtual_parts > 1) && !g_build_keep_values &&
-              m >= k + 4;
+  c->paired = c->lagged && opts.reorth != 2 && !g_build_keep_values && m >= k + 4 &&
+              (!(opts.comm || opts.virtual_parts > 1) || m <= kPairMaxM);  // (dist: the basis size is final here)
   if (opts.reorth == 3 && !c->paired)
-    return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth=3 needs a single-GPU group-fairness build and m >= k + 4"));
+    return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth=3 needs a group-fairness build and k + 4 <= m (<= 186)"));
   if (is_dist) {  // row-partitioned single-sweep Lanczos (dist.cu)
-    if (!c->lagged) return bail(fail(SFAIRSC_E_INVALID_ARG, "row-partitioned builds need h <= 16, block_size 1, reorth 0/2"));
+    if (!c->lagged) return bail(fail(SFAIRSC_E_INVALID_ARG, "row-partitioned builds need h <= 16, block_size 1, reorth 0/2/3"));
     {
       const double mean_deg = (double)W->nnz / std::max(1, n_rows);
       int vs = 2;

@@ -283,10 +283,12 @@ struct DistPart {
   bool skewed = false;  // heavy-tailed local degrees: long rows get a whole warp in the SpMV
   bool unit = false;    // unnormalized unit-weight rows: the pattern-only SpMV (GraphDev::unit)
   double *vr = nullptr, *vy = nullptr, *vt = nullptr;  // v~ (lagged), w, t
+  double* vrB = nullptr;  // paired steps: the pair's second lagged vector
   double *V = nullptr, *Vb = nullptr, *X = nullptr;
   double *partials = nullptr, *partials2 = nullptr;
   unsigned* counters = nullptr;
-  double* small = nullptr;  // bs_t [0,64), bs_v [64,128), bs_w [128,192), nb [192,256), scal [256,320), dd [512, 1024)
+  double* small = nullptr;  // bs_t [0,64), bs_v [64,128), bs_w [128,192), nb [192,256), scal [256,320), dd [512, 1024),
+                            // pair dots dd2 [1024, 2048)
   int* flags = nullptr;
   GraphDev g(bool normalized) const {
     GraphDev G;
@@ -309,6 +311,7 @@ struct DistPart {
   double* nb() const { return small + 192; }
   double* scal() const { return small + 256; }
   double* dd() const { return small + 512; }
+  double* dd2() const { return small + 1024; }
 };
 
 struct DistCtx {
@@ -327,6 +330,7 @@ struct DistCtx {
   cudaEvent_t ev_ready = nullptr, ev_gathered = nullptr;
   // replicated Lanczos state (one copy per process)
   double *H = nullptr, *sv = nullptr, *lz = nullptr, *cs = nullptr, *cg = nullptr, *Ydev = nullptr;
+  double* lzp = nullptr;  // paired steps: epend | econv | cA | tr (4 kMaxJ)
   int ldH = 0;
   int* bflags = nullptr;
   double* hp = nullptr;
@@ -399,12 +403,12 @@ void dist_free(DistCtx* D) {
   if (!D) return;
   for (auto& p : D->parts) {
     void* ptrs[] = {p.rp, p.ci, p.row_split, p.vv, p.dg, p.s, p.grp, p.isb, p.uh, p.vr, p.vy, p.vt, p.V, p.Vb, p.X,
-                    p.partials, p.partials2, p.counters, p.small, p.flags, p.rpb};
+                    p.partials, p.partials2, p.counters, p.small, p.flags, p.rpb, p.vrB};
     for (void* x : ptrs)
       if (x) cudaFree(x);
   }
   void* ptrs[] = {D->cuts_dev, D->p_full, D->s_full, D->ptr_tab, D->H, D->sv, D->lz, D->cs, D->cg, D->Ydev,
-                  D->bflags, D->X_full, D->s_compact};
+                  D->bflags, D->X_full, D->s_compact, D->lzp};
   for (void* x : ptrs)
     if (x) cudaFree(x);
   if (D->hp) cudaFreeHost(D->hp);
@@ -541,8 +545,12 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
     CU(dal(&p.flags, 8));
     CU(cudaMemsetAsync(p.flags, 0, 8 * sizeof(int), st));
     unsigned long long* psym = reinterpret_cast<unsigned long long*>(p.flags + 2);
-    CU(dal(&p.small, 1024));
-    CU(cudaMemsetAsync(p.small, 0, 1024 * sizeof(double), st));
+    CU(dal(&p.small, 2048));
+    CU(cudaMemsetAsync(p.small, 0, 2048 * sizeof(double), st));
+    if (c->paired) {
+      CU(dal(&p.vrB, p.ldv));
+      CU(cudaMemsetAsync(p.vrB, 0, sizeof(double) * p.ldv, st));
+    }
     for (double** v : {&p.vr, &p.vy, &p.vt}) {
       CU(dal(v, p.ldv));
       CU(cudaMemsetAsync(*v, 0, sizeof(double) * p.ldv, st));
@@ -761,6 +769,10 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
   CU(dal(&D->Ydev, (size_t)(m + 1) * (m + 1)));
   CU(dal(&D->bflags, kMaxJ + 8));
   CU(cudaMemsetAsync(D->bflags, 0, sizeof(int) * (kMaxJ + 8), st));
+  if (c->paired) {
+    CU(dal(&D->lzp, 4 * kMaxJ));
+    CU(cudaMemsetAsync(D->lzp, 0, sizeof(double) * 4 * kMaxJ, st));
+  }
   CU(cudaStreamSynchronize(st));
   return SFAIRSC_OK;
 }
@@ -801,7 +813,97 @@ struct DistLanczos {
     d.flag = D->bflags + flag_idx;
     d.sigma = c->sigma;
     d.bd_tol = bd_tol;
+    d.epend = c->paired ? D->lzp : nullptr;
+    d.econv = c->paired ? D->lzp + kMaxJ : nullptr;
     return d;
+  }
+  bool pend = false;  // host mirror of LZ_PEND >= 0
+  sfairsc_status clear_pair_state() {
+    pend = false;
+    if (!c->paired) return SFAIRSC_OK;
+    const double m1[5] = {-1.0, 1.0, -1.0, 1.0, 1.0};  // LZ_PEND, LZ_PRHO, LZ_CONV, LZ_CRHO, LZ_INVMU_A
+    std::memcpy(D->hp + 2048, m1, sizeof(m1));
+    CU(cudaMemcpyAsync(D->lz + LZ_PEND, D->hp + 2048, sizeof(m1), cudaMemcpyHostToDevice, st()));
+    CU(cudaStreamSynchronize(st()));
+    return SFAIRSC_OK;
+  }
+
+  // two Lanczos steps j, j+1 with one basis sweep per part (partitioned: the three-term
+  // vector's |u|^2 / B^T u, the pair sweep's 2J + 3 dots and |w|^2 / B^T w / |v'|^2 are all-reduced)
+  sfairsc_status pair(int j) {
+    const bool rewrite = pend;
+    {
+      ProfScope ps(c, K_SPMV, 0.0);
+      TRY(dist_spmv(D, c, st()));
+      TRY(allreduce(D, st(), kBT, [](const DistPart& p) { return p.bs_t(); }));
+    }
+    launch_lz_coef(dev(D->parts[0], j), j, st());
+    {
+      ProfScope ps(c, K_NORMALIZE, 0.0);
+      bool first = true;
+      for (auto& p : D->parts) {
+        const int G = std::max(1, std::min((p.n_loc + kThreads - 1) / kThreads, c->num_sms * 8));
+        launch_lz_three(p.g(c->normalized), pd(p), p.vt, p.vr, p.V + (long long)(j - 1) * p.ldv, dev(p, j), j, p.vy,
+                        p.dd(), D->lzp + 2 * kMaxJ, D->lzp + 3 * kMaxJ, p.partials, p.counters + 7, p.nb(), G, first,
+                        st());
+        first = false;
+      }
+      TRY(allreduce(D, st(), 1 + kHB, [](const DistPart& p) { return p.nb(); }));
+      for (auto& p : D->parts)
+        launch_lz_norm(p.g(c->normalized), pd(p), p.vy, p.nb(), p.dd(), j + 1, dev(p, j), j + 1, p.vrB, pseg(p),
+                       p.bs_v(), st());
+    }
+    {
+      ProfScope ps(c, K_SPMV, 0.0);
+      TRY(dist_spmv(D, c, st()));
+      TRY(allreduce(D, st(), kBT, [](const DistPart& p) { return p.bs_t(); }));
+    }
+    launch_lz_coef(dev(D->parts[0], j + 1), j + 1, st());
+    {
+      ProfScope ps(c, K_UPDDOT, 0.0);
+      for (auto& p : D->parts) {
+        LzPairArgs a{};
+        a.V = p.V;
+        a.ld = p.ldv;
+        a.J = j;
+        a.vtA = p.vr;
+        a.vtB = p.vrB;
+        a.t = p.vt;
+        a.vj_out = p.V + (long long)j * p.ldv;
+        a.vj1_out = p.V + (long long)(j + 1) * p.ldv;
+        a.w_out = p.vy;
+        a.conv_out = rewrite ? p.V + (long long)(j - 1) * p.ldv : nullptr;
+        a.cA = D->lzp + 2 * kMaxJ;
+        a.cB = D->cs;
+        a.gB = D->cg;
+        a.tr = D->lzp + 3 * kMaxJ;
+        a.lz = D->lz;
+        a.bs_t = p.bs_t();
+        a.bs_v = p.bs_v();
+        a.sigma = c->sigma;
+        a.partials = p.partials;
+        a.partials2 = p.partials2;
+        a.counter = p.counters + 6;
+        a.nb = p.nb();
+        const int G = std::max(1, std::min((p.n_loc + 63) / 64, c->num_sms));
+        launch_lz_pair(p.g(c->normalized), pd(p), a, G, st());
+        launch_reduce_cols(p.partials, G, 2 * j + 3, p.dd2(), st());
+      }
+      // (one all-reduce each: 2 j + 3 dots, and |w|^2, B^T w, |v'|^2)
+      TRY(allreduce(D, st(), 2 * j + 3, [](const DistPart& p) { return p.dd2(); }));
+      TRY(allreduce(D, st(), 2 + kHB, [](const DistPart& p) { return p.nb(); }));
+    }
+    // the replicated bookkeeping once (part 0's reduced dots; every part then normalises with part 0's dd)
+    launch_lz_pairpost(dev(D->parts[0], j + 1), j, D->parts[0].dd2(), D->parts[0].dd(), D->parts[0].nb(), D->bflags + j,
+                       st());
+    for (auto& p : D->parts)
+      launch_lz_norm(p.g(c->normalized), pd(p), p.vy, p.nb(), D->parts[0].dd(), j + 2, dev(p, j + 1), j + 2, p.vr,
+                     pseg(p), p.bs_v(), st());
+    CHECK_LAUNCH();
+    pend = true;
+    applies += 2;
+    steps += 2;
+    return SFAIRSC_OK;
   }
 
   // v~ = P(w/|w|) on every part from the reduced nb (and dots)
@@ -910,6 +1012,7 @@ struct DistLanczos {
 
   // v~_j = P(random) orthogonalised (CGS2 twice) against V[:, 0:j]; s = 0; H row j = 0
   sfairsc_status random_start(int j) {
+    TRY(clear_pair_state());
     for (int attempt = 0; attempt < 5; ++attempt) {
       for (auto& p : D->parts) {
         bump_launch();
@@ -995,15 +1098,25 @@ sfairsc_status dist_eigs(sfairsc_ctx* c, int k, double tol, double* evals_out, d
   double gap = std::numeric_limits<double>::quiet_NaN();
   double max_resid = std::numeric_limits<double>::infinity();
   for (;;) {
-    while (j < m) TRY(L.step(j++));
+    {  // single first step(s) of a cycle, then pairs (paired builds), as in lanczos1.cu
+      const int j0 = j;
+      while (j < m) {
+        if (!c->paired || j == j0 || (m - j) % 2 == 1) TRY(L.step(j++));
+        else {
+          TRY(L.pair(j));
+          j += 2;
+        }
+      }
+    }
     CU(cudaMemcpyAsync(Hh.data(), D->H, sizeof(double) * ldH * ldH, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(sh.data(), D->sv, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(D->hp, D->lz, sizeof(double) * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(D->hp + 8, D->bflags, sizeof(int) * (m + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(D->hp, D->lz, sizeof(double) * 16, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(D->hp + 16, D->bflags, sizeof(int) * (m + 1), cudaMemcpyDeviceToHost, st));
+    if (L.pend) CU(cudaMemcpyAsync(D->hp + 1024, D->lzp, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (c->prof.on) c->prof.resolve();
     int jb = -1;
-    const int* fl = reinterpret_cast<const int*>(D->hp + 8);
+    const int* fl = reinterpret_cast<const int*>(D->hp + 16);
     for (int q = jsync; q < m; ++q)
       if (fl[q]) {
         jb = q;
@@ -1018,6 +1131,17 @@ sfairsc_status dist_eigs(sfairsc_ctx* c, int k, double tol, double* evals_out, d
       jsync = j;
       continue;
     }
+    // paired steps: the last pair's odd column m-1 is still the stored v'
+    const bool tconv = L.pend;
+    const double prho = D->hp[LZ_PRHO];
+    std::vector<double> pdef(tconv ? m - 1 : 0);
+    if (tconv) {
+      for (int l = 0; l < m - 1; ++l) pdef[l] = D->hp[1024 + l];
+      pair_pending_to_orthonormal(m, ldH, Hh, sh, pdef.data(), prho);
+    }
+    auto to_stored = [&](double* x) {
+      if (tconv) pair_coef_to_stored(m, x, pdef.data(), prho);
+    };
     const double om = D->hp[LZ_OMEGA];
     double s2 = 0.0;
     for (int l = 0; l < m; ++l) s2 += sh[l] * sh[l];
@@ -1042,8 +1166,10 @@ sfairsc_status dist_eigs(sfairsc_ctx* c, int k, double tol, double* evals_out, d
     converged = maxres <= target;
     if (converged || L.restarts >= c->max_restarts) {
       std::vector<double> Yc((size_t)m * k);
-      for (int cc = 0; cc < k; ++cc)
+      for (int cc = 0; cc < k; ++cc) {
         for (int l = 0; l < m; ++l) Yc[(size_t)cc * m + l] = Y[(size_t)l * m + cc];
+        to_stored(Yc.data() + (size_t)cc * m);
+      }
       CU(cudaMemcpyAsync(D->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, st));
       L.ritz(m, k, true);
       CHECK_LAUNCH();
@@ -1057,6 +1183,7 @@ sfairsc_status dist_eigs(sfairsc_ctx* c, int k, double tol, double* evals_out, d
       for (int l = 0; l < m; ++l) Yc[(size_t)cc * me + l] = Y[(size_t)l * m + cc];
     for (int l = 0; l < m; ++l) Yc[(size_t)keep * me + l] = -sh[l] / mu;
     Yc[(size_t)keep * me + m] = 1.0 / mu;
+    for (int cc = 0; cc <= keep; ++cc) to_stored(Yc.data() + (size_t)cc * me);
     CU(cudaMemcpyAsync(D->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, st));
     {
       ProfScope ps(c, K_RITZ, 0.0);
@@ -1085,6 +1212,7 @@ sfairsc_status dist_eigs(sfairsc_ctx* c, int k, double tol, double* evals_out, d
     TRY(allreduce(D, st, 1 + kHB, [](const DistPart& p) { return p.nb(); }));
     L.norm_all(false, 0, -1, kMaxJ);
     CHECK_LAUNCH();
+    TRY(L.clear_pair_state());
     j = keep;
     jsync = keep;
     L.restarts++;

@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_three(GraphDev g, ProjDesc pd, 
                                                        const double* __restrict__ vt, const double* __restrict__ vprev,
                                                        LzDev d, int j, double* __restrict__ u_out, double* dots,
                                                        double* cA, double* tr, double* partials, unsigned* counter,
-                                                       double* nb) {
+                                                       double* nb, bool fix_h) {
   __shared__ double gam[kHB];
   if (threadIdx.x == 0) {
     double gw[kHB];
@@ -641,7 +641,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_three(GraphDev g, ProjDesc pd, 
     for (int l = threadIdx.x; l <= j; l += blockDim.x) {
       const double gf = (l >= j - 1) ? 0.0 : d.cg[l];
       dots[l] = gf;
-      if (l < j) d.H[(size_t)j * d.ldH + l] -= gf;
+      if (fix_h && l < j) d.H[(size_t)j * d.ldH + l] -= gf;  // (once per process: the replicated H)
     }
     // the pair's sweep needs step j's v_j coefficients after step j+1's coefficient step overwrote d.cs, and
     // the rewrite coefficients of the stored column LZ_CONV (v'' = (v' - V[:, :q] e) / rho)
@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_three(GraphDev g, ProjDesc pd, 
       cA[l] = d.cs[l];
       tr[l] = l < q ? -d.econv[l] * ir : (l == q ? ir : 0.0);
     }
-    if (threadIdx.x == 0) d.lz[LZ_INVMU_A] = d.lz[LZ_INVMU];
+    if (threadIdx.x == 0 && fix_h) d.lz[LZ_INVMU_A] = d.lz[LZ_INVMU];
   }
   block_reduce_store<1 + kHB>(acc, partials + (size_t)blockIdx.x * (1 + kHB));
   ticket_finalize<1 + kHB>(partials, counter, nb, 1 + min(pd.h, kHB));
@@ -665,30 +665,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_three(GraphDev g, ProjDesc pd, 
 // writes V[:, j] = v_j, V[:, j+1] = v', w, V[:, conv] = v''; dots V^T w (J), V^T v' (J), v_j.w, v'.w,
 // v_j.v' -> partials [grid][2J + 3]; |w|^2, B^T w, |v'|^2 (ticket) -> nb [0], [1..16], [1 + kHB].
 // Stage (doubles): [J][kR] basis | v~_j | v~_{j+1} | t | s | grp bytes (the TMA ring of k_lz_update_p).
-struct LzPairArgs {
-  const double* V;
-  long long ld;
-  int J;
-  const double* vtA;  // v~_j
-  const double* vtB;  // v~_{j+1}
-  const double* t;    // L p~_{j+1}
-  double* vj_out;     // V[:, J]
-  double* vj1_out;    // V[:, J + 1]
-  double* w_out;
-  double* conv_out;   // V[:, conv] (nullptr: no rewrite)
-  const double* cA;   // step j: s/mu (stored basis, J)
-  const double* cB;   // step j+1: s/mu (J + 1)
-  const double* gB;   // step j+1: g (J + 1)
-  const double* tr;   // rewrite coefficients (J; zero beyond the rewritten column)
-  const double* lz;
-  const double* bs_t;
-  const double* bs_v;
-  double sigma;
-  double* partials;   // [grid][2J + 3]
-  double* partials2;  // [grid][2 + kHB]
-  unsigned* counter;
-  double* nb;
-};
+
 constexpr int kPairExtra = 3;  // vectors in a stage beside the basis and the s/grp rows: v~_j, v~_{j+1}, t
 __host__ __device__ constexpr size_t lzp_stage_doubles(int J) { return (size_t)(J + kPairExtra) * kR + kR + 16; }
 
@@ -1046,6 +1023,62 @@ void launch_lz_norm(const GraphDev& g, const ProjDesc& pd, const double* w, cons
     k_lz_norm<false><<<lz_sgrid(g.n), kThreads, 0, st>>>(g, pd, w, nb, dots, nd, d, jrow, vt, p, bs_v, q);
 }
 
+void launch_lz_three(const GraphDev& g, const ProjDesc& pd, const double* t, const double* vt, const double* vprev,
+                     const LzDev& d, int j, double* u_out, double* dots, double* cA, double* tr, double* partials,
+                     unsigned* counter, double* nb, int grid, bool fix_h, cudaStream_t st) {
+  bump_launch();
+  if (g.normalized)
+    k_lz_three<true><<<grid, kThreads, 0, st>>>(g, pd, t, vt, vprev, d, j, u_out, dots, cA, tr, partials, counter, nb,
+                                                fix_h);
+  else
+    k_lz_three<false><<<grid, kThreads, 0, st>>>(g, pd, t, vt, vprev, d, j, u_out, dots, cA, tr, partials, counter, nb,
+                                                 fix_h);
+}
+void launch_lz_pair(const GraphDev& g, const ProjDesc& pd, const LzPairArgs& a, int grid, cudaStream_t st) {
+  bump_launch();
+  if (g.normalized) lz_pair_m<true>(g, pd, a, grid, st);
+  else lz_pair_m<false>(g, pd, a, grid, st);
+}
+void launch_lz_pairpost(const LzDev& d, int J, const double* dd2, double* dd, const double* nb, const int* flags,
+                        cudaStream_t st) {
+  bump_launch();
+  k_lz_pairpost<<<1, kCoefT, 0, st>>>(d, J, dd2, dd, nb, flags);
+}
+
+// host side of the paired steps' basis change at a restart sync (the coefficient kernel's prologue on the
+// host copies): the stored odd column p = m - 1 is V'' T (column p of T = [e; rho])
+void pair_pending_to_orthonormal(int m, int ldH, std::vector<double>& Hh, std::vector<double>& sh, const double* e,
+                                 double rho) {
+  const int pq = m - 1;
+  auto H = [&](int r, int col) -> double& { return Hh[(size_t)col * ldH + r]; };
+  std::vector<double> hle(pq + 2, 0.0);
+  for (int l = 0; l <= pq + 1; ++l) {
+    const int row = (l == pq + 1) ? m : l;
+    double acc = 0.0;
+    for (int cc = 0; cc < pq; ++cc) acc += H(row, cc) * e[cc];
+    hle[l] = acc;
+  }
+  double es = 0.0;
+  for (int l = 0; l < pq; ++l) es += e[l] * sh[l];
+  const double hpp = H(pq, pq);
+  for (int l = 0; l < pq; ++l) H(l, pq) = (H(l, pq) + e[l] * hpp - hle[l] - e[l] * hle[pq]) / rho;
+  H(pq, pq) = hpp - hle[pq];
+  H(m, pq) = (H(m, pq) - hle[pq + 1]) / rho;
+  for (int cc = 0; cc < pq; ++cc) {
+    const double hpc = H(pq, cc);
+    for (int l = 0; l < pq; ++l) H(l, cc) += e[l] * hpc;
+    H(pq, cc) = rho * hpc;
+  }
+  sh[pq] = (sh[pq] - es) / rho;
+}
+// coefficients x (m entries) over V'' -> T^-1 x over the stored columns
+void pair_coef_to_stored(int m, double* x, const double* e, double rho) {
+  const int pq = m - 1;
+  const double xq = x[pq] / rho;
+  for (int l = 0; l < pq; ++l) x[l] -= e[l] * xq;
+  x[pq] = xq;
+}
+
 // ---------------------------------------------------------------------------
 // driver
 // ---------------------------------------------------------------------------
@@ -1108,13 +1141,8 @@ struct Lagged {
       bump_launch();
       // 8 CTAs per SM (partials: the SpMV's buffer, free again once its ticket is done)
       const int G = std::max(1, std::min((c->n + kThreads - 1) / kThreads, c->num_sms * 8));
-      const double* vprev = c->V + (long long)(j - 1) * c->ldv;
-      if (c->normalized)
-        k_lz_three<true><<<G, kThreads, 0, c->st>>>(g, c->pd(), c->vt, c->vr, vprev, dev(j), j, c->vy, c->dd, cA(),
-                                                    trc(), c->partials, c->counters + 7, c->nb);
-      else
-        k_lz_three<false><<<G, kThreads, 0, c->st>>>(g, c->pd(), c->vt, c->vr, vprev, dev(j), j, c->vy, c->dd, cA(),
-                                                     trc(), c->partials, c->counters + 7, c->nb);
+      launch_lz_three(g, c->pd(), c->vt, c->vr, c->V + (long long)(j - 1) * c->ldv, dev(j), j, c->vy, c->dd, cA(),
+                      trc(), c->partials, c->counters + 7, c->nb, G, true, c->st);
     }
     {
       ProfScope ps(c, K_NORMALIZE, 3 * c->vb() + c->sgb());
@@ -1156,15 +1184,12 @@ struct Lagged {
       a.counter = c->counters + 6;
       a.nb = c->nb;
       const int G = sweep_tma_grid(c->n, c->num_sms);
-      bump_launch();
-      if (c->normalized) lz_pair_m<true>(g, c->pd(), a, G, c->st);
-      else lz_pair_m<false>(g, c->pd(), a, G, c->st);
+      launch_lz_pair(g, c->pd(), a, G, c->st);
       launch_reduce_cols(c->partials, G, 2 * j + 3, dd2(), c->st);
     }
     {
       ProfScope ps(c, K_OTHER, 0.0);
-      bump_launch();
-      k_lz_pairpost<<<1, kCoefT, 0, c->st>>>(dev(j + 1), j, dd2(), c->dd, c->nb, c->bflags + j);
+      launch_lz_pairpost(dev(j + 1), j, dd2(), c->dd, c->nb, c->bflags + j, c->st);
     }
     norm(c->vy, c->dd, j + 2, j + 2, j + 1);
     CHECK_LAUNCH();
@@ -1350,33 +1375,10 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
     std::vector<double> pdef(tconv ? pq : 0);  // the pending column's defect e
     if (tconv) {
       for (int l = 0; l < pq; ++l) pdef[l] = c->hp[1024 + l];
-      auto H = [&](int r, int col) -> double& { return Hh[(size_t)col * ldH + r]; };
-      std::vector<double> hle(pq + 2, 0.0);
-      for (int l = 0; l <= pq + 1; ++l) {
-        const int row = (l == pq + 1) ? m : l;
-        double a = 0.0;
-        for (int cc = 0; cc < pq; ++cc) a += H(row, cc) * pdef[cc];
-        hle[l] = a;
-      }
-      double es = 0.0;
-      for (int l = 0; l < pq; ++l) es += pdef[l] * sh[l];
-      const double hpp = H(pq, pq);
-      for (int l = 0; l < pq; ++l) H(l, pq) = (H(l, pq) + pdef[l] * hpp - hle[l] - pdef[l] * hle[pq]) / prho;
-      H(pq, pq) = hpp - hle[pq];
-      H(m, pq) = (H(m, pq) - hle[pq + 1]) / prho;
-      for (int cc = 0; cc < pq; ++cc) {
-        const double hpc = H(pq, cc);
-        for (int l = 0; l < pq; ++l) H(l, cc) += pdef[l] * hpc;
-        H(pq, cc) = prho * hpc;
-      }
-      sh[pq] = (sh[pq] - es) / prho;
+      pair_pending_to_orthonormal(m, ldH, Hh, sh, pdef.data(), prho);
     }
-    // coefficients x over V'' -> T^-1 x over the stored columns
     auto to_stored = [&](double* x) {
-      if (!tconv) return;
-      const double xq = x[pq] / prho;
-      for (int l = 0; l < pq; ++l) x[l] -= pdef[l] * xq;
-      x[pq] = xq;
+      if (tconv) pair_coef_to_stored(m, x, pdef.data(), prho);
     };
     // ---- Rayleigh-Ritz on sym(H_m + s b~^T) ----
     const double om = c->hp[LZ_OMEGA];

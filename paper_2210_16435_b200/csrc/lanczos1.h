@@ -3,6 +3,8 @@
 #pragma once
 #include "kernels.cuh"
 
+#include <vector>
+
 namespace sfz {
 
 // scalar slots of the device state `lz`
@@ -57,5 +59,45 @@ void launch_lz_update(const GraphDev& g, const ProjDesc& pd, const LzSweepArgs& 
 void launch_lz_norm(const GraphDev& g, const ProjDesc& pd, const double* w, const double* nb, const double* dots,
                     int nd, const LzDev& d, int jrow, double* vt, double* p, double* bs_v, cudaStream_t st,
                     double* q = nullptr);
+
+// the pair sweep of two Lanczos steps (k_lz_pair)
+struct LzPairArgs {
+  const double* V;
+  long long ld;
+  int J;
+  const double* vtA;  // v~_j
+  const double* vtB;  // v~_{j+1}
+  const double* t;    // L p~_{j+1}
+  double* vj_out;     // V[:, J]
+  double* vj1_out;    // V[:, J + 1]
+  double* w_out;
+  double* conv_out;   // V[:, conv] (nullptr: no rewrite)
+  const double* cA;   // step j: s/mu (stored basis, J)
+  const double* cB;   // step j+1: s/mu (J + 1)
+  const double* gB;   // step j+1: g (J + 1)
+  const double* tr;   // rewrite coefficients (J; zero beyond the rewritten column)
+  const double* lz;
+  const double* bs_t;
+  const double* bs_v;
+  double sigma;
+  double* partials;   // [grid][2J + 3]
+  double* partials2;  // [grid][2 + kHB]
+  unsigned* counter;
+  double* nb;
+};
+
+// paired steps: the three-term vector of the pair's first step (+ its g_far dots; fix_h:
+// this call owns the replicated H / lz updates), the pair sweep, and the post-sweep dot bookkeeping
+void launch_lz_three(const GraphDev& g, const ProjDesc& pd, const double* t, const double* vt, const double* vprev,
+                     const LzDev& d, int j, double* u_out, double* dots, double* cA, double* tr, double* partials,
+                     unsigned* counter, double* nb, int grid, bool fix_h, cudaStream_t st);
+void launch_lz_pair(const GraphDev& g, const ProjDesc& pd, const LzPairArgs& a, int grid, cudaStream_t st);
+void launch_lz_pairpost(const LzDev& d, int J, const double* dd2, double* dd, const double* nb, const int* flags,
+                        cudaStream_t st);
+// host side of the pending odd column's basis change at a restart sync (H, lagged row, s), and the Ritz
+// coefficients back to the stored columns
+void pair_pending_to_orthonormal(int m, int ldH, std::vector<double>& Hh, std::vector<double>& sh, const double* e,
+                                 double rho);
+void pair_coef_to_stored(int m, double* x, const double* e, double rho);
 
 }  // namespace sfz
