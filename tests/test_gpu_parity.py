@@ -659,3 +659,43 @@ def test_paired_steps_option_errors(gpu_lib):
     with pytest.raises(gpu_lib.SfairscError) as e:
         _ctx(gpu_lib, g, 4, True, reorth=4)
     assert e.value.name == "E_INVALID_ARG"
+
+
+def test_binding_rejects_wrong_output_shapes(gpu_lib):
+    """Advisor r1: the binding checks the caller's output buffers before handing pointers to the library
+    (which writes k x n doubles / n labels / vectors of length n)."""
+    g = random_graph(300, 3, p=0.05, seed=2, weights="uniform")
+    ctx = _ctx(gpu_lib, g, 4, True)
+    with pytest.raises(ValueError):
+        gpu_lib.sfairsc_eigs(ctx, 4, 1e-10, evecs=np.zeros((3, g.n)))
+    with pytest.raises(ValueError):
+        gpu_lib.sfairsc_eigs(ctx, 4, 1e-10, evecs=np.zeros((4, g.n - 1)))
+    gpu_lib.sfairsc_eigs(ctx, 4, 1e-10)
+    with pytest.raises(ValueError):
+        gpu_lib.sfairsc_embed_kmeans(ctx, 1, labels=np.zeros(g.n - 1, np.int32))
+    x = np.random.default_rng(0).standard_normal(g.n)
+    with pytest.raises(ValueError):
+        gpu_lib.sfairsc_apply(ctx, x[:-1])
+    with pytest.raises(ValueError):
+        gpu_lib.sfairsc_apply(ctx, x, np.zeros(g.n + 1))
+    y = gpu_lib.sfairsc_apply(ctx, x)
+    assert y.shape == x.shape
+    ctx.close()
+
+
+@pytest.mark.parametrize("parts", [1, 3])
+def test_paired_row_partitioned_matches_single_gpu(gpu_lib, parts):
+    """Paired steps in the row-partitioned solver (virtual parts) against the single-GPU paired solver and
+    the one-step partitioned solver: the same eigenvalues (R6) on a ragged n."""
+    g = random_graph(1777, 4, p=0.006, seed=21, weights="uniform")
+    k = 7
+    ctx = _ctx(gpu_lib, g, k, True)
+    ev1, _, st1 = gpu_lib.sfairsc_eigs(ctx, k, 1e-10)
+    ctx.close()
+    kw = {"virtual_parts": parts} if parts > 1 else {}
+    for reorth in (3, 2):
+        ctx = _ctx(gpu_lib, g, k, True, reorth=reorth, **kw)
+        ev, _, st = gpu_lib.sfairsc_eigs(ctx, k, 1e-10)
+        ctx.close()
+        assert st["converged"] == 1 and st["max_resid_rel"] <= 1e-9
+        assert np.all(np.abs(ev - ev1) <= 1e-8 * np.abs(ev1) + 1e-12 * st1["sigma"])
