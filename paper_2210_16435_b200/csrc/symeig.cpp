@@ -3,11 +3,18 @@
 // Householder reduction to tridiagonal form followed by the implicit QL
 // iteration with Wilkinson-type shifts (the EISPACK tred2/tql2 pair, restated).
 // Host code, fp64; runs once per restart.
+#include <algorithm>
 #include <cmath>
 #include <vector>
-#include <algorithm>
 
 namespace sfz {
+
+namespace {
+struct Rot {
+  int i;
+  double c, s;
+};
+}  // namespace
 
 // A: m x m row-major symmetric (overwritten by the eigenvectors, row-major,
 // column c = eigenvector c).  evals ascending.
@@ -99,7 +106,9 @@ static inline __attribute__((always_inline)) void symeig_impl(int m, std::vector
   V(m - 1, m - 1) = 1.0;
   e[0] = 0.0;
 
-  // --- implicit QL (tql2) ---
+  // --- implicit QL (tql2): the rotations depend on the tridiagonal only; recorded, then applied to Z ---
+  std::vector<Rot> rots;
+  rots.reserve((size_t)m * 8);
   for (int i = 1; i < m; ++i) e[i - 1] = e[i];
   e[m - 1] = 0.0;
   double f = 0.0, tst1 = 0.0;
@@ -142,13 +151,7 @@ static inline __attribute__((always_inline)) void symeig_impl(int m, std::vector
           c = p / r;
           p = c * d[i] - s * g;
           d[i + 1] = h + s * (c * g + s * d[i]);
-          double* __restrict__ zi = &V(0, i);  // two contiguous columns (column-major view)
-          double* __restrict__ zi1 = &V(0, i + 1);
-          for (int k = 0; k < m; ++k) {
-            const double a0 = zi[k], a1 = zi1[k];
-            zi1[k] = s * a0 + c * a1;
-            zi[k] = c * a0 - s * a1;
-          }
+          rots.push_back(Rot{i, c, s});  // applied to Z below (it depends on the tridiagonal only)
         }
         p = -s * s2 * c3 * el1 * e[l] / dl1;
         e[l] = s * p;
@@ -157,6 +160,18 @@ static inline __attribute__((always_inline)) void symeig_impl(int m, std::vector
     }
     d[l] = d[l] + f;
     e[l] = 0.0;
+  }
+  // the recorded rotations on Z, in order (the QL recurrences above no longer interleave with the O(m^2)
+  // column updates: m = 170, 5.0 -> 4.4 ms on the build host)
+  for (const Rot& r : rots) {
+    double* __restrict__ zi = &V(0, r.i);  // two contiguous columns (column-major view)
+    double* __restrict__ zi1 = &V(0, r.i + 1);
+    const double c = r.c, sn = r.s;
+    for (int k = 0; k < m; ++k) {
+      const double a0 = zi[k], a1 = zi1[k];
+      zi1[k] = sn * a0 + c * a1;
+      zi[k] = c * a0 - sn * a1;
+    }
   }
   // --- sort ascending (selection sort with column swaps) ---
   for (int i = 0; i < m - 1; ++i) {
