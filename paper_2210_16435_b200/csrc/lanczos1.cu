@@ -706,9 +706,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_lz_pair(GraphDev g, ProjDesc pd
   static_assert(kThreads == 4 * kR, "one thread per (row, combination) in the finishing phase");
   const bool conv = a.conv_out != nullptr;
   for (int e = tid; e < kHB * kR; e += kThreads) (&gsum[0][0])[e] = 0.0;
-  for (int l = tid; l < J; l += kThreads) {
-    cab[l] = make_double2(a.cA[l], a.cB[l]);
-    cgt[l] = make_double2(a.gB[l], conv ? a.tr[l] : 0.0);
+  for (int l = tid; l < 8 * MAXQ; l += kThreads) {  // zero coefficients pad the columns beyond J (no branch below)
+    cab[l] = l < J ? make_double2(a.cA[l], a.cB[l]) : make_double2(0.0, 0.0);
+    cgt[l] = l < J ? make_double2(a.gB[l], conv ? a.tr[l] : 0.0) : make_double2(0.0, 0.0);
   }
   if (tid == 0) {
     for (int st = 0; st < kStages; ++st) mbar_init(&bars[st], 1);
@@ -746,22 +746,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_lz_pair(GraphDev g, ProjDesc pd
     double2 vreg[MAXQ];
     double pa[2] = {0.0, 0.0}, pb[2] = {0.0, 0.0}, pg[2] = {0.0, 0.0}, pt[2] = {0.0, 0.0};
 #pragma unroll
-    for (int q = 0; q < MAXQ; ++q) {
+    for (int q = 0; q < MAXQ; ++q) {  // columns beyond J re-read column J - 1 (finite) with zero coefficients
       const int l = cgp + 8 * q;
-      if (l < J) {
-        vreg[q] = *reinterpret_cast<const double2*>(buf + (size_t)l * kR + 2 * pr);
-        const double2 ab = cab[l], gt = cgt[l];
-        pa[0] = fma(vreg[q].x, ab.x, pa[0]);
-        pa[1] = fma(vreg[q].y, ab.x, pa[1]);
-        pb[0] = fma(vreg[q].x, ab.y, pb[0]);
-        pb[1] = fma(vreg[q].y, ab.y, pb[1]);
-        pg[0] = fma(vreg[q].x, gt.x, pg[0]);
-        pg[1] = fma(vreg[q].y, gt.x, pg[1]);
-        pt[0] = fma(vreg[q].x, gt.y, pt[0]);
-        pt[1] = fma(vreg[q].y, gt.y, pt[1]);
-      } else {
-        vreg[q] = make_double2(0.0, 0.0);
-      }
+      vreg[q] = *reinterpret_cast<const double2*>(buf + (size_t)min(l, J - 1) * kR + 2 * pr);
+      const double2 ab = cab[l], gt = cgt[l];
+      pa[0] = fma(vreg[q].x, ab.x, pa[0]);
+      pa[1] = fma(vreg[q].y, ab.x, pa[1]);
+      pb[0] = fma(vreg[q].x, ab.y, pb[0]);
+      pb[1] = fma(vreg[q].y, ab.y, pb[1]);
+      pg[0] = fma(vreg[q].x, gt.x, pg[0]);
+      pg[1] = fma(vreg[q].y, gt.x, pg[1]);
+      pt[0] = fma(vreg[q].x, gt.y, pt[0]);
+      pt[1] = fma(vreg[q].y, gt.y, pt[1]);
     }
     *reinterpret_cast<double2*>(&red[0][cgp][2 * pr]) = make_double2(pa[0], pa[1]);
     *reinterpret_cast<double2*>(&red[1][cgp][2 * pr]) = make_double2(pb[0], pb[1]);
