@@ -105,6 +105,19 @@ typedef struct {
                              rows; h must be given; evecs/labels/apply vectors hold the rank's rows */
   int32_t virtual_parts;  /* > 1 (test/emulation): split the full W into this many nnz-balanced row blocks
                              inside one process and GPU and run the row-partitioned solver over them */
+  int32_t filter_degree;  /* SURVEY §8(f) N2 (every kernel stays an SpMV): 0 or 1 = no
+                             filter; d >= 2 (<= 64) = thick-restart Lanczos on the Chebyshev filter
+                             -p(L^sigma), p(x) = (-1)^d T_d((x - c)/e), c = (a + sigma)/2, e = (sigma - a)/2,
+                             which maps [a, sigma] into [-1, 1] and the wanted eigenvalues below a, in the
+                             same order, below -1.  Each Lanczos step applies L^sigma d times
+                             (three-term recurrence fused into the apply's last kernel).  Eigenvalues are the
+                             Rayleigh quotients x^T L^sigma x of the filter's Ritz vectors; convergence is
+                             decided on their explicit L^sigma residuals.  Needs a group-fairness build,
+                             block_size 0/1, reorth 0/1 (the CGS2 solver runs), single GPU; else
+                             SFAIRSC_E_INVALID_ARG */
+  double filter_cut;      /* the filter's a: > 0 fixed (must be < sigma); <= 0 automatic: one unfiltered
+                             cycle of m steps, a = its keep-th Ritz value, and the filtered solve restarts
+                             from the sum of the cycle's k lowest Ritz vectors */
 } sfairsc_opts;
 
 typedef struct {
@@ -121,6 +134,7 @@ typedef struct {
   int32_t basis_size;    /* m used */
   int32_t kept;          /* Ritz vectors kept per restart */
   int32_t reserved;
+  double filter_cut;     /* the Chebyshev filter's a used (opts.filter_degree >= 2), else 0 */
 } sfairsc_stats;
 
 typedef struct {
@@ -233,6 +247,10 @@ sfairsc_status sfairsc_comm_unique_id(uint8_t id_out[128]);
 sfairsc_status sfairsc_comm_init(const uint8_t id[128], int32_t rank, int32_t nranks, int32_t device,
                                  sfairsc_comm **out);
 void sfairsc_comm_destroy(sfairsc_comm *comm);
+
+/* Host-only: sizeof of the ABI structs (0 sfairsc_csr, 1 sfairsc_opts, 2 sfairsc_stats, 3 sfairsc_info;
+ * -1 otherwise), so that a binding can verify its struct mirrors at load time. */
+int64_t sfairsc_struct_size(int32_t which);
 
 void sfairsc_destroy(sfairsc_ctx *ctx);
 const char *sfairsc_last_error(void);

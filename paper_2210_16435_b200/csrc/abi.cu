@@ -99,7 +99,7 @@ static void free_ctx(sfairsc_ctx* c) {
                   c->bs_w, c->bs_t, c->bs_v, c->nb, c->scal, c->c1, c->c2, c->vp, c->vt, c->vr, c->vy, c->V,
                   c->Vb, c->Ydev, c->X, c->flags, c->talpha, c->tbeta,
                   c->bP, c->bT, c->bR, c->Tdev, c->g2, c->bflags, c->Hdev, c->sdev, c->lz, c->partials2, c->dd, c->rpb,
-                  c->pairP, c->pairT, c->pairY, c->Qr, c->vq, c->vq_lz, c->vrB, c->lzp};
+                  c->pairP, c->pairT, c->pairY, c->Qr, c->vq, c->vq_lz, c->vrB, c->lzp, c->fbuf, c->fth};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hp) cudaFreeHost(c->hp);
@@ -130,6 +130,8 @@ extern "C" void sfairsc_default_opts(sfairsc_opts* o) {
   o->reorth = 0;
   o->comm = nullptr;
   o->virtual_parts = 0;
+  o->filter_degree = 0;
+  o->filter_cut = 0.0;
 }
 
 extern "C" const char* sfairsc_last_error(void) { return g_err.c_str(); }
@@ -428,6 +430,18 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
   // single-vector reorthogonalisation: 0 auto (= paired lagged sweeps where allowed, else lagged), 1 CGS2 (three
   // sweeps per step), 2 lagged (one sweep per step), 3 paired (one sweep per two steps)
   if (opts.reorth < 0 || opts.reorth > 3) return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth must be 0, 1, 2 or 3"));
+  // Chebyshev filter (§8(f) N2): the CGS2 solver on -p(L^sigma); group-fairness builds, single GPU
+  if (opts.filter_degree < 0 || opts.filter_degree > 64)
+    return bail(fail(SFAIRSC_E_INVALID_ARG, "filter_degree must be in [0, 64]"));
+  if (opts.filter_degree >= 2) {
+    if (opts.reorth > 1 || opts.block_size > 1 || is_dist || g_build_keep_values)
+      return bail(fail(SFAIRSC_E_INVALID_ARG,
+                       "filter_degree >= 2 needs a group-fairness build, block_size 0/1, reorth 0/1 and one GPU"));
+    c->filter_deg = opts.filter_degree;
+    c->filter_cut = opts.filter_cut;
+    c->bsz = 1;
+    opts.reorth = 1;
+  }
   c->lagged = c->bsz == 1 && opts.reorth != 1 && hh <= kHB && m <= 192 && m <= n - hh && m > k;
   if ((opts.reorth == 2 || opts.reorth == 3) && !c->lagged)
     return bail(fail(SFAIRSC_E_INVALID_ARG, "reorth=2/3 need block_size 1, h <= 16 and k < m <= min(192, n-h)"));
@@ -732,6 +746,11 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
     CUB(dalloc(&c->dd, kMaxJ + 8));
     CUB(dalloc(&c->bflags, kMaxJ + 8));
     CUB(cudaMemsetAsync(c->bflags, 0, sizeof(int) * (kMaxJ + 8), c->st));
+  }
+  if (c->filter_deg >= 2) {
+    CUB(dalloc(&c->fbuf, 2 * (size_t)c->ldv));
+    CUB(cudaMemsetAsync(c->fbuf, 0, sizeof(double) * 2 * c->ldv, c->st));
+    CUB(dalloc(&c->fth, kMaxJ));
   }
   if (c->bsz > 1) {  // block Lanczos buffers (m + bsz basis columns: V/Vb above hold m + 1 <= m + bsz)
     const int nbz = c->bsz;
@@ -1121,10 +1140,52 @@ struct Lanczos {
     return SFAIRSC_OK;
   }
 
+  // §8(f) N2: r = -p(L^sigma) x0 into vr, p(x) = (-1)^d T_d((x - cc)/e), by the Chebyshev three-term
+  // recurrence y_1 = (A x0 - cc x0)/e, y_{i+1} = 2 (A y_i - cc y_i)/e - y_{i-1} (d applies; each apply's
+  // finish kernel carries the recurrence)
+  sfairsc_status filter_apply(const double* x0, double cut) {
+    const int d = c->filter_deg;
+    const double cc = 0.5 * (cut + c->sigma), e = 0.5 * (c->sigma - cut);
+    const double sign = (d % 2 == 0) ? -1.0 : 1.0;  // -p = (-1)^(d+1) T_d
+    double* F0 = c->fbuf;
+    double* F1 = c->fbuf + c->ldv;
+    const double* ycur = x0;
+    const double* yprev = x0;
+    for (int i = 1; i <= d; ++i) {
+      {
+        ProfScope ps(c, K_PROJ, c->gpasses() * (c->vb() + c->sgb()) + 2 * c->vb() + c->sgb());
+        gsum_all(c, ycur, c->bs_w);
+        launch_project(c->g(), c->pd(), ycur, c->bs_w, 1.0, c->vp, c->st);
+      }
+      {
+        ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
+        ctx_spmv(c, c->vp, c->vt);
+      }
+      if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
+      double a = (i == 1 ? 1.0 : 2.0) / e, b = (i == 1 ? 0.0 : -1.0);
+      if (i == d) {
+        a *= sign;
+        b *= sign;
+      }
+      // y_new: F0, then F1, then in place over y_{i-1} (never over x0, a basis column); the last into vr
+      double* ynew = (i == d) ? c->vr : (i == 1 ? F0 : (i == 2 ? F1 : const_cast<double*>(yprev)));
+      {
+        ProfScope ps(c, K_FINISH, 4 * c->vb() + c->sgb());
+        launch_finish_cheb(c->g(), c->pd(), c->vt, c->bs_t, c->bs_w, c->sigma, ycur, yprev, a, cc, b, ynew, c->st);
+      }
+      yprev = ycur;
+      ycur = ynew;
+    }
+    CHECK_LAUNCH();
+    applies += d;
+    return SFAIRSC_OK;
+  }
+
   // random vector orthogonalised (CGS2 twice) against V[:, 0:J], normalised into column J
-  sfairsc_status random_vector(int J, bool project_first) {
+  sfairsc_status random_vector(int J, bool project_first, bool from_vr = false) {
     for (int attempt = 0; attempt < 5; ++attempt) {
-      if (project_first) {  // r = P u
+      if (from_vr && attempt == 0) {  // the caller's vector already in vr (filtered start, N2)
+      } else if (project_first) {  // r = P u
         launch_random(c->vt, c->n, c->seed, inject++, 7u, c->st);
         gsum_all(c, c->vt, c->bs_w);
         launch_project(c->g(), c->pd(), c->vt, c->bs_w, 1.0, c->vr, c->st);
@@ -1169,6 +1230,53 @@ struct Lanczos {
   }
 };
 
+// §8(f) N2: for the k columns of X (Ritz vectors of the filter, unit norm), theta_i = x_i^T L^sigma x_i and
+// max_i ||L^sigma x_i - theta_i x_i|| / sigma (k applies); X's columns are put in increasing theta order
+static sfairsc_status filter_check(sfairsc_ctx* c, int k, std::vector<double>* th, double* max_out) {
+  std::vector<double> res(k);
+  th->assign(k, 0.0);
+  for (int i = 0; i < k; ++i) {
+    const double* xi = c->X + (long long)i * c->ldv;
+    TRY(apply_dev(c, xi, c->vy));
+    launch_dot(xi, c->vy, c->n, c->partials, c->counters + 4, c->fth + i, c->st);
+    launch_resid_dev(c->vy, xi, c->fth + i, c->n, c->partials, c->counters + 4, c->scal + 8 + i % 64, c->st);
+    CHECK_LAUNCH();
+    if (i % 64 == 63 || i == k - 1) {
+      const int base = i - i % 64;
+      CU(cudaMemcpyAsync(c->hp, c->scal + 8, sizeof(double) * (i - base + 1), cudaMemcpyDeviceToHost, c->st));
+      CU(cudaStreamSynchronize(c->st));
+      for (int q = base; q <= i; ++q) res[q] = std::sqrt(c->hp[q - base]) / c->sigma;
+    }
+  }
+  CU(cudaMemcpyAsync(c->hp, c->fth, sizeof(double) * k, cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  std::vector<int> idx(k);
+  for (int i = 0; i < k; ++i) {
+    (*th)[i] = c->hp[i];
+    idx[i] = i;
+  }
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return (*th)[a] < (*th)[b]; });
+  bool ident = true;
+  for (int i = 0; i < k; ++i) ident = ident && idx[i] == i;
+  if (!ident) {  // reorder X (Vb is free scratch at a convergence check)
+    CU(cudaMemcpyAsync(c->Vb, c->X, sizeof(double) * (size_t)k * c->ldv, cudaMemcpyDeviceToDevice, c->st));
+    std::vector<double> t2(k), r2(k);
+    for (int i = 0; i < k; ++i) {
+      CU(cudaMemcpyAsync(c->X + (long long)i * c->ldv, c->Vb + (long long)idx[i] * c->ldv, sizeof(double) * c->ldv,
+                         cudaMemcpyDeviceToDevice, c->st));
+      t2[i] = (*th)[idx[i]];
+      r2[i] = res[idx[i]];
+    }
+    CU(cudaStreamSynchronize(c->st));
+    *th = t2;
+    res = r2;
+  }
+  double mx = 0.0;
+  for (int i = 0; i < k; ++i) mx = std::max(mx, res[i]);
+  *max_out = mx;
+  return SFAIRSC_OK;
+}
+
 extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, double* evals_out, double* evecs_out,
                                        int32_t evecs_memspace, sfairsc_stats* stats) {
   const double t0 = now_s();
@@ -1208,17 +1316,30 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
   std::vector<double> theta, Y;
   int m_eff = 0;
   double gap = std::numeric_limits<double>::quiet_NaN();
+  // §8(f) N2: Lanczos on B = -p(L^sigma); automatic cut: one unfiltered cycle first
+  const bool filter = c->filter_deg >= 2;
+  double cut = c->filter_cut;
+  bool filtering = filter && cut > 0.0;
+  if (filter && cut >= c->sigma) return fail(SFAIRSC_E_INVALID_ARG, "filter_cut=%g must be below sigma=%g", cut, c->sigma);
+  double fthr = 0.0;        // filtered: B-residual estimate below which the explicit L^sigma check runs
+  double fres = 0.0;        // filtered: the explicit check's max residual / sigma
+  std::vector<double> thA;  // filtered: Rayleigh quotients x^T L^sigma x of the check
   for (;;) {
-    // ---- expand column j: r = L^sigma v_j, CGS2 against V[:, 0:j+1], v_{j+1} = r/|r| ----
-    // (no host synchronisation inside the expansion; breakdowns are detected at the next sync)
-    {
-      ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
-      ctx_spmv(c, c->vp, c->vt);
+    // ---- expand column j: r = L^sigma v_j (filtered: -p(L^sigma) v_j), CGS2 against V[:, 0:j+1],
+    // v_{j+1} = r/|r| (no host synchronisation inside the expansion; breakdowns are detected at the next sync)
+    if (filtering) {
+      TRY(L.filter_apply(L.col(j), cut));
+      TRY(L.cgs2(j + 1, false));
+    } else {
+      {
+        ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
+        ctx_spmv(c, c->vp, c->vt);
+      }
+      if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
+      TRY(L.cgs2(j + 1, true));
+      L.applies++;
     }
-    if (c->h > kHB) extra_gsums(c, c->vt, c->bs_t);
-    TRY(L.cgs2(j + 1, true));
     TRY(L.normalize_step(j));
-    L.applies++;
     L.steps++;
     if (c->debug > 1) {
       cudaError_t e = cudaStreamSynchronize(c->st);
@@ -1279,6 +1400,51 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
     for (int i = 0; i < k; ++i) maxres = std::max(maxres, std::fabs(bm * Y[(size_t)(me - 1) * me + i]));
     if (k < me) gap = theta[k] - theta[k - 1];
     converged = complete || maxres <= target;
+    if (filter && !filtering && !converged) {
+      // end of the unfiltered cycle: a = the keep-th Ritz value (>= lambda_keep > lambda_k by interlacing),
+      // restart the filtered solve from the sum of the k lowest Ritz vectors (tests/tools: proto_filter.py)
+      const int q = std::min(L.keep, me) - 1;
+      cut = std::min(theta[q], 0.5 * c->sigma);
+      if (!(cut > theta[k - 1])) cut = 0.5 * (theta[k - 1] + c->sigma);
+      filtering = true;
+      std::vector<double> ys(me, 0.0);
+      for (int cc = 0; cc < k; ++cc)
+        for (int l = 0; l < me; ++l) ys[l] += Y[(size_t)l * me + cc];
+      CU(cudaMemcpyAsync(c->Ydev, ys.data(), sizeof(double) * me, cudaMemcpyHostToDevice, c->st));
+      launch_ritz(c->V, c->ldv, n, me, c->Ydev, 1, c->vr, c->st);
+      CU(cudaStreamSynchronize(c->st));
+      TRY(L.random_vector(0, false, true));
+      L.pk = 0;
+      j = 0;
+      jsync = 0;
+      L.restarts++;
+      if (c->debug) fprintf(stderr, "[sfairsc] filter cut a=%.17g (theta_%d), degree %d\n", cut, q, c->filter_deg);
+      continue;
+    }
+    if (filtering && !complete) {
+      // the B-estimate is in units of B's spectrum (|p| <= 1 on [a, sigma]); below the threshold, decide on
+      // the explicit L^sigma residuals of the Ritz vectors (k applies) and tighten the threshold if they miss
+      if (fthr == 0.0) fthr = 1e-6 * std::max(1.0, std::fabs(theta[0]));
+      converged = false;
+      if (maxres <= fthr) {
+        std::vector<double> Yc((size_t)me * k);
+        for (int cc = 0; cc < k; ++cc)
+          for (int l = 0; l < me; ++l) Yc[(size_t)cc * me + l] = Y[(size_t)l * me + cc];
+        CU(cudaMemcpyAsync(c->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, c->st));
+        {
+          ProfScope ps(c, K_RITZ, (double)(me + k) * c->vb());
+          launch_ritz(c->V, c->ldv, n, me, c->Ydev, k, c->X, c->st);
+        }
+        TRY(filter_check(c, k, &thA, &fres));
+        L.applies += k;
+        if (c->debug)
+          fprintf(stderr, "[sfairsc] filter check: B-est %g (thr %g) L-resid %g target %g\n", maxres, fthr, fres,
+                  tol_eff);
+        if (fres <= tol_eff) converged = true;
+        else fthr *= std::max(1e-3, std::min(0.1, 0.5 * tol_eff / fres));
+      }
+    }
+    if (converged && filtering && !complete) break;  // X and thA from the check
     if (c->debug)
       fprintf(stderr, "[sfairsc] RR me=%d maxres=%g target=%g theta0=%.17g theta_k-1=%.17g\n", me, maxres, target,
               theta[0], theta[k - 1]);
@@ -1319,10 +1485,26 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
     L.restarts++;
   }
 
-  // ---- A11: true residuals with k fresh applies ----
+  // ---- A11: true residuals with k fresh applies (filtered: the check's Rayleigh quotients and residuals) ----
   double max_resid = 0.0;
-  TRY(true_residuals(c, theta.data(), k, &max_resid));
-  L.applies += k;
+  if (filtering) {
+    if (!converged || complete) {  // X from the final Ritz vectors: their Rayleigh quotients and residuals
+      TRY(filter_check(c, k, &thA, &fres));
+      L.applies += k;
+    }
+    // gap estimate: lambda of the (k+1)-th B Ritz value through p^{-1} where it lies below a (p >= 1)
+    gap = std::numeric_limits<double>::quiet_NaN();
+    if ((int)theta.size() > k && -theta[k] >= 1.0) {
+      const double pc = 0.5 * (cut + c->sigma), pe = 0.5 * (c->sigma - cut);
+      const double lam1 = pc - pe * std::cosh(std::acosh(-theta[k]) / c->filter_deg);
+      gap = lam1 - thA[k - 1];
+    }
+    theta = thA;
+    max_resid = fres;
+  } else {
+    TRY(true_residuals(c, theta.data(), k, &max_resid));
+    L.applies += k;
+  }
   if (c->prof.on) c->prof.resolve();
   c->evals.assign(theta.begin(), theta.begin() + k);
   c->k_eigs = k;
@@ -1347,6 +1529,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
   S.converged = converged ? 1 : 0;
   S.basis_size = L.m;
   S.kept = L.keep;
+  S.filter_cut = filtering ? cut : 0.0;
   c->last = S;
   if (stats) *stats = S;
   if (!converged) return fail(SFAIRSC_E_NO_CONVERGENCE, "no convergence after %lld restarts", (long long)L.restarts);
@@ -1365,6 +1548,16 @@ extern "C" sfairsc_status sfairsc_embed_kmeans(sfairsc_ctx* c, uint64_t seed, in
 }
 
 extern "C" int64_t sfairsc_launch_count(void) { return (int64_t)launch_count(); }
+
+extern "C" int64_t sfairsc_struct_size(int32_t which) {
+  switch (which) {
+    case 0: return (int64_t)sizeof(sfairsc_csr);
+    case 1: return (int64_t)sizeof(sfairsc_opts);
+    case 2: return (int64_t)sizeof(sfairsc_stats);
+    case 3: return (int64_t)sizeof(sfairsc_info);
+    default: return -1;
+  }
+}
 
 // host utility exported for tests of the Rayleigh-Ritz step
 extern "C" int sfairsc_host_symeig(int32_t m, const double* A, double* evals, double* evecs) {

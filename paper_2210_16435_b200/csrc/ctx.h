@@ -113,6 +113,12 @@ struct sfairsc_ctx {
   bool paired = false;     // lagged solver with two Lanczos steps per basis sweep (reorth 3, default where allowed)
   double* vrB = nullptr;   // paired steps: the second lagged vector of a pair
   double* lzp = nullptr;   // paired steps: epend | econv | cA | tr | pair dots (8 kMaxJ doubles)
+  // Chebyshev-filtered Lanczos (§8(f) N2): degree (>= 2: on), cut a (<= 0: automatic),
+  // two recurrence vectors, the Rayleigh quotients of the explicit check
+  int filter_deg = 0;
+  double filter_cut = 0.0;
+  double* fbuf = nullptr;  // 2 ldv
+  double* fth = nullptr;   // kMaxJ
   double *Hdev = nullptr, *sdev = nullptr, *lz = nullptr, *partials2 = nullptr, *dd = nullptr;
   // column-blocked CSR (the gathered vector exceeds L2, e.g. config 5): block-major copy of the CSR,
   // rpb[b*(n+1) + i] = start of row i in column block b; nblk = 1: plain CSR

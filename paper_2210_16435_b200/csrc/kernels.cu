@@ -207,6 +207,29 @@ __global__ void __launch_bounds__(kThreads) k_finish(GraphDev g, ProjDesc pd, co
   }
 }
 
+// Chebyshev three-term step (§8(f) N2) fused into the apply's finish:
+// y_new = a (finish(t) - cc y_cur) + b y_prev, finish(t) = L^sigma y_cur as in k_finish (group projector).
+// y_new may alias y_prev (each element is read before it is written by the same thread).
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) k_finish_cheb(GraphDev g, ProjDesc pd, const double* __restrict__ t,
+                                                          const double* bsum_t, const double* bsum_w, double sigma,
+                                                          const double* __restrict__ ycur, const double* yprev,
+                                                          double a, double cc, double b, double* ynew) {
+  __shared__ double gt[256], gw[256];
+  if (threadIdx.x == 0) {
+    gamma_serial(bsum_t, 1.0, pd, gt);
+    gamma_serial(bsum_w, 1.0, pd, gw);
+    for (int s = 0; s < pd.h; ++s) gt[s] = gt[s] - sigma * gw[s];
+  }
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const double gi = gt[g.grp[i]];
+    const double ay = NORM ? fma(-g.s[i], gi, t[i]) : t[i] - gi;  // (L^sigma y_cur)_i
+    const double r = a * fma(-cc, ycur[i], ay);
+    ynew[i] = b != 0.0 ? fma(b, yprev[i], r) : r;
+  }
+}
+
 // ----------------------------------------------------------------------------
 // Krylov sweeps (A7-A9)
 // ----------------------------------------------------------------------------
@@ -365,14 +388,25 @@ __global__ void k_random(double* x, int n, uint64_t seed, unsigned c1, unsigned 
 }
 
 __global__ void __launch_bounds__(kThreads) k_resid(const double* __restrict__ y, const double* __restrict__ x,
-                                                    double theta, int n, double* partials, unsigned* counter,
-                                                    double* out) {
+                                                    double theta, const double* theta_dev, int n, double* partials,
+                                                    unsigned* counter, double* out) {
+  if (theta_dev) theta = *theta_dev;
   double v[1] = {0.0};
   const int i0 = (int)((long long)n * blockIdx.x / gridDim.x), i1 = (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
   for (int i = i0 + threadIdx.x; i < i1; i += kThreads) {
     const double r = fma(-theta, x[i], y[i]);
     v[0] = fma(r, r, v[0]);
   }
+  block_reduce_store<1>(v, partials + blockIdx.x);
+  ticket_finalize<1>(partials, counter, out, 1);
+}
+
+// out = x^T y (ticket reduced)
+__global__ void __launch_bounds__(kThreads) k_dot(const double* __restrict__ x, const double* __restrict__ y, int n,
+                                                  double* partials, unsigned* counter, double* out) {
+  double v[1] = {0.0};
+  const int i0 = (int)((long long)n * blockIdx.x / gridDim.x), i1 = (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
+  for (int i = i0 + threadIdx.x; i < i1; i += kThreads) v[0] = fma(x[i], y[i], v[0]);
   block_reduce_store<1>(v, partials + blockIdx.x);
   ticket_finalize<1>(partials, counter, out, 1);
 }
@@ -572,7 +606,28 @@ void launch_ritz(const double* V, long long ld, int n, int m, const double* Y, i
 void launch_resid(const double* y, const double* x, double theta, int n, double* partials, unsigned* counter,
                   double* out, cudaStream_t st) {
   bump();
-  k_resid<<<reduce_grid(n), kThreads, 0, st>>>(y, x, theta, n, partials, counter, out);
+  k_resid<<<reduce_grid(n), kThreads, 0, st>>>(y, x, theta, nullptr, n, partials, counter, out);
+}
+void launch_resid_dev(const double* y, const double* x, const double* theta_dev, int n, double* partials,
+                      unsigned* counter, double* out, cudaStream_t st) {
+  bump();
+  k_resid<<<reduce_grid(n), kThreads, 0, st>>>(y, x, 0.0, theta_dev, n, partials, counter, out);
+}
+void launch_dot(const double* x, const double* y, int n, double* partials, unsigned* counter, double* out,
+                cudaStream_t st) {
+  bump();
+  k_dot<<<reduce_grid(n), kThreads, 0, st>>>(x, y, n, partials, counter, out);
+}
+void launch_finish_cheb(const GraphDev& g, const ProjDesc& pd, const double* t, const double* bsum_t,
+                        const double* bsum_w, double sigma, const double* ycur, const double* yprev, double a,
+                        double cc, double b, double* ynew, cudaStream_t st) {
+  bump();
+  if (g.normalized)
+    k_finish_cheb<true><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_w, sigma, ycur, yprev, a, cc, b,
+                                                                ynew);
+  else
+    k_finish_cheb<false><<<stream_grid(g.n), kThreads, 0, st>>>(g, pd, t, bsum_t, bsum_w, sigma, ycur, yprev, a, cc,
+                                                                 b, ynew);
 }
 
 }  // namespace sfz

@@ -126,6 +126,17 @@ void launch_ritz(const double* V, long long ld, int n, int m, const double* Y, i
 // out = |y - theta x|^2 (ticket reduced)
 void launch_resid(const double* y, const double* x, double theta, int n, double* partials, unsigned* counter,
                   double* out, cudaStream_t st);
+// the same with theta read on the device (*theta_dev)
+void launch_resid_dev(const double* y, const double* x, const double* theta_dev, int n, double* partials,
+                      unsigned* counter, double* out, cudaStream_t st);
+// out = x^T y (ticket reduced)
+void launch_dot(const double* x, const double* y, int n, double* partials, unsigned* counter, double* out,
+                cudaStream_t st);
+// Chebyshev step (§8(f) N2): y_new = a (L^sigma y_cur - cc y_cur) + b y_prev, L^sigma y_cur = finish(t) with
+// t = L P y_cur (bsum_t = B^T t, bsum_w = B^T y_cur); group projector only; y_new may alias y_prev
+void launch_finish_cheb(const GraphDev& g, const ProjDesc& pd, const double* t, const double* bsum_t,
+                        const double* bsum_w, double sigma, const double* ycur, const double* yprev, double a,
+                        double cc, double b, double* ynew, cudaStream_t st);
 
 // ---- block Krylov kernels (block.cu) ---------------------------------
 // NB in {1, 2, 4}; blocks of NB n-vectors are interleaved (row-major, ldv rows x NB).

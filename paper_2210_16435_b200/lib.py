@@ -49,14 +49,15 @@ class Opts(C.Structure):
                 ("max_restarts", C.c_int32), ("start_seed", C.c_uint64), ("tol_eff_cap", C.c_double),
                 ("cuda_stream", C.c_void_p), ("check_symmetry", C.c_int32), ("spmv_vector", C.c_int32),
                 ("block_size", C.c_int32), ("reorth", C.c_int32), ("comm", C.c_void_p),
-                ("virtual_parts", C.c_int32)]
+                ("virtual_parts", C.c_int32), ("filter_degree", C.c_int32), ("filter_cut", C.c_double)]
 
 
 class Stats(C.Structure):
     _fields_ = [("applies", C.c_int64), ("steps", C.c_int64), ("restarts", C.c_int64), ("breakdowns", C.c_int64),
                 ("sigma", C.c_double), ("max_resid_rel", C.c_double), ("gap_est", C.c_double),
                 ("t_build_s", C.c_double), ("t_eigs_s", C.c_double), ("converged", C.c_int32),
-                ("basis_size", C.c_int32), ("kept", C.c_int32), ("reserved", C.c_int32)]
+                ("basis_size", C.c_int32), ("kept", C.c_int32), ("reserved", C.c_int32),
+                ("filter_cut", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
@@ -101,11 +102,17 @@ def _load():
         "sfairsc_comm_unique_id": (C.c_int, [P]),
         "sfairsc_comm_init": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
         "sfairsc_comm_destroy": (None, [P]),
+        "sfairsc_struct_size": (C.c_int64, [C.c_int32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    # the struct mirrors above must match the library's layout (include/sfairsc.h)
+    for which, st in enumerate((CSR, Opts, Stats, Info)):
+        if lib.sfairsc_struct_size(which) != C.sizeof(st):
+            raise ImportError(f"{st.__name__}: ctypes size {C.sizeof(st)} != library {lib.sfairsc_struct_size(which)}"
+                              " (stale build of libsfairsc.so?)")
     return lib
 
 

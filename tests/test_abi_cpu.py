@@ -35,6 +35,17 @@ def test_library_exports_every_declared_symbol():
     assert "sm_100a" in lib.version()
 
 
+def test_struct_mirrors_match_library_layout():
+    """The binding's ctypes mirrors of sfairsc_csr / _opts / _stats / _info have the library's sizes
+    (the binding also checks this at load time) and the default options match the header's defaults."""
+    from paper_2210_16435_b200 import lib
+    for which, st in enumerate((lib.CSR, lib.Opts, lib.Stats, lib.Info)):
+        assert lib._lib.sfairsc_struct_size(which) == ctypes.sizeof(st), st.__name__
+    assert lib._lib.sfairsc_struct_size(9) == -1
+    o = lib.default_opts()
+    assert (o.reorth, o.block_size, o.filter_degree, o.filter_cut, o.tol_eff_cap) == (0, 0, 0, 0.0, 1e-10)
+
+
 def test_library_is_sm100a_cubin():
     import subprocess
     from paper_2210_16435_b200 import lib

@@ -129,8 +129,9 @@ def test_operator_device_tensors(gpu_lib):
 
 # eigensolver variants of the C ABI (sfairsc_opts): the default (paired steps: two Lanczos steps per
 # basis sweep, reorth 3, where allowed), one lagged step per sweep (reorth 2), three-sweep CGS2, and block
-# Lanczos with b = 2
-SOLVERS = {"default": {}, "lagged1": {"reorth": 2}, "cgs2": {"reorth": 1}, "block2": {"block_size": 2}}
+# Lanczos with b = 2, and the Chebyshev-filtered CGS2 solver of degree 3 (§8(f) N2)
+SOLVERS = {"default": {}, "lagged1": {"reorth": 2}, "cgs2": {"reorth": 1}, "block2": {"block_size": 2},
+           "cheb3": {"filter_degree": 3}}
 
 
 def _check_eigs(lib, g, k, normalized, tol, dense=None, ref_evals=None, ref_X=None, gap=None, **kw):
