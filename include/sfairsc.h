@@ -238,6 +238,10 @@ sfairsc_status sfairsc_profile_reset(sfairsc_ctx *ctx);
  * symmetric; evals[m] ascending; evecs (m x m row-major, column c = vector c,
  * may be NULL).  Returns 0 on success.  Exported so tests can pin it on CPU. */
 int sfairsc_host_symeig(int32_t m, const double *A, double *evals, double *evecs);
+/* Same, with only the eigenvectors of the nvec smallest eigenvalues (what a thick restart keeps): all m
+ * evals ascending; evecs m x m row-major with columns c < nvec written (the others untouched).
+ * 0 <= nvec <= m.  Returns 0 on success, 1 on bad arguments. */
+int sfairsc_host_symeig_sel(int32_t m, const double *A, double *evals, double *evecs, int32_t nvec);
 
 /* Multi-GPU bootstrap: rank 0 calls sfairsc_comm_unique_id and
  * broadcasts the 128 bytes (e.g. with torch.distributed); every rank then calls

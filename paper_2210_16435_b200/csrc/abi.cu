@@ -17,12 +17,14 @@
 
 namespace sfz {
 void symeig(int m, std::vector<double>& A, std::vector<double>& evals);
+void symeig(int m, std::vector<double>& A, std::vector<double>& evals, int nvec);
 sfairsc_status eigs_block(sfairsc_ctx* c, int k, double tol, double* evals_out, double* evecs_out,
                           int evecs_memspace, sfairsc_stats* stats);
 sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out, double* evecs_out,
                            int evecs_memspace, sfairsc_stats* stats);
 sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* groups, int hh,
                           const std::vector<int64_t>& cnt_local, const sfairsc_opts& opts);
+sfairsc_status dist_agree(sfairsc_comm* comm, int local_status, cudaStream_t st);
 sfairsc_status dist_eigs(sfairsc_ctx* c, int k, double tol, double* evals_out, double* evecs_out, int evecs_memspace,
                          sfairsc_stats* stats);
 sfairsc_status dist_apply(sfairsc_ctx* c, const double* x, double* y);
@@ -286,9 +288,28 @@ extern "C" sfairsc_status sfairsc_build_operator(const sfairsc_csr* W, const int
   return sfairsc_build_operator_ex(W, groups, h, k, normalized, nullptr, out);
 }
 
+static sfairsc_status build_impl(const sfairsc_csr* W, const int32_t* groups, int32_t h, int32_t k,
+                                 int32_t normalized, const sfairsc_opts* opts_in, sfairsc_ctx** out,
+                                 bool* reached_dist);
+
 extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const int32_t* groups, int32_t h,
                                                     int32_t k, int32_t normalized, const sfairsc_opts* opts_in,
                                                     sfairsc_ctx** out) {
+  bool reached_dist = false;
+  const sfairsc_status st = build_impl(W, groups, h, k, normalized, opts_in, out, &reached_dist);
+  if (st != SFAIRSC_OK && !reached_dist && opts_in && opts_in->comm) {
+    // this rank failed before the row-partitioned build's first collective: take part in the agreement the
+    // other ranks wait in (dist_build), so that they fail too instead of blocking; keep this rank's message
+    const std::string msg = g_err;
+    dist_agree(opts_in->comm, (int)st, (cudaStream_t)opts_in->cuda_stream);
+    g_err = msg;
+  }
+  return st;
+}
+
+static sfairsc_status build_impl(const sfairsc_csr* W, const int32_t* groups, int32_t h, int32_t k,
+                                 int32_t normalized, const sfairsc_opts* opts_in, sfairsc_ctx** out,
+                                 bool* reached_dist) {
   const double t0 = now_s();
   if (!W || !groups || !out) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
   *out = nullptr;
@@ -459,6 +480,7 @@ extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const 
       while (vs < 32 && vs * 4 < mean_deg) vs *= 2;
       c->vs = opts.spmv_vector > 0 ? opts.spmv_vector : vs;
     }
+    *reached_dist = true;
     sfairsc_status ds = dist_build(c, W, groups, hh, cnt, opts);
     if (ds != SFAIRSC_OK) return bail(ds);
     c->t_build = now_s() - t0;
@@ -1567,5 +1589,15 @@ extern "C" int sfairsc_host_symeig(int32_t m, const double* A, double* evals, do
   for (int i = 0; i < m; ++i) evals[i] = ev[i];
   if (evecs)
     for (size_t i = 0; i < (size_t)m * m; ++i) evecs[i] = M[i];
+  return 0;
+}
+extern "C" int sfairsc_host_symeig_sel(int32_t m, const double* A, double* evals, double* evecs, int32_t nvec) {
+  if (m < 0 || nvec < 0 || nvec > m || (m > 0 && (!A || !evals))) return 1;
+  std::vector<double> M(A, A + (size_t)m * m), ev;
+  symeig(m, M, ev, nvec);
+  for (int i = 0; i < m; ++i) evals[i] = ev[i];
+  if (evecs)
+    for (int l = 0; l < m; ++l)
+      for (int c = 0; c < nvec; ++c) evecs[(size_t)l * m + c] = M[(size_t)l * m + c];
   return 0;
 }

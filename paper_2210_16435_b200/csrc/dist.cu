@@ -122,6 +122,7 @@ extern "C" void sfairsc_comm_destroy(sfairsc_comm* c) {
 namespace sfz {
 
 void symeig(int m, std::vector<double>& A, std::vector<double>& evals);
+void symeig(int m, std::vector<double>& A, std::vector<double>& evals, int nvec);
 void bump_launch();
 sfairsc_status kmeans_run(sfairsc_ctx* ctx, uint64_t seed, int32_t* labels_out, int32_t memspace, double* objective);
 
@@ -432,6 +433,28 @@ static cudaError_t dal(T** p, size_t count) {
 }
 
 // ---------------------------------------------------------------------------
+// build-time agreement (advisor r1): every rank of a row-partitioned build takes part in exactly one
+// max-all-reduce of its local validation status before any other collective, so a rank whose own checks
+// fail (group ids, row block, CSR sizes) makes every rank return instead of leaving the others blocked in
+// the first all-gather.  Ranks that pass their checks call it at the start of dist_build; a rank that
+// fails calls it from sfairsc_build_operator_ex before returning.
+// ---------------------------------------------------------------------------
+sfairsc_status dist_agree(sfairsc_comm* comm, int local_status, cudaStream_t st) {
+  if (!comm || !comm->comm || !nccl().ok) return SFAIRSC_OK;
+  double* b = nullptr;
+  if (cudaMalloc((void**)&b, sizeof(double)) != cudaSuccess) return fail(SFAIRSC_E_OOM, "agreement buffer");
+  double v = (double)local_status, r = 0.0;
+  cudaMemcpy(b, &v, sizeof(double), cudaMemcpyHostToDevice);
+  const ncclResult_t nr = nccl().AllReduce(b, b, 1, ncclDouble, ncclMax, comm->comm, st);
+  cudaError_t e = cudaMemcpyAsync(&r, b, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(b);
+  if (nr != ncclSuccess) return fail(SFAIRSC_E_NCCL, "build agreement: %s", nccl().GetErrorString(nr));
+  if (e != cudaSuccess) return fail(SFAIRSC_E_CUDA, "build agreement: %s", cudaGetErrorString(e));
+  return (sfairsc_status)(int)r;
+}
+
+// ---------------------------------------------------------------------------
 // build (A0-A3, partitioned)
 // ---------------------------------------------------------------------------
 sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* groups, int hh,
@@ -448,6 +471,11 @@ sfairsc_status dist_build(sfairsc_ctx* c, const sfairsc_csr* W, const int32_t* g
   CU(cudaMemcpy(hrp.data(), W->row_ptr, sizeof(int32_t) * (W->n_rows + 1),
                 dev_in ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
   if (D->comm) {
+    // local checks passed on this rank: agree with the others (a failed rank joins from the ABI)
+    const sfairsc_status ag = dist_agree(D->comm, SFAIRSC_OK, st);
+    if (ag != SFAIRSC_OK)
+      return ag == SFAIRSC_E_NCCL || ag == SFAIRSC_E_CUDA || ag == SFAIRSC_E_OOM
+                 ? ag : fail(ag, "another rank's build failed its input checks (status %d)", (int)ag);
     D->P = 1;
     D->P_total = D->comm->nranks;
     D->part0 = D->comm->rank;
@@ -1153,10 +1181,12 @@ sfairsc_status dist_eigs(sfairsc_ctx* c, int k, double tol, double* evals_out, d
       for (int q = 0; q < m; ++q)
         A[(size_t)r * m + q] = 0.5 * ((Hh[(size_t)q * ldH + r] + sh[r] * bt[q]) + (Hh[(size_t)r * ldH + q] + sh[q] * bt[r]));
     Y = A;
-    symeig(m, Y, theta);
+    // only the kept (>= k) smallest Ritz vectors are used below: the selected-vector eigensolver
+    const int nsel = std::min(m, std::max(keep, k));
+    symeig(m, Y, theta, nsel);
     std::vector<double> bY(m, 0.0);
     double maxres = 0.0;
-    for (int i = 0; i < m; ++i) {
+    for (int i = 0; i < nsel; ++i) {
       double acc = 0.0;
       for (int l = 0; l < m; ++l) acc += bt[l] * Y[(size_t)l * m + i];
       bY[i] = mu * acc;

@@ -38,6 +38,7 @@
 namespace sfz {
 
 void symeig(int m, std::vector<double>& A, std::vector<double>& evals);
+void symeig(int m, std::vector<double>& A, std::vector<double>& evals, int nvec);
 void bump_launch();
 
 namespace {
@@ -988,11 +989,23 @@ static void lz_pair_launch(const GraphDev& g, const ProjDesc& pd, const LzPairAr
   if (a.J > 0) encode_colmajor_map(a.V, a.ld, a.J, kR, &tmap);
   k_lz_pair<MAXQ, NORM><<<grid, kThreads, stages * stage, st>>>(g, pd, a, stages, tmap);
 }
+// one instantiation per column-group count MAXQ = ceil(J / 8): the sweep's time follows the padded column
+// count 8 MAXQ, not J (ncu launch list, profiles/r2_final_launches.csv: 778 us at J = 127 with MAXQ = 16,
+// 929 us at J = 129 with MAXQ = 24), so the padding stays below 8 columns
+template <bool NORM, int Q = 1>
+static void lz_pair_q(int maxq, const GraphDev& g, const ProjDesc& pd, const LzPairArgs& a, int grid,
+                      cudaStream_t st) {
+  if constexpr (Q < 24) {
+    if (maxq > Q) {
+      lz_pair_q<NORM, Q + 1>(maxq, g, pd, a, grid, st);
+      return;
+    }
+  }
+  lz_pair_launch<Q, NORM>(g, pd, a, grid, st);
+}
 template <bool NORM>
 static void lz_pair_m(const GraphDev& g, const ProjDesc& pd, const LzPairArgs& a, int grid, cudaStream_t st) {
-  if (a.J <= 64) lz_pair_launch<8, NORM>(g, pd, a, grid, st);
-  else if (a.J <= 128) lz_pair_launch<16, NORM>(g, pd, a, grid, st);
-  else lz_pair_launch<24, NORM>(g, pd, a, grid, st);
+  lz_pair_q<NORM>(std::max(1, (a.J + 7) / 8), g, pd, a, grid, st);
 }
 
 void launch_lz_coef(const LzDev& d, int j, cudaStream_t st) {
@@ -1391,10 +1404,12 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
         A[(size_t)r * m + q] = 0.5 * (hrq + hqr);
       }
     Y = A;
-    symeig(m, Y, theta);
+    // only the kept (>= k) smallest Ritz vectors are used below: the selected-vector eigensolver
+    const int nsel = std::min(m, std::max(keep, k));
+    symeig(m, Y, theta, nsel);
     double maxres = 0.0;
     std::vector<double> bY(m, 0.0);
-    for (int i = 0; i < m; ++i) {
+    for (int i = 0; i < nsel; ++i) {
       double acc = 0.0;
       for (int l = 0; l < m; ++l) acc += bt[l] * Y[(size_t)l * m + i];
       bY[i] = mu * acc;  // b = mu b~ : coupling of Ritz vector i to v_m

@@ -10,20 +10,143 @@
 namespace sfz {
 
 namespace {
+// sqrt(a^2 + b^2) without std::hypot's scaling (its libm call is ~0.5 ms of a 170 x 170 restart) when the
+// squares can neither overflow nor underflow; std::hypot otherwise
+inline double hyp(double a, double b) {
+  const double m = std::max(std::fabs(a), std::fabs(b));
+  if (m < 1e150 && m > 1e-150) return std::sqrt(a * a + b * b);
+  return std::hypot(a, b);
+}
 struct Rot {
   int i;
   double c, s;
 };
 }  // namespace
 
+// Selected-vector completion of symeig_impl after the Householder reduction (tred2 without accumulation):
+// reflector i (i = 1 .. m-1) is P_i = I - u_i u_i^T / h_i with u_i = V(0 .. i-1, i), h_i = d[i] (skipped when
+// 0), T = diag(V(i, i)) + offdiag(e[1 .. m-1]), and Q = P_{m-1} ... P_1 (the order the EISPACK accumulation
+// builds it in).  QL (tql2) on T records its rotations Z <- Z G_t; the selected eigenvectors are
+// Q G_1 ... G_N E_S, evaluated right to left.
+template <int kDummy>
+static inline __attribute__((always_inline)) void symeig_select(int m, std::vector<double>& A,
+                                                                 std::vector<double>& evals, int nvec,
+                                                                 std::vector<double>& d, std::vector<double>& e) {
+#define V(i, j) A[(size_t)(j) * m + (i)]
+  std::vector<double> hv(m, 0.0);
+  for (int i = 1; i < m; ++i) hv[i] = d[i];
+  for (int j = 0; j < m; ++j) d[j] = V(j, j);
+  e[0] = 0.0;
+  std::vector<Rot> rots;
+  rots.reserve((size_t)m * 8);
+  for (int i = 1; i < m; ++i) e[i - 1] = e[i];
+  e[m - 1] = 0.0;
+  double f = 0.0, tst1 = 0.0;
+  const double eps = std::ldexp(1.0, -52);
+  for (int l = 0; l < m; ++l) {
+    tst1 = std::max(tst1, std::fabs(d[l]) + std::fabs(e[l]));
+    int mm = l;
+    while (mm < m) {
+      if (std::fabs(e[mm]) <= eps * tst1) break;
+      ++mm;
+    }
+    if (mm == m) mm = m - 1;
+    if (mm > l) {
+      int iter = 0;
+      do {
+        ++iter;
+        double g = d[l];
+        double p = (d[l + 1] - g) / (2.0 * e[l]);
+        double r = hyp(p, 1.0);
+        if (p < 0) r = -r;
+        d[l] = e[l] / (p + r);
+        d[l + 1] = e[l] * (p + r);
+        const double dl1 = d[l + 1];
+        double h = g - d[l];
+        for (int i = l + 2; i < m; ++i) d[i] -= h;
+        f += h;
+        p = d[mm];
+        double c = 1.0, c2 = c, c3 = c;
+        const double el1 = e[l + 1];
+        double s = 0.0, s2 = 0.0;
+        for (int i = mm - 1; i >= l; --i) {
+          c3 = c2;
+          c2 = c;
+          s2 = s;
+          g = c * e[i];
+          h = c * p;
+          r = hyp(p, e[i]);
+          e[i + 1] = s * r;
+          s = e[i] / r;
+          c = p / r;
+          p = c * d[i] - s * g;
+          d[i + 1] = h + s * (c * g + s * d[i]);
+          rots.push_back(Rot{i, c, s});
+        }
+        p = -s * s2 * c3 * el1 * e[l] / dl1;
+        e[l] = s * p;
+        d[l] = c * p;
+      } while (std::fabs(e[l]) > eps * tst1 && iter < 200);
+    }
+    d[l] = d[l] + f;
+    e[l] = 0.0;
+  }
+  // ascending order (stable for ties: the lowest index first, as the selection sort of the full path)
+  std::vector<int> idx(m);
+  for (int i = 0; i < m; ++i) idx[i] = i;
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a] < d[b]; });
+  // M = E_S (m x nvec, row-major: row i contiguous over the selected vectors), G_N first
+  const int w = nvec;
+  std::vector<double> M((size_t)m * w, 0.0);
+  for (int c = 0; c < w; ++c) M[(size_t)idx[c] * w + c] = 1.0;
+  for (size_t t = rots.size(); t-- > 0;) {
+    const Rot& r = rots[t];
+    double* __restrict__ mi = &M[(size_t)r.i * w];
+    double* __restrict__ mi1 = &M[(size_t)(r.i + 1) * w];
+    const double c = r.c, sn = r.s;
+    for (int q = 0; q < w; ++q) {  // [M_i; M_i+1] <- G_t [M_i; M_i+1], G_t = [[c, s], [-s, c]]
+      const double a0 = mi[q], a1 = mi1[q];
+      mi[q] = c * a0 + sn * a1;
+      mi1[q] = c * a1 - sn * a0;
+    }
+  }
+  // X_S = Q M = P_{m-1} ( ... (P_1 M)): reflector i touches rows 0 .. i-1
+  std::vector<double> gq(w);
+  for (int i = 1; i < m; ++i) {
+    const double h = hv[i];
+    if (h == 0.0) continue;
+    for (int q = 0; q < w; ++q) gq[q] = 0.0;
+    for (int k = 0; k < i; ++k) {
+      const double uk = V(k, i);
+      const double* __restrict__ mk = &M[(size_t)k * w];
+      for (int q = 0; q < w; ++q) gq[q] += uk * mk[q];
+    }
+    for (int q = 0; q < w; ++q) gq[q] /= h;
+    for (int k = 0; k < i; ++k) {
+      const double uk = V(k, i);
+      double* __restrict__ mk = &M[(size_t)k * w];
+      for (int q = 0; q < w; ++q) mk[q] -= uk * gq[q];
+    }
+  }
+  evals.resize(m);
+  for (int i = 0; i < m; ++i) evals[i] = d[idx[i]];
+  for (int l = 0; l < m; ++l)  // row-major output, column c < nvec = eigenvector c
+    for (int c = 0; c < w; ++c) A[(size_t)l * m + c] = M[(size_t)l * w + c];
+#undef V
+}
+
 // A: m x m row-major symmetric (overwritten by the eigenvectors, row-major,
 // column c = eigenvector c).  evals ascending.
 // Compiled twice (the body is an always-inline template): an AVX2/FMA copy chosen at run time when the
 // host supports it, and a baseline x86-64 copy; the rotations and reflector updates vectorise 4-wide
 // (m = 170: 9.1 -> ~5 ms per restart on the build host).
+// nvec < m (the thick restart keeps only the nvec smallest Ritz pairs): the Householder vectors are kept
+// instead of accumulated, the QL rotations are applied in reverse order to the nvec selected unit vectors
+// (rows of an m x nvec block: 6 nvec instead of 6 m flops per rotation), and the reflectors then map that
+// block back (2 m^2 nvec instead of 4/3 m^3 flops); only columns c < nvec of the output are written.
 template <int kDummy>
 static inline __attribute__((always_inline)) void symeig_impl(int m, std::vector<double>& A,
-                                                               std::vector<double>& evals) {
+                                                               std::vector<double>& evals, int nvec) {
   std::vector<double> d(m), e(m);
   // column-major view (A is symmetric): the EISPACK loops then walk contiguous memory (the QL rotations
   // touch two contiguous columns instead of two strided ones); transposed to the row-major output at the end
@@ -62,11 +185,27 @@ static inline __attribute__((always_inline)) void symeig_impl(int m, std::vector
         f = d[j];
         V(j, i) = f;
         g = e[j] + V(j, j) * f;
-        for (int k = j + 1; k <= i - 1; ++k) {
-          g += V(k, j) * d[k];
-          e[k] += V(k, j) * f;
+        // column j below the diagonal: a dot (four partial sums, fixed order) and an axpy into e
+        const double* __restrict__ col = &V(0, j);
+        const double* __restrict__ dp = d.data();
+        double* __restrict__ ep = e.data();
+        double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+        int k = j + 1;
+        for (; k + 3 <= i - 1; k += 4) {
+          g0 += col[k] * dp[k];
+          g1 += col[k + 1] * dp[k + 1];
+          g2 += col[k + 2] * dp[k + 2];
+          g3 += col[k + 3] * dp[k + 3];
+          ep[k] += col[k] * f;
+          ep[k + 1] += col[k + 1] * f;
+          ep[k + 2] += col[k + 2] * f;
+          ep[k + 3] += col[k + 3] * f;
         }
-        e[j] = g;
+        for (; k <= i - 1; ++k) {
+          g0 += col[k] * dp[k];
+          ep[k] += col[k] * f;
+        }
+        e[j] = g + ((g0 + g1) + (g2 + g3));
       }
       f = 0.0;
       for (int j = 0; j < i; ++j) {
@@ -78,12 +217,20 @@ static inline __attribute__((always_inline)) void symeig_impl(int m, std::vector
       for (int j = 0; j < i; ++j) {
         f = d[j];
         g = e[j];
-        for (int k = j; k <= i - 1; ++k) V(k, j) -= (f * e[k] + g * d[k]);
+        double* __restrict__ col = &V(0, j);
+        const double* __restrict__ dp = d.data();
+        const double* __restrict__ ep = e.data();
+        for (int k = j; k <= i - 1; ++k) col[k] -= (f * ep[k] + g * dp[k]);
         d[j] = V(i - 1, j);
         V(i, j) = 0.0;
       }
     }
     d[i] = h;
+  }
+  const bool sel = nvec >= 0 && nvec < m;
+  if (sel) {
+    symeig_select<kDummy>(m, A, evals, nvec, d, e);
+    return;
   }
   for (int i = 0; i < m - 1; ++i) {
     V(m - 1, i) = V(i, i);
@@ -127,7 +274,7 @@ static inline __attribute__((always_inline)) void symeig_impl(int m, std::vector
         ++iter;
         double g = d[l];
         double p = (d[l + 1] - g) / (2.0 * e[l]);
-        double r = std::hypot(p, 1.0);
+        double r = hyp(p, 1.0);
         if (p < 0) r = -r;
         d[l] = e[l] / (p + r);
         d[l + 1] = e[l] * (p + r);
@@ -145,7 +292,7 @@ static inline __attribute__((always_inline)) void symeig_impl(int m, std::vector
           s2 = s;
           g = c * e[i];
           h = c * p;
-          r = std::hypot(p, e[i]);
+          r = hyp(p, e[i]);
           e[i + 1] = s * r;
           s = e[i] / r;
           c = p / r;
@@ -194,15 +341,19 @@ static inline __attribute__((always_inline)) void symeig_impl(int m, std::vector
 #undef V
 }
 
-__attribute__((target("avx2,fma"))) static void symeig_avx2(int m, std::vector<double>& A, std::vector<double>& ev) {
-  symeig_impl<1>(m, A, ev);
+__attribute__((target("avx2,fma"))) static void symeig_avx2(int m, std::vector<double>& A, std::vector<double>& ev,
+                                                            int nvec) {
+  symeig_impl<1>(m, A, ev, nvec);
 }
-static void symeig_base(int m, std::vector<double>& A, std::vector<double>& ev) { symeig_impl<0>(m, A, ev); }
+static void symeig_base(int m, std::vector<double>& A, std::vector<double>& ev, int nvec) {
+  symeig_impl<0>(m, A, ev, nvec);
+}
 
-void symeig(int m, std::vector<double>& A, std::vector<double>& evals) {
+void symeig(int m, std::vector<double>& A, std::vector<double>& evals, int nvec) {
   static const bool avx2 = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
-  if (avx2) symeig_avx2(m, A, evals);
-  else symeig_base(m, A, evals);
+  if (avx2) symeig_avx2(m, A, evals, nvec);
+  else symeig_base(m, A, evals, nvec);
 }
+void symeig(int m, std::vector<double>& A, std::vector<double>& evals) { symeig(m, A, evals, -1); }
 
 }  // namespace sfz

@@ -97,6 +97,7 @@ def _load():
         "sfairsc_last_error": (C.c_char_p, []),
         "sfairsc_version": (C.c_char_p, []),
         "sfairsc_host_symeig": (C.c_int, [C.c_int32, P, P, P]),
+        "sfairsc_host_symeig_sel": (C.c_int, [C.c_int32, P, P, P, C.c_int32]),
         "sfairsc_build_operator_dense": (C.c_int, [C.POINTER(CSR), P, C.c_int32, C.c_int32, C.c_int32,
                                                    C.POINTER(Opts), C.POINTER(P)]),
         "sfairsc_comm_unique_id": (C.c_int, [P]),
@@ -364,6 +365,16 @@ def host_symeig(A: np.ndarray):
     V = np.zeros((m, m))
     _check(_lib.sfairsc_host_symeig(m, A.ctypes.data, ev.ctypes.data, V.ctypes.data))
     return ev, V
+
+
+def host_symeig_sel(A: np.ndarray, nvec: int):
+    """The thick restart's selected-vector variant: all eigenvalues, the nvec smallest eigenvectors."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    m = A.shape[0]
+    ev = np.zeros(m)
+    V = np.zeros((m, m))
+    _check(_lib.sfairsc_host_symeig_sel(m, A.ctypes.data, ev.ctypes.data, V.ctypes.data, int(nvec)))
+    return ev, V[:, :nvec]
 
 
 # --- multi-GPU (row-partitioned, SURVEY §8(e)) ---------------------------------------

@@ -83,3 +83,54 @@ def test_host_symeig_arrowhead_degenerate():
     ev, V = lib.host_symeig(T)
     assert np.allclose(ev, np.linalg.eigvalsh(T), atol=1e-13 * 10)
     assert np.allclose(T @ V, V * ev, atol=1e-12)
+
+
+@pytest.mark.parametrize("m,nvec,seed", [(1, 1, 0), (2, 1, 1), (7, 3, 2), (40, 0, 3), (40, 17, 4), (130, 60, 5),
+                                         (170, 81, 6), (170, 170, 7)])
+def test_host_symeig_sel_vs_lapack(m, nvec, seed):
+    """The thick restart's selected-vector Rayleigh-Ritz (Householder vectors kept, QL rotations applied in
+    reverse to the selected unit vectors, reflectors applied after): all eigenvalues and the nvec smallest
+    eigenpairs against LAPACK (numpy eigh), and the same vectors as the full solver up to sign."""
+    from paper_2210_16435_b200 import lib
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((m, m))
+    A = A + A.T
+    ev, V = lib.host_symeig_sel(A, nvec)
+    ref, U = np.linalg.eigh(A)
+    scale = max(1.0, np.abs(ref).max())
+    assert np.allclose(ev, ref, atol=1e-13 * scale * m)
+    assert V.shape == (m, nvec)
+    assert np.allclose(V.T @ V, np.eye(nvec), atol=1e-13 * m)
+    assert np.allclose(A @ V, V * ev[:nvec], atol=1e-12 * scale * m)
+    evf, Vf = lib.host_symeig(A)
+    assert np.array_equal(ev, evf)  # the same QL recurrences: identical eigenvalues
+    sgn = np.sign(np.sum(V * Vf[:, :nvec], axis=0))
+    assert np.allclose(V * sgn, Vf[:, :nvec], atol=1e-12 * m)
+
+
+def test_host_symeig_sel_thick_restart_structure():
+    """Thick-restart shape (diagonal Ritz block + arrow + tridiagonal tail) with repeated and tightly
+    clustered eigenvalues (config 4's lambda_2..lambda_50 lie within 2.4e-4 of each other), and a
+    zero-scale Householder step (an exact zero row below the diagonal)."""
+    from paper_2210_16435_b200 import lib
+    rng = np.random.default_rng(11)
+    p, m = 80, 170
+    T = np.zeros((m, m))
+    T[np.arange(p), np.arange(p)] = 0.6515 + 2.4e-4 * np.sort(rng.random(p))
+    T[:3, :3] = np.diag([0.0, 0.0, 0.0])
+    T[:p, p] = T[p, :p] = 1e-6 * rng.standard_normal(p)
+    for i in range(p, m):
+        T[i, i] = rng.uniform(0.6, 1.4)
+        if i + 1 < m:
+            T[i, i + 1] = T[i + 1, i] = rng.uniform(0, 0.2)
+    T[m - 1, m - 2] = T[m - 2, m - 1] = 0.0
+    ev, V = lib.host_symeig_sel(T, p)
+    assert np.allclose(ev, np.linalg.eigvalsh(T), atol=1e-14)
+    assert np.allclose(V.T @ V, np.eye(p), atol=1e-13)
+    assert np.allclose(T @ V, V * ev[:p], atol=1e-14)
+
+
+def test_host_symeig_sel_bad_args():
+    from paper_2210_16435_b200 import lib
+    with pytest.raises(Exception):
+        lib.host_symeig_sel(np.eye(4), 5)

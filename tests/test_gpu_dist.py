@@ -114,3 +114,28 @@ def test_nccl_one_rank(gpu_lib):
     assert st["converged"] == 1 and st["max_resid_rel"] <= 1e-9
     assert np.all(np.abs(ev - dense.evals[:5]) <= 1e-8 * np.abs(dense.evals[:5]) + 1e-12 * st["sigma"])
     assert subspace_sin(Xt.T, dense.X) <= 1e-6
+
+
+def test_nccl_failed_rank_agreement(gpu_lib):
+    """Advisor r1: a rank whose own input checks fail takes part in the build's agreement all-reduce
+    (dist_agree) before returning, so the other ranks fail with it instead of blocking in the first
+    all-gather.  With one rank: the local status comes back (not a hang, not E_NCCL), the message is this
+    rank's, and the communicator is still usable for a correct build afterwards (the collective matched)."""
+    import torch
+    torch.cuda.set_device(0)
+    g, cfg = baseline_config(1)
+    comm = gpu_lib.Comm(gpu_lib.comm_unique_id(), 0, 1, 0)
+    cuts = gpu_lib.partition_rows(g.row_ptr, 1)
+    rp, ci, vv, gr = gpu_lib.row_block(g.row_ptr, g.col, g.val, g.groups, int(cuts[0]), int(cuts[1]))
+    bad = np.array(gr, copy=True)
+    bad[3] = g.h + 7  # group id out of [0, h): a per-rank check before any collective
+    with pytest.raises(gpu_lib.SfairscError) as ei:
+        gpu_lib.sfairsc_build_operator(rp, ci, vv, bad, cfg["k_eig"], cfg["normalized"], h=g.h, comm=comm,
+                                       n_global=g.n, row_offset=int(cuts[0]))
+    assert ei.value.status == 1 and "group id" in str(ei.value)
+    ctx = gpu_lib.sfairsc_build_operator(rp, ci, vv, gr, cfg["k_eig"], cfg["normalized"], h=g.h, comm=comm,
+                                         n_global=g.n, row_offset=int(cuts[0]))
+    ev, _, st = gpu_lib.sfairsc_eigs(ctx, cfg["k_eig"], cfg["tol"])
+    ctx.close()
+    comm.close()
+    assert st["converged"] == 1
