@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kThreads) k_ritz_rb(const double* __restrict__
 
 // ---------------------------------------------------------------------------
 // Ritz GEMM v2 (default): Vout = V Y on the fp64 tensor cores (DMMA
-// m8n8k4), CTA tile 128 rows x GN columns (GN = 64 / 96 / 128: the smallest
+// m8n8k4), CTA tile 128 rows x GN columns (GN = 64 / 80 / 96 / 112 / 128: the smallest
 // that covers p, so V is streamed once for p <= 128 with little padding), 8 warps
 // as 4 (rows) x 2 (cols), each 32 x GN/2 = 4 x GN/16 DMMA tiles.  The V
 // tile (16 columns x 128 rows) arrives by cp.async into a double-buffered
@@ -268,7 +268,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_b
                : "memory");
 }
 
-template <int GN>  // CTA tile columns: 64, 96 or 128 (the smallest that covers p, else 128)
+template <int GN>  // CTA tile columns: 64, 80, 96, 112 or 128 (the smallest that covers p, else 128)
 __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __restrict__ V, long long ld, int n, int m,
                                                             const double* __restrict__ Y, int p,
                                                             double* __restrict__ Vout) {
@@ -449,13 +449,17 @@ void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_ritz_dmma2<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_ritz_dmma2<80>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(k_ritz_dmma2<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_ritz_dmma2<112>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(k_ritz_dmma2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
     const long long rows = (n + kGM - 1) / kGM;
     if (p <= 64) k_ritz_dmma2<64><<<rows, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
+    else if (p <= 80) k_ritz_dmma2<80><<<rows, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
     else if (p <= 96) k_ritz_dmma2<96><<<rows, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
+    else if (p <= 112) k_ritz_dmma2<112><<<rows, kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
     else k_ritz_dmma2<128><<<rows * ((p + kGN - 1) / kGN), kThreads, smem, st>>>(V, ld, n, m, Y, p, Vout);
     return;
   }

@@ -1100,6 +1100,7 @@ struct Lagged {
   double bd_tol = 0.0;
   bool paired = false;  // two Lanczos steps per basis sweep (reorth 3)
   bool pend = false;    // host mirror of LZ_PEND >= 0: the last pair's odd column awaits its rewrite
+  bool spmv_ready = false;  // the next step's SpMV (t = L p~) already ran (the restart prefetch)
 
   LzDev dev(int j) const {
     LzDev d{};
@@ -1216,7 +1217,9 @@ struct Lagged {
 
   // one Lanczos step at column j (A5-A9)
   sfairsc_status step(int j) {
-    {
+    if (spmv_ready) {
+      spmv_ready = false;  // t = L p~ of the continuation vector ran beside the host Rayleigh-Ritz
+    } else {
       ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
       ctx_spmv(c, c->vp, c->vt, c->vq_lz);  // epilogue: B^T t and p~^T t (bs_t[kHB]); vq_lz = s o p~ (unit)
     }
@@ -1395,6 +1398,48 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
     for (int l = 0; l < m; ++l) s2 += sh[l] * sh[l];
     double mu = std::sqrt(std::max(om - s2, 0.0));
     if (!(mu > 0.0)) mu = 1.0;
+    // ---- restart prefetch, enqueued before the host Rayleigh-Ritz below and run beside it: the continuation
+    // vector v_m = (v~ - V s)/mu depends on s only, not on the Ritz vectors, so its pass over the basis
+    // (x = v~ - V s in the stored basis, |x|^2, B^T x), its normalisation (v~, p~ of the next cycle's first step)
+    // and that step's SpMV run on the GPU while the host solves the RR problem; the Ritz GEMM then forms only
+    // the kept columns, and the first step's sweep writes column keep (v~/|v~|) without reading it.  Wasted
+    // (one pass) at the final sync.
+    {
+      std::vector<double> x(m + 1, 0.0);
+      for (int l = 0; l < m; ++l) x[l] = -sh[l] / mu;
+      x[m] = 1.0 / mu;
+      to_stored(x.data());
+      double* hc = c->hp + 3072;  // pinned scratch (m <= 192)
+      for (int l = 0; l < m; ++l) hc[l] = -x[l] * mu;  // x = v~ - V coef = mu v_m
+      double* dcoef = c->Ydev + (size_t)(m + 1) * m;   // the last m + 1 entries: beyond every Ritz coefficient block
+      CU(cudaMemcpyAsync(dcoef, hc, sizeof(double) * m, cudaMemcpyHostToDevice, c->st));
+      {
+        ProfScope ps(c, K_UPDDOT, (m + 2) * c->vb() + c->sgb());
+        SweepArgs a{};
+        a.V = c->V;
+        a.ld = c->ldv;
+        a.J = m;
+        a.xin = c->vr;
+        a.xout = c->vy;
+        a.coef = dcoef;
+        a.bsum_t = c->bs_t;
+        a.bsum_w = c->bs_v;
+        a.sigma = c->sigma;
+        a.partials = c->partials;
+        a.counter = c->counters + 2;
+        a.norm_bsum = c->nb;
+        launch_sweep(2, c->g(), c->pd(), a, c->sgrid, c->st);  // update + |x|^2 + B^T x
+        if (c->h > kHB)
+          for (int gb = kHB; gb < c->h; gb += kHB)
+            launch_gsum(c->g(), c->vy, gb, c->partials, c->counters + 3, c->nb + 1, c->st);
+      }
+      L.norm(c->vy, nullptr, 0, -1, kMaxJ);
+      {
+        ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
+        ctx_spmv(c, c->vp, c->vt, c->vq_lz);
+      }
+      CHECK_LAUNCH();
+    }
     std::vector<double> bt(m), A((size_t)m * m);
     for (int l = 0; l < m; ++l) bt[l] = Hh[(size_t)l * ldH + m];
     for (int r = 0; r < m; ++r)
@@ -1434,24 +1479,20 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
       CHECK_LAUNCH();
       break;
     }
-    // ---- thick restart: [V_m Y_keep, v_m], v_m = (v~ - V_m s)/mu as one GEMM with v~ in column m ----
-    CU(cudaMemcpyAsync(c->V + (long long)m * c->ldv, c->vr, sizeof(double) * c->ldv, cudaMemcpyDeviceToDevice,
-                       c->st));
-    const int me = m + 1, pe = keep + 1;
-    std::vector<double> Yc((size_t)me * pe, 0.0);
-    for (int cc = 0; cc < keep; ++cc)
-      for (int l = 0; l < m; ++l) Yc[(size_t)cc * me + l] = Y[(size_t)l * m + cc];
-    for (int l = 0; l < m; ++l) Yc[(size_t)keep * me + l] = -sh[l] / mu;
-    Yc[(size_t)keep * me + m] = 1.0 / mu;
-    for (int cc = 0; cc <= keep; ++cc) to_stored(Yc.data() + (size_t)cc * me);
+    // ---- thick restart: V_m Y_keep (the continuation vector v_m is already normalised into v~, p~: prefetch) ----
+    std::vector<double> Yc((size_t)m * keep, 0.0);
+    for (int cc = 0; cc < keep; ++cc) {
+      for (int l = 0; l < m; ++l) Yc[(size_t)cc * m + l] = Y[(size_t)l * m + cc];
+      to_stored(Yc.data() + (size_t)cc * m);
+    }
     CU(cudaMemcpyAsync(c->Ydev, Yc.data(), sizeof(double) * Yc.size(), cudaMemcpyHostToDevice, c->st));
     {
-      ProfScope ps(c, K_RITZ, (double)(me + pe) * c->vb());
-      launch_ritz(c->V, c->ldv, n, me, c->Ydev, pe, c->Vb, c->st);
+      ProfScope ps(c, K_RITZ, (double)(m + keep) * c->vb());
+      launch_ritz(c->V, c->ldv, n, m, c->Ydev, keep, c->Vb, c->st);
     }
     CHECK_LAUNCH();
     std::swap(c->V, c->Vb);
-    // state at j = keep: v~ = v_m exactly (s = 0), coupling row b~ = (b Y)_i for the kept vectors
+    // state at j = keep: v~ = v_m (s = 0), coupling row b~ = (b Y)_i for the kept vectors
     std::fill(Hh.begin(), Hh.end(), 0.0);
     for (int i = 0; i < keep; ++i) {
       Hh[(size_t)i * ldH + i] = theta[i];
@@ -1459,26 +1500,7 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
     }
     CU(cudaMemcpyAsync(c->Hdev, Hh.data(), sizeof(double) * ldH * ldH, cudaMemcpyHostToDevice, c->st));
     CU(cudaMemsetAsync(c->sdev, 0, sizeof(double) * (m + 2), c->st));
-    {
-      // v~ <- column keep; p~ = P v~; B^T v~; omega, |p~|^2 via the normalise kernel (|v|^2 and B^T v first)
-      SweepArgs a{};
-      a.V = c->V;
-      a.ld = c->ldv;
-      a.J = 0;
-      a.xin = c->V + (long long)keep * c->ldv;
-      a.xout = c->vy;
-      a.bsum_t = c->bs_t;
-      a.bsum_w = c->bs_v;
-      a.partials = c->partials;
-      a.counter = c->counters + 2;
-      a.norm_bsum = c->nb;
-      launch_sweep(2, c->g(), c->pd(), a, c->sgrid, c->st);  // J = 0: copy + |v|^2 + B^T v
-      if (c->h > kHB)
-        for (int gb = kHB; gb < c->h; gb += kHB)
-          launch_gsum(c->g(), c->vy, gb, c->partials, c->counters + 3, c->nb + 1, c->st);
-      L.norm(c->vy, nullptr, 0, -1, kMaxJ);
-    }
-    CHECK_LAUNCH();
+    L.spmv_ready = true;
     TRY(L.clear_pair_state());
     j = keep;
     jsync = keep;
