@@ -59,11 +59,57 @@ __device__ __forceinline__ void ticket_finalize(const double* partials, unsigned
   if (!s_last) return;
   __threadfence();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int q = w; q < nout; q += NT / 32) {
-    double acc = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(partials + (size_t)b * NV + q);
-    acc = warp_sum(acc);
-    if (lane == 0) out[q] = acc;
+  if constexpr (NV > 20) {  // wide rows (block Lanczos): a warp per output, four rows in flight per lane
+    for (int q = w; q < nout; q += NT / 32) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int b = lane;
+      for (; b + 96 < (int)gridDim.x; b += 128) {
+        a0 += __ldcg(partials + (size_t)b * NV + q);
+        a1 += __ldcg(partials + (size_t)(b + 32) * NV + q);
+        a2 += __ldcg(partials + (size_t)(b + 64) * NV + q);
+        a3 += __ldcg(partials + (size_t)(b + 96) * NV + q);
+      }
+      for (; b < (int)gridDim.x; b += 32) a0 += __ldcg(partials + (size_t)b * NV + q);
+      const double acc = warp_sum((a0 + a1) + (a2 + a3));
+      if (lane == 0) out[q] = acc;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+    return;
+  }
+  // thread t sums the partial rows t, t + NT, ... (all NV entries of a row are independent loads, two rows in
+  // flight: a few L2 round trips instead of one per 32 rows), then warp shuffles and the warps in order
+  __shared__ double wsum[NT / 32][NV];
+  double acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  const int G = (int)gridDim.x;
+  int b = threadIdx.x;
+  for (; b + NT < G; b += 2 * NT) {
+    double x0[NV], x1[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      x0[q] = q < nout ? __ldcg(partials + (size_t)b * NV + q) : 0.0;
+      x1[q] = q < nout ? __ldcg(partials + (size_t)(b + NT) * NV + q) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] += x0[q] + x1[q];
+  }
+  if (b < G) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+      if (q < nout) acc[q] += __ldcg(partials + (size_t)b * NV + q);
+  }
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const double x = warp_sum(acc[q]);
+    if (lane == 0) wsum[w][q] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < nout) {
+    double a = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < NT / 32; ++ww) a += wsum[ww][threadIdx.x];
+    out[threadIdx.x] = a;
   }
   if (threadIdx.x == 0) *counter = 0u;
 }

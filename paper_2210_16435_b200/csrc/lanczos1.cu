@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_norm(GraphDev g, ProjDesc pd, c
 // 1/mu_j for the pair's sweep.
 // ---------------------------------------------------------------------------
 template <bool NORM>
-__global__ void __launch_bounds__(kThreads) k_lz_three(GraphDev g, ProjDesc pd, const double* __restrict__ t,
+__global__ void __launch_bounds__(kThreads, 4) k_lz_three(GraphDev g, ProjDesc pd, const double* __restrict__ t,
                                                        const double* __restrict__ vt, const double* __restrict__ vprev,
                                                        LzDev d, int j, double* __restrict__ u_out, double* dots,
                                                        double* cA, double* tr, double* partials, unsigned* counter,
@@ -627,6 +627,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_three(GraphDev g, ProjDesc pd, 
   double acc[1 + kHB];
 #pragma unroll
   for (int q = 0; q < 1 + kHB; ++q) acc[q] = 0.0;
+  // (the 17 accumulators keep this kernel at 4 CTAs per SM: one wave of 4 x #SMs CTAs)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
     const int gg = g.grp[i];
     const double y = NORM ? fma(-g.s[i], gam[gg], t[i]) : t[i] - gam[gg];
@@ -1149,8 +1150,8 @@ struct Lagged {
     {
       ProfScope ps(c, K_NORMALIZE, 4 * c->vb() + c->sgb());
       bump_launch();
-      // 8 CTAs per SM (partials: the SpMV's buffer, free again once its ticket is done)
-      const int G = std::max(1, std::min((c->n + kThreads - 1) / kThreads, c->num_sms * 8));
+      // one wave of 4 CTAs per SM (partials: the SpMV's buffer, free again once its ticket is done)
+      const int G = std::max(1, std::min((c->n + kThreads - 1) / kThreads, c->num_sms * 4));
       launch_lz_three(g, c->pd(), c->vt, c->vr, c->V + (long long)(j - 1) * c->ldv, dev(j), j, c->vy, c->dd, cA(),
                       trc(), c->partials, c->counters + 7, c->nb, G, true, c->st);
     }
