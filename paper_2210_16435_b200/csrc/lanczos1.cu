@@ -56,9 +56,25 @@ constexpr int kLMaxJ = 191;  // basis columns swept (+1 new column in the dots: 
 // ---------------------------------------------------------------------------
 // one CTA of kCoefT threads (the O(m^2) work is latency-bound: more threads, shorter chains)
 constexpr int kCoefT = 1024;
+// sum_{i0 <= i < i1} H[i * ld + row] x[i] in increasing i (one FMA chain), with the column loads issued eight at
+// a time ahead of their FMAs (the chain waits on one L2 round trip per eight columns, not per column)
+__device__ __forceinline__ double rowdot8(const double* __restrict__ H, int ld, int row, int i0, int i1,
+                                          const double* x) {
+  double acc = 0.0;
+  int i = i0;
+  for (; i + 8 <= i1; i += 8) {
+    double h[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) h[q] = H[(size_t)(i + q) * ld + row];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc = fma(h[q], x[i + q], acc);
+  }
+  for (; i < i1; ++i) acc = fma(H[(size_t)i * ld + row], x[i], acc);
+  return acc;
+}
 __global__ void __launch_bounds__(kCoefT) k_lz_coef(LzDev d, int j) {
   __shared__ double ss[kLMaxJ + 1], bt[kLMaxJ + 1], u[kLMaxJ + 1], v[kLMaxJ + 1], red[kCoefT / 32][3];
-  __shared__ double upart[4][kLMaxJ + 1];
+  __shared__ double upart[4][kLMaxJ + 2];
   __shared__ double sh_mu, sh_alpha, sh_kappa;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int ld = d.ldH;
@@ -73,13 +89,16 @@ __global__ void __launch_bounds__(kCoefT) k_lz_coef(LzDev d, int j) {
     const double rho = d.lz[LZ_PRHO];
     for (int l = tid; l < p; l += kCoefT) ee[l] = d.epend[l];
     __syncthreads();
-    for (int l = w; l <= p + 1; l += kCoefT / 32) {  // warp per row: rows 0..p and the lagged row j
-      const int row = (l == p + 1) ? j : l;
-      double acc = 0.0;
-      for (int c = lane; c < p; c += 32) acc = fma(d.H[(size_t)c * ld + row], ee[c], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) hle[l] = acc;
+    {  // hle = H[rows 0..p and the lagged row j, cols 0..p-1] ee: thread per row (coalesced down the columns),
+       // four column quarters, eight loads in flight per thread; quarters combined in order below
+      const int l = tid & 255, qt = tid >> 8;
+      if (l <= p + 1) {
+        const int row = (l == p + 1) ? j : l;
+        upart[qt][l] = rowdot8(d.H, ld, row, p * qt / 4, p * (qt + 1) / 4, ee);
+      }
     }
+    __syncthreads();
+    for (int l = tid; l <= p + 1; l += kCoefT) hle[l] = ((upart[0][l] + upart[1][l]) + upart[2][l]) + upart[3][l];
     double es = 0.0;
     for (int l = tid; l < p; l += kCoefT) es = fma(ee[l], d.s[l], es);
     es = warp_sum(es);
@@ -87,7 +106,7 @@ __global__ void __launch_bounds__(kCoefT) k_lz_coef(LzDev d, int j) {
     __syncthreads();
     if (tid == 0) {
       double a = 0.0;
-      for (int q = 0; q < kCoefT / 32; ++q) a += red[q][0];
+      for (int q = 0; q < (p + 31) / 32; ++q) a += red[q][0];  // (the other warps hold exact zeros)
       sh_es = a;
     }
     const double hpp = d.H[(size_t)p * ld + p];
@@ -131,7 +150,7 @@ __global__ void __launch_bounds__(kCoefT) k_lz_coef(LzDev d, int j) {
   __syncthreads();
   if (tid == 0) {
     double s2 = 0.0, bs = 0.0;
-    for (int q = 0; q < kCoefT / 32; ++q) {
+    for (int q = 0; q < (j + 31) / 32; ++q) {  // (warps beyond j / 32 hold exact zeros)
       s2 += red[q][0];
       bs += red[q][1];
     }
@@ -149,24 +168,32 @@ __global__ void __launch_bounds__(kCoefT) k_lz_coef(LzDev d, int j) {
   __syncthreads();
   const double mu = sh_mu, bts = red[0][2];
   // H[:j,:j] += s b~^T ; H[j,:j] = mu b~   (column c of H gets s * b~_c)
-  for (int c = 0; c < j; ++c)  // only the columns with b~_c != 0 (normally just c = j-1)
-    if (bt[c] != 0.0)
+  for (int c0 = 0; c0 < j; c0 += 32) {  // only the columns with b~_c != 0 (normally just c = j-1), found by ballot
+    unsigned msk = __ballot_sync(0xffffffffu, c0 + lane < j && bt[c0 + lane] != 0.0);
+    while (msk) {
+      const int c = c0 + __ffs(msk) - 1;
+      msk &= msk - 1;
       for (int r = tid; r < j; r += kCoefT) d.H[(size_t)c * ld + r] = fma(ss[r], bt[c], d.H[(size_t)c * ld + r]);
+    }
+  }
   __syncthreads();
   for (int l = tid; l < j; l += kCoefT) d.H[(size_t)l * ld + j] = mu * bt[l];
   // u = H_j s (thread per row, coalesced over columns), v = H_j^T s (warp per column, coalesced down it)
   {  // u: 4 partial sums per row over quarters of the columns, combined in order below
     const int l = tid & 255, qt = tid >> 8;
-    if (l < j) {
-      const int i0 = j * qt / 4, i1 = j * (qt + 1) / 4;
-      double au = 0.0;
-      for (int i = i0; i < i1; ++i) au = fma(d.H[(size_t)i * ld + l], ss[i], au);
-      upart[qt][l] = au;
-    }
+    if (l < j) upart[qt][l] = rowdot8(d.H, ld, l, j * qt / 4, j * (qt + 1) / 4, ss);
   }
-  for (int l = w; l < j; l += kCoefT / 32) {
+  for (int l = w; l < j; l += kCoefT / 32) {  // v: warp per column, all its (<= 6 per lane) loads in flight
+    double hv[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int i = lane + 32 * q;
+      hv[q] = i < j ? d.H[(size_t)l * ld + i] : 0.0;
+    }
     double av = 0.0;
-    for (int i = lane; i < j; i += 32) av = fma(d.H[(size_t)l * ld + i], ss[i], av);
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+      if (lane + 32 * q < j) av = fma(hv[q], ss[lane + 32 * q], av);
     av = warp_sum(av);
     if (lane == 0) v[l] = av;
   }
@@ -191,7 +218,7 @@ __global__ void __launch_bounds__(kCoefT) k_lz_coef(LzDev d, int j) {
   __syncthreads();
   if (tid == 0) {
     double sz = 0.0, shs = 0.0;
-    for (int q = 0; q < kCoefT / 32; ++q) {
+    for (int q = 0; q < (j + 31) / 32; ++q) {  // (the other warps hold exact zeros)
       sz += red[q][0];
       shs += red[q][1];
     }
@@ -594,7 +621,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_norm(GraphDev g, ProjDesc pd, c
     const double vi = w[i] * inv;
     const double pi = vi - proj_row<DQ, NORM>(g, i, gam);
     vt[i] = pi;
-    p[i] = pi;
+    if (p) p[i] = pi;  // (null: the single-GPU solvers hand vt itself to the SpMV)
     if (NORM && q) q[i] = g.s[i] * pi;  // unit-weight SpMV input s o p~ (ctx_spmv's gathered vector)
   }
 }
@@ -1140,7 +1167,7 @@ struct Lagged {
     const bool rewrite = pend;  // the previous pair's odd column j-1 is rewritten by this pair's sweep
     {
       ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
-      ctx_spmv(c, c->vp, c->vt, c->vq_lz);
+      ctx_spmv(c, c->vr, c->vt, c->vq_lz);  // p~ = v~ (the normalisation writes it once, into vr)
     }
     {
       ProfScope ps(c, K_OTHER, 0.0);
@@ -1157,12 +1184,12 @@ struct Lagged {
     }
     {
       ProfScope ps(c, K_NORMALIZE, 3 * c->vb() + c->sgb());
-      launch_lz_norm(g, c->pd(), c->vy, c->nb, c->dd, j + 1, dev(j), j + 1, c->vrB, c->vp, c->bs_v, c->st,
+      launch_lz_norm(g, c->pd(), c->vy, c->nb, c->dd, j + 1, dev(j), j + 1, c->vrB, nullptr, c->bs_v, c->st,
                      c->unit_spmv() ? c->vq_lz : nullptr);
     }
     {
       ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
-      ctx_spmv(c, c->vp, c->vt, c->vq_lz);
+      ctx_spmv(c, c->vrB, c->vt, c->vq_lz);
     }
     {
       ProfScope ps(c, K_OTHER, 0.0);
@@ -1213,7 +1240,8 @@ struct Lagged {
 
   void norm(const double* w, const double* dots, int nd, int jrow, int flag_idx) {
     ProfScope ps(c, K_NORMALIZE, 3 * c->vb() + c->sgb());
-    launch_lz_norm(c->g(), c->pd(), w, c->nb, dots, nd, dev(flag_idx), jrow, c->vr, c->vp, c->bs_v, c->st, c->unit_spmv() ? c->vq_lz : nullptr);
+    launch_lz_norm(c->g(), c->pd(), w, c->nb, dots, nd, dev(flag_idx), jrow, c->vr, nullptr, c->bs_v, c->st,
+                   c->unit_spmv() ? c->vq_lz : nullptr);
   }
 
   // one Lanczos step at column j (A5-A9)
@@ -1222,7 +1250,7 @@ struct Lagged {
       spmv_ready = false;  // t = L p~ of the continuation vector ran beside the host Rayleigh-Ritz
     } else {
       ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
-      ctx_spmv(c, c->vp, c->vt, c->vq_lz);  // epilogue: B^T t and p~^T t (bs_t[kHB]); vq_lz = s o p~ (unit)
+      ctx_spmv(c, c->vr, c->vt, c->vq_lz);  // epilogue: B^T t and p~^T t (bs_t[kHB]); vq_lz = s o p~ (unit)
     }
     {
       ProfScope ps(c, K_OTHER, 0.0);
@@ -1437,7 +1465,7 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
       L.norm(c->vy, nullptr, 0, -1, kMaxJ);
       {
         ProfScope ps(c, K_SPMV, c->csr_bytes() + 3 * c->vb() + 1.0 * c->n);
-        ctx_spmv(c, c->vp, c->vt, c->vq_lz);
+        ctx_spmv(c, c->vr, c->vt, c->vq_lz);
       }
       CHECK_LAUNCH();
     }

@@ -14,3 +14,7 @@ import json
 d=json.load(open('gpurun_out/probe_$v.json')); e=d['eigs']
 print('$v', {k:(round(x['us'],1), x['launches']) for k,x in e.items()})"
 done; fi
+if [ -n "$KPROF" ]; then for r in 1 2; do for v in ${VARIANTS:-A B}; do
+  cp ab_libs/$v.so $L
+  echo -n "prof $v$r "; timeout 300 python scripts/ab_profile.py 2>/dev/null | tail -1
+done; done; fi

@@ -88,9 +88,10 @@ def test_host_symeig_arrowhead_degenerate():
 @pytest.mark.parametrize("m,nvec,seed", [(1, 1, 0), (2, 1, 1), (7, 3, 2), (40, 0, 3), (40, 17, 4), (130, 60, 5),
                                          (170, 81, 6), (170, 170, 7)])
 def test_host_symeig_sel_vs_lapack(m, nvec, seed):
-    """The thick restart's selected-vector Rayleigh-Ritz (Householder vectors kept, QL rotations applied in
-    reverse to the selected unit vectors, reflectors applied after): all eigenvalues and the nvec smallest
-    eigenpairs against LAPACK (numpy eigh), and the same vectors as the full solver up to sign."""
+    """The thick restart's selected-vector Rayleigh-Ritz (row-contiguous Householder reduction with the
+    reflectors kept, QL rotations applied in reverse to the selected unit vectors, reflectors applied after):
+    all eigenvalues and the nvec smallest eigenpairs against LAPACK (numpy eigh), and the same pairs as the
+    full solver (eigenvalues to rounding, vectors up to sign where the eigenvalues are simple)."""
     from paper_2210_16435_b200 import lib
     rng = np.random.default_rng(seed)
     A = rng.standard_normal((m, m))
@@ -102,10 +103,12 @@ def test_host_symeig_sel_vs_lapack(m, nvec, seed):
     assert V.shape == (m, nvec)
     assert np.allclose(V.T @ V, np.eye(nvec), atol=1e-13 * m)
     assert np.allclose(A @ V, V * ev[:nvec], atol=1e-12 * scale * m)
-    evf, Vf = lib.host_symeig(A)
-    assert np.array_equal(ev, evf)  # the same QL recurrences: identical eigenvalues
+    evf, Vf = lib.host_symeig(A)  # the full solver (EISPACK tred2/tql2): same pairs to rounding
+    assert np.allclose(ev, evf, atol=1e-13 * scale * m)
     sgn = np.sign(np.sum(V * Vf[:, :nvec], axis=0))
-    assert np.allclose(V * sgn, Vf[:, :nvec], atol=1e-12 * m)
+    gaps = np.diff(ref)
+    if nvec and (nvec == m or gaps[:nvec].min() > 1e-3):  # vectors are unique up to sign for simple eigenvalues
+        assert np.allclose(V * sgn, Vf[:, :nvec], atol=1e-10 * m)
 
 
 def test_host_symeig_sel_thick_restart_structure():
