@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(kCoefT) k_lz_pairpost(LzDev d, int J, const do
   __syncthreads();
   if (tid == 0) {
     double s0 = 0.0, s1 = 0.0;
-    for (int k = 0; k < kCoefT / 32; ++k) {
+    for (int k = 0; k < (q + 31) / 32; ++k) {  // (warps beyond q / 32 hold exact zeros)
       s0 += r[0][k];
       s1 += r[1][k];
     }
@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(kCoefT) k_lz_pairpost(LzDev d, int J, const do
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
-    for (int k = 0; k < kCoefT / 32; ++k) s += r[0][k];
+    for (int k = 0; k < (J + 2 + 31) / 32; ++k) s += r[0][k];  // (warps beyond (J + 2) / 32 hold exact zeros)
     const double nv = nb[1 + kHB];  // |v'|^2
     const double rho = sqrt(fmax(nv - s, 0.0));
     // a breakdown in the pair (flags of steps J, J+1 so far) leaves v' to the restart sync's roll-back: no basis
