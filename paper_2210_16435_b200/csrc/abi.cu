@@ -251,6 +251,7 @@ void sfz::ctx_spmv(sfairsc_ctx* c, const double* p, double* t, const double* q_p
 
 // max_i ||L^sigma x_i - theta_i x_i|| / sigma over the k columns of X (A11), k fresh applies
 sfairsc_status sfz::true_residuals(sfairsc_ctx* c, const double* theta, int k, double* max_out) {
+  NvtxRange nv("sfairsc.true_residuals");
   std::vector<double> res(k);
   if (pair_ok(c) && !c->pairY) CU(cudaMalloc(&c->pairY, sizeof(double) * c->ldv));
   for (int i = 0; i < k; ++i) {
@@ -295,6 +296,7 @@ static sfairsc_status build_impl(const sfairsc_csr* W, const int32_t* groups, in
 extern "C" sfairsc_status sfairsc_build_operator_ex(const sfairsc_csr* W, const int32_t* groups, int32_t h,
                                                     int32_t k, int32_t normalized, const sfairsc_opts* opts_in,
                                                     sfairsc_ctx** out) {
+  NvtxRange nv("sfairsc.build");
   bool reached_dist = false;
   const sfairsc_status st = build_impl(W, groups, h, k, normalized, opts_in, out, &reached_dist);
   if (st != SFAIRSC_OK && !reached_dist && opts_in && opts_in->comm) {
@@ -1028,6 +1030,7 @@ extern "C" sfairsc_status sfairsc_apply(sfairsc_ctx* c, const double* x, double*
 }
 extern "C" sfairsc_status sfairsc_apply_ex(sfairsc_ctx* c, const double* x, double* y, int32_t nvec,
                                            int32_t memspace, int32_t flags) {
+  NvtxRange nv("sfairsc.apply");
   if (flags & ~SFAIRSC_APPLY_SINGLE) return fail(SFAIRSC_E_INVALID_ARG, "unknown apply flags");
   return vec_io(c, x, y, nvec, memspace, apply_dev, (flags & SFAIRSC_APPLY_SINGLE) == 0);
 }
@@ -1301,6 +1304,7 @@ static sfairsc_status filter_check(sfairsc_ctx* c, int k, std::vector<double>* t
 
 extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, double* evals_out, double* evecs_out,
                                        int32_t evecs_memspace, sfairsc_stats* stats) {
+  NvtxRange nv("sfairsc.eigs");
   const double t0 = now_s();
   if (c && c->debug) fprintf(stderr, "[sfairsc] eigs enter k=%d tol=%g\n", k, tol);
   if (!c || !evals_out) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
@@ -1562,6 +1566,7 @@ extern "C" sfairsc_status sfairsc_eigs(sfairsc_ctx* c, int32_t k, double tol, do
 
 extern "C" sfairsc_status sfairsc_embed_kmeans(sfairsc_ctx* c, uint64_t seed, int32_t* labels_out, int32_t memspace,
                                                double* objective_out) {
+  NvtxRange nv("sfairsc.kmeans");
   if (!c || !labels_out) return fail(SFAIRSC_E_INVALID_ARG, "null argument");
   if (!c->have_eigs) return fail(SFAIRSC_E_STATE, "sfairsc_eigs must succeed before sfairsc_embed_kmeans");
   if (memspace != SFAIRSC_MEM_HOST && memspace != SFAIRSC_MEM_DEVICE) return fail(SFAIRSC_E_INVALID_ARG, "memspace");

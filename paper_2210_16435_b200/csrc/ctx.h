@@ -5,6 +5,7 @@
 #include "kernels.cuh"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <string>
 #include <vector>
@@ -202,6 +203,16 @@ double now_s();
 }
 
 // profiling scope: one event pair around a launch group (sfairsc_profile_*)
+// NVTX range per library phase (SURVEY §5 tracing): sfairsc.build, sfairsc.eigs, sfairsc.restart_sync,
+// sfairsc.rayleigh_ritz (host), sfairsc.true_residuals, sfairsc.kmeans, sfairsc.apply.  NVTX3 is header-only: the
+// calls are no-ops unless a tool (Nsight Systems / Compute with --nvtx) injects itself.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct ProfScope {
   sfairsc_ctx* c;
   int kind;

@@ -1379,6 +1379,7 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
       }
     }
     // ---- sync ----
+    NvtxRange nv_sync("sfairsc.restart_sync");
     CU(cudaMemcpyAsync(Hh.data(), c->Hdev, sizeof(double) * ldH * ldH, cudaMemcpyDeviceToHost, c->st));
     CU(cudaMemcpyAsync(sh.data(), c->sdev, sizeof(double) * m, cudaMemcpyDeviceToHost, c->st));
     CU(cudaMemcpyAsync(c->hp, c->lz, sizeof(double) * 16, cudaMemcpyDeviceToHost, c->st));
@@ -1480,7 +1481,10 @@ sfairsc_status eigs_lagged(sfairsc_ctx* c, int k, double tol, double* evals_out,
     Y = A;
     // only the kept (>= k) smallest Ritz vectors are used below: the selected-vector eigensolver
     const int nsel = std::min(m, std::max(keep, k));
-    symeig(m, Y, theta, nsel);
+    {
+      NvtxRange nv_rr("sfairsc.rayleigh_ritz");
+      symeig(m, Y, theta, nsel);
+    }
     double maxres = 0.0;
     std::vector<double> bY(m, 0.0);
     for (int i = 0; i < nsel; ++i) {
