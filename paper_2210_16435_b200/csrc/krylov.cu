@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) k_ritz_rb(const double* __restrict__
 // register-staged and stored transposed.  Shared-memory row stride 136
 // doubles (= 8 mod 16): every fragment load is 2 wavefronts (conflict-free).
 // ---------------------------------------------------------------------------
-constexpr int kGM = 128, kGN = 128, kGK = 16, kGS = 136;
+constexpr int kGM = 128, kGN = 128, kGK = 16, kGS = 136, kGStages = 4;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(src_bytes)
@@ -273,8 +273,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __rest
                                                             const double* __restrict__ Y, int p,
                                                             double* __restrict__ Vout) {
   extern __shared__ __align__(16) double gsm[];
-  double* As = gsm;                      // [2][kGK][kGS]
-  double* Bs = gsm + 2 * kGK * kGS;      // [2][kGK][kGS]
+  double* As = gsm;                           // [kGStages][kGK][kGS]
+  double* Bs = gsm + kGStages * kGK * kGS;    // [kGStages][kGK][kGS]
   constexpr int NBT = GN / 16;  // 8-column DMMA tiles per warp (2 warp columns)
   const int ncol = (p + GN - 1) / GN;
   const int col0 = (int)(blockIdx.x % ncol) * GN;
@@ -283,11 +283,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __rest
   const int wr = w & 3, wc = w >> 2;
   const int gq = lane >> 2, tq = lane & 3;
   const int nk = (m + kGK - 1) / kGK;
-  // B staging: thread -> (col = tid / 2, 8 consecutive k starting at (tid & 1) * 8)
+  // B staging: thread -> (col = tid / 2, 8 consecutive k starting at (tid & 1) * 8), 8-byte cp.async each (the
+  // transpose of Y's column-major layout), zero-filled beyond p and m
   const int bcol = tid >> 1, bk0 = (tid & 1) * 8;
-  double breg[8];
-  auto load_a = [&](int buf, int k0) {
-    double* dst = As + buf * kGK * kGS;
+  // one k-tile (16 basis columns x 128 rows of V, 16 x GN of Y) into ring stage st as ONE cp.async group
+  auto load_tile = [&](int st, int k0) {
+    double* dst = As + st * kGK * kGS;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int e = tid + q * kThreads;     // 16 columns x 64 pairs of rows
@@ -296,20 +297,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __rest
       const double* src = V + (long long)min(l, m - 1) * ld + row0 + 2 * r2;
       cp_async16(dst + kk * kGS + 2 * r2, src, l < m ? 16 : 0);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  auto load_b = [&](int k0) {
-    const int c = col0 + bcol;
+    if (bcol < GN) {
+      double* bd = Bs + st * kGK * kGS;
+      const int c = col0 + bcol;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int l = k0 + bk0 + q;
-      breg[q] = (bcol < GN && c < p && l < m) ? __ldg(Y + (size_t)c * m + l) : 0.0;
+      for (int q = 0; q < 8; ++q) {
+        const int l = k0 + bk0 + q;
+        const bool ok = c < p && l < m;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_addr(bd + (bk0 + q) * kGS + bcol)),
+                     "l"(ok ? Y + (size_t)c * m + l : Y), "r"(ok ? 8 : 0)
+                     : "memory");
+      }
     }
-  };
-  auto store_b = [&](int buf) {
-    double* dst = Bs + buf * kGK * kGS;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) dst[(bk0 + q) * kGS + bcol] = breg[q];
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
   double acc[4][NBT][2];
 #pragma unroll
@@ -317,21 +317,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __rest
 #pragma unroll
     for (int b = 0; b < NBT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  load_a(0, 0);
-  load_b(0);
-  store_b(0);
+  // kGStages-deep ring: tiles kt+1 .. kt+kGStages-1 are in flight while tile kt is multiplied (a V tile arrives
+  // from HBM in about one tile's DMMA time, so two stages left its latency exposed); one barrier per tile
+#pragma unroll
+  for (int s0 = 0; s0 < kGStages - 1; ++s0) {
+    if (s0 < nk) load_tile(s0, s0 * kGK);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (int kt = 0; kt < nk; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < nk) {
-      load_a(buf ^ 1, (kt + 1) * kGK);
-      load_b((kt + 1) * kGK);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const double* A = As + buf * kGK * kGS;
-    const double* B = Bs + buf * kGK * kGS;
+    asm volatile("cp.async.wait_group %0;" ::"n"(kGStages - 2) : "memory");
+    __syncthreads();  // tile kt visible to all; stage (kt - 1) % kGStages free (everyone finished tile kt - 1)
+    const int kn = kt + kGStages - 1;
+    if (kn < nk) load_tile(kn % kGStages, kn * kGK);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    const double* A = As + (kt % kGStages) * kGK * kGS;
+    const double* B = Bs + (kt % kGStages) * kGK * kGS;
 #pragma unroll
     for (int ks = 0; ks < kGK; ks += 4) {
       double af[4], bf[NBT];
@@ -347,9 +347,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ritz_dmma2(const double* __rest
                        : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
                        : "d"(af[a]), "d"(bf[b]));
     }
-    if (kt + 1 < nk) store_b(buf ^ 1);  // buffer buf^1 was last read in iteration kt-1 (synced below)
-    __syncthreads();
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const long long i = row0 + wr * 32 + a * 8 + gq;
@@ -445,7 +444,7 @@ void launch_ritz_rb(const double* V, long long ld, int n, int m, const double* Y
   if (p <= 0 || n <= 0) return;
   bump_launch();
   if (ld % 2 == 0 && ld >= (long long)((n + kGM - 1) / kGM) * kGM) {  // DMMA tiles (every library-owned basis)
-    const int smem = 4 * kGK * kGS * (int)sizeof(double);
+    const int smem = 2 * kGStages * kGK * kGS * (int)sizeof(double);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_ritz_dmma2<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
