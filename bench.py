@@ -66,6 +66,26 @@ def _peaks():
     return FALLBACK_HBM_GBS, "fallback"
 
 
+# Random 8-byte gathers through the L1tex -> L2 request path: 287 G sectors/s on one B200 whatever the occupancy
+# or gathers in flight (scripts/micro/gather_paths.cu, profiles/r2_exp/gather_paths_ABC.txt).
+GATHER_SECTORS_PER_S = 287e9
+
+
+def _gather_ceiling(info, nnz, n, d):
+    """The SpMV's own ceiling beside the HBM roofline: one L2 sector per gathered entry plus the
+    CSR stream's sectors, at the measured random-sector rate."""
+    if 8.0 * n > 1.34 * 48 * 2**20:
+        return None  # column-blocked SpMV (gathered vector beyond L2): DESIGN.md §10
+    nnz = int(info.get("nnz", nnz))  # this rank's rows (row-partitioned runs)
+    stream_bytes = (4 if info.get("unit_weights") else 12) * nnz + 4 * (n + 1)
+    sectors = nnz + stream_bytes / 32.0
+    floor_us = 1e6 * sectors / GATHER_SECTORS_PER_S
+    us = 1e3 * d["ms"] / max(1, d["launches"])
+    return {"sectors_per_launch": sectors, "rate_sectors_per_s": GATHER_SECTORS_PER_S, "floor_us": floor_us,
+            "us_per_launch": us, "frac": floor_us / us if us > 0 else None,
+            "source": "measured random-gather sector rate, profiles/r2_exp/gather_paths_ABC.txt (DESIGN.md §6.1)"}
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -390,6 +410,7 @@ def main():
                     "measured": "one profiled solve right after the timed region: CUDA events around every launch "
                                 "on the library's (= the bench's) stream; algorithmic bytes per DESIGN.md §6",
                     "profiled_solve_ms": prof_ms, "profiled_solve_applies": pst["applies"],
+                    "gather_ceiling": _gather_ceiling(info, nnz_glob, n_glob, d) if dom == "spmv" else None,
                     "per_kernel": {kk: {"ms": v["ms"], "launches": v["launches"],
                                         "us_per_launch": 1e3 * v["ms"] / v["launches"],
                                         "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
