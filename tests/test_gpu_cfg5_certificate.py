@@ -1,7 +1,7 @@
 """BASELINE config 5 at full size (n = 5e7, 1.6e9 entries): two GPU solves and the SURVEY §8(c)
 host certificate through the Tier S oracle (tests/tools/cfg5_certificate.py; ~20-30 min on one
 B200 + its host).  Opt-in: SFAIRSC_CFG5_CERT=1 (the default GPU suite stays within minutes; the
-committed record is profiles/r2_cfg5_certificate.json).  SFAIRSC_CFG5_N overrides n."""
+committed record is profiles/r2x_cfg5_certificate.json).  SFAIRSC_CFG5_N overrides n."""
 import json
 import os
 import subprocess
